@@ -1,0 +1,197 @@
+/*
+ * include/nss.h -- C ABI of the B200-native Nested Slice Sampling hot path
+ * (arXiv 2601.23252).  Shared library: paper_2601_23252_b200/libnss.so.
+ *
+ * "P:n" cites /root/reference/PAPER.md line n; "R-n" cites a reading in
+ * DESIGN.md section 2 where the paper is silent or ambiguous.
+ *
+ * Conventions (all entry points):
+ *  - Every call returns nss_status; nothing throws across the ABI.
+ *  - All pointers are HOST pointers unless stated otherwise.  Input arrays are
+ *    copied during the call; the caller keeps ownership and may free them when
+ *    the call returns.  Output arrays are caller-owned host buffers.
+ *  - The context owns all device memory (allocated in nss_init, released in
+ *    nss_destroy) and runs every kernel on one CUDA stream (nss_dist.cuda_stream
+ *    or a stream it creates).  Calls are asynchronous unless they return data.
+ *  - A CUDA failure poisons the context: every later call except nss_destroy and
+ *    nss_last_error returns NSS_ERR_CUDA.
+ *  - One host thread per context; several contexts may coexist.
+ *  - Positions and energies are fp32 on the device; covariance, Cholesky and
+ *    evidence accumulators are fp64 (R-22).
+ */
+#ifndef NSS_H
+#define NSS_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  NSS_OK = 0,
+  NSS_ERR_INVALID_ARG = 1,   /* bad config / null pointer / unknown kind          */
+  NSS_ERR_PRIOR_SUPPORT = 2, /* init: no finite energy within 100 n prior draws (R-20) */
+  NSS_ERR_NAN = 3,           /* an energy evaluation returned NaN                 */
+  NSS_ERR_CUDA = 4,          /* CUDA runtime failure (context poisoned)           */
+  NSS_ERR_COMM = 5,          /* inter-rank communication failure                  */
+  NSS_ERR_OOM = 6,           /* device allocation failed                          */
+  NSS_ERR_STATE = 7,         /* call not valid in the current state               */
+  NSS_ERR_CAPACITY = 8,      /* dead store full (R-26) or output buffer too small */
+  NSS_ERR_UNSUPPORTED = 9    /* configuration not implemented on this device path */
+} nss_status;
+
+/* ---- reference density Pi ---- */
+typedef enum { NSS_PRIOR_BOX = 0, NSS_PRIOR_GAUSS_DIAG = 1 } nss_prior_kind;
+typedef struct {
+  int32_t kind;             /* nss_prior_kind                                    */
+  int32_t d;                /* dimension, 1 <= d <= NSS_MAX_DIM                  */
+  const double *lo, *hi;    /* BOX: d each, lo < hi; log Pi = -sum log(hi-lo)    */
+  const double *mean, *sd;  /* GAUSS_DIAG: d each, sd > 0                        */
+} nss_prior;
+
+#define NSS_MAX_DIM 128
+
+/* ---- energy E(x) = -log L(x) ---- */
+typedef enum {
+  NSS_E_GAUSS = 0,      /* 1/2 sum_i ((x_i-mu_i)/sigma_i)^2 + c                          */
+  NSS_E_MOG = 1,        /* -log sum_j w_j N(x; mu_j, diag sigma_j^2)       */
+  NSS_E_CORR_GAUSS = 2, /* 1/2 (x-mu)^T P (x-mu) + c           */
+  NSS_E_FUNNEL = 3,     /* -log N(x_0;0,sy^2) - sum_{n>=1} log N(x_n;0,e^{x_0}) (R-23) */
+  NSS_E_LOGREG = 4,     /* sum_r softplus(a_r.x) - y_r a_r.x                             */
+  NSS_E_GP_ARD = 5,     /* GP ARD-RBF negative log marginal likelihood       */
+  NSS_E_FLAT = 6        /* E = c (level-set / flat-likelihood tests)                     */
+} nss_energy_kind;
+typedef struct {
+  int32_t kind;         /* nss_energy_kind                                  */
+  int32_t d;            /* must equal the prior's d                         */
+  int32_t n_comp;       /* MOG: number of components K (1..16)              */
+  int64_t n_data;       /* LOGREG / GP: rows N                              */
+  int32_t d_in;         /* GP: inputs per row; d = d_in + 2                 */
+  const double *w;      /* MOG: K weights                                   */
+  const double *mu;     /* GAUSS, CORR_GAUSS: d;  MOG: K*d row-major        */
+  const double *sigma;  /* GAUSS: d;  MOG: K*d                              */
+  const double *prec;   /* CORR_GAUSS: d*d row-major symmetric precision    */
+  const double *data_x; /* LOGREG: N*d;  GP: N*d_in (row-major)             */
+  const double *data_y; /* LOGREG: N labels in {0,1};  GP: N targets        */
+  double c;             /* GAUSS / CORR_GAUSS / FLAT additive constant      */
+  double sigma_y;       /* FUNNEL: standard deviation of x_0                */
+  double jitter;        /* GP: added to sigma_n^2 on the diagonal           */
+} nss_energy;
+
+typedef enum { NSS_W_OPTIMAL = 0, NSS_W_FIXED = 1 } nss_width_rule;       /* R-7 */
+typedef enum { NSS_DIR_MAHALANOBIS = 0, NSS_DIR_EUCLIDEAN = 1 } nss_dir_norm; /* R-6 */
+typedef enum { NSS_Q_TRAPEZOID = 0, NSS_Q_RECTANGLE = 1 } nss_quadrature;  /* R-16 */
+
+typedef struct {
+  int64_t n_live;        /* m, >= 2                                        */
+  int64_t k;             /* deleted per iteration, 1 <= k <= n_live-1      */
+  int32_t steps;         /* p HRSS steps per replacement, >= 0             */
+  int32_t width_rule;    /* nss_width_rule                                         */
+  double width;          /* FIXED: w;  OPTIMAL: scale c on 4 kappa sqrt(2/(pi mu d)) */
+  int32_t dir_norm;      /* nss_dir_norm                                           */
+  int32_t max_stepout;   /* expansions per side, 10 in the paper           */
+  int32_t max_shrink;    /* shrink proposals, 100 in the paper             */
+  int32_t quadrature;    /* nss_quadrature                                         */
+  double metric_reg;     /* ridge * mean diag (R-8), 1e-6                          */
+  double term_log_ratio; /* termination threshold, -3 (R-19)                */
+  int32_t n_volume_sims; /* R volume replicas, >= 2                       */
+  int64_t max_dead;      /* dead-store capacity in records, >= n_live (R-26)       */
+  uint64_t seed;         /* Philox key                          */
+} nss_config;
+
+/* Multi-GPU: one process per GPU, live set sharded by gid blocks (DESIGN 9).
+ * Pass NULL for a single GPU. */
+typedef struct {
+  int32_t rank, world;
+  const uint8_t *nccl_uid; /* 128 bytes from nss_get_unique_id on rank 0      */
+  void *cuda_stream;       /* cudaStream_t to run on, or NULL for a new stream */
+} nss_dist;
+
+typedef struct {
+  int64_t iteration;      /* outer iterations completed                         */
+  double e_star;          /* threshold E* of the last iteration         */
+  int64_t probes;         /* slice-membership tests (R-11)                      */
+  int64_t energy_evals;   /* energies evaluated inside HRSS (R-11)              */
+  int64_t expansions;     /* stepping-out expansions (N_out)                    */
+  int64_t shrinks;        /* shrink proposals (N_shrink)                        */
+  int64_t null_moves;     /* steps that hit the shrink cap              */
+  int64_t init_evals;     /* energies evaluated by nss_init                     */
+  double log_z_det;       /* replica-0 accumulated log Z                        */
+  double log_z_live;      /* -min E_live + log X (replica 0)            */
+  int32_t terminated;     /* termination criterion met (R-19)                   */
+  int32_t finalised;      /* live set appended to the dead store (R-18)         */
+} nss_step_info;
+
+typedef struct nss_ctx nss_ctx;
+
+/* Rank 0 of a multi-GPU run: fills 128 bytes to broadcast to the other ranks. */
+nss_status nss_get_unique_id(uint8_t out[128]);
+
+/* Validate, allocate, upload prior/energy data, draw the n initial live points
+ * from the prior with rejection (R-20) and compute the first metric.
+ * Errors: INVALID_ARG (k not in [1,n-1], d out of range, steps < 0, caps < 1,
+ * R < 2, max_dead < n, unknown kind), PRIOR_SUPPORT, NAN, OOM, CUDA,
+ * UNSUPPORTED. */
+nss_status nss_init(const nss_prior *prior, const nss_energy *energy, const nss_config *cfg,
+                    const nss_dist *dist, nss_ctx **out);
+
+/* One outer iteration: delete, record dead, resample, p HRSS steps,
+ * replace, metric, evidence, termination flag.  Asynchronous when info == NULL;
+ * a non-NULL info synchronises and reports.  A call after termination is a
+ * no-op on the device.  Errors: STATE (finalised), CAPACITY, NAN, CUDA. */
+nss_status nss_step(nss_ctx *ctx, nss_step_info *info);
+
+/* Enqueue `count` iterations without synchronising (benchmark / driver loop). */
+nss_status nss_steps(nss_ctx *ctx, int64_t count);
+
+/* Iterate until the termination criterion (R-19) or max_iters, then finalise. */
+nss_status nss_run(nss_ctx *ctx, int64_t max_iters, nss_step_info *info);
+
+/* Append the live set to the dead store and close the quadrature (R-18). */
+nss_status nss_finalise(nss_ctx *ctx);
+
+/* log Z = mean of log Z^(r), r=1..R; err = their sample std (R-17).
+ * Errors: STATE when the dead store is empty. */
+nss_status nss_evidence(nss_ctx *ctx, double *log_z, double *log_z_err);
+/* All R+1 replica values (replica 0 deterministic). */
+nss_status nss_evidence_reps(nss_ctx *ctx, double *log_z_reps /* R+1 */);
+
+/* Dead points with normalised geometric-mean log weights.
+ * Two-call pattern: x == NULL and log_w == NULL -> only *n_out.  x: n_out*d
+ * row-major fp64.  Errors: STATE (empty), CAPACITY (cap < n_out). */
+nss_status nss_samples(nss_ctx *ctx, double *x, double *log_w, int64_t cap, int64_t *n_out);
+
+nss_status nss_info(nss_ctx *ctx, nss_step_info *info);   /* synchronises */
+nss_status nss_sync(nss_ctx *ctx);
+nss_status nss_destroy(nss_ctx *ctx);
+const char *nss_last_error(const nss_ctx *ctx);
+
+/* ---- parity hooks (exported for the tests; not on the user path) ---- */
+/* Inject a live set (n*d fp32 positions, n fp32 energies); the next nss_step
+ * is iteration `next_iteration`.  Recomputes the metric from x. */
+nss_status nss_set_live(nss_ctx *ctx, const float *x, const float *e, int64_t next_iteration);
+nss_status nss_get_live(nss_ctx *ctx, float *x, float *e);
+nss_status nss_get_metric(nss_ctx *ctx, double *chol /* d*d lower, fp64 */, double *width);
+/* Last iteration: dead gids (key-descending), destination gids (ascending),
+ * parent gid per destination, per (chain, step) counts packed as bytes
+ * {n_left, n_right, n_shrink, accepted}, E*. Any pointer may be NULL. */
+nss_status nss_get_trace(nss_ctx *ctx, int32_t *dead_gid, int32_t *dest_gid, int32_t *parent_gid,
+                         uint8_t *counts /* k*p*4 */, float *e_star);
+nss_status nss_dead(nss_ctx *ctx, float *e, int32_t *n_live, float *birth, int32_t *gid, float *x,
+                    int64_t cap, int64_t *n_out);
+nss_status nss_volume_reps(nss_ctx *ctx, double *log_x /* R+1 */);
+
+/* ---- measurement hooks ---- */
+/* When enabled, the HRSS kernel launch of every iteration is bracketed by CUDA
+ * events on the context's stream; nss_kernel_time returns the summed elapsed
+ * milliseconds and the number of launches since the last reset. */
+nss_status nss_set_kernel_timing(nss_ctx *ctx, int32_t enable);
+nss_status nss_kernel_time(nss_ctx *ctx, double *ms, int64_t *launches);
+/* Kernels launched by this context since creation (all kinds). */
+nss_status nss_launch_count(nss_ctx *ctx, int64_t *launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

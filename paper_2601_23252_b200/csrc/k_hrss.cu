@@ -1,0 +1,540 @@
+// A6 mutate / A7 replace / A1 energies: Hit-and-Run Slice Sampling chains
+// and the prior draws of nss_init (R-20).
+//
+// One warp per chain.  Coordinates are spread over the lanes (lane l holds
+// coordinates l, l+32, ...; NPL = ceil(d/32) registers), so x' = x + t v is one
+// FMA per lane, energies are warp-cooperative (lane-partial sums + xor-shuffle
+// reduction) and every slice decision is warp-uniform: no intra-warp divergence
+// in the step-out / shrink loops, the cost of uneven chains is paid as a tail
+// across warps instead.  The whitening factor L and the
+// energy parameters are staged once per CTA in shared memory; the direction's
+// normals are staged per warp.  Every random number comes from the counter-based
+// Philox stream (iter, dest gid, HRSS, step), so a chain's result does not
+// depend on where or when it runs.
+#include "nss_internal.cuh"
+
+namespace nss {
+
+namespace {
+
+constexpr float kLn2Pi = 1.8378770664093453f;
+constexpr unsigned kFull = 0xffffffffu;
+
+struct ESm {          // shared-memory image of the energy parameters
+  const float *mu;    // GAUSS/CORR: d; MOG: K*d
+  const float *isig;  // GAUSS: d; MOG: K*d
+  const float *logc;  // MOG: K
+  const float *prec;  // CORR: d rows of stride ldp
+  int ldp;
+};
+
+__host__ __device__ inline int odd_stride(int d) { return d | 1; }
+
+// number of floats of energy parameters staged in shared memory
+__host__ __device__ inline int energy_param_floats(int kind, int d, int K) {
+  switch (kind) {
+    case NSS_E_GAUSS: return 2 * d;
+    case NSS_E_MOG: return 2 * K * d + K;
+    case NSS_E_CORR_GAUSS: return d + d * odd_stride(d);
+    default: return 0;
+  }
+}
+
+__device__ void stage_energy(const EnergyDev &en, float *sp, ESm &es) {
+  const int d = en.d, tid = threadIdx.x, nt = blockDim.x;
+  es.ldp = odd_stride(d);
+  if (en.kind == NSS_E_GAUSS) {
+    for (int i = tid; i < d; i += nt) { sp[i] = en.mu[i]; sp[d + i] = en.isig[i]; }
+    es.mu = sp; es.isig = sp + d;
+  } else if (en.kind == NSS_E_MOG) {
+    const int K = en.n_comp;
+    for (int i = tid; i < K * d; i += nt) { sp[i] = en.mu[i]; sp[K * d + i] = en.isig[i]; }
+    for (int j = tid; j < K; j += nt) sp[2 * K * d + j] = en.logc[j];
+    es.mu = sp; es.isig = sp + K * d; es.logc = sp + 2 * K * d;
+  } else if (en.kind == NSS_E_CORR_GAUSS) {
+    for (int i = tid; i < d; i += nt) sp[i] = en.mu[i];
+    float *P = sp + d;
+    for (int e = tid; e < d * d; e += nt) {
+      int i = e / d, j = e - i * d;
+      P[i * es.ldp + j] = en.prec[e];
+    }
+    es.mu = sp; es.prec = P;
+  }
+}
+
+__device__ __forceinline__ float softplusf(float a) {
+  return a > 0.f ? a + log1pf(expf(-a)) : log1pf(expf(a));
+}
+
+// Warp-cooperative energy E(x); the result is identical in every lane.
+// `wbuf` is a per-warp shared buffer of NPL*32 floats.
+template <int NPL, int KIND>
+__device__ __forceinline__ float warp_energy(const float (&x)[NPL], const EnergyDev &en, const ESm &es,
+                                             float *wbuf, int lane) {
+  const int d = en.d;
+  if constexpr (KIND == NSS_E_FLAT) {
+    return en.c;
+  } else if constexpr (KIND == NSS_E_GAUSS) {
+    float s = 0.f;
+#pragma unroll
+    for (int t = 0; t < NPL; ++t) {
+      const int i = lane + 32 * t;
+      if (i < d) {
+        float u = (x[t] - es.mu[i]) * es.isig[i];
+        s = fmaf(u, u, s);
+      }
+    }
+    return 0.5f * warp_sum(s) + en.c;
+  } else if constexpr (KIND == NSS_E_MOG) {
+    const int K = en.n_comp;
+    float s[kMaxComp];
+#pragma unroll
+    for (int j = 0; j < kMaxComp; ++j) {
+      s[j] = 0.f;
+      if (j < K) {
+#pragma unroll
+        for (int t = 0; t < NPL; ++t) {
+          const int i = lane + 32 * t;
+          if (i < d) {
+            float u = (x[t] - es.mu[j * d + i]) * es.isig[j * d + i];
+            s[j] = fmaf(u, u, s[j]);
+          }
+        }
+      }
+    }
+    // interleaved butterflies: the K reductions are independent
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+      for (int j = 0; j < kMaxComp; ++j)
+        if (j < K) s[j] += __shfl_xor_sync(kFull, s[j], o);
+    }
+    float m = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < kMaxComp; ++j)
+      if (j < K) m = fmaxf(m, es.logc[j] - 0.5f * s[j]);
+    float acc = 0.f;
+#pragma unroll
+    for (int j = 0; j < kMaxComp; ++j)
+      if (j < K) acc += expf(es.logc[j] - 0.5f * s[j] - m);
+    return -(m + logf(acc));
+  } else if constexpr (KIND == NSS_E_CORR_GAUSS) {
+#pragma unroll
+    for (int t = 0; t < NPL; ++t) {
+      const int i = lane + 32 * t;
+      if (i < d) wbuf[i] = x[t] - es.mu[i];
+    }
+    __syncwarp();
+    float q = 0.f;
+#pragma unroll
+    for (int t = 0; t < NPL; ++t) {
+      const int i = lane + 32 * t;
+      if (i < d) {
+        const float *row = es.prec + i * es.ldp;
+        float py = 0.f;
+        for (int m = 0; m < d; ++m) py = fmaf(row[m], wbuf[m], py);
+        q = fmaf(wbuf[i], py, q);
+      }
+    }
+    q = warp_sum(q);
+    __syncwarp();
+    return 0.5f * q + en.c;
+  } else if constexpr (KIND == NSS_E_FUNNEL) {
+    // P:885 (R-23): x_0 = y ~ N(0, sy^2), x_n ~ N(0, e^y)
+    const float y = __shfl_sync(kFull, x[0], 0);
+    float s = 0.f;
+#pragma unroll
+    for (int t = 0; t < NPL; ++t) {
+      const int i = lane + 32 * t;
+      if (i >= 1 && i < d) s = fmaf(x[t], x[t], s);
+    }
+    s = warp_sum(s);
+    const float sy = en.sigma_y;
+    const float yy = y / sy;
+    return 0.5f * yy * yy + logf(sy) + 0.5f * kLn2Pi + 0.5f * s * expf(-y) +
+           static_cast<float>(d - 1) * 0.5f * (y + kLn2Pi);
+  } else if constexpr (KIND == NSS_E_LOGREG) {
+    // naive warp path (lanes over data rows); the batched tensor-core engine is
+    // the production path for large N
+#pragma unroll
+    for (int t = 0; t < NPL; ++t) {
+      const int i = lane + 32 * t;
+      if (i < d) wbuf[i] = x[t];
+    }
+    __syncwarp();
+    float acc = 0.f;
+    for (long long rr = lane; rr < en.n_data; rr += 32) {
+      const float *row = en.data_x + rr * d;
+      float a = 0.f;
+      for (int m = 0; m < d; ++m) a = fmaf(row[m], wbuf[m], a);
+      acc += softplusf(a) - en.data_y[rr] * a;
+    }
+    acc = warp_sum(acc);
+    __syncwarp();
+    return acc;
+  } else {
+    return NAN;
+  }
+}
+
+// log Pi(x) and support test (box: all lanes inside; Gaussian: always inside).
+template <int NPL>
+__device__ __forceinline__ float prior_logp(const float (&x)[NPL], const PriorDev &pr, const float (&pa)[NPL],
+                                            const float (&pb)[NPL], int lane, int d, bool &inside) {
+  if (pr.kind == NSS_PRIOR_BOX) {
+    bool ok = true;
+#pragma unroll
+    for (int t = 0; t < NPL; ++t) {
+      const int i = lane + 32 * t;
+      if (i < d) ok = ok && (x[t] >= pa[t]) && (x[t] <= pb[t]);
+    }
+    inside = __all_sync(kFull, ok);
+    return pr.log_norm;
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int t = 0; t < NPL; ++t) {
+    const int i = lane + 32 * t;
+    if (i < d) {
+      float u = (x[t] - pa[t]) * pb[t];
+      s = fmaf(u, u, s);
+    }
+  }
+  inside = true;
+  return -0.5f * warp_sum(s) + pr.log_norm;
+}
+
+template <int NPL>
+__device__ __forceinline__ void load_prior_lane(const PriorDev &pr, int lane, int d, float (&pa)[NPL],
+                                                float (&pb)[NPL]) {
+#pragma unroll
+  for (int t = 0; t < NPL; ++t) {
+    const int i = lane + 32 * t;
+    if (pr.kind == NSS_PRIOR_BOX) {
+      pa[t] = i < d ? pr.lo[i] : 0.f;
+      pb[t] = i < d ? pr.hi[i] : 0.f;
+    } else {
+      pa[t] = i < d ? pr.mean[i] : 0.f;
+      pb[t] = i < d ? pr.isd[i] : 0.f;
+    }
+  }
+}
+
+struct Probe {
+  float e;
+  float lp;
+};
+
+template <int NPL, int KIND>
+__global__ void __launch_bounds__(256) k_hrss(RunDev r, PriorDev pr, EnergyDev en) {
+  extern __shared__ float sm[];
+  __shared__ int sh_flag;
+  const int d = r.d, lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  const int ldl = odd_stride(d);
+  float *sL = sm;
+  float *sP = sL + d * ldl;
+  const int npar = energy_param_floats(KIND, d, en.n_comp);
+  float *sZ = sP + npar + wib * (2 * NPL * 32);
+  float *sY = sZ + NPL * 32;
+  if (threadIdx.x == 0) sh_flag = (r.st->terminated || r.st->error || r.st->finalised) ? 1 : 0;
+  for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
+    int i = e / d, j = e - i * d;
+    sL[i * ldl + j] = r.L[i * r.dp + j];
+  }
+  ESm es;
+  stage_energy(en, sP, es);
+  __syncthreads();
+  if (sh_flag) return;
+  const int c = blockIdx.x * wpb + wib;
+  if (c >= r.k) return;
+
+  DevState *st = r.st;
+  const uint32_t it = static_cast<uint32_t>(st->iter + 1);
+  const int s = r.dest_gid[c];
+  const int par = r.parent_gid[c];
+  const float e_star = st->e_star;
+  const float w = st->width;
+  const int p = r.p;
+  const bool euclid = r.dir_norm == NSS_DIR_EUCLIDEAN;
+  const int h = 2 * ((d + 1) / 2);           // first non-normal draw index
+  const int nblk_norm = h >> 2;              // Philox blocks fully made of normals
+  const int nblk_all = (h + 3) >> 2;         // blocks touching the normals
+
+  float pa[NPL], pb[NPL];
+  load_prior_lane<NPL>(pr, lane, d, pa, pb);
+  float x[NPL], v[NPL], xp[NPL];
+#pragma unroll
+  for (int t = 0; t < NPL; ++t) {
+    const int i = lane + 32 * t;
+    x[t] = i < d ? r.X[static_cast<long long>(par) * r.dp + i] : 0.f;
+  }
+  float e = r.E[par];
+  bool dummy;
+  float lp = prior_logp<NPL>(x, pr, pa, pb, lane, d, dummy);
+
+  unsigned long long n_probe = 0, n_eval = 0, n_exp = 0, n_shr = 0, n_null = 0;
+
+  for (int j = 0; j < p; ++j) {
+    // ---- direction v = L z / |z| (Mahalanobis, R-6) or L z / |L z| ----
+    for (int b = lane; b < nblk_all; b += 32) {
+      uint4 u4 = philox_block(r, it, s, kPhaseHrss, j, b);
+      float u0 = u01(u4.x), u1 = u01(u4.y), u2 = u01(u4.z), u3 = u01(u4.w);
+      float r0 = sqrtf(-2.f * logf(u0)), r1 = sqrtf(-2.f * logf(u2));
+      float s0, c0, s1, c1;
+      sincospif(2.f * u1, &s0, &c0);
+      sincospif(2.f * u3, &s1, &c1);
+      const int i0 = 4 * b;
+      if (i0 < d) sZ[i0] = r0 * c0;
+      if (i0 + 1 < d) sZ[i0 + 1] = r0 * s0;
+      if (b < nblk_norm) {  // the partial last block carries u_h, u_b in words 2, 3
+        if (i0 + 2 < d) sZ[i0 + 2] = r1 * c1;
+        if (i0 + 3 < d) sZ[i0 + 3] = r1 * s1;
+      }
+    }
+    __syncwarp();
+    float zz = 0.f, vv = 0.f;
+#pragma unroll
+    for (int t = 0; t < NPL; ++t) {
+      const int i = lane + 32 * t;
+      float acc = 0.f;
+      if (i < d) {
+        const float zi = sZ[i];
+        zz = fmaf(zi, zi, zz);
+        const float *row = sL + i * ldl;
+        for (int m = 0; m <= i; ++m) acc = fmaf(row[m], sZ[m], acc);
+      }
+      v[t] = acc;
+      vv = fmaf(acc, acc, vv);
+    }
+    const float nrm = sqrtf(warp_sum(euclid ? vv : zz));
+    const float inv = 1.f / nrm;
+#pragma unroll
+    for (int t = 0; t < NPL; ++t) v[t] *= inv;
+    __syncwarp();
+
+    // ---- slice height and initial bracket (R-9) ----
+    const uint4 hb = philox_block(r, it, s, kPhaseHrss, j, h >> 2);
+    const float u_h = u01(word(hb, h & 3));
+    const float u_b = u01(word(hb, (h + 1) & 3));
+    const float log_y = lp + logf(u_h);
+    float lft = -w * u_b;
+    float rgt = lft + w;
+
+    Probe pr_last{0.f, 0.f};
+    // in(t): x + t v in the support, log Pi >= log y, E < E*  (R-2, R-11)
+    auto in_slice = [&](float tt) -> bool {
+      ++n_probe;
+#pragma unroll
+      for (int t = 0; t < NPL; ++t) xp[t] = fmaf(tt, v[t], x[t]);
+      bool inside;
+      float lpp = prior_logp<NPL>(xp, pr, pa, pb, lane, d, inside);
+      if (!inside || !(lpp >= log_y)) return false;
+      float ep = warp_energy<NPL, KIND>(xp, en, es, sY, lane);
+      ++n_eval;
+      if (isnan(ep)) {
+        if (lane == 0) raise_error(st, NSS_ERR_NAN);
+        return false;
+      }
+      pr_last.e = ep;
+      pr_last.lp = lpp;
+      return ep < e_star;
+    };
+
+    // ---- linear stepping-out, capped per side (R-10) ----
+    int nl = 0, nr = 0;
+    while (nl < r.max_stepout && in_slice(lft)) { lft -= w; ++nl; }
+    while (nr < r.max_stepout && in_slice(rgt)) { rgt += w; ++nr; }
+
+    // ---- shrinkage, capped; null move at the cap (R-12/R-13) ----
+    int ns = 0, acc = 0;
+    int cached_blk = -1;
+    uint4 cb = make_uint4(0, 0, 0, 0);
+    for (int i = 0; i < r.max_shrink; ++i) {
+      const int q = h + 2 + i;
+      if ((q >> 2) != cached_blk) {
+        cached_blk = q >> 2;
+        cb = philox_block(r, it, s, kPhaseHrss, j, cached_blk);
+      }
+      const float u = u01(word(cb, q & 3));
+      const float tt = fmaf(u, rgt - lft, lft);
+      ++ns;
+      if (in_slice(tt)) {
+#pragma unroll
+        for (int t = 0; t < NPL; ++t) x[t] = xp[t];
+        e = pr_last.e;
+        lp = pr_last.lp;
+        acc = 1;
+        break;
+      }
+      if (tt < 0.f) lft = tt; else rgt = tt;
+    }
+    n_exp += nl + nr;
+    n_shr += ns;
+    n_null += acc ? 0 : 1;
+    if (lane == 0)
+      r.counts[static_cast<long long>(c) * p + j] =
+          static_cast<uint32_t>(nl) | (static_cast<uint32_t>(nr) << 8) | (static_cast<uint32_t>(ns) << 16) |
+          (static_cast<uint32_t>(acc) << 24);
+  }
+
+  // ---- replace ----
+#pragma unroll
+  for (int t = 0; t < NPL; ++t) {
+    const int i = lane + 32 * t;
+    if (i < d) r.X[static_cast<long long>(s) * r.dp + i] = x[t];
+  }
+  if (lane == 0) {
+    r.E[s] = e;
+    r.birth[s] = e_star;
+    atomicAdd(&st->probes, n_probe);
+    atomicAdd(&st->evals, n_eval);
+    atomicAdd(&st->expansions, n_exp);
+    atomicAdd(&st->shrinks, n_shr);
+    atomicAdd(&st->nulls, n_null);
+  }
+}
+
+// Prior draws with rejection until E is finite (R-20); one warp per gid.
+template <int NPL, int KIND>
+__global__ void __launch_bounds__(256) k_init(RunDev r, PriorDev pr, EnergyDev en) {
+  extern __shared__ float sm[];
+  const int d = r.d, lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  const int npar = energy_param_floats(KIND, d, en.n_comp);
+  float *sP = sm;
+  float *sY = sP + npar + wib * (NPL * 32);
+  ESm es;
+  stage_energy(en, sP, es);
+  __syncthreads();
+  const int g = blockIdx.x * wpb + wib;
+  if (g >= r.n) return;
+  DevState *st = r.st;
+  const unsigned long long budget = 100ull * static_cast<unsigned long long>(r.n);
+  float pa[NPL], pb[NPL];
+  load_prior_lane<NPL>(pr, lane, d, pa, pb);
+  for (uint32_t a = 0;; ++a) {
+    unsigned long long used = 0;
+    if (lane == 0) used = atomicAdd(&st->init_attempts, 1ull);
+    used = __shfl_sync(kFull, used, 0);
+    if (used >= budget) {
+      if (lane == 0) raise_error(st, NSS_ERR_PRIOR_SUPPORT);
+      return;
+    }
+    float x[NPL];
+#pragma unroll
+    for (int t = 0; t < NPL; ++t) {
+      const int i = lane + 32 * t;
+      x[t] = 0.f;
+      if (i < d) {
+        if (pr.kind == NSS_PRIOR_BOX) {
+          uint4 b = philox_block(r, 0, g, kPhaseInit, a, i >> 2);
+          x[t] = fmaf(u01(word(b, i & 3)), pb[t] - pa[t], pa[t]);
+        } else {
+          const int m = i >> 1;  // Box-Muller pair (2m, 2m+1)
+          uint4 b = philox_block(r, 0, g, kPhaseInit, a, (2 * m) >> 2);
+          const float u1 = u01(word(b, (2 * m) & 3)), u2 = u01(word(b, (2 * m + 1) & 3));
+          const float rr = sqrtf(-2.f * logf(u1));
+          float sn, cs;
+          sincospif(2.f * u2, &sn, &cs);
+          const float z = (i & 1) ? rr * sn : rr * cs;
+          x[t] = fmaf(z, pr.sd[i], pa[t]);
+        }
+      }
+    }
+    float e = warp_energy<NPL, KIND>(x, en, es, sY, lane);
+    if (lane == 0) atomicAdd(&st->init_evals, 1ull);
+    if (isnan(e)) {
+      if (lane == 0) raise_error(st, NSS_ERR_NAN);
+      return;
+    }
+    if (isfinite(e)) {
+#pragma unroll
+      for (int t = 0; t < NPL; ++t) {
+        const int i = lane + 32 * t;
+        if (i < d) r.X[static_cast<long long>(g) * r.dp + i] = x[t];
+      }
+      if (lane == 0) {
+        r.E[g] = e;
+        r.birth[g] = INFINITY;
+      }
+      return;
+    }
+  }
+}
+
+template <int NPL, int KIND>
+void launch_hrss_t(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc) {
+  const int ldl = odd_stride(r.d);
+  int wpb = r.k / 296;
+  wpb = wpb < 1 ? 1 : (wpb > 8 ? 8 : wpb);
+  const size_t smem = (static_cast<size_t>(r.d) * ldl + energy_param_floats(KIND, r.d, en.n_comp) +
+                       static_cast<size_t>(wpb) * 2 * NPL * 32) * sizeof(float);
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && attr < smem) {
+    cudaFuncSetAttribute(k_hrss<NPL, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    attr = smem;
+  }
+  const int blocks = (r.k + wpb - 1) / wpb;
+  k_hrss<NPL, KIND><<<blocks, wpb * 32, smem, lc.stream>>>(r, pr, en);
+  ++*lc.launch_counter;
+}
+
+template <int NPL, int KIND>
+void launch_init_t(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc) {
+  const int wpb = 8;
+  const size_t smem = (energy_param_floats(KIND, r.d, en.n_comp) + static_cast<size_t>(wpb) * NPL * 32) * sizeof(float);
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && attr < smem) {
+    cudaFuncSetAttribute(k_init<NPL, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    attr = smem;
+  }
+  const int blocks = (r.n + wpb - 1) / wpb;
+  k_init<NPL, KIND><<<blocks, wpb * 32, smem, lc.stream>>>(r, pr, en);
+  ++*lc.launch_counter;
+}
+
+#define NSS_DISPATCH(FN, ...)                                                     \
+  do {                                                                            \
+    const int npl = (r.d + 31) / 32;                                              \
+    switch (en.kind) {                                                            \
+      case NSS_E_FLAT: NSS_DISPATCH_NPL(FN, NSS_E_FLAT, __VA_ARGS__); break;      \
+      case NSS_E_GAUSS: NSS_DISPATCH_NPL(FN, NSS_E_GAUSS, __VA_ARGS__); break;    \
+      case NSS_E_MOG: NSS_DISPATCH_NPL(FN, NSS_E_MOG, __VA_ARGS__); break;        \
+      case NSS_E_CORR_GAUSS: NSS_DISPATCH_NPL(FN, NSS_E_CORR_GAUSS, __VA_ARGS__); break; \
+      case NSS_E_FUNNEL: NSS_DISPATCH_NPL(FN, NSS_E_FUNNEL, __VA_ARGS__); break;  \
+      case NSS_E_LOGREG: NSS_DISPATCH_NPL(FN, NSS_E_LOGREG, __VA_ARGS__); break;  \
+      default: break;                                                             \
+    }                                                                             \
+  } while (0)
+#define NSS_DISPATCH_NPL(FN, KIND, ...)                   \
+  switch (npl) {                                          \
+    case 1: FN<1, KIND>(__VA_ARGS__); break;              \
+    case 2: FN<2, KIND>(__VA_ARGS__); break;              \
+    case 3: FN<3, KIND>(__VA_ARGS__); break;              \
+    default: FN<4, KIND>(__VA_ARGS__); break;             \
+  }
+
+}  // namespace
+
+bool energy_supported(const EnergyDev &en) {
+  switch (en.kind) {
+    case NSS_E_FLAT: case NSS_E_GAUSS: case NSS_E_MOG: case NSS_E_CORR_GAUSS: case NSS_E_FUNNEL:
+    case NSS_E_LOGREG:
+      return en.n_comp <= kMaxComp;
+    default:
+      return false;
+  }
+}
+
+size_t energy_smem_bytes(const EnergyDev &en) {
+  return static_cast<size_t>(energy_param_floats(en.kind, en.d, en.n_comp)) * sizeof(float);
+}
+
+void launch_hrss(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc) {
+  NSS_DISPATCH(launch_hrss_t, r, pr, en, lc);
+}
+
+void launch_init(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc) {
+  NSS_DISPATCH(launch_init_t, r, pr, en, lc);
+}
+
+}  // namespace nss

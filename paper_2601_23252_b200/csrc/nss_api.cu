@@ -1,0 +1,664 @@
+// C ABI (include/nss.h) and host orchestration of one NSS run on one GPU.
+//
+// The host only validates, allocates, uploads the problem once, enqueues the
+// per-iteration kernels on one stream and copies results back; every step of
+// the method runs on the device.  Iterations after the
+// termination criterion is met are no-ops on the device, so nss_run can enqueue
+// ahead and poll a small state struct instead of synchronising every iteration.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "nss_internal.cuh"
+
+#define NSS_API extern "C" __attribute__((visibility("default")))
+
+using namespace nss;
+
+namespace nss {
+void launch_evidence_summary(const RunDev &r, double *out, const LaunchCtx &lc);
+void launch_samples(const RunDev &r, long long N, double *logw, double *scratch, int chunk, const LaunchCtx &lc);
+}  // namespace nss
+
+struct nss_ctx {
+  nss_config cfg{};
+  int d = 0, dp = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  RunDev r{};
+  PriorDev pr{};
+  EnergyDev en{};
+  std::vector<void *> allocs;
+  double *partials = nullptr;
+  int nblk = 1;
+  double *summary = nullptr;  // device: [mean, std, closed lz_0..R]
+  DevState *h_st = nullptr;   // pinned mirror of the device state
+  int *h_one = nullptr;       // pinned constant 1 (finalised flag)
+  bool poisoned = false;
+  std::string err;
+  long long launches = 0;
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_free, ev_pending;
+  double time_ms = 0.0;
+  long long timed = 0;
+  int host_finalised = 0;
+};
+
+namespace {
+
+nss_status fail(nss_ctx *c, nss_status s, const std::string &msg) {
+  if (c) c->err = msg;
+  return s;
+}
+
+#define CK(call)                                                                   \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess) {                                                       \
+      c->poisoned = true;                                                          \
+      return fail(c, NSS_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    }                                                                              \
+  } while (0)
+
+template <class T>
+nss_status dalloc(nss_ctx *c, T **p, size_t count) {
+  void *q = nullptr;
+  cudaError_t e = cudaMalloc(&q, count * sizeof(T) + 16);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    return fail(c, NSS_ERR_OOM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  }
+  cudaMemset(q, 0, count * sizeof(T) + 16);
+  c->allocs.push_back(q);
+  *p = static_cast<T *>(q);
+  return NSS_OK;
+}
+
+nss_status upload_f32(nss_ctx *c, float **dst, const double *src, size_t count) {
+  nss_status s = dalloc(c, dst, count ? count : 1);
+  if (s != NSS_OK) return s;
+  if (!count || !src) return NSS_OK;
+  std::vector<float> tmp(count);
+  for (size_t i = 0; i < count; ++i) tmp[i] = static_cast<float>(src[i]);
+  CK(cudaMemcpy(*dst, tmp.data(), count * sizeof(float), cudaMemcpyHostToDevice));
+  return NSS_OK;
+}
+
+bool validate(const nss_prior *p, const nss_energy *e, const nss_config *cfg) {
+  if (!p || !e || !cfg) return false;
+  const int d = p->d;
+  if (d < 1 || d > NSS_MAX_DIM || e->d != d) return false;
+  if (cfg->n_live < 2 || cfg->n_live > (1 << 30) || cfg->k < 1 || cfg->k > cfg->n_live - 1) return false;
+  if (cfg->steps < 0 || cfg->max_stepout < 1 || cfg->max_shrink < 1 || cfg->max_stepout > 255 ||
+      cfg->max_shrink > 255)
+    return false;
+  if (cfg->n_volume_sims < 2 || !(cfg->width > 0.0) || cfg->max_dead < cfg->n_live) return false;
+  if (cfg->width_rule != NSS_W_OPTIMAL && cfg->width_rule != NSS_W_FIXED) return false;
+  if (cfg->dir_norm != NSS_DIR_MAHALANOBIS && cfg->dir_norm != NSS_DIR_EUCLIDEAN) return false;
+  if (cfg->quadrature != NSS_Q_TRAPEZOID && cfg->quadrature != NSS_Q_RECTANGLE) return false;
+  if (p->kind == NSS_PRIOR_BOX) {
+    if (!p->lo || !p->hi) return false;
+    for (int i = 0; i < d; ++i)
+      if (!(p->lo[i] < p->hi[i])) return false;
+  } else if (p->kind == NSS_PRIOR_GAUSS_DIAG) {
+    if (!p->mean || !p->sd) return false;
+    for (int i = 0; i < d; ++i)
+      if (!(p->sd[i] > 0.0)) return false;
+  } else {
+    return false;
+  }
+  switch (e->kind) {
+    case NSS_E_FLAT: case NSS_E_FUNNEL: return true;
+    case NSS_E_GAUSS: return e->mu && e->sigma;
+    case NSS_E_MOG: return e->n_comp >= 1 && e->w && e->mu && e->sigma;
+    case NSS_E_CORR_GAUSS: return e->mu && e->prec;
+    case NSS_E_LOGREG: return e->n_data >= 1 && e->data_x && e->data_y;
+    case NSS_E_GP_ARD: return e->n_data >= 1 && e->d_in >= 1 && d == e->d_in + 2 && e->data_x && e->data_y;
+    default: return false;
+  }
+}
+
+LaunchCtx lctx(nss_ctx *c) { return LaunchCtx{c->stream, &c->launches}; }
+
+nss_status device_error(nss_ctx *c) {
+  if (c->h_st->error) {
+    int code = c->h_st->error;
+    const char *what = code == NSS_ERR_NAN ? "energy returned NaN"
+                       : code == NSS_ERR_CAPACITY ? "dead store full"
+                       : code == NSS_ERR_PRIOR_SUPPORT ? "no finite energy within 100 n prior draws"
+                                                       : "device error";
+    return fail(c, static_cast<nss_status>(code), what);
+  }
+  return NSS_OK;
+}
+
+nss_status pull_state(nss_ctx *c) {
+  CK(cudaMemcpyAsync(c->h_st, c->r.st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return NSS_OK;
+}
+
+void fill_info(nss_ctx *c, nss_step_info *info) {
+  const DevState &s = *c->h_st;
+  info->iteration = s.iter;
+  info->e_star = s.e_star;
+  info->probes = static_cast<int64_t>(s.probes);
+  info->energy_evals = static_cast<int64_t>(s.evals);
+  info->expansions = static_cast<int64_t>(s.expansions);
+  info->shrinks = static_cast<int64_t>(s.shrinks);
+  info->null_moves = static_cast<int64_t>(s.nulls);
+  info->init_evals = static_cast<int64_t>(s.init_evals);
+  info->log_z_live = s.log_z_live;
+  info->terminated = s.terminated;
+  info->finalised = s.finalised;
+  double lz0 = -INFINITY;
+  cudaMemcpy(&lz0, c->r.lz, sizeof(double), cudaMemcpyDeviceToHost);
+  info->log_z_det = lz0;
+}
+
+nss_status collect_timing(nss_ctx *c) {
+  for (size_t i = 0; i + 1 < c->ev_pending.size(); i += 2) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->ev_pending[i], c->ev_pending[i + 1]));
+    c->time_ms += ms;
+    c->timed += 1;
+    c->ev_free.push_back(c->ev_pending[i]);
+    c->ev_free.push_back(c->ev_pending[i + 1]);
+  }
+  c->ev_pending.clear();
+  return NSS_OK;
+}
+
+cudaEvent_t take_event(nss_ctx *c) {
+  if (c->ev_free.empty()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  cudaEvent_t e = c->ev_free.back();
+  c->ev_free.pop_back();
+  return e;
+}
+
+nss_status enqueue_iteration(nss_ctx *c) {
+  LaunchCtx lc = lctx(c);
+  launch_select(c->r, lc);
+  launch_evidence(c->r, 0, lc);
+  if (c->timing) {
+    cudaEvent_t a = take_event(c), b = take_event(c);
+    CK(cudaEventRecord(a, c->stream));
+    launch_hrss(c->r, c->pr, c->en, lc);
+    CK(cudaEventRecord(b, c->stream));
+    c->ev_pending.push_back(a);
+    c->ev_pending.push_back(b);
+  } else {
+    launch_hrss(c->r, c->pr, c->en, lc);
+  }
+  launch_metric(c->r, c->cfg.metric_reg, c->cfg.width_rule, c->cfg.width, 1, c->partials, c->nblk, lc);
+  CK(cudaGetLastError());
+  return NSS_OK;
+}
+
+nss_status check_usable(nss_ctx *c) {
+  if (!c) return NSS_ERR_INVALID_ARG;
+  if (c->poisoned) return fail(c, NSS_ERR_CUDA, "context poisoned by an earlier CUDA failure");
+  return NSS_OK;
+}
+
+}  // namespace
+
+NSS_API nss_status nss_get_unique_id(uint8_t out[128]) {
+  if (!out) return NSS_ERR_INVALID_ARG;
+  std::memset(out, 0, 128);
+  return NSS_ERR_UNSUPPORTED;  // multi-GPU build: see DESIGN section 9
+}
+
+NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, const nss_config *cfg,
+                            const nss_dist *dist, nss_ctx **out) {
+  if (!out) return NSS_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (!validate(prior, energy, cfg)) return NSS_ERR_INVALID_ARG;
+  if (dist && dist->world > 1) return NSS_ERR_UNSUPPORTED;
+  nss_ctx *c = new nss_ctx();
+  c->cfg = *cfg;
+  const int d = prior->d;
+  c->d = d;
+  c->dp = (d + 3) & ~3;
+  const long long n = cfg->n_live, k = cfg->k;
+  const int R = cfg->n_volume_sims;
+  auto bail = [&](nss_status s) {
+    nss_destroy(c);
+    return s;
+  };
+  if (dist && dist->cuda_stream) {
+    c->stream = static_cast<cudaStream_t>(dist->cuda_stream);
+  } else {
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) return bail(NSS_ERR_CUDA);
+    c->own_stream = true;
+  }
+  if (cudaMallocHost(&c->h_st, sizeof(DevState)) != cudaSuccess) return bail(NSS_ERR_CUDA);
+  if (cudaMallocHost(&c->h_one, sizeof(int)) != cudaSuccess) return bail(NSS_ERR_CUDA);
+  *c->h_one = 1;
+
+  // ---- energy parameters (fp64 host -> fp32 device) ----
+  EnergyDev &en = c->en;
+  en.kind = energy->kind;
+  en.d = d;
+  en.n_comp = energy->n_comp;
+  en.d_in = energy->d_in;
+  en.n_data = energy->n_data;
+  en.c = static_cast<float>(energy->c);
+  en.sigma_y = static_cast<float>(energy->sigma_y);
+  en.jitter = static_cast<float>(energy->jitter);
+  if (!energy_supported(en)) {
+    nss_destroy(c);
+    return NSS_ERR_UNSUPPORTED;
+  }
+  nss_status s = NSS_OK;
+  float *tmp = nullptr;
+  if (en.kind == NSS_E_GAUSS) {
+    std::vector<double> is(d);
+    for (int i = 0; i < d; ++i) is[i] = 1.0 / energy->sigma[i];
+    if ((s = upload_f32(c, &tmp, energy->mu, d))) return bail(s);
+    en.mu = tmp;
+    if ((s = upload_f32(c, &tmp, is.data(), d))) return bail(s);
+    en.isig = tmp;
+  } else if (en.kind == NSS_E_MOG) {
+    const int K = en.n_comp;
+    std::vector<double> is(static_cast<size_t>(K) * d), lc(K);
+    for (int j = 0; j < K; ++j) {
+      double acc = std::log(energy->w[j]) - 0.5 * d * std::log(2.0 * M_PI);
+      for (int i = 0; i < d; ++i) {
+        is[j * d + i] = 1.0 / energy->sigma[j * d + i];
+        acc -= std::log(energy->sigma[j * d + i]);
+      }
+      lc[j] = acc;
+    }
+    if ((s = upload_f32(c, &tmp, energy->mu, static_cast<size_t>(K) * d))) return bail(s);
+    en.mu = tmp;
+    if ((s = upload_f32(c, &tmp, is.data(), is.size()))) return bail(s);
+    en.isig = tmp;
+    if ((s = upload_f32(c, &tmp, lc.data(), K))) return bail(s);
+    en.logc = tmp;
+  } else if (en.kind == NSS_E_CORR_GAUSS) {
+    if ((s = upload_f32(c, &tmp, energy->mu, d))) return bail(s);
+    en.mu = tmp;
+    if ((s = upload_f32(c, &tmp, energy->prec, static_cast<size_t>(d) * d))) return bail(s);
+    en.prec = tmp;
+  } else if (en.kind == NSS_E_LOGREG) {
+    if ((s = upload_f32(c, &tmp, energy->data_x, static_cast<size_t>(energy->n_data) * d))) return bail(s);
+    en.data_x = tmp;
+    if ((s = upload_f32(c, &tmp, energy->data_y, energy->n_data))) return bail(s);
+    en.data_y = tmp;
+  }
+
+  // ---- prior ----
+  PriorDev &pr = c->pr;
+  pr.kind = prior->kind;
+  if (pr.kind == NSS_PRIOR_BOX) {
+    double ln = 0.0;
+    for (int i = 0; i < d; ++i) ln -= std::log(prior->hi[i] - prior->lo[i]);
+    pr.log_norm = static_cast<float>(ln);
+    if ((s = upload_f32(c, &tmp, prior->lo, d))) return bail(s);
+    pr.lo = tmp;
+    if ((s = upload_f32(c, &tmp, prior->hi, d))) return bail(s);
+    pr.hi = tmp;
+  } else {
+    std::vector<double> is(d);
+    double ln = -0.5 * d * std::log(2.0 * M_PI);
+    for (int i = 0; i < d; ++i) {
+      is[i] = 1.0 / prior->sd[i];
+      ln -= std::log(prior->sd[i]);
+    }
+    pr.log_norm = static_cast<float>(ln);
+    if ((s = upload_f32(c, &tmp, prior->mean, d))) return bail(s);
+    pr.mean = tmp;
+    if ((s = upload_f32(c, &tmp, is.data(), d))) return bail(s);
+    pr.isd = tmp;
+    if ((s = upload_f32(c, &tmp, prior->sd, d))) return bail(s);
+    pr.sd = tmp;
+  }
+
+  // ---- live set, dead store, scratch ----
+  RunDev &r = c->r;
+  r.n = static_cast<int>(n);
+  r.k = static_cast<int>(k);
+  r.d = d;
+  r.dp = c->dp;
+  r.p = cfg->steps;
+  r.max_stepout = cfg->max_stepout;
+  r.max_shrink = cfg->max_shrink;
+  r.dir_norm = cfg->dir_norm;
+  r.quadrature = cfg->quadrature;
+  r.R = R;
+  r.max_dead = cfg->max_dead;
+  r.seed_lo = static_cast<uint32_t>(cfg->seed);
+  r.seed_hi = static_cast<uint32_t>(cfg->seed >> 32);
+  r.term_log_ratio = static_cast<float>(cfg->term_log_ratio);
+  const size_t cap = static_cast<size_t>(cfg->max_dead);
+  if ((s = dalloc(c, &r.X, static_cast<size_t>(n) * c->dp))) return bail(s);
+  if ((s = dalloc(c, &r.E, n))) return bail(s);
+  if ((s = dalloc(c, &r.birth, n))) return bail(s);
+  if ((s = dalloc(c, &r.L, static_cast<size_t>(d) * c->dp))) return bail(s);
+  if ((s = dalloc(c, &r.L64, static_cast<size_t>(d) * d))) return bail(s);
+  if ((s = dalloc(c, &r.dE, cap))) return bail(s);
+  if ((s = dalloc(c, &r.dbirth, cap))) return bail(s);
+  if ((s = dalloc(c, &r.dX, cap * c->dp))) return bail(s);
+  if ((s = dalloc(c, &r.dnlive, cap))) return bail(s);
+  if ((s = dalloc(c, &r.dgid, cap))) return bail(s);
+  if ((s = dalloc(c, &r.dord, cap))) return bail(s);
+  if ((s = dalloc(c, &r.diter, cap))) return bail(s);
+  if ((s = dalloc(c, &r.dead_gid, k))) return bail(s);
+  if ((s = dalloc(c, &r.dest_gid, k))) return bail(s);
+  if ((s = dalloc(c, &r.parent_gid, k))) return bail(s);
+  if ((s = dalloc(c, &r.surv, n))) return bail(s);
+  if ((s = dalloc(c, &r.counts, static_cast<size_t>(k) * (cfg->steps > 0 ? cfg->steps : 1)))) return bail(s);
+  size_t P = 1;
+  while (P < static_cast<size_t>(n)) P <<= 1;
+  if ((s = dalloc(c, &r.sort_scratch, P))) return bail(s);
+  if ((s = dalloc(c, &r.lx_prev, R + 1))) return bail(s);
+  if ((s = dalloc(c, &r.lx_cur, R + 1))) return bail(s);
+  if ((s = dalloc(c, &r.lz, R + 1))) return bail(s);
+  if ((s = dalloc(c, &r.st, 1))) return bail(s);
+  if ((s = dalloc(c, &c->summary, R + 3))) return bail(s);
+  c->nblk = metric_blocks(r.n, d);
+  const int nent = d * (d + 1) / 2 + d + 1;
+  if ((s = dalloc(c, &c->partials, static_cast<size_t>(c->nblk) * nent))) return bail(s);
+  {
+    std::vector<double> ninf(R + 1, -INFINITY);
+    if (cudaMemcpy(r.lz, ninf.data(), (R + 1) * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
+      return bail(NSS_ERR_CUDA);
+  }
+  // ---- init: prior draws (R-20), then the first metric ----
+  LaunchCtx lc = lctx(c);
+  launch_init(r, pr, en, lc);
+  launch_metric(r, cfg->metric_reg, cfg->width_rule, cfg->width, 0, c->partials, c->nblk, lc);
+  if (cudaGetLastError() != cudaSuccess) return bail(NSS_ERR_CUDA);
+  if ((s = pull_state(c))) return bail(s);
+  if ((s = device_error(c))) return bail(s);
+  *out = c;
+  return NSS_OK;
+}
+
+NSS_API nss_status nss_step(nss_ctx *c, nss_step_info *info) {
+  nss_status s = check_usable(c);
+  if (s) return s;
+  if (c->host_finalised) return fail(c, NSS_ERR_STATE, "run already finalised");
+  if ((s = enqueue_iteration(c))) return s;
+  if (info) {
+    if ((s = pull_state(c))) return s;
+    if ((s = device_error(c))) return s;
+    fill_info(c, info);
+  }
+  return NSS_OK;
+}
+
+NSS_API nss_status nss_steps(nss_ctx *c, int64_t count) {
+  nss_status s = check_usable(c);
+  if (s) return s;
+  if (c->host_finalised) return fail(c, NSS_ERR_STATE, "run already finalised");
+  for (int64_t i = 0; i < count; ++i)
+    if ((s = enqueue_iteration(c))) return s;
+  return NSS_OK;
+}
+
+NSS_API nss_status nss_finalise(nss_ctx *c) {
+  nss_status s = check_usable(c);
+  if (s) return s;
+  if (c->host_finalised) return NSS_OK;
+  LaunchCtx lc = lctx(c);
+  launch_finalise_sort(c->r, lc);
+  launch_evidence(c->r, 1, lc);
+  CK(cudaMemcpyAsync(&c->r.st->finalised, c->h_one, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaGetLastError());
+  if ((s = pull_state(c))) return s;
+  if ((s = device_error(c))) return s;
+  c->host_finalised = 1;
+  return NSS_OK;
+}
+
+NSS_API nss_status nss_run(nss_ctx *c, int64_t max_iters, nss_step_info *info) {
+  nss_status s = check_usable(c);
+  if (s) return s;
+  if (c->host_finalised) return fail(c, NSS_ERR_STATE, "run already finalised");
+  if ((s = pull_state(c))) return s;
+  const long long start = c->h_st->iter;
+  long long enq = 0;
+  int batch = 4;
+  while (enq < max_iters && !c->h_st->terminated) {
+    const long long todo = std::min<long long>(batch, max_iters - enq);
+    for (long long i = 0; i < todo; ++i)
+      if ((s = enqueue_iteration(c))) return s;
+    enq += todo;
+    if ((s = pull_state(c))) return s;
+    if ((s = device_error(c))) return s;
+    if (c->h_st->iter - start >= max_iters) break;
+    batch = std::min(batch * 2, 64);
+  }
+  if ((s = nss_finalise(c))) return s;
+  if (info) {
+    if ((s = pull_state(c))) return s;
+    fill_info(c, info);
+  }
+  return NSS_OK;
+}
+
+NSS_API nss_status nss_evidence_reps(nss_ctx *c, double *reps) {
+  nss_status s = check_usable(c);
+  if (s) return s;
+  if ((s = pull_state(c))) return s;
+  if (c->h_st->n_dead == 0) return fail(c, NSS_ERR_STATE, "no dead points yet");
+  LaunchCtx lc = lctx(c);
+  launch_evidence_summary(c->r, c->summary, lc);
+  CK(cudaGetLastError());
+  if (reps) CK(cudaMemcpyAsync(reps, c->summary + 2, (c->r.R + 1) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return NSS_OK;
+}
+
+NSS_API nss_status nss_evidence(nss_ctx *c, double *log_z, double *log_z_err) {
+  nss_status s = nss_evidence_reps(c, nullptr);
+  if (s) return s;
+  double ms[2];
+  CK(cudaMemcpy(ms, c->summary, 2 * sizeof(double), cudaMemcpyDeviceToHost));
+  if (log_z) *log_z = ms[0];
+  if (log_z_err) *log_z_err = ms[1];
+  return NSS_OK;
+}
+
+NSS_API nss_status nss_samples(nss_ctx *c, double *x, double *log_w, int64_t cap, int64_t *n_out) {
+  nss_status s = check_usable(c);
+  if (s) return s;
+  if (!n_out) return NSS_ERR_INVALID_ARG;
+  if ((s = pull_state(c))) return s;
+  const long long N = c->h_st->n_dead;
+  *n_out = N;
+  if (N == 0) return fail(c, NSS_ERR_STATE, "no dead points yet");
+  if (!x && !log_w) return NSS_OK;
+  if (cap < N) return fail(c, NSS_ERR_CAPACITY, "output buffer smaller than the dead store");
+  const int d = c->d, dp = c->dp;
+  if (x) {
+    std::vector<float> tmp(static_cast<size_t>(N) * dp);
+    CK(cudaMemcpy(tmp.data(), c->r.dX, tmp.size() * sizeof(float), cudaMemcpyDeviceToHost));
+    for (long long i = 0; i < N; ++i)
+      for (int j = 0; j < d; ++j) x[i * d + j] = tmp[static_cast<size_t>(i) * dp + j];
+  }
+  if (log_w) {
+    const int chunk = 1 << 16;
+    double *logw = nullptr, *scratch = nullptr;
+    CK(cudaMalloc(&logw, N * sizeof(double)));
+    CK(cudaMalloc(&scratch, (static_cast<size_t>(c->r.R) * (chunk + 3)) * sizeof(double)));
+    launch_samples(c->r, N, logw, scratch, chunk, lctx(c));
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(log_w, logw, N * sizeof(double), cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    cudaFree(logw);
+    cudaFree(scratch);
+    if (e != cudaSuccess) {
+      c->poisoned = true;
+      return fail(c, NSS_ERR_CUDA, cudaGetErrorString(e));
+    }
+  }
+  return NSS_OK;
+}
+
+NSS_API nss_status nss_info(nss_ctx *c, nss_step_info *info) {
+  nss_status s = check_usable(c);
+  if (s) return s;
+  if (!info) return NSS_ERR_INVALID_ARG;
+  if ((s = pull_state(c))) return s;
+  fill_info(c, info);
+  return device_error(c);
+}
+
+NSS_API nss_status nss_sync(nss_ctx *c) {
+  nss_status s = check_usable(c);
+  if (s) return s;
+  if ((s = pull_state(c))) return s;
+  return device_error(c);
+}
+
+NSS_API nss_status nss_destroy(nss_ctx *c) {
+  if (!c) return NSS_ERR_INVALID_ARG;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (void *p : c->allocs) cudaFree(p);
+  for (auto e : c->ev_free) cudaEventDestroy(e);
+  for (auto e : c->ev_pending) cudaEventDestroy(e);
+  if (c->h_st) cudaFreeHost(c->h_st);
+  if (c->h_one) cudaFreeHost(c->h_one);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return NSS_OK;
+}
+
+NSS_API const char *nss_last_error(const nss_ctx *c) { return c ? c->err.c_str() : "null context"; }
+
+// ---- parity hooks ----
+NSS_API nss_status nss_set_live(nss_ctx *c, const float *x, const float *e, int64_t next_iteration) {
+  nss_status s = check_usable(c);
+  if (s) return s;
+  if (!x || !e || next_iteration < 1) return NSS_ERR_INVALID_ARG;
+  if (c->host_finalised) return fail(c, NSS_ERR_STATE, "run already finalised");
+  const int n = c->r.n, d = c->d, dp = c->dp;
+  std::vector<float> tmp(static_cast<size_t>(n) * dp, 0.f);
+  for (int g = 0; g < n; ++g)
+    for (int j = 0; j < d; ++j) tmp[static_cast<size_t>(g) * dp + j] = x[static_cast<size_t>(g) * d + j];
+  CK(cudaMemcpyAsync(c->r.X, tmp.data(), tmp.size() * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->r.E, e, n * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+  if ((s = pull_state(c))) return s;
+  c->h_st->iter = static_cast<int>(next_iteration - 1);
+  c->h_st->terminated = 0;
+  CK(cudaMemcpyAsync(c->r.st, c->h_st, sizeof(DevState), cudaMemcpyHostToDevice, c->stream));
+  launch_metric(c->r, c->cfg.metric_reg, c->cfg.width_rule, c->cfg.width, 0, c->partials, c->nblk, lctx(c));
+  CK(cudaGetLastError());
+  if ((s = pull_state(c))) return s;
+  return NSS_OK;
+}
+
+NSS_API nss_status nss_get_live(nss_ctx *c, float *x, float *e) {
+  nss_status s = check_usable(c);
+  if (s) return s;
+  const int n = c->r.n, d = c->d, dp = c->dp;
+  CK(cudaStreamSynchronize(c->stream));
+  if (x) {
+    std::vector<float> tmp(static_cast<size_t>(n) * dp);
+    CK(cudaMemcpy(tmp.data(), c->r.X, tmp.size() * sizeof(float), cudaMemcpyDeviceToHost));
+    for (int g = 0; g < n; ++g)
+      for (int j = 0; j < d; ++j) x[static_cast<size_t>(g) * d + j] = tmp[static_cast<size_t>(g) * dp + j];
+  }
+  if (e) CK(cudaMemcpy(e, c->r.E, n * sizeof(float), cudaMemcpyDeviceToHost));
+  return NSS_OK;
+}
+
+NSS_API nss_status nss_get_metric(nss_ctx *c, double *chol, double *width) {
+  nss_status s = check_usable(c);
+  if (s) return s;
+  CK(cudaStreamSynchronize(c->stream));
+  if (chol) CK(cudaMemcpy(chol, c->r.L64, static_cast<size_t>(c->d) * c->d * sizeof(double), cudaMemcpyDeviceToHost));
+  if (width) {
+    if ((s = pull_state(c))) return s;
+    *width = c->h_st->width;
+  }
+  return NSS_OK;
+}
+
+NSS_API nss_status nss_get_trace(nss_ctx *c, int32_t *dead_gid, int32_t *dest_gid, int32_t *parent_gid,
+                                 uint8_t *counts, float *e_star) {
+  nss_status s = check_usable(c);
+  if (s) return s;
+  CK(cudaStreamSynchronize(c->stream));
+  const size_t k = c->r.k;
+  if (dead_gid) CK(cudaMemcpy(dead_gid, c->r.dead_gid, k * sizeof(int), cudaMemcpyDeviceToHost));
+  if (dest_gid) CK(cudaMemcpy(dest_gid, c->r.dest_gid, k * sizeof(int), cudaMemcpyDeviceToHost));
+  if (parent_gid) CK(cudaMemcpy(parent_gid, c->r.parent_gid, k * sizeof(int), cudaMemcpyDeviceToHost));
+  if (counts) {
+    const size_t p = c->cfg.steps > 0 ? c->cfg.steps : 1;
+    CK(cudaMemcpy(counts, c->r.counts, k * p * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  }
+  if (e_star) {
+    if ((s = pull_state(c))) return s;
+    *e_star = c->h_st->e_star;
+  }
+  return NSS_OK;
+}
+
+NSS_API nss_status nss_dead(nss_ctx *c, float *e, int32_t *n_live, float *birth, int32_t *gid, float *x,
+                            int64_t cap, int64_t *n_out) {
+  nss_status s = check_usable(c);
+  if (s) return s;
+  if (!n_out) return NSS_ERR_INVALID_ARG;
+  if ((s = pull_state(c))) return s;
+  const long long N = c->h_st->n_dead;
+  *n_out = N;
+  if (!e && !n_live && !birth && !gid && !x) return NSS_OK;
+  if (cap < N) return fail(c, NSS_ERR_CAPACITY, "output buffer smaller than the dead store");
+  if (e) CK(cudaMemcpy(e, c->r.dE, N * sizeof(float), cudaMemcpyDeviceToHost));
+  if (n_live) CK(cudaMemcpy(n_live, c->r.dnlive, N * sizeof(int), cudaMemcpyDeviceToHost));
+  if (birth) CK(cudaMemcpy(birth, c->r.dbirth, N * sizeof(float), cudaMemcpyDeviceToHost));
+  if (gid) CK(cudaMemcpy(gid, c->r.dgid, N * sizeof(int), cudaMemcpyDeviceToHost));
+  if (x) {
+    std::vector<float> tmp(static_cast<size_t>(N) * c->dp);
+    CK(cudaMemcpy(tmp.data(), c->r.dX, tmp.size() * sizeof(float), cudaMemcpyDeviceToHost));
+    for (long long i = 0; i < N; ++i)
+      for (int j = 0; j < c->d; ++j) x[i * c->d + j] = tmp[static_cast<size_t>(i) * c->dp + j];
+  }
+  return NSS_OK;
+}
+
+NSS_API nss_status nss_volume_reps(nss_ctx *c, double *log_x) {
+  nss_status s = check_usable(c);
+  if (s) return s;
+  if (!log_x) return NSS_ERR_INVALID_ARG;
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaMemcpy(log_x, c->r.lx_cur, (c->r.R + 1) * sizeof(double), cudaMemcpyDeviceToHost));
+  return NSS_OK;
+}
+
+NSS_API nss_status nss_set_kernel_timing(nss_ctx *c, int32_t enable) {
+  nss_status s = check_usable(c);
+  if (s) return s;
+  CK(cudaStreamSynchronize(c->stream));
+  if ((s = collect_timing(c))) return s;
+  c->timing = enable != 0;
+  c->time_ms = 0.0;
+  c->timed = 0;
+  return NSS_OK;
+}
+
+NSS_API nss_status nss_kernel_time(nss_ctx *c, double *ms, int64_t *launches) {
+  nss_status s = check_usable(c);
+  if (s) return s;
+  CK(cudaStreamSynchronize(c->stream));
+  if ((s = collect_timing(c))) return s;
+  if (ms) *ms = c->time_ms;
+  if (launches) *launches = c->timed;
+  return NSS_OK;
+}
+
+NSS_API nss_status nss_launch_count(nss_ctx *c, int64_t *launches) {
+  if (!c || !launches) return NSS_ERR_INVALID_ARG;
+  *launches = c->launches;
+  return NSS_OK;
+}

@@ -1,0 +1,161 @@
+// Internal declarations of the B200 NSS library (not part of the ABI).
+// "P:n" cites /root/reference/PAPER.md; "R-n" a DESIGN.md section 2 reading.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "nss.h"
+
+namespace nss {
+
+constexpr int kMaxDim = NSS_MAX_DIM;
+constexpr int kMaxComp = 16;
+constexpr uint32_t kPhaseInit = 1, kPhaseResample = 2, kPhaseHrss = 3, kPhaseVolume = 4;
+
+// ----------------------------------------------------------------------------
+// Device-resident run state (one small struct, read by every kernel).
+// ----------------------------------------------------------------------------
+struct DevState {
+  long long n_dead;        // records in the dead store
+  long long dead_base;     // first dead record of the current iteration
+  int iter;                // completed iterations (next one is iter + 1)
+  int terminated;          // R-19 criterion met after the last iteration
+  int error;               // nss_status raised on the device (NaN, capacity, support)
+  int has_pend;            // trapezoid point waiting for X_{i+1}
+  float e_star;            // E* of the last iteration
+  float width;             // slice width for the next iteration (R-7)
+  float emin;              // min live energy after the last iteration
+  int finalised;
+  double pend_e;           // energy of the pending trapezoid point
+  double log_z_live;
+  unsigned long long probes, evals, expansions, shrinks, nulls;
+  unsigned long long init_evals, init_attempts;
+};
+
+// Energy parameters laid out for the kernels (device pointers, fp32).
+struct EnergyDev {
+  int kind;
+  int d;
+  int n_comp;
+  int d_in;
+  long long n_data;
+  float c;
+  float sigma_y;
+  float jitter;
+  const float *mu;      // GAUSS/CORR: d; MOG: K*d
+  const float *isig;    // GAUSS: d; MOG: K*d  (1/sigma)
+  const float *logc;    // MOG: K  (log w_j - sum log sigma_j - d/2 log 2pi)
+  const float *prec;    // CORR: d*d
+  const float *data_x;  // LOGREG: N*d; GP: N*d_in
+  const float *data_y;  // LOGREG / GP: N
+};
+
+struct PriorDev {
+  int kind;
+  const float *lo, *hi;       // BOX
+  const float *mean, *isd, *sd;  // GAUSS_DIAG (isd = 1/sd)
+  float log_norm;             // BOX: -sum log(hi-lo); GAUSS: -sum log sd - d/2 log 2pi
+};
+
+// Everything a kernel needs about the live set and the run.
+struct RunDev {
+  int n, k, d, dp, p;         // dp = row stride of X (floats)
+  int max_stepout, max_shrink;
+  int dir_norm, quadrature;
+  int R;
+  long long max_dead;
+  uint32_t seed_lo, seed_hi;
+  float term_log_ratio;
+  float *X, *E, *birth;       // live set
+  float *L;                   // lower Cholesky of Sigma, fp32, row stride dp
+  double *L64;                // fp64 copy, d*d
+  // dead store
+  float *dE, *dbirth, *dX;
+  int *dnlive, *dgid, *dord, *diter;
+  // per-iteration scratch
+  int *dead_gid, *dest_gid, *parent_gid, *surv;
+  uint32_t *counts;           // k*p packed {nL, nR, nS, acc}
+  unsigned long long *sort_scratch;  // max(n, k) rounded to a power of two
+  // evidence replicas
+  double *lx_prev, *lx_cur, *lz;
+  DevState *st;
+};
+
+// ----------------------------------------------------------------------------
+// Philox4x32-10 and the draw contract
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ uint4 philox(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return c;
+}
+
+__device__ __forceinline__ uint4 philox_block(const RunDev &r, uint32_t iter, uint32_t gid,
+                                              uint32_t phase, uint32_t sub, uint32_t block) {
+  return philox(make_uint4(block, (phase << 24) | (sub & 0xFFFFFFu), gid, iter), r.seed_lo,
+                r.seed_hi);
+}
+
+__device__ __forceinline__ uint32_t word(uint4 b, uint32_t w) {
+  return w == 0 ? b.x : (w == 1 ? b.y : (w == 2 ? b.z : b.w));
+}
+
+// u = ((r >> 9) + 1/2) * 2^-23, exact in fp32 (R-25)
+__device__ __forceinline__ float u01(uint32_t r) {
+  return (static_cast<float>(r >> 9) + 0.5f) * 1.1920928955078125e-07f;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Orderable u32 of an fp32 (ascending), -0 canonicalised to +0 (R-1).
+__device__ __forceinline__ uint32_t ord_f32(float e) {
+  uint32_t b = __float_as_uint(e);
+  if (b == 0x80000000u) b = 0u;
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ unsigned long long key_of(float e, int gid) {
+  return (static_cast<unsigned long long>(ord_f32(e)) << 32) | static_cast<uint32_t>(gid);
+}
+
+__device__ __forceinline__ void raise_error(DevState *st, int code) { atomicCAS(&st->error, 0, code); }
+
+// ----------------------------------------------------------------------------
+// Launchers (host side, one per kernel file)
+// ----------------------------------------------------------------------------
+struct LaunchCtx {
+  cudaStream_t stream;
+  long long *launch_counter;
+};
+
+// k_select.cu: A2 delete + A3 dead records + A4 resample (one iteration)
+void launch_select(const RunDev &r, const LaunchCtx &lc);
+// k_select.cu: finalisation (R-18): all n live points become dead records
+void launch_finalise_sort(const RunDev &r, const LaunchCtx &lc);
+// k_evidence.cu: A8 volume replicas + quadrature for `count` new deaths
+void launch_evidence(const RunDev &r, int finalise, const LaunchCtx &lc);
+// k_hrss.cu: A6/A7 (+A1) HRSS chains; init draws
+void launch_hrss(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc);
+void launch_init(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc);
+size_t energy_smem_bytes(const EnergyDev &en);
+bool energy_supported(const EnergyDev &en);
+// k_metric.cu: A5 metric (+ A9 termination when iterating)
+void launch_metric(const RunDev &r, double metric_reg, int width_rule, double width_param,
+                   int end_of_iteration, double *partials, int n_blocks, const LaunchCtx &lc);
+int metric_blocks(int n, int d);
+
+}  // namespace nss

@@ -1,0 +1,287 @@
+"""Python binding of the B200 NSS library (include/nss.h, libnss.so).
+
+Argument marshalling only: every step of the method runs in the CUDA kernels
+behind the C ABI.  There is no CPU fallback -- importing this module on a
+machine without the built library, or calling it without a GPU, raises.
+PyTorch is used only for device selection and, in multi-GPU runs, to broadcast
+the communicator id (torch.distributed); the library owns its device memory.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Dict, Optional
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libnss.so")
+
+STATUS = {0: "OK", 1: "INVALID_ARG", 2: "PRIOR_SUPPORT", 3: "NAN", 4: "CUDA", 5: "COMM", 6: "OOM",
+          7: "STATE", 8: "CAPACITY", 9: "UNSUPPORTED"}
+
+
+class NssError(RuntimeError):
+    def __init__(self, code: int, where: str, msg: str = ""):
+        super().__init__(f"{where}: nss status {code} ({STATUS.get(code, '?')}) {msg}".strip())
+        self.code = code
+
+
+class nss_prior(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("d", C.c_int32),
+                ("lo", C.POINTER(C.c_double)), ("hi", C.POINTER(C.c_double)),
+                ("mean", C.POINTER(C.c_double)), ("sd", C.POINTER(C.c_double))]
+
+
+class nss_energy(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("d", C.c_int32), ("n_comp", C.c_int32),
+                ("n_data", C.c_int64), ("d_in", C.c_int32),
+                ("w", C.POINTER(C.c_double)), ("mu", C.POINTER(C.c_double)),
+                ("sigma", C.POINTER(C.c_double)), ("prec", C.POINTER(C.c_double)),
+                ("data_x", C.POINTER(C.c_double)), ("data_y", C.POINTER(C.c_double)),
+                ("c", C.c_double), ("sigma_y", C.c_double), ("jitter", C.c_double)]
+
+
+class nss_config(C.Structure):
+    _fields_ = [("n_live", C.c_int64), ("k", C.c_int64), ("steps", C.c_int32),
+                ("width_rule", C.c_int32), ("width", C.c_double), ("dir_norm", C.c_int32),
+                ("max_stepout", C.c_int32), ("max_shrink", C.c_int32),
+                ("quadrature", C.c_int32), ("metric_reg", C.c_double),
+                ("term_log_ratio", C.c_double), ("n_volume_sims", C.c_int32),
+                ("max_dead", C.c_int64), ("seed", C.c_uint64)]
+
+
+class nss_dist(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("nccl_uid", C.POINTER(C.c_uint8)),
+                ("cuda_stream", C.c_void_p)]
+
+
+class nss_step_info(C.Structure):
+    _fields_ = [("iteration", C.c_int64), ("e_star", C.c_double), ("probes", C.c_int64),
+                ("energy_evals", C.c_int64), ("expansions", C.c_int64), ("shrinks", C.c_int64),
+                ("null_moves", C.c_int64), ("init_evals", C.c_int64),
+                ("log_z_det", C.c_double), ("log_z_live", C.c_double),
+                ("terminated", C.c_int32), ("finalised", C.c_int32)]
+
+    def as_dict(self) -> Dict:
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+EXPORTS = ["nss_get_unique_id", "nss_init", "nss_step", "nss_steps", "nss_run", "nss_finalise",
+           "nss_evidence", "nss_evidence_reps", "nss_samples", "nss_info", "nss_sync", "nss_destroy",
+           "nss_last_error", "nss_set_live", "nss_get_live", "nss_get_metric", "nss_get_trace",
+           "nss_dead", "nss_volume_reps", "nss_set_kernel_timing", "nss_kernel_time",
+           "nss_launch_count"]
+
+_lib = None
+
+
+def lib():
+    """Load libnss.so (built by __graft_entry__.build()); raises if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+    L = C.CDLL(LIB_PATH)
+    P, vp = C.POINTER, C.c_void_p
+    L.nss_get_unique_id.argtypes = [P(C.c_uint8)]
+    L.nss_init.argtypes = [P(nss_prior), P(nss_energy), P(nss_config), P(nss_dist), P(vp)]
+    L.nss_step.argtypes = [vp, P(nss_step_info)]
+    L.nss_steps.argtypes = [vp, C.c_int64]
+    L.nss_run.argtypes = [vp, C.c_int64, P(nss_step_info)]
+    L.nss_finalise.argtypes = [vp]
+    L.nss_evidence.argtypes = [vp, P(C.c_double), P(C.c_double)]
+    L.nss_evidence_reps.argtypes = [vp, P(C.c_double)]
+    L.nss_samples.argtypes = [vp, P(C.c_double), P(C.c_double), C.c_int64, P(C.c_int64)]
+    L.nss_info.argtypes = [vp, P(nss_step_info)]
+    L.nss_sync.argtypes = [vp]
+    L.nss_destroy.argtypes = [vp]
+    L.nss_last_error.argtypes = [vp]
+    L.nss_last_error.restype = C.c_char_p
+    L.nss_set_live.argtypes = [vp, P(C.c_float), P(C.c_float), C.c_int64]
+    L.nss_get_live.argtypes = [vp, P(C.c_float), P(C.c_float)]
+    L.nss_get_metric.argtypes = [vp, P(C.c_double), P(C.c_double)]
+    L.nss_get_trace.argtypes = [vp, P(C.c_int32), P(C.c_int32), P(C.c_int32), P(C.c_uint8),
+                                P(C.c_float)]
+    L.nss_dead.argtypes = [vp, P(C.c_float), P(C.c_int32), P(C.c_float), P(C.c_int32),
+                           P(C.c_float), C.c_int64, P(C.c_int64)]
+    L.nss_volume_reps.argtypes = [vp, P(C.c_double)]
+    L.nss_set_kernel_timing.argtypes = [vp, C.c_int32]
+    L.nss_kernel_time.argtypes = [vp, P(C.c_double), P(C.c_int64)]
+    L.nss_launch_count.argtypes = [vp, P(C.c_int64)]
+    _lib = L
+    return L
+
+
+def _f64(a) -> Optional[np.ndarray]:
+    if a is None:
+        return None
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def _dp(a):
+    return None if a is None else a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _fp(a):
+    return None if a is None else a.ctypes.data_as(C.POINTER(C.c_float))
+
+
+def _ip(a):
+    return None if a is None else a.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+class Sampler:
+    """One NSS run on one GPU (nss_ctx).  `problem` is a workloads.Problem and
+    `cfg` a workloads.config() dict."""
+
+    def __init__(self, problem, cfg: Dict, stream: Optional[int] = None):
+        self.problem = problem
+        self.cfg = dict(cfg)
+        self._keep = []
+        self._h = C.c_void_p()
+
+        def keep(a):
+            a = _f64(a)
+            if a is not None:
+                self._keep.append(a)
+            return a
+
+        d = problem.d
+        pr = nss_prior(kind=problem.prior_kind, d=d, lo=_dp(keep(problem.lo)), hi=_dp(keep(problem.hi)),
+                       mean=_dp(keep(problem.mean)), sd=_dp(keep(problem.sd)))
+        en = nss_energy(kind=problem.energy_kind, d=d, n_comp=problem.n_comp, n_data=problem.n_data,
+                        d_in=problem.d_in, w=_dp(keep(problem.w)), mu=_dp(keep(problem.mu)),
+                        sigma=_dp(keep(problem.sigma)), prec=_dp(keep(problem.prec)),
+                        data_x=_dp(keep(problem.data_x)), data_y=_dp(keep(problem.data_y)),
+                        c=problem.c, sigma_y=problem.sigma_y, jitter=problem.jitter)
+        cf = nss_config(**self.cfg)
+        dist = None
+        if stream is not None:
+            dist = nss_dist(rank=0, world=1, nccl_uid=None, cuda_stream=C.c_void_p(stream))
+        st = lib().nss_init(C.byref(pr), C.byref(en), C.byref(cf),
+                            C.byref(dist) if dist is not None else None, C.byref(self._h))
+        if st != 0:
+            raise NssError(st, "nss_init")
+        self.d, self.n, self.k = d, self.cfg["n_live"], self.cfg["k"]
+        self.p, self.R = self.cfg["steps"], self.cfg["n_volume_sims"]
+
+    def _check(self, st: int, where: str):
+        if st != 0:
+            msg = lib().nss_last_error(self._h) if self._h else b""
+            raise NssError(st, where, (msg or b"").decode())
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().nss_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- sampler ----
+    def step(self, sync: bool = True) -> Optional[Dict]:
+        if not sync:
+            self._check(lib().nss_step(self._h, None), "nss_step")
+            return None
+        info = nss_step_info()
+        self._check(lib().nss_step(self._h, C.byref(info)), "nss_step")
+        return info.as_dict()
+
+    def steps(self, count: int):
+        self._check(lib().nss_steps(self._h, count), "nss_steps")
+
+    def run(self, max_iters: int = 1 << 40) -> Dict:
+        info = nss_step_info()
+        self._check(lib().nss_run(self._h, max_iters, C.byref(info)), "nss_run")
+        return info.as_dict()
+
+    def finalise(self):
+        self._check(lib().nss_finalise(self._h), "nss_finalise")
+
+    def sync(self):
+        self._check(lib().nss_sync(self._h), "nss_sync")
+
+    def info(self) -> Dict:
+        info = nss_step_info()
+        self._check(lib().nss_info(self._h, C.byref(info)), "nss_info")
+        return info.as_dict()
+
+    def evidence(self):
+        lz, err = C.c_double(), C.c_double()
+        self._check(lib().nss_evidence(self._h, C.byref(lz), C.byref(err)), "nss_evidence")
+        return lz.value, err.value
+
+    def evidence_reps(self) -> np.ndarray:
+        out = np.zeros(self.R + 1)
+        self._check(lib().nss_evidence_reps(self._h, _dp(out)), "nss_evidence_reps")
+        return out
+
+    def samples(self):
+        n = C.c_int64()
+        self._check(lib().nss_samples(self._h, None, None, 0, C.byref(n)), "nss_samples")
+        x = np.zeros((n.value, self.d))
+        lw = np.zeros(n.value)
+        self._check(lib().nss_samples(self._h, _dp(x), _dp(lw), n.value, C.byref(n)), "nss_samples")
+        return x, lw
+
+    def dead(self) -> Dict:
+        n = C.c_int64()
+        self._check(lib().nss_dead(self._h, None, None, None, None, None, 0, C.byref(n)), "nss_dead")
+        N = n.value
+        e, b = np.zeros(N, np.float32), np.zeros(N, np.float32)
+        x = np.zeros((N, self.d), np.float32)
+        nl, g = np.zeros(N, np.int32), np.zeros(N, np.int32)
+        self._check(lib().nss_dead(self._h, _fp(e), _ip(nl), _fp(b), _ip(g), _fp(x), N, C.byref(n)), "nss_dead")
+        return dict(e=e, n_live=nl, birth=b, gid=g, x=x)
+
+    # ---- parity hooks ----
+    def set_live(self, x: np.ndarray, e: np.ndarray, next_iteration: int):
+        x = np.ascontiguousarray(np.asarray(x, dtype=np.float32).reshape(self.n, self.d))
+        e = np.ascontiguousarray(np.asarray(e, dtype=np.float32).reshape(self.n))
+        self._check(lib().nss_set_live(self._h, _fp(x), _fp(e), next_iteration), "nss_set_live")
+
+    def get_live(self):
+        x = np.zeros((self.n, self.d), np.float32)
+        e = np.zeros(self.n, np.float32)
+        self._check(lib().nss_get_live(self._h, _fp(x), _fp(e)), "nss_get_live")
+        return x, e
+
+    def metric(self):
+        L = np.zeros((self.d, self.d))
+        w = C.c_double()
+        self._check(lib().nss_get_metric(self._h, _dp(L), C.byref(w)), "nss_get_metric")
+        return L, w.value
+
+    def trace(self) -> Dict:
+        k, p = self.k, max(self.p, 1)
+        dead, dest, par = (np.zeros(k, np.int32) for _ in range(3))
+        counts = np.zeros((k, p, 4), np.uint8)
+        es = C.c_float()
+        self._check(lib().nss_get_trace(self._h, _ip(dead), _ip(dest), _ip(par),
+                                        counts.ctypes.data_as(C.POINTER(C.c_uint8)), C.byref(es)),
+                    "nss_get_trace")
+        return dict(dead_gid=dead, dest_gid=dest, parent_gid=par, counts=counts, e_star=es.value)
+
+    def volume_reps(self) -> np.ndarray:
+        out = np.zeros(self.R + 1)
+        self._check(lib().nss_volume_reps(self._h, _dp(out)), "nss_volume_reps")
+        return out
+
+    # ---- measurement ----
+    def set_kernel_timing(self, on: bool):
+        self._check(lib().nss_set_kernel_timing(self._h, 1 if on else 0), "nss_set_kernel_timing")
+
+    def kernel_time(self):
+        ms, n = C.c_double(), C.c_int64()
+        self._check(lib().nss_kernel_time(self._h, C.byref(ms), C.byref(n)), "nss_kernel_time")
+        return ms.value, n.value
+
+    def launch_count(self) -> int:
+        n = C.c_int64()
+        self._check(lib().nss_launch_count(self._h, C.byref(n)), "nss_launch_count")
+        return n.value

@@ -5,7 +5,7 @@ datasets -- and the run configurations for the five configurations named in
 BASELINE.json (DESIGN.md section 5 gives the recipe).  It holds none of the
 method's arithmetic: no energies, no slice sampling, no evidence.  Both the
 CUDA binding (`paper_2601_23252_b200.nss`) and the oracle binding
-(`oracle.nsso`) consume the same `Problem` objects, so they never share
+(in the test-only oracle package) consume the same `Problem` objects, so they never share
 generation code with each other.
 
 Shapes follow the paper's workloads (P:760 kappa=100 Gaussian, P:836-840

@@ -1,0 +1,266 @@
+"""CUDA path vs fp64 oracle, through the C ABI (needs a B200).
+
+Single-iteration parity on every energy / prior / option, metric and evidence
+parity, init parity, full-run log Z against the analytic values, error paths.
+"""
+import math
+
+import numpy as np
+import pytest
+from scipy import special, stats
+
+from paper_2601_23252_b200 import workloads as W
+from tests.parity_util import compare_iteration, inject_pair
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2601_23252_b200 import nss
+    nss.lib()
+
+
+def _mog_small(d=6, K=3):
+    return W.mog(d, n_comp=K, seed=17, half_width=8.0, mean_box=4.0, min_sep=4.0)
+
+
+CASES = {
+    # name: (problem factory, config kwargs, warm iterations)
+    "c1_gauss2": (lambda: W.gauss(2), dict(n_live=200, k=20, steps=10), 5),
+    "c2_mog10": (lambda: W.mog(10), dict(n_live=2000, k=200, steps=10), 3),
+    "mog_ragged": (_mog_small, dict(n_live=777, k=91, steps=5), 2),
+    "corr_gauss_d40": (lambda: W.corr_gauss(40, seed=5), dict(n_live=600, k=60, steps=8), 2),
+    "corr_gauss_d100": (lambda: W.corr_gauss(100, seed=5), dict(n_live=1000, k=100, steps=6), 0),
+    "funnel_d16": (lambda: W.funnel(16), dict(n_live=500, k=50, steps=6), 2),
+    "funnel_d100": (lambda: W.funnel(100), dict(n_live=800, k=80, steps=4), 0),
+    "logreg_small": (lambda: W.logreg(5, n_data=300, seed=3), dict(n_live=300, k=30, steps=5), 2),
+    "flat_d1": (lambda: W.flat(1), dict(n_live=64, k=7, steps=3), 1),
+    "d33_ragged_lanes": (lambda: W.gauss(33, half_width=4.0), dict(n_live=333, k=33, steps=3), 1),
+    "k_n_minus_1": (lambda: W.gauss(3), dict(n_live=50, k=49, steps=3), 0),
+    "k1": (lambda: W.gauss(3), dict(n_live=50, k=1, steps=3), 2),
+    "p0": (lambda: W.gauss(3), dict(n_live=50, k=5, steps=0), 2),
+    "euclidean": (lambda: W.corr_gauss(8, seed=2), dict(n_live=300, k=30, steps=5, dir_norm=W.DIR_EUCLIDEAN), 2),
+    "fixed_width": (lambda: W.mog(4, n_comp=2, seed=4, mean_box=3.0, min_sep=3.0),
+                    dict(n_live=300, k=30, steps=5, width_rule=W.W_FIXED, width=1.0), 2),
+    "width_scale_quarter": (lambda: W.gauss(5), dict(n_live=300, k=30, steps=5, width=0.25), 2),
+    "stepout_cap": (lambda: W.gauss(2, half_width=50.0, sigma=20.0),
+                    dict(n_live=100, k=10, steps=4, width_rule=W.W_FIXED, width=0.05, max_stepout=3), 0),
+    "shrink_cap": (lambda: W.gauss(4), dict(n_live=100, k=10, steps=4, max_shrink=2), 2),
+}
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_single_iteration_parity(name):
+    make, kw, warm = CASES[name]
+    prob = make()
+    cfg = W.config(seed=11, **kw)
+    gpu, ref = inject_pair(prob, cfg, warm_iters=warm)
+    # metric from the same injected cloud
+    Lg, wg = gpu.metric()
+    Lr, wr = ref.metric()
+    assert np.allclose(Lg, Lr, rtol=1e-5, atol=1e-7 * np.abs(Lr).max())
+    assert abs(wg - wr) <= 1e-6 * wr
+    st = compare_iteration(gpu, ref, prob)
+    if name == "shrink_cap":
+        assert (st["counts_g"][:, :, 3] == 0).any()  # some null moves happened
+    if name == "stepout_cap":
+        assert (st["counts_g"][:, :, 0] == 3).any()
+    # dead records identical
+    dg, dr = gpu.dead(), ref.dead()
+    assert np.array_equal(dg["n_live"], dr["n_live"])
+    assert np.array_equal(dg["gid"], dr["gid"])
+    assert np.array_equal(dg["e"].astype(np.float64), dr["e"])
+    assert np.array_equal(dg["x"].astype(np.float64), dr["x"])
+    # evidence replicas after one iteration (same dead energies, same draws)
+    assert np.allclose(gpu.volume_reps(), ref.volume_reps(), rtol=0, atol=1e-12)
+    assert np.allclose(gpu.evidence_reps(), ref.evidence_reps(), rtol=0, atol=1e-10)
+    gpu.close()
+
+
+def test_several_iterations_teacher_forced():
+    """Re-inject the oracle state every iteration (SURVEY C-9 T3) for 6 iterations of C2."""
+    prob = W.mog(10)
+    cfg = W.config(n_live=2000, k=200, steps=10, seed=5)
+    from oracle import nsso
+    ref = nsso.Oracle(prob, cfg)
+    from paper_2601_23252_b200 import nss
+    gpu = nss.Sampler(prob, cfg)
+    for it in range(1, 7):
+        x, _ = ref.get_live()
+        x32 = x.astype(np.float32)
+        e32 = np.array([ref.energy(xi.astype(np.float64)) for xi in x32]).astype(np.float32)
+        ref.set_live(x32.astype(np.float64), e32.astype(np.float64), it)
+        gpu.set_live(x32, e32, it)
+        compare_iteration(gpu, ref, prob)
+
+
+def test_init_parity():
+    for prob, kw in ((W.gauss(2), dict(n_live=200, k=20, steps=2)),
+                     (W.mog(10), dict(n_live=500, k=50, steps=2)),
+                     (W.corr_gauss(12, seed=3), dict(n_live=300, k=30, steps=2)),
+                     (W.logreg(4, n_data=100, seed=2), dict(n_live=100, k=10, steps=2))):
+        from oracle import nsso
+        from paper_2601_23252_b200 import nss
+        cfg = W.config(seed=21, **kw)
+        ref = nsso.Oracle(prob, cfg)
+        gpu = nss.Sampler(prob, cfg)
+        xg, eg = gpu.get_live()
+        xr, er = ref.get_live()
+        scale = 1.0 if prob.prior_kind == W.PRIOR_BOX else 5.0
+        assert np.allclose(xg, xr, rtol=1e-6, atol=1e-6 * scale)
+        assert np.allclose(eg, er, rtol=1e-5, atol=1e-5)
+        assert gpu.info()["init_evals"] == ref.info()["init_evals"]
+        gpu.close()
+
+
+def test_evidence_and_weights_exact_on_flat():
+    """Flat energy, p = 0: both sides hold identical dead lists, so every replica's
+    log Z, log X and the posterior weights must agree to fp64 rounding."""
+    from oracle import nsso
+    from paper_2601_23252_b200 import nss
+    for quad in (W.Q_TRAPEZOID, W.Q_RECTANGLE):
+        prob = W.flat(2, c=0.7)
+        cfg = W.config(n_live=97, k=13, steps=0, seed=4, quadrature=quad, n_volume_sims=50)
+        ref = nsso.Oracle(prob, cfg)
+        gpu = nss.Sampler(prob, cfg)
+        x, e = ref.get_live()
+        e = (np.arange(97, dtype=np.float64)[::-1] * 0.01).astype(np.float32).astype(np.float64)
+        ref.set_live(x.astype(np.float32).astype(np.float64), e, 1)
+        gpu.set_live(x.astype(np.float32), e.astype(np.float32), 1)
+        for _ in range(9):
+            gpu.step()
+            ref.step()
+        assert np.allclose(gpu.evidence_reps(), ref.evidence_reps(), rtol=0, atol=1e-10)
+        gpu.finalise()
+        ref.finalise()
+        assert np.allclose(gpu.volume_reps(), ref.volume_reps(), rtol=0, atol=1e-10)
+        assert np.allclose(gpu.evidence_reps(), ref.evidence_reps(), rtol=0, atol=1e-10)
+        lg, sg = gpu.evidence()
+        lr, sr = ref.evidence()
+        assert abs(lg - lr) < 1e-10 and abs(sg - sr) < 1e-10
+        xg, wg = gpu.samples()
+        xr, wr = ref.samples()
+        assert np.allclose(wg, wr, rtol=0, atol=1e-9)
+        assert np.allclose(xg, xr, rtol=0, atol=0)
+        gpu.close()
+
+
+def _run_logz(prob, kw, seeds):
+    from paper_2601_23252_b200 import nss
+    out = []
+    for s in seeds:
+        g = nss.Sampler(prob, W.config(seed=s, **kw))
+        info = g.run()
+        out.append(g.evidence() + (info,))
+        g.close()
+    return out
+
+
+def test_full_run_c1_analytic():
+    """north_star: |log Z - analytic| <= max(3 sigma, 0.05) on C1 (P14)."""
+    truth = 2 * math.log(math.erf(5 / math.sqrt(2))) - 2 * math.log(10)
+    res = _run_logz(W.gauss(2), dict(n_live=200, k=20, steps=10), range(1, 9))
+    lz = np.array([r[0] for r in res])
+    sig = np.array([r[1] for r in res])
+    assert np.all(np.abs(lz - truth) <= np.maximum(4 * sig, 0.05)), (lz, sig)
+    assert abs(lz.mean() - truth) <= max(3 * sig.mean() / math.sqrt(len(lz)), 0.05)
+    assert all(r[2]["terminated"] and r[2]["finalised"] for r in res)
+
+
+def test_full_run_c2_analytic():
+    prob = W.mog(10)
+    mass = [prob.w[j] * np.prod(stats.norm(prob.mu[j], prob.sigma[j]).cdf(prob.hi) -
+                                 stats.norm(prob.mu[j], prob.sigma[j]).cdf(prob.lo)) for j in range(4)]
+    truth = math.log(sum(mass)) - np.sum(np.log(prob.hi - prob.lo))
+    res = _run_logz(prob, dict(n_live=2000, k=200, steps=10), range(1, 4))
+    for lz, sig, info in res:
+        assert abs(lz - truth) <= max(3 * sig, 0.05), (lz, sig, truth)
+
+
+def test_full_run_gpu_vs_oracle_c1():
+    """Same seed: GPU and oracle full runs agree within the combined spread."""
+    from oracle import nsso
+    prob = W.gauss(2)
+    kw = dict(n_live=200, k=20, steps=10)
+    diffs = []
+    for s in range(1, 7):
+        o = nsso.Oracle(prob, W.config(seed=s, **kw))
+        o.run()
+        (lg, sg, _), = _run_logz(prob, kw, [s])
+        lr, sr = o.evidence()
+        diffs.append((lg - lr) / math.hypot(sg, sr))
+    assert np.all(np.abs(diffs) < 4), diffs
+
+
+def test_posterior_weights_c1():
+    from paper_2601_23252_b200 import nss
+    g = nss.Sampler(W.gauss(2), W.config(n_live=200, k=20, steps=10, seed=3))
+    g.run()
+    x, lw = g.samples()
+    assert abs(special.logsumexp(lw)) < 1e-9
+    w = np.exp(lw)
+    ess = 1 / np.sum(w ** 2)
+    m = w @ x
+    assert np.all(np.abs(m) < 4 / math.sqrt(ess))
+    assert np.all(np.abs(w @ (x - m) ** 2 - 1) < 0.25)
+
+
+def test_determinism_gpu():
+    from paper_2601_23252_b200 import nss
+    prob = W.mog(10)
+    cfg = W.config(n_live=2000, k=200, steps=10, seed=8)
+    a, b = nss.Sampler(prob, cfg), nss.Sampler(prob, cfg)
+    a.steps(20)
+    b.steps(20)
+    da, db = a.dead(), b.dead()
+    for key in da:
+        assert np.array_equal(da[key], db[key])
+    assert np.array_equal(a.evidence_reps(), b.evidence_reps())
+
+
+def test_termination_flat_matches_oracle():
+    from oracle import nsso
+    from paper_2601_23252_b200 import nss
+    prob = W.flat(2)
+    cfg = W.config(n_live=100, k=10, steps=1, seed=2)
+    g = nss.Sampler(prob, cfg)
+    o = nsso.Oracle(prob, cfg)
+    ig, io = g.run(), o.run()
+    assert ig["iteration"] == io["iteration"]
+    assert ig["terminated"] == io["terminated"] == 1
+
+
+def test_errors():
+    from paper_2601_23252_b200 import nss
+    with pytest.raises(nss.NssError) as ei:
+        nss.Sampler(W.gauss(2), W.config(n_live=10, k=10, steps=1))
+    assert ei.value.code == 1
+    with pytest.raises(nss.NssError) as ei:
+        nss.Sampler(W.gp_ard(2, n_data=8), W.config(n_live=10, k=1, steps=1))
+    assert ei.value.code in (9,)
+    p = W.gauss(2, half_width=1.0)
+    p.c = float("inf")
+    with pytest.raises(nss.NssError) as ei:
+        nss.Sampler(p, W.config(n_live=10, k=1, steps=1))
+    assert ei.value.code == 2
+    p = W.gauss(2)
+    p.c = float("nan")
+    with pytest.raises(nss.NssError) as ei:
+        nss.Sampler(p, W.config(n_live=10, k=1, steps=1))
+    assert ei.value.code == 3
+    g = nss.Sampler(W.gauss(2), W.config(n_live=10, k=5, steps=1, max_dead=14))
+    with pytest.raises(nss.NssError) as ei:
+        g.step()
+    assert ei.value.code == 8
+    g2 = nss.Sampler(W.gauss(2), W.config(n_live=10, k=5, steps=1))
+    with pytest.raises(nss.NssError) as ei:
+        g2.evidence()
+    assert ei.value.code == 7
+    g2.run()
+    with pytest.raises(nss.NssError) as ei:
+        g2.step()
+    assert ei.value.code == 7
