@@ -182,6 +182,15 @@ nss_status nss_dead(nss_ctx *ctx, float *e, int32_t *n_live, float *birth, int32
                     int64_t cap, int64_t *n_out);
 nss_status nss_volume_reps(nss_ctx *ctx, double *log_x /* R+1 */);
 
+/* HRSS engine.  AUTO picks LANE (one probe per lane,
+ * speculative rounds) when d <= 32 and the energy is cheap, WARP (warp-
+ * cooperative energy, one probe at a time) otherwise; forcing LANE where it
+ * does not apply falls back to WARP.  Both compute the same algorithm. */
+typedef enum { NSS_ENGINE_AUTO = 0, NSS_ENGINE_WARP = 1, NSS_ENGINE_LANE = 2 } nss_hrss_engine;
+nss_status nss_set_hrss_engine(nss_ctx *ctx, int32_t engine);
+/* The engine the next iteration will use (resolved: WARP or LANE). */
+nss_status nss_get_hrss_engine(nss_ctx *ctx, int32_t *engine);
+
 /* ---- measurement hooks ---- */
 /* When enabled, the HRSS kernel launch of every iteration is bracketed by CUDA
  * events on the context's stream; nss_kernel_time returns the summed elapsed

@@ -11,60 +11,11 @@
 // normals are staged per warp.  Every random number comes from the counter-based
 // Philox stream (iter, dest gid, HRSS, step), so a chain's result does not
 // depend on where or when it runs.
-#include "nss_internal.cuh"
+#include "energy.cuh"
 
 namespace nss {
 
 namespace {
-
-constexpr float kLn2Pi = 1.8378770664093453f;
-constexpr unsigned kFull = 0xffffffffu;
-
-struct ESm {          // shared-memory image of the energy parameters
-  const float *mu;    // GAUSS/CORR: d; MOG: K*d
-  const float *isig;  // GAUSS: d; MOG: K*d
-  const float *logc;  // MOG: K
-  const float *prec;  // CORR: d rows of stride ldp
-  int ldp;
-};
-
-__host__ __device__ inline int odd_stride(int d) { return d | 1; }
-
-// number of floats of energy parameters staged in shared memory
-__host__ __device__ inline int energy_param_floats(int kind, int d, int K) {
-  switch (kind) {
-    case NSS_E_GAUSS: return 2 * d;
-    case NSS_E_MOG: return 2 * K * d + K;
-    case NSS_E_CORR_GAUSS: return d + d * odd_stride(d);
-    default: return 0;
-  }
-}
-
-__device__ void stage_energy(const EnergyDev &en, float *sp, ESm &es) {
-  const int d = en.d, tid = threadIdx.x, nt = blockDim.x;
-  es.ldp = odd_stride(d);
-  if (en.kind == NSS_E_GAUSS) {
-    for (int i = tid; i < d; i += nt) { sp[i] = en.mu[i]; sp[d + i] = en.isig[i]; }
-    es.mu = sp; es.isig = sp + d;
-  } else if (en.kind == NSS_E_MOG) {
-    const int K = en.n_comp;
-    for (int i = tid; i < K * d; i += nt) { sp[i] = en.mu[i]; sp[K * d + i] = en.isig[i]; }
-    for (int j = tid; j < K; j += nt) sp[2 * K * d + j] = en.logc[j];
-    es.mu = sp; es.isig = sp + K * d; es.logc = sp + 2 * K * d;
-  } else if (en.kind == NSS_E_CORR_GAUSS) {
-    for (int i = tid; i < d; i += nt) sp[i] = en.mu[i];
-    float *P = sp + d;
-    for (int e = tid; e < d * d; e += nt) {
-      int i = e / d, j = e - i * d;
-      P[i * es.ldp + j] = en.prec[e];
-    }
-    es.mu = sp; es.prec = P;
-  }
-}
-
-__device__ __forceinline__ float softplusf(float a) {
-  return a > 0.f ? a + log1pf(expf(-a)) : log1pf(expf(a));
-}
 
 // Warp-cooperative energy E(x); the result is identical in every lane.
 // `wbuf` is a per-warp shared buffer of NPL*32 floats.
@@ -86,38 +37,30 @@ __device__ __forceinline__ float warp_energy(const float (&x)[NPL], const Energy
     }
     return 0.5f * warp_sum(s) + en.c;
   } else if constexpr (KIND == NSS_E_MOG) {
-    const int K = en.n_comp;
-    float s[kMaxComp];
+    // online log-sum-exp over components; unrolling lets the K independent
+    // butterfly reductions overlap
+    float m = -INFINITY, acc = 0.f;
+#pragma unroll 4
+    for (int j = 0; j < en.n_comp; ++j) {
+      float s = 0.f;
 #pragma unroll
-    for (int j = 0; j < kMaxComp; ++j) {
-      s[j] = 0.f;
-      if (j < K) {
-#pragma unroll
-        for (int t = 0; t < NPL; ++t) {
-          const int i = lane + 32 * t;
-          if (i < d) {
-            float u = (x[t] - es.mu[j * d + i]) * es.isig[j * d + i];
-            s[j] = fmaf(u, u, s[j]);
-          }
+      for (int t = 0; t < NPL; ++t) {
+        const int i = lane + 32 * t;
+        if (i < d) {
+          float u = (x[t] - es.mu[j * d + i]) * es.isig[j * d + i];
+          s = fmaf(u, u, s);
         }
       }
+      s = warp_sum(s);
+      const float l = es.logc[j] - 0.5f * s;
+      if (l > m) {
+        acc = acc * __expf(m - l) + 1.f;
+        m = l;
+      } else {
+        acc += __expf(l - m);
+      }
     }
-    // interleaved butterflies: the K reductions are independent
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-      for (int j = 0; j < kMaxComp; ++j)
-        if (j < K) s[j] += __shfl_xor_sync(kFull, s[j], o);
-    }
-    float m = -INFINITY;
-#pragma unroll
-    for (int j = 0; j < kMaxComp; ++j)
-      if (j < K) m = fmaxf(m, es.logc[j] - 0.5f * s[j]);
-    float acc = 0.f;
-#pragma unroll
-    for (int j = 0; j < kMaxComp; ++j)
-      if (j < K) acc += expf(es.logc[j] - 0.5f * s[j] - m);
-    return -(m + logf(acc));
+    return -(m + __logf(acc));
   } else if constexpr (KIND == NSS_E_CORR_GAUSS) {
 #pragma unroll
     for (int t = 0; t < NPL; ++t) {
@@ -202,22 +145,6 @@ __device__ __forceinline__ float prior_logp(const float (&x)[NPL], const PriorDe
   }
   inside = true;
   return -0.5f * warp_sum(s) + pr.log_norm;
-}
-
-template <int NPL>
-__device__ __forceinline__ void load_prior_lane(const PriorDev &pr, int lane, int d, float (&pa)[NPL],
-                                                float (&pb)[NPL]) {
-#pragma unroll
-  for (int t = 0; t < NPL; ++t) {
-    const int i = lane + 32 * t;
-    if (pr.kind == NSS_PRIOR_BOX) {
-      pa[t] = i < d ? pr.lo[i] : 0.f;
-      pb[t] = i < d ? pr.hi[i] : 0.f;
-    } else {
-      pa[t] = i < d ? pr.mean[i] : 0.f;
-      pb[t] = i < d ? pr.isd[i] : 0.f;
-    }
-  }
 }
 
 struct Probe {
@@ -529,7 +456,20 @@ size_t energy_smem_bytes(const EnergyDev &en) {
   return static_cast<size_t>(energy_param_floats(en.kind, en.d, en.n_comp)) * sizeof(float);
 }
 
+// Engine choice: one probe per lane for small d and cheap energies
+// (k_hrss_lane.cu), warp-cooperative energies otherwise.  RunDev::engine
+// (nss_set_hrss_engine) can force either one; the tests run both.
+int hrss_engine(const RunDev &r, const EnergyDev &en) {
+  const bool lane_ok = lane_engine_ok(r, en);
+  if (r.engine == NSS_ENGINE_WARP || !lane_ok) return 0;
+  return 1;
+}
+
 void launch_hrss(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc) {
+  if (hrss_engine(r, en) == 1) {
+    launch_hrss_lane(r, pr, en, lc);
+    return;
+  }
   NSS_DISPATCH(launch_hrss_t, r, pr, en, lc);
 }
 

@@ -657,6 +657,22 @@ NSS_API nss_status nss_kernel_time(nss_ctx *c, double *ms, int64_t *launches) {
   return NSS_OK;
 }
 
+NSS_API nss_status nss_set_hrss_engine(nss_ctx *c, int32_t engine) {
+  nss_status s = check_usable(c);
+  if (s) return s;
+  if (engine < NSS_ENGINE_AUTO || engine > NSS_ENGINE_LANE) return NSS_ERR_INVALID_ARG;
+  c->r.engine = engine;
+  return NSS_OK;
+}
+
+NSS_API nss_status nss_get_hrss_engine(nss_ctx *c, int32_t *engine) {
+  nss_status s = check_usable(c);
+  if (s) return s;
+  if (!engine) return NSS_ERR_INVALID_ARG;
+  *engine = hrss_engine(c->r, c->en) == 1 ? NSS_ENGINE_LANE : NSS_ENGINE_WARP;
+  return NSS_OK;
+}
+
 NSS_API nss_status nss_launch_count(nss_ctx *c, int64_t *launches) {
   if (!c || !launches) return NSS_ERR_INVALID_ARG;
   *launches = c->launches;

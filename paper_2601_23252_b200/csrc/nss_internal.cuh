@@ -63,6 +63,7 @@ struct RunDev {
   int max_stepout, max_shrink;
   int dir_norm, quadrature;
   int R;
+  int engine;                 // nss_hrss_engine (host-side choice)
   long long max_dead;
   uint32_t seed_lo, seed_hi;
   float term_log_ratio;
@@ -153,6 +154,10 @@ void launch_hrss(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const
 void launch_init(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc);
 size_t energy_smem_bytes(const EnergyDev &en);
 bool energy_supported(const EnergyDev &en);
+int hrss_engine(const RunDev &r, const EnergyDev &en);  // 0 warp-cooperative, 1 one probe per lane
+// k_hrss_lane.cu
+bool lane_engine_ok(const RunDev &r, const EnergyDev &en);
+void launch_hrss_lane(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc);
 // k_metric.cu: A5 metric (+ A9 termination when iterating)
 void launch_metric(const RunDev &r, double metric_reg, int width_rule, double width_param,
                    int end_of_iteration, double *partials, int n_blocks, const LaunchCtx &lc);

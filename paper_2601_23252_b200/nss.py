@@ -71,7 +71,7 @@ EXPORTS = ["nss_get_unique_id", "nss_init", "nss_step", "nss_steps", "nss_run", 
            "nss_evidence", "nss_evidence_reps", "nss_samples", "nss_info", "nss_sync", "nss_destroy",
            "nss_last_error", "nss_set_live", "nss_get_live", "nss_get_metric", "nss_get_trace",
            "nss_dead", "nss_volume_reps", "nss_set_kernel_timing", "nss_kernel_time",
-           "nss_launch_count"]
+           "nss_launch_count", "nss_set_hrss_engine", "nss_get_hrss_engine"]
 
 _lib = None
 
@@ -110,6 +110,8 @@ def lib():
     L.nss_set_kernel_timing.argtypes = [vp, C.c_int32]
     L.nss_kernel_time.argtypes = [vp, P(C.c_double), P(C.c_int64)]
     L.nss_launch_count.argtypes = [vp, P(C.c_int64)]
+    L.nss_set_hrss_engine.argtypes = [vp, C.c_int32]
+    L.nss_get_hrss_engine.argtypes = [vp, P(C.c_int32)]
     _lib = L
     return L
 
@@ -280,6 +282,16 @@ class Sampler:
         ms, n = C.c_double(), C.c_int64()
         self._check(lib().nss_kernel_time(self._h, C.byref(ms), C.byref(n)), "nss_kernel_time")
         return ms.value, n.value
+
+    def set_engine(self, engine: str):
+        """'auto', 'warp' or 'lane' (include/nss.h nss_hrss_engine)."""
+        code = {"auto": 0, "warp": 1, "lane": 2}[engine]
+        self._check(lib().nss_set_hrss_engine(self._h, code), "nss_set_hrss_engine")
+
+    def engine(self) -> str:
+        e = C.c_int32()
+        self._check(lib().nss_get_hrss_engine(self._h, C.byref(e)), "nss_get_hrss_engine")
+        return {1: "warp", 2: "lane"}[e.value]
 
     def launch_count(self) -> int:
         n = C.c_int64()

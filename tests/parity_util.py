@@ -16,7 +16,7 @@ TIE = 1e-5
 RTOL = 1e-5
 
 
-def inject_pair(prob, cfg, warm_iters=0, it=None):
+def inject_pair(prob, cfg, warm_iters=0, it=None, engine="auto"):
     from oracle import nsso
     from paper_2601_23252_b200 import nss
 
@@ -31,6 +31,7 @@ def inject_pair(prob, cfg, warm_iters=0, it=None):
     nxt = warm_iters + 1 if it is None else it
     ref.set_live(x32.astype(np.float64), e32.astype(np.float64), nxt)
     gpu = nss.Sampler(prob, cfg)
+    gpu.set_engine(engine)
     gpu.set_live(x32, e32, nxt)
     return gpu, ref
 

@@ -53,12 +53,15 @@ CASES = {
 }
 
 
+@pytest.mark.parametrize("engine", ["warp", "lane"])
 @pytest.mark.parametrize("name", sorted(CASES))
-def test_single_iteration_parity(name):
+def test_single_iteration_parity(name, engine):
     make, kw, warm = CASES[name]
     prob = make()
     cfg = W.config(seed=11, **kw)
-    gpu, ref = inject_pair(prob, cfg, warm_iters=warm)
+    gpu, ref = inject_pair(prob, cfg, warm_iters=warm, engine=engine)
+    if engine == "lane" and gpu.engine() != "lane":
+        pytest.skip("lane engine does not apply to this case")
     # metric from the same injected cloud
     Lg, wg = gpu.metric()
     Lr, wr = ref.metric()
