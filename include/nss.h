@@ -197,6 +197,18 @@ nss_status nss_get_hrss_engine(nss_ctx *ctx, int32_t *engine);
  * milliseconds and the number of launches since the last reset. */
 nss_status nss_set_kernel_timing(nss_ctx *ctx, int32_t enable);
 nss_status nss_kernel_time(nss_ctx *ctx, double *ms, int64_t *launches);
+/* Per-phase totals of the same timing mode: ms[4] and launches[4] for
+ * {HRSS, select/dead/resample, evidence, metric+termination}. */
+nss_status nss_phase_times(nss_ctx *ctx, double *ms /* 4 */, int64_t *launches /* 4 */);
+/* overlap != 0 (default): the evidence kernel runs on a side stream
+ * concurrently with HRSS; 0: all kernels in sequence on one stream. */
+nss_status nss_set_overlap(nss_ctx *ctx, int32_t overlap);
+/* enable != 0 (default): each iteration is replayed from a captured CUDA
+ * graph; 0: kernels are launched one by one (timing mode always does). */
+nss_status nss_set_graph(nss_ctx *ctx, int32_t enable);
+/* Device %globaltimer stamps (ns) written at phase boundaries of the select
+ * (0-6) and metric (8-13) kernels during the last iteration. */
+nss_status nss_debug_stamps(nss_ctx *ctx, uint64_t *stamps /* 16 */);
 /* Kernels launched by this context since creation (all kinds). */
 nss_status nss_launch_count(nss_ctx *ctx, int64_t *launches);
 

@@ -268,9 +268,11 @@ __global__ void __launch_bounds__(256) k_hrss(RunDev r, PriorDev pr, EnergyDev e
     };
 
     // ---- linear stepping-out, capped per side (R-10) ----
+    // endpoint m is L0 - m w (R0 + m w) with one rounding, as in k_hrss_lane.cu
     int nl = 0, nr = 0;
-    while (nl < r.max_stepout && in_slice(lft)) { lft -= w; ++nl; }
-    while (nr < r.max_stepout && in_slice(rgt)) { rgt += w; ++nr; }
+    const float l0 = lft, r0 = rgt;
+    while (nl < r.max_stepout && in_slice(lft)) { ++nl; lft = fmaf(-static_cast<float>(nl), w, l0); }
+    while (nr < r.max_stepout && in_slice(rgt)) { ++nr; rgt = fmaf(static_cast<float>(nr), w, r0); }
 
     // ---- shrinkage, capped; null move at the cap (R-12/R-13) ----
     int ns = 0, acc = 0;
@@ -401,6 +403,7 @@ void launch_hrss_t(const RunDev &r, const PriorDev &pr, const EnergyDev &en, con
     attr = smem;
   }
   const int blocks = (r.k + wpb - 1) / wpb;
+  NSS_PIN_CARVEOUT((k_hrss<NPL, KIND>));
   k_hrss<NPL, KIND><<<blocks, wpb * 32, smem, lc.stream>>>(r, pr, en);
   ++*lc.launch_counter;
 }
@@ -415,6 +418,7 @@ void launch_init_t(const RunDev &r, const PriorDev &pr, const EnergyDev &en, con
     attr = smem;
   }
   const int blocks = (r.n + wpb - 1) / wpb;
+  NSS_PIN_CARVEOUT((k_init<NPL, KIND>));
   k_init<NPL, KIND><<<blocks, wpb * 32, smem, lc.stream>>>(r, pr, en);
   ++*lc.launch_counter;
 }

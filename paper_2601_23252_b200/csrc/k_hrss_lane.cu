@@ -3,60 +3,107 @@
 //
 // HRSS is a chain of dependent slice tests, so at small d a warp-per-chain
 // kernel is latency-bound: every probe waits for the previous decision.  But
-// all the points the sequential algorithm could visit next are
-// known in advance:
-//   * stepping-out endpoints are L - m w and R + m w (m = 0..cap-1);
+// every point the sequential algorithm can visit next is known in
+// advance:
+//   * stepping-out endpoints are L0 - m w and R0 + m w (m = 0..cap-1);
 //   * along the all-rejected path every shrink proposal is fixed too, because a
 //     rejected proposal t moves the left end if t < 0 and the right end
 //     otherwise (R-13): proposal i is L_i + u_i (R_i - L_i) with (L_i, R_i)
 //     obtained from proposals 0..i-1.
-// So the warp evaluates 16 left + 16 right endpoints in one round (lanes
-// 0-15 / 16-31) and 16 shrink proposals in a second round, then takes the
-// first outcome the sequential algorithm would have taken (ballot + ffs).
-// Every point is computed with the same fp32 operations, in the same order, as
-// the sequential kernel (repeated subtraction of w; the same fma for t), so
-// decisions, counters and results are those of the sequential algorithm;
-// only the number of dependent rounds changes (about 2 per step instead of
-// ~5-7).  Counters report the algorithm's probes, not the speculative ones,
-// and a NaN raises an error only if the sequential algorithm would have
-// evaluated that point.
+// So the warp evaluates 16 left + 16 right endpoints in one round (lanes 0-15
+// / 16-31) and kShrink shrink proposals in a second round, and takes the first
+// outcome the sequential algorithm would take (ballot + ffs).  Every point is
+// computed with the same fp32 operations as the sequential engine (k_hrss.cu),
+// so decisions and counters are those of the sequential algorithm; only the
+// number of dependent rounds changes (about 2 per step instead of ~5-7).
+// Counters report the algorithm's probes, not the speculative ones, and a NaN
+// raises an error only if the sequential algorithm would have evaluated it.
+//
+// Instruction diet (the kernel is issue-latency bound):
+// coordinates are padded to a compile-time D with neutral values (zero
+// direction, infinite box, zero precision) so no loop carries a predicate;
+// small mixtures keep their parameters in registers; one Philox pass per step
+// produces the normals, the slice height, the bracket offset and the first
+// shrink uniforms, distributed by shuffles.
 #include "energy.cuh"
 
 namespace nss {
 
 namespace {
 
-constexpr int kRound = 16;  // endpoints per side / shrink proposals per round
+constexpr int kRound = 16;   // stepping-out endpoints per side per round
+constexpr int kShrink = 8;   // shrink proposals per round
 
-// Thread-local energy of the point xp (coordinates >= d are ignored).
-template <int D, int KIND>
-__device__ __forceinline__ float lane_energy(const float (&xp)[D], const EnergyDev &en, const ESm &es, int d) {
+template <int D, int KIND, int K>
+struct LaneParams {
+  // GAUSS: a = 1/sigma, b = -mu/sigma (u = x a + b); MOG with compile-time K: per component
+  float a[K > 0 ? K : 1][D], b[K > 0 ? K : 1][D], logc[K > 0 ? K : 1];
+};
+
+template <int D, int KIND, int K>
+__device__ __forceinline__ void load_params(LaneParams<D, KIND, K> &lp, const EnergyDev &en) {
+  if constexpr (KIND == NSS_E_GAUSS || (KIND == NSS_E_MOG && K > 0)) {
+    constexpr int KK = KIND == NSS_E_GAUSS ? 1 : K;
+    // host-built padded table [K][2][32]: {1/sigma, -mu/sigma}, zeros past d
+#pragma unroll
+    for (int j = 0; j < KK; ++j) {
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        lp.a[j][i] = __ldg(en.lane_ab + j * 64 + i);
+        lp.b[j][i] = __ldg(en.lane_ab + j * 64 + 32 + i);
+      }
+      lp.logc[j] = KIND == NSS_E_MOG ? __ldg(en.logc + j) : 0.f;
+    }
+  }
+}
+
+// Thread-local energy of the padded point xp.
+template <int D, int KIND, int K>
+__device__ __forceinline__ float lane_energy(const float (&xp)[D], const LaneParams<D, KIND, K> &P,
+                                             const EnergyDev &en, const float *sA, const float *sB,
+                                             const float *sC, int ldD, int d) {
   if constexpr (KIND == NSS_E_FLAT) {
     return en.c;
   } else if constexpr (KIND == NSS_E_GAUSS) {
     float s = 0.f;
 #pragma unroll
-    for (int i = 0; i < D; ++i)
-      if (i < d) {
-        const float u = (xp[i] - es.mu[i]) * es.isig[i];
-        s = fmaf(u, u, s);
-      }
+    for (int i = 0; i < D; ++i) {
+      const float u = fmaf(xp[i], P.a[0][i], P.b[0][i]);
+      s = fmaf(u, u, s);
+    }
     return 0.5f * s + en.c;
-  } else if constexpr (KIND == NSS_E_MOG) {
-    // -log sum_j exp(logc_j - 1/2 |(x - mu_j) / sigma_j|^2), online log-sum-exp
-    float m = -INFINITY, acc = 0.f;
-#pragma unroll 4
-    for (int j = 0; j < en.n_comp; ++j) {
-      const float *mu = es.mu + j * d;
-      const float *is = es.isig + j * d;
+  } else if constexpr (KIND == NSS_E_MOG && K > 0) {
+    float l[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
       float s = 0.f;
 #pragma unroll
-      for (int i = 0; i < D; ++i)
-        if (i < d) {
-          const float u = (xp[i] - mu[i]) * is[i];
-          s = fmaf(u, u, s);
-        }
-      const float l = es.logc[j] - 0.5f * s;
+      for (int i = 0; i < D; ++i) {
+        const float u = fmaf(xp[i], P.a[j][i], P.b[j][i]);
+        s = fmaf(u, u, s);
+      }
+      l[j] = fmaf(-0.5f, s, P.logc[j]);
+    }
+    float m = l[0];
+#pragma unroll
+    for (int j = 1; j < K; ++j) m = fmaxf(m, l[j]);
+    float acc = 0.f;
+#pragma unroll
+    for (int j = 0; j < K; ++j) acc += __expf(l[j] - m);
+    return -(m + __logf(acc));
+  } else if constexpr (KIND == NSS_E_MOG) {
+    // runtime K: parameters in shared memory (a, b padded to D; logc)
+    float m = -INFINITY, acc = 0.f;
+#pragma unroll 2
+    for (int j = 0; j < en.n_comp; ++j) {
+      const float *a = sA + j * D, *b = sB + j * D;
+      float s = 0.f;
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        const float u = fmaf(xp[i], a[i], b[i]);
+        s = fmaf(u, u, s);
+      }
+      const float l = fmaf(-0.5f, s, sC[j]);
       if (l > m) {
         acc = acc * __expf(m - l) + 1.f;
         m = l;
@@ -69,26 +116,24 @@ __device__ __forceinline__ float lane_energy(const float (&xp)[D], const EnergyD
     const float y = xp[0];
     float s = 0.f;
 #pragma unroll
-    for (int i = 1; i < D; ++i)
-      if (i < d) s = fmaf(xp[i], xp[i], s);
+    for (int i = 1; i < D; ++i) s = fmaf(xp[i], xp[i], s);
     const float sy = en.sigma_y, yy = y / sy;
     return 0.5f * yy * yy + logf(sy) + 0.5f * kLn2Pi + 0.5f * s * expf(-y) +
            static_cast<float>(d - 1) * 0.5f * (y + kLn2Pi);
   } else if constexpr (KIND == NSS_E_CORR_GAUSS) {
+    // sA: mu padded to D; sB: precision padded to D x ldD (zeros outside d x d)
     float y[D];
 #pragma unroll
-    for (int i = 0; i < D; ++i) y[i] = i < d ? xp[i] - es.mu[i] : 0.f;
+    for (int i = 0; i < D; ++i) y[i] = xp[i] - sA[i];
     float q = 0.f;
 #pragma unroll
-    for (int i = 0; i < D; ++i)
-      if (i < d) {
-        const float *row = es.prec + i * es.ldp;
-        float py = 0.f;
+    for (int i = 0; i < D; ++i) {
+      const float *row = sB + i * ldD;
+      float py = 0.f;
 #pragma unroll
-        for (int m = 0; m < D; ++m)
-          if (m < d) py = fmaf(row[m], y[m], py);
-        q = fmaf(y[i], py, q);
-      }
+      for (int m = 0; m < D; ++m) py = fmaf(row[m], y[m], py);
+      q = fmaf(y[i], py, q);
+    }
     return 0.5f * q + en.c;
   } else {
     return NAN;
@@ -102,34 +147,33 @@ struct LaneProbe {
   float e, lp;
 };
 
-template <int D, int KIND>
-__device__ __forceinline__ LaneProbe lane_probe(float t, const float (&x)[D], const float (&v)[D],
-                                                const PriorDev &pr, const float *sPr, const EnergyDev &en,
-                                                const ESm &es, int d, float log_y, float e_star) {
+template <int D, int KIND, int K>
+__device__ __forceinline__ LaneProbe lane_probe(float t, const float (&x)[D], const float (&v)[D], bool box,
+                                                const float (&pa)[D], const float (&pb)[D], float log_norm,
+                                                const LaneParams<D, KIND, K> &P, const EnergyDev &en,
+                                                const float *sA, const float *sB, const float *sC, int ldD,
+                                                int d, float log_y, float e_star) {
   float xp[D];
 #pragma unroll
   for (int i = 0; i < D; ++i) xp[i] = fmaf(t, v[i], x[i]);
-  LaneProbe o{false, false, false, 0.f, 0.f};
-  if (pr.kind == NSS_PRIOR_BOX) {
+  LaneProbe o{false, false, false, 0.f, log_norm};
+  if (box) {
     bool in = true;
 #pragma unroll
-    for (int i = 0; i < D; ++i)
-      if (i < d) in = in && (xp[i] >= sPr[i]) && (xp[i] <= sPr[d + i]);
-    o.lp = pr.log_norm;
-    o.pass = in && (o.lp >= log_y);
+    for (int i = 0; i < D; ++i) in = in && (xp[i] >= pa[i]) && (xp[i] <= pb[i]);
+    o.pass = in && (log_norm >= log_y);
   } else {
     float s = 0.f;
 #pragma unroll
-    for (int i = 0; i < D; ++i)
-      if (i < d) {
-        const float u = (xp[i] - sPr[i]) * sPr[d + i];
-        s = fmaf(u, u, s);
-      }
-    o.lp = -0.5f * s + pr.log_norm;
+    for (int i = 0; i < D; ++i) {
+      const float u = (xp[i] - pa[i]) * pb[i];
+      s = fmaf(u, u, s);
+    }
+    o.lp = fmaf(-0.5f, s, log_norm);
     o.pass = o.lp >= log_y;
   }
   if (o.pass) {
-    o.e = lane_energy<D, KIND>(xp, en, es, d);
+    o.e = lane_energy<D, KIND, K>(xp, P, en, sA, sB, sC, ldD, d);
     o.nan = isnan(o.e);
     o.ok = !o.nan && o.e < e_star;
   }
@@ -140,79 +184,100 @@ __device__ __forceinline__ unsigned low_mask(int n) {  // bits 0..n-1
   return n >= 32 ? 0xffffffffu : ((1u << n) - 1u);
 }
 
-template <int D, int KIND>
+template <int D, int KIND, int K>
 __global__ void __launch_bounds__(256) k_hrss_lane(RunDev r, PriorDev pr, EnergyDev en) {
   extern __shared__ float sm[];
-  __shared__ int sh_flag;
   const int d = r.d, lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
-  const int ldl = odd_stride(d);
-  float *sL = sm;
-  float *sPr = sL + d * ldl;
-  float *sP = sPr + 2 * d;
-  if (threadIdx.x == 0) sh_flag = (r.st->terminated || r.st->error || r.st->finalised) ? 1 : 0;
-  for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
-    const int i = e / d, j = e - i * d;
-    sL[i * ldl + j] = r.L[i * r.dp + j];
+  constexpr int ldD = D | 1;
+  constexpr bool kSmemTables = (KIND == NSS_E_MOG && K == 0) || KIND == NSS_E_CORR_GAUSS;
+  // shared memory only for the runtime-K mixture and the correlated Gaussian
+  float *sA = sm;
+  float *sB = sA + (KIND == NSS_E_MOG ? kMaxComp * D : D);
+  float *sC = sB + (KIND == NSS_E_MOG ? kMaxComp * D : D * ldD);
+  if constexpr (KIND == NSS_E_MOG && K == 0) {
+    for (int e = threadIdx.x; e < en.n_comp * D; e += blockDim.x) {
+      const int j = e / D, i = e - j * D;
+      sA[e] = en.lane_ab[j * 64 + i];
+      sB[e] = en.lane_ab[j * 64 + 32 + i];
+    }
+    for (int j = threadIdx.x; j < en.n_comp; j += blockDim.x) sC[j] = en.logc[j];
   }
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    sPr[i] = pr.kind == NSS_PRIOR_BOX ? pr.lo[i] : pr.mean[i];
-    sPr[d + i] = pr.kind == NSS_PRIOR_BOX ? pr.hi[i] : pr.isd[i];
+  if constexpr (KIND == NSS_E_CORR_GAUSS) {
+    for (int i = threadIdx.x; i < D; i += blockDim.x) sA[i] = i < d ? en.mu[i] : 0.f;
+    for (int e = threadIdx.x; e < D * ldD; e += blockDim.x) {
+      const int i = e / ldD, j = e - i * ldD;
+      sB[e] = (i < d && j < d) ? en.prec[i * d + j] : 0.f;
+    }
   }
-  ESm es;
-  stage_energy(en, sP, es);
-  __syncthreads();
-  if (sh_flag) return;
+  if constexpr (kSmemTables) __syncthreads();
   const int c = blockIdx.x * wpb + wib;
   if (c >= r.k) return;
 
   DevState *st = r.st;
-  const uint32_t it = static_cast<uint32_t>(st->iter + 1);
+  // issue the independent loads first; the flags are checked after
   const int s = r.dest_gid[c];
   const int par = r.parent_gid[c];
-  const float e_star = st->e_star;
-  const float w = st->width;
-  const int p = r.p, cap = r.max_stepout, maxs = r.max_shrink;
-  const bool euclid = r.dir_norm == NSS_DIR_EUCLIDEAN;
-  const int h = 2 * ((d + 1) / 2);
-  const int nblk_norm = h >> 2, nblk_all = (h + 3) >> 2;
-  const int side = lane >> 4, m = lane & 15;
-
+  LaneParams<D, KIND, K> P;
+  load_params<D, KIND, K>(P, en);
+  // row `lane` of L (zeros past d), held in registers for the whole chain
+  float Lrow[D];
+  {
+    const float *row = r.L + static_cast<long long>(lane < d ? lane : 0) * r.dp;
+#pragma unroll
+    for (int i = 0; i < D; ++i) Lrow[i] = (lane < d && i < d) ? row[i] : 0.f;
+  }
+  // prior, padded with neutral values (infinite box / zero inverse sd)
+  float pa[D], pb[D];
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    pa[i] = __ldg(pr.lane_pab + i);
+    pb[i] = __ldg(pr.lane_pab + 32 + i);
+  }
   float x[D], v[D];
 #pragma unroll
   for (int i = 0; i < D; ++i) x[i] = i < d ? r.X[static_cast<long long>(par) * r.dp + i] : 0.f;
   float e = r.E[par];
-  float lp;
-  if (pr.kind == NSS_PRIOR_BOX) {
-    lp = pr.log_norm;
-  } else {
+  if (st->terminated || st->error || st->finalised) return;
+  const uint32_t it = static_cast<uint32_t>(st->iter + 1);
+  const float e_star = st->e_star;
+  const float w = st->width;
+  const int p = r.p, cap = r.max_stepout, maxs = r.max_shrink;
+  const bool euclid = r.dir_norm == NSS_DIR_EUCLIDEAN;
+  const bool box = pr.kind == NSS_PRIOR_BOX;
+  const float log_norm = pr.log_norm;
+  const int h = 2 * ((d + 1) / 2);
+  const int nblk = (h + 2 + kShrink + 3) >> 2;  // normals, u_h, u_b, first shrink round
+  const int side = lane >> 4, m = lane & 15;
+  float lp = log_norm;
+  if (!box) {
     float acc = 0.f;
 #pragma unroll
-    for (int i = 0; i < D; ++i)
-      if (i < d) {
-        const float u = (x[i] - sPr[i]) * sPr[d + i];
-        acc = fmaf(u, u, acc);
-      }
-    lp = -0.5f * acc + pr.log_norm;
+    for (int i = 0; i < D; ++i) {
+      const float u = (x[i] - pa[i]) * pb[i];
+      acc = fmaf(u, u, acc);
+    }
+    lp = fmaf(-0.5f, acc, log_norm);
   }
 
   unsigned long long n_probe = 0, n_eval = 0, n_exp = 0, n_shr = 0, n_null = 0;
   bool nan_seen = false;
 
   for (int j = 0; j < p; ++j) {
-    // ---- direction (R-6): lane b holds normals 4b..4b+3 of stream (it, s, HRSS, j) ----
+    // ---- one Philox pass: lane b holds block b of stream (it, s, HRSS, j) ----
+    uint4 blk = make_uint4(0, 0, 0, 0);
+    if (lane < nblk) blk = philox_block(r, it, s, kPhaseHrss, j, lane);
+    // Box-Muller pairs (4b, 4b+1) and (4b+2, 4b+3) that are normals (index < h).
+    // The angle 2 pi u is reduced to 2 pi (u - 1/2) in [-pi, pi) (u - 1/2 is
+    // exact) so the fast sin/cos stays within its accurate range:
+    // cos(2 pi u) = -cos(2 pi (u - 1/2)), sin likewise.
     float zb0 = 0.f, zb1 = 0.f, zb2 = 0.f, zb3 = 0.f;
-    if (lane < nblk_all) {
-      const uint4 u4 = philox_block(r, it, s, kPhaseHrss, j, lane);
-      const float r0 = sqrtf(-2.f * logf(u01(u4.x))), r1 = sqrtf(-2.f * logf(u01(u4.z)));
+    {
+      const float r0 = sqrtf(-2.f * logf(u01(blk.x))), r1 = sqrtf(-2.f * logf(u01(blk.z)));
       float s0, c0, s1, c1;
-      sincospif(2.f * u01(u4.y), &s0, &c0);
-      sincospif(2.f * u01(u4.w), &s1, &c1);
-      zb0 = r0 * c0;
-      zb1 = r0 * s0;
-      if (lane < nblk_norm) {
-        zb2 = r1 * c1;
-        zb3 = r1 * s1;
-      }
+      __sincosf(6.283185307179586f * (u01(blk.y) - 0.5f), &s0, &c0);
+      __sincosf(6.283185307179586f * (u01(blk.w) - 0.5f), &s1, &c1);
+      if (4 * lane + 1 < h) { zb0 = -r0 * c0; zb1 = -r0 * s0; }
+      if (4 * lane + 3 < h) { zb2 = -r1 * c1; zb3 = -r1 * s1; }
     }
     float z[D];
 #pragma unroll
@@ -222,14 +287,10 @@ __global__ void __launch_bounds__(256) k_hrss_lane(RunDev r, PriorDev pr, Energy
       const float zi = __shfl_sync(kFull, mine, i >> 2);
       z[i] = i < d ? zi : 0.f;
     }
-    // row `lane` of L z, then broadcast
+    // direction (R-6): lane i computes (L z)_i from its register row, then broadcast
     float vl = 0.f;
-    if (lane < d) {
-      const float *row = sL + lane * ldl;
 #pragma unroll
-      for (int i = 0; i < D; ++i)
-        if (i <= lane && i < d) vl = fmaf(row[i], z[i], vl);
-    }
+    for (int i = 0; i < D; ++i) vl = fmaf(Lrow[i], z[i], vl);
     float zz = 0.f, vv = 0.f;
 #pragma unroll
     for (int i = 0; i < D; ++i) {
@@ -241,75 +302,75 @@ __global__ void __launch_bounds__(256) k_hrss_lane(RunDev r, PriorDev pr, Energy
 #pragma unroll
     for (int i = 0; i < D; ++i) v[i] *= inv;
 
-    // ---- slice height and initial bracket (R-9) ----
-    const uint4 hb = philox_block(r, it, s, kPhaseHrss, j, h >> 2);
-    const float log_y = lp + logf(u01(word(hb, h & 3)));
-    float lft = -w * u01(word(hb, (h + 1) & 3));
-    float rgt = lft + w;
+    // ---- slice height, bracket offset, first shrink uniforms (draws h, h+1, h+2..) ----
+    const float u_h = u01(__shfl_sync(kFull, word(blk, h & 3), h >> 2));
+    const float u_b = u01(__shfl_sync(kFull, word(blk, (h + 1) & 3), (h + 1) >> 2));
+    float us[kShrink];
+#pragma unroll
+    for (int i = 0; i < kShrink; ++i) {
+      const int q = h + 2 + i;
+      us[i] = u01(__shfl_sync(kFull, word(blk, q & 3), q >> 2));
+    }
+    const float log_y = lp + logf(u_h);
+    const float l0 = -w * u_b;
+    const float r0 = l0 + w;
 
     // ---- stepping-out: lanes 0-15 left endpoints, 16-31 right ----
     int nl = 0, nr = 0;
     bool ldone = false, rdone = false;
     while (!(ldone && rdone)) {
-      const bool mine_done = side == 0 ? ldone : rdone;
-      const int mine_n = side == 0 ? nl : nr;
-      float t = side == 0 ? lft : rgt;
-#pragma unroll
-      for (int q = 0; q < kRound - 1; ++q)
-        if (q < m) t = side == 0 ? t - w : t + w;
-      const bool act = !mine_done && (mine_n + m < cap);
+      const int idx = (side == 0 ? nl : nr) + m;
+      const bool act = !(side == 0 ? ldone : rdone) && idx < cap;
+      const float t = side == 0 ? fmaf(-static_cast<float>(idx), w, l0) : fmaf(static_cast<float>(idx), w, r0);
       LaneProbe o{false, false, false, 0.f, 0.f};
-      if (act) o = lane_probe<D, KIND>(t, x, v, pr, sPr, en, es, d, log_y, e_star);
+      if (act) o = lane_probe<D, KIND, K>(t, x, v, box, pa, pb, log_norm, P, en, sA, sB, sC, ldD, d, log_y, e_star);
       const unsigned bok = __ballot_sync(kFull, o.ok);
       const unsigned bpass = __ballot_sync(kFull, act && o.pass);
       const unsigned bnan = __ballot_sync(kFull, act && o.nan);
 #pragma unroll
       for (int sd = 0; sd < 2; ++sd) {
-        const bool done = sd == 0 ? ldone : rdone;
+        if (sd == 0 ? ldone : rdone) continue;
         const int navail = min(kRound, cap - (sd == 0 ? nl : nr));
         const unsigned bits = (bok >> (16 * sd)) & 0xffffu;
-        const unsigned pbits = (bpass >> (16 * sd)) & 0xffffu;
-        const unsigned nbits = (bnan >> (16 * sd)) & 0xffffu;
-        const int run = __ffs(~bits) - 1;  // consecutive in-slice endpoints from m = 0
+        const int run = __ffs(~bits) - 1;  // consecutive in-slice endpoints
         const int tested = run < navail ? run + 1 : navail;
-        const int src = 16 * sd + (run < navail ? run : navail - 1);
-        const float tsrc = __shfl_sync(kFull, t, src);
-        if (!done) {
-          n_probe += tested;
-          n_eval += __popc(pbits & low_mask(tested));
-          nan_seen = nan_seen || (nbits & low_mask(tested));
-          if (run < navail) {
-            if (sd == 0) { lft = tsrc; nl += run; ldone = true; }
-            else { rgt = tsrc; nr += run; rdone = true; }
-          } else {
-            const float nxt = sd == 0 ? tsrc - w : tsrc + w;
-            if (sd == 0) { lft = nxt; nl += navail; ldone = nl >= cap; }
-            else { rgt = nxt; nr += navail; rdone = nr >= cap; }
-          }
-        }
+        n_probe += tested;
+        n_eval += __popc((bpass >> (16 * sd)) & low_mask(tested));
+        nan_seen = nan_seen || (((bnan >> (16 * sd)) & low_mask(tested)) != 0);
+        const int add = run < navail ? run : navail;
+        if (sd == 0) { nl += add; ldone = run < navail || nl >= cap; }
+        else { nr += add; rdone = run < navail || nr >= cap; }
       }
     }
+    float lft = fmaf(-static_cast<float>(nl), w, l0);
+    float rgt = fmaf(static_cast<float>(nr), w, r0);
 
-    // ---- shrinkage: 16 proposals of the all-rejected path per round ----
+    // ---- shrinkage: kShrink proposals of the all-rejected path per round ----
     int ns = 0;
     bool accepted = false;
     float t_acc = 0.f, e_acc = 0.f, lp_acc = 0.f;
-    for (int base = 0; base < maxs && !accepted; base += kRound) {
-      const int q = h + 2 + base + m;
-      const uint4 ub = philox_block(r, it, s, kPhaseHrss, j, static_cast<uint32_t>(q >> 2));
-      const float u = u01(word(ub, q & 3));
+    for (int base = 0; base < maxs && !accepted; base += kShrink) {
+      if (base > 0) {  // rare: next uniforms h+2+base.. (one more Philox pass)
+        const int q0 = h + 2 + base;
+        uint4 b2 = make_uint4(0, 0, 0, 0);
+        if (lane < ((kShrink + 3) >> 2) + 1) b2 = philox_block(r, it, s, kPhaseHrss, j, (q0 >> 2) + lane);
+#pragma unroll
+        for (int i = 0; i < kShrink; ++i) {
+          const int q = q0 + i;
+          us[i] = u01(__shfl_sync(kFull, word(b2, q & 3), (q >> 2) - (q0 >> 2)));
+        }
+      }
       float mine = 0.f, l2 = lft, r2 = rgt;
 #pragma unroll
-      for (int i = 0; i < kRound; ++i) {
-        const float ui = __shfl_sync(kFull, u, i);
-        const float ti = fmaf(ui, r2 - l2, l2);
+      for (int i = 0; i < kShrink; ++i) {
+        const float ti = fmaf(us[i], r2 - l2, l2);
         if (lane == i) mine = ti;
         if (ti < 0.f) l2 = ti; else r2 = ti;  // R-13
       }
-      const int navail = min(kRound, maxs - base);
+      const int navail = min(kShrink, maxs - base);
       const bool act = lane < navail;
       LaneProbe o{false, false, false, 0.f, 0.f};
-      if (act) o = lane_probe<D, KIND>(mine, x, v, pr, sPr, en, es, d, log_y, e_star);
+      if (act) o = lane_probe<D, KIND, K>(mine, x, v, box, pa, pb, log_norm, P, en, sA, sB, sC, ldD, d, log_y, e_star);
       const unsigned bok = __ballot_sync(kFull, act && o.ok);
       const unsigned bpass = __ballot_sync(kFull, act && o.pass);
       const unsigned bnan = __ballot_sync(kFull, act && o.nan);
@@ -321,7 +382,7 @@ __global__ void __launch_bounds__(256) k_hrss_lane(RunDev r, PriorDev pr, Energy
       const float ll = __shfl_sync(kFull, o.lp, src);
       n_probe += tested;
       n_eval += __popc(bpass & low_mask(tested));
-      nan_seen = nan_seen || (bnan & low_mask(tested));
+      nan_seen = nan_seen || ((bnan & low_mask(tested)) != 0);
       ns += tested;
       if (first >= 0) {
         accepted = true;
@@ -349,13 +410,11 @@ __global__ void __launch_bounds__(256) k_hrss_lane(RunDev r, PriorDev pr, Energy
   }
 
   // ---- replace ----
-  if (lane < d) {
-    float xv = 0.f;
+  float xv = 0.f;
 #pragma unroll
-    for (int i = 0; i < D; ++i)
-      if (i == lane) xv = x[i];
-    r.X[static_cast<long long>(s) * r.dp + lane] = xv;
-  }
+  for (int i = 0; i < D; ++i)
+    if (i == lane) xv = x[i];
+  if (lane < d) r.X[static_cast<long long>(s) * r.dp + lane] = xv;
   if (lane == 0) {
     r.E[s] = e;
     r.birth[s] = e_star;
@@ -368,46 +427,63 @@ __global__ void __launch_bounds__(256) k_hrss_lane(RunDev r, PriorDev pr, Energy
   }
 }
 
-template <int D, int KIND>
+template <int D, int KIND, int K>
 void launch_lane_t(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc) {
-  const int ldl = odd_stride(r.d);
+  constexpr int ldD = D | 1;
   int wpb = r.k / (148 * 4);
   wpb = wpb < 1 ? 1 : (wpb > 8 ? 8 : wpb);
-  const size_t smem = (static_cast<size_t>(r.d) * ldl + 2 * r.d + energy_param_floats(KIND, r.d, en.n_comp)) *
-                      sizeof(float);
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && attr < smem) {
-    cudaFuncSetAttribute(k_hrss_lane<D, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    attr = smem;
-  }
+  size_t floats = 1;
+  if (KIND == NSS_E_MOG) floats += 2 * kMaxComp * D + kMaxComp;
+  if (KIND == NSS_E_CORR_GAUSS) floats += D + static_cast<size_t>(D) * ldD;
+  const size_t smem = floats * sizeof(float);
   const int blocks = (r.k + wpb - 1) / wpb;
-  k_hrss_lane<D, KIND><<<blocks, wpb * 32, smem, lc.stream>>>(r, pr, en);
+  NSS_PIN_CARVEOUT((k_hrss_lane<D, KIND, K>));
+  k_hrss_lane<D, KIND, K><<<blocks, wpb * 32, smem, lc.stream>>>(r, pr, en);
   ++*lc.launch_counter;
+}
+
+template <int D, int KIND>
+void launch_lane_k(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc) {
+  if constexpr (KIND == NSS_E_MOG && D <= 16) {
+    switch (en.n_comp) {
+      case 1: launch_lane_t<D, KIND, 1>(r, pr, en, lc); return;
+      case 2: launch_lane_t<D, KIND, 2>(r, pr, en, lc); return;
+      case 3: launch_lane_t<D, KIND, 3>(r, pr, en, lc); return;
+      case 4: launch_lane_t<D, KIND, 4>(r, pr, en, lc); return;
+      default: break;
+    }
+  }
+  launch_lane_t<D, KIND, 0>(r, pr, en, lc);
 }
 
 template <int KIND>
 void launch_lane_kind(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc) {
   const int d = r.d;
-  if (d <= 2) launch_lane_t<2, KIND>(r, pr, en, lc);
-  else if (d <= 4) launch_lane_t<4, KIND>(r, pr, en, lc);
-  else if (d <= 8) launch_lane_t<8, KIND>(r, pr, en, lc);
-  else if (d <= 10) launch_lane_t<10, KIND>(r, pr, en, lc);
-  else if (d <= 12) launch_lane_t<12, KIND>(r, pr, en, lc);
-  else if (d <= 16) launch_lane_t<16, KIND>(r, pr, en, lc);
-  else if (d <= 24) launch_lane_t<24, KIND>(r, pr, en, lc);
-  else launch_lane_t<32, KIND>(r, pr, en, lc);
+  if constexpr (KIND == NSS_E_CORR_GAUSS) {
+    if (d <= 4) launch_lane_k<4, KIND>(r, pr, en, lc);
+    else if (d <= 8) launch_lane_k<8, KIND>(r, pr, en, lc);
+    else launch_lane_k<12, KIND>(r, pr, en, lc);
+  } else {
+    if (d <= 2) launch_lane_k<2, KIND>(r, pr, en, lc);
+    else if (d <= 4) launch_lane_k<4, KIND>(r, pr, en, lc);
+    else if (d <= 8) launch_lane_k<8, KIND>(r, pr, en, lc);
+    else if (d <= 10) launch_lane_k<10, KIND>(r, pr, en, lc);
+    else if (d <= 12) launch_lane_k<12, KIND>(r, pr, en, lc);
+    else if (d <= 16) launch_lane_k<16, KIND>(r, pr, en, lc);
+    else if (d <= 24) launch_lane_k<24, KIND>(r, pr, en, lc);
+    else launch_lane_k<32, KIND>(r, pr, en, lc);
+  }
 }
 
 }  // namespace
 
-// Whether the one-probe-per-lane engine applies: d <= 32, a thread-local
-// energy of at most a few hundred flops, step-out cap <= 16 per round handled
-// by the round loop (any cap works).
+// Whether the one-probe-per-lane engine applies: d <= 32 and a thread-local
+// energy of at most a few hundred flops.
 bool lane_engine_ok(const RunDev &r, const EnergyDev &en) {
   if (r.d > 32) return false;
   switch (en.kind) {
     case NSS_E_FLAT: case NSS_E_GAUSS: case NSS_E_FUNNEL: return true;
-    case NSS_E_MOG: return en.n_comp * r.d <= 256;
+    case NSS_E_MOG: return en.n_comp <= kMaxComp && en.n_comp * r.d <= 256;
     case NSS_E_CORR_GAUSS: return r.d <= 12;
     default: return false;
   }

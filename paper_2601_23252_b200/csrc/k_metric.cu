@@ -1,192 +1,240 @@
 // A5 metric: live-set covariance (1/(n-1)) + ridge reg*mean(diag) (P:326-332,
 // R-8), Cholesky in fp64, fallback to the diagonal, and the slice width rule
-// (R-7).  At the end of an iteration the same finishing kernel
-// evaluates the termination criterion (A9, R-19) and advances the iteration
-// counter.
+// (R-7).  At the end of an iteration the same kernel evaluates the
+// termination criterion (A9, R-19) and advances the iteration counter.
 //
-// Two kernels: k_cov_partial (B CTAs over fixed gid chunks, shifted fp64 sums,
-// no atomics) and k_cov_final (one CTA: fixed-order sum of the B partials, then
-// Cholesky).  The reduction order is fixed, so the metric is bit-reproducible.
+// One launch: B CTAs accumulate shifted fp64 sums over fixed gid chunks and
+// write them to `partials`; the last CTA to finish (atomic ticket) sums the B
+// partials in block order -- so the result does not depend on which CTA is
+// last and the metric is bit-reproducible -- and factorises.  The Cholesky is
+// row-owner, one barrier per column: thread i owns row i, every thread reads
+// the pivot directly, the column is written to L (never re-read from A), so the
+// trailing update needs no second barrier.  For d <= 32 it runs in one warp
+// with __syncwarp.
 #include "nss_internal.cuh"
 
 namespace nss {
 
 namespace {
 
-constexpr int kPartialThreads = 256;
-constexpr int kTileRows = 32;
+constexpr int kThreads = 256;
 constexpr double kKappaInf = 1.3035;
 constexpr double kPi = 3.14159265358979323846;
 
-__global__ void __launch_bounds__(kPartialThreads) k_cov_partial(RunDev r, double *partials, int end_of_iter) {
+__global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials, unsigned *ticket, int nblk,
+                                                     double reg, int width_rule, double width_param,
+                                                     int end_of_iter) {
   DevState *st = r.st;
   if (st->error) return;
   if (end_of_iter && (st->terminated || st->finalised)) return;
   extern __shared__ double sm[];
-  const int d = r.d, n = r.n;
+  const int d = r.d, n = r.n, tid = threadIdx.x;
   const int npair = d * (d + 1) / 2;
   const int nent = npair + d;
-  double *S = sm;                                             // nent accumulators
-  double *tile = S + nent;                                    // kTileRows * d centred rows
-  double *shift = tile + kTileRows * d;
+  double *S = sm;                         // nent accumulators
+  double *shift = S + nent;               // d
   unsigned char *pi = reinterpret_cast<unsigned char *>(shift + d);
   unsigned char *pj = pi + npair;
-  __shared__ float red_min[kPartialThreads / 32];
+  // this CTA's rows as stored (fp32, row stride dp), after the pair tables
+  float *raw = reinterpret_cast<float *>(sm + nent + d + (2 * npair + 7) / 8);
+  __shared__ float red_min[kThreads / 32];
+  __shared__ int sh_last;
 
-  for (int e = threadIdx.x; e < nent; e += blockDim.x) S[e] = 0.0;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) shift[i] = static_cast<double>(r.X[i]);  // row 0
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    int base = i * (i + 1) / 2;
-    for (int j = 0; j <= i; ++j) {
-      pi[base + j] = static_cast<unsigned char>(i);
-      pj[base + j] = static_cast<unsigned char>(j);
-    }
-  }
-  const int chunk = (n + gridDim.x - 1) / gridDim.x;
+  if (tid == 0 && blockIdx.x == 0) st->stamp[8] = global_ns();
+  // ---------------- phase 1: partial shifted sums of this CTA's rows ----------------
+  const int chunk = (n + nblk - 1) / nblk;
   const int g0 = min(n, static_cast<int>(blockIdx.x) * chunk), g1 = min(n, g0 + chunk);
-  float emin = INFINITY;
-  for (int g = g0 + threadIdx.x; g < g1; g += blockDim.x) emin = fminf(emin, r.E[g]);
-  __syncthreads();
-  for (int t0 = g0; t0 < g1; t0 += kTileRows) {
-    const int rows = min(kTileRows, g1 - t0);
-    for (int e = threadIdx.x; e < rows * d; e += blockDim.x) {
-      int rr = e / d, i = e - rr * d;
-      tile[e] = static_cast<double>(r.X[static_cast<long long>(t0 + rr) * r.dp + i]) - shift[i];
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < nent; e += blockDim.x) {
-      double acc = 0.0;
-      if (e < npair) {
-        const int i = pi[e], j = pj[e];
-        for (int rr = 0; rr < rows; ++rr)
-          acc += tile[rr * d + i] * tile[rr * d + j];
-      } else {
-        const int i = e - npair;
-        for (int rr = 0; rr < rows; ++rr) acc += tile[rr * d + i];
-      }
-      S[e] += acc;
-    }
-    __syncthreads();
+  const int rows = g1 - g0;
+  const int dp = r.dp;
+  // one batch of loads: the chunk is contiguous in X
+  {
+    const float *src = r.X + static_cast<long long>(g0) * dp;
+    for (int q = tid; q < rows * dp; q += blockDim.x) raw[q] = src[q];
   }
+  float emin = INFINITY;
+  for (int g = g0 + tid; g < g1; g += blockDim.x) emin = fminf(emin, r.E[g]);
+  for (int e = tid; e < nent; e += blockDim.x) S[e] = 0.0;
+  for (int i = tid; i < d; i += blockDim.x) shift[i] = static_cast<double>(r.X[i]);  // row 0
+  for (int i = tid; i < d; i += blockDim.x) {
+    const int b0 = i * (i + 1) / 2;
+    for (int j = 0; j <= i; ++j) {
+      pi[b0 + j] = static_cast<unsigned char>(i);
+      pj[b0 + j] = static_cast<unsigned char>(j);
+    }
+  }
+  __syncthreads();
+  if (tid == 0 && blockIdx.x == 0) st->stamp[9] = global_ns();
+  for (int e = tid; e < nent; e += blockDim.x) {
+    // four independent accumulators (fixed assignment: row mod 4) break the
+    // DFMA dependency chain
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    if (e < npair) {
+      const int i = pi[e], j = pj[e];
+      const double si = shift[i], sj = shift[j];
+      int rr = 0;
+      for (; rr + 3 < rows; rr += 4) {
+        a0 = fma(static_cast<double>(raw[rr * dp + i]) - si, static_cast<double>(raw[rr * dp + j]) - sj, a0);
+        a1 = fma(static_cast<double>(raw[(rr + 1) * dp + i]) - si, static_cast<double>(raw[(rr + 1) * dp + j]) - sj, a1);
+        a2 = fma(static_cast<double>(raw[(rr + 2) * dp + i]) - si, static_cast<double>(raw[(rr + 2) * dp + j]) - sj, a2);
+        a3 = fma(static_cast<double>(raw[(rr + 3) * dp + i]) - si, static_cast<double>(raw[(rr + 3) * dp + j]) - sj, a3);
+      }
+      for (; rr < rows; ++rr)
+        a0 = fma(static_cast<double>(raw[rr * dp + i]) - si, static_cast<double>(raw[rr * dp + j]) - sj, a0);
+    } else {
+      const int i = e - npair;
+      const double si = shift[i];
+      int rr = 0;
+      for (; rr + 3 < rows; rr += 4) {
+        a0 += static_cast<double>(raw[rr * dp + i]) - si;
+        a1 += static_cast<double>(raw[(rr + 1) * dp + i]) - si;
+        a2 += static_cast<double>(raw[(rr + 2) * dp + i]) - si;
+        a3 += static_cast<double>(raw[(rr + 3) * dp + i]) - si;
+      }
+      for (; rr < rows; ++rr) a0 += static_cast<double>(raw[rr * dp + i]) - si;
+    }
+    S[e] = (a0 + a1) + (a2 + a3);
+  }
+  __syncthreads();
   double *out = partials + static_cast<long long>(blockIdx.x) * (nent + 1);
-  for (int e = threadIdx.x; e < nent; e += blockDim.x) out[e] = S[e];
+  for (int e = tid; e < nent; e += blockDim.x) out[e] = S[e];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) emin = fminf(emin, __shfl_xor_sync(0xffffffffu, emin, o));
-  if ((threadIdx.x & 31) == 0) red_min[threadIdx.x >> 5] = emin;
+  if ((tid & 31) == 0) red_min[tid >> 5] = emin;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    float m = red_min[0];
-    for (int w = 1; w < kPartialThreads / 32; ++w) m = fminf(m, red_min[w]);
-    out[nent] = static_cast<double>(m);
+  if (tid == 0) {
+    float mn = red_min[0];
+    for (int w = 1; w < kThreads / 32; ++w) mn = fminf(mn, red_min[w]);
+    out[nent] = static_cast<double>(mn);
+    __threadfence();
+    sh_last = atomicAdd(ticket, 1u) == static_cast<unsigned>(nblk - 1);
   }
-}
-
-__global__ void __launch_bounds__(1024) k_cov_final(RunDev r, const double *partials, int nblk, double reg,
-                                                    int width_rule, double width_param, int end_of_iter) {
-  DevState *st = r.st;
-  __shared__ int sh_flag;
-  if (threadIdx.x == 0) sh_flag = (st->error || (end_of_iter && (st->terminated || st->finalised))) ? 1 : 0;
   __syncthreads();
-  if (sh_flag) return;
-  extern __shared__ double A[];  // d*d fp64 (symmetric fill, then Cholesky in the lower part)
-  const int d = r.d, n = r.n, tid = threadIdx.x;
-  const int npair = d * (d + 1) / 2, nent = npair + d;
-  double *S1 = A + d * d;        // d
+  if (!sh_last) return;
+  __threadfence();
+  if (tid == 0) st->stamp[10] = global_ns();
+
+  // ---------------- phase 2 (last CTA): reduce, regularise, factorise ----------------
+  const int ld = d | 1;       // odd stride: column walks are bank-conflict free
+  double *A = sm;            // d*ld (reuses phase-1 shared memory)
+  double *Lo = r.L64;        // d*d  output factor, written straight to global
+  double *S1 = A + d * ld;   // d
+  // lower-triangle pairs in column-major order: column j's trailing block
+  // {(i, l): j < l <= i} is a contiguous suffix starting at coff(j + 1)
+  unsigned char *ti = reinterpret_cast<unsigned char *>(S1 + d);
+  unsigned char *tl = ti + npair;
   __shared__ double sh_md;
+  __shared__ double sh_red[kThreads / 32];
   __shared__ int sh_fail;
-  __shared__ double sh_red[32];
-  // fixed-order sum over the partial blocks
-  for (int e = tid; e < nent; e += blockDim.x) {
-    double acc = 0.0;
-    for (int b = 0; b < nblk; ++b) acc += partials[static_cast<long long>(b) * (nent + 1) + e];
-    if (e < npair) {
-      int i = 0;
+  __shared__ float sh_emin;
+  for (int l = tid; l < d; l += blockDim.x) {
+    const int off = l * d - l * (l - 1) / 2;  // sum_{c<l} (d - c)
+    for (int i = l; i < d; ++i) {
+      ti[off + i - l] = static_cast<unsigned char>(i);
+      tl[off + i - l] = static_cast<unsigned char>(l);
+    }
+  }
+  for (int e = tid; e <= nent; e += blockDim.x) {
+    // fixed block order; loads issued 8 at a time (independent addresses);
+    // entry nent holds the per-block minimum energy
+    const bool is_min = e == nent;
+    double acc = is_min ? INFINITY : 0.0;
+    int b = 0;
+    for (; b + 7 < nblk; b += 8) {
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = partials[static_cast<long long>(b + q) * (nent + 1) + e];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc = is_min ? fmin(acc, v[q]) : acc + v[q];
+    }
+    for (; b < nblk; ++b) {
+      const double v = partials[static_cast<long long>(b) * (nent + 1) + e];
+      acc = is_min ? fmin(acc, v) : acc + v;
+    }
+    if (is_min) {
+      sh_emin = static_cast<float>(acc);
+    } else if (e < npair) {
+      int i = static_cast<int>((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+      while (i * (i + 1) / 2 > e) --i;
       while ((i + 1) * (i + 2) / 2 <= e) ++i;
-      int j = e - i * (i + 1) / 2;
-      A[i * d + j] = acc;   // S2_ij (shifted)
+      A[i * ld + (e - i * (i + 1) / 2)] = acc;  // S2_ij (shifted), i >= j
     } else {
-      S1[e - npair] = acc;  // S1_i  (shifted)
+      S1[e - npair] = acc;                      // S1_i  (shifted)
     }
   }
   __syncthreads();
+  if (tid == 0) st->stamp[11] = global_ns();
   const double nn = static_cast<double>(n);
   for (int e = tid; e < d * d; e += blockDim.x) {
-    int i = e / d, j = e - i * d;
-    if (j <= i) A[e] = (A[e] - S1[i] * S1[j] / nn) / (nn - 1.0);
+    const int i = e / d, j = e - i * d;
+    if (j <= i) A[i * ld + j] = (A[i * ld + j] - S1[i] * S1[j] / nn) / (nn - 1.0);
+    Lo[e] = 0.0;
   }
   __syncthreads();
-  for (int e = tid; e < d * d; e += blockDim.x) {
-    int i = e / d, j = e - i * d;
-    if (j > i) A[e] = A[j * d + i];
-  }
   if (tid == 0) {
     double md = 0.0;
-    for (int i = 0; i < d; ++i) md += A[i * d + i];
+    for (int i = 0; i < d; ++i) md += A[i * ld + i];
     sh_md = md / d;
     sh_fail = 0;
   }
   __syncthreads();
   for (int i = tid; i < d; i += blockDim.x) {
-    A[i * d + i] += reg * sh_md;
-    S1[i] = A[i * d + i];  // keep the regularised diagonal for the fallback
+    A[i * ld + i] += reg * sh_md;
+    S1[i] = A[i * ld + i];  // regularised diagonal, kept for the fallback
   }
   __syncthreads();
-  // right-looking Cholesky, lower triangle in place
-  for (int j = 0; j < d; ++j) {
-    if (tid == 0) {
-      double v = A[j * d + j];
-      if (!(v > 0.0) || !isfinite(v)) sh_fail = 1;
-      A[j * d + j] = sqrt(fmax(v, 0.0));
+  // right-looking Cholesky, one barrier per column: every thread reads the
+  // pivot, writes its share of column j of L and of the trailing update
+  // A_il -= A_ij A_lj / A_jj (column j itself is never rewritten)
+  const bool one_warp = d <= 32;
+  const int nthr = one_warp ? 32 : static_cast<int>(blockDim.x);
+  if (tid < nthr) {
+    for (int j = 0; j < d; ++j) {
+      const double ajj = A[j * ld + j];
+      if (!(ajj > 0.0) || !isfinite(ajj)) {
+        if (tid == 0) sh_fail = 1;
+        break;  // uniform: every thread read the same value
+      }
+      const double ipiv = rsqrt(ajj), inv = 1.0 / ajj;
+      for (int i = j + tid; i < d; i += nthr) Lo[i * d + j] = (i == j) ? ajj * ipiv : A[i * ld + j] * ipiv;
+      const int off = (j + 1) * d - (j + 1) * j / 2;
+      for (int q = off + tid; q < npair; q += nthr) {
+        const int i = ti[q], l = tl[q];
+        A[i * ld + l] -= A[i * ld + j] * A[l * ld + j] * inv;
+      }
+      if (one_warp) __syncwarp(); else __syncthreads();
     }
-    __syncthreads();
-    if (sh_fail) break;
-    const double piv = A[j * d + j];
-    for (int i = j + 1 + tid; i < d; i += blockDim.x) A[i * d + j] /= piv;
-    __syncthreads();
-    const int m = d - j - 1;
-    for (int e = tid; e < m * m; e += blockDim.x) {
-      int i = j + 1 + e / m, l = j + 1 + e % m;
-      if (l <= i) A[i * d + l] -= A[i * d + j] * A[l * d + j];
-    }
-    __syncthreads();
   }
+  __syncthreads();
   if (sh_fail) {  // R-8 fallback: diag(sqrt(Sigma_jj)), 1 where the variance is 0
     for (int e = tid; e < d * d; e += blockDim.x) {
-      int i = e / d, j = e - i * d;
-      A[e] = (i == j) ? (S1[i] > 0.0 ? sqrt(S1[i]) : 1.0) : 0.0;
+      const int i = e / d, j = e - i * d;
+      Lo[e] = (i == j) ? (S1[i] > 0.0 ? sqrt(S1[i]) : 1.0) : 0.0;
     }
     __syncthreads();
   }
-  for (int e = tid; e < d * d; e += blockDim.x) {
-    int i = e / d, j = e - i * d;
-    double v = (j <= i) ? A[e] : 0.0;
-    r.L64[e] = v;
-  }
+  __syncthreads();
   for (int e = tid; e < d * r.dp; e += blockDim.x) {
-    int i = e / r.dp, j = e - i * r.dp;
-    r.L[e] = (j < d && j <= i) ? static_cast<float>(A[i * d + j]) : 0.0f;
+    const int i = e / r.dp, j = e - i * r.dp;
+    r.L[e] = j < d ? static_cast<float>(Lo[i * d + j]) : 0.0f;
   }
+  if (tid == 0) st->stamp[12] = global_ns();
   // slice width (R-7)
   double w;
   if (width_rule == NSS_W_FIXED) {
     w = width_param;
   } else if (r.dir_norm == NSS_DIR_MAHALANOBIS) {
-    double mu = 1.0 / (d + 2.0);
+    const double mu = 1.0 / (d + 2.0);
     w = width_param * 4.0 * kKappaInf * sqrt(2.0 / (kPi * mu * d));
   } else {
     // tr(Sigma^-1) = |L^-1|_F^2: one thread per column of L^-1 (forward substitution)
-    __syncthreads();
     double part = 0.0;
     for (int c = tid; c < d; c += blockDim.x) {
-      // solve L y = e_c, only entries i >= c are non-zero
-      // y_i = (delta_ic - sum_{t<i} L_it y_t) / L_ii ; keep y in registers via a small loop
-      // (d <= 128: store y in local memory)
       double y[kMaxDim];
       for (int i = 0; i < d; ++i) {
         if (i < c) { y[i] = 0.0; continue; }
         double s = (i == c) ? 1.0 : 0.0;
-        for (int t = c; t < i; ++t) s -= A[i * d + t] * y[t];
-        y[i] = s / A[i * d + i];
+        for (int t = c; t < i; ++t) s -= Lo[i * d + t] * y[t];
+        y[i] = s / Lo[i * d + i];
         part += y[i] * y[i];
       }
     }
@@ -195,21 +243,22 @@ __global__ void __launch_bounds__(1024) k_cov_final(RunDev r, const double *part
     if ((tid & 31) == 0) sh_red[tid >> 5] = part;
     __syncthreads();
     double tr = 0.0;
-    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) tr += sh_red[i];
-    double mu = tr / (static_cast<double>(d) * (d + 2.0));
+    for (int i = 0; i < kThreads / 32; ++i) tr += sh_red[i];
+    const double mu = tr / (static_cast<double>(d) * (d + 2.0));
     w = width_param * 4.0 * kKappaInf * sqrt(2.0 / (kPi * mu * d));
   }
   if (tid == 0) {
+    *ticket = 0u;  // re-arm for the next launch
+    st->stamp[13] = global_ns();
     st->width = static_cast<float>(w);
     if (end_of_iter) {
-      float emin = INFINITY;
-      for (int b = 0; b < nblk; ++b) emin = fminf(emin, static_cast<float>(partials[static_cast<long long>(b) * (nent + 1) + nent]));
-      st->emin = emin;
+      const float emin2 = sh_emin;
+      st->emin = emin2;
       // A9 / R-19: stop when the live bound is below e^{term} of the total
-      double lz_live = -static_cast<double>(emin) + r.lx_cur[0];
-      double lz0 = r.lz[0];
-      double mm = fmax(lz0, lz_live);
-      double tot = (mm == -INFINITY) ? -INFINITY : mm + log(exp(lz0 - mm) + exp(lz_live - mm));
+      const double lz_live = -static_cast<double>(emin2) + r.lx_cur[0];
+      const double lz0 = r.lz[0];
+      const double mm = fmax(lz0, lz_live);
+      const double tot = (mm == -INFINITY) ? -INFINITY : mm + log(exp(lz0 - mm) + exp(lz_live - mm));
       st->log_z_live = lz_live;
       if (st->n_dead > 0 && (lz_live - tot) < static_cast<double>(r.term_log_ratio)) st->terminated = 1;
       st->iter += 1;
@@ -217,36 +266,39 @@ __global__ void __launch_bounds__(1024) k_cov_final(RunDev r, const double *part
   }
 }
 
+size_t metric_smem(int n, int d, int nblk) {
+  const int npair = d * (d + 1) / 2, nent = npair + d;
+  const int dp = (d + 3) & ~3;
+  const int rows = (n + nblk - 1) / nblk;
+  const size_t p1 = static_cast<size_t>(nent + d) * 8 + ((2 * static_cast<size_t>(npair) + 7) / 8) * 8 +
+                    static_cast<size_t>(rows) * dp * 4 + 64;
+  const size_t p2 = (static_cast<size_t>(d) * (d | 1) + d) * 8 + 2 * static_cast<size_t>(npair) + 16;
+  return p1 > p2 ? p1 : p2;
+}
+
 }  // namespace
 
 int metric_blocks(int n, int d) {
-  int npair = d * (d + 1) / 2;
-  // enough rows per block to amortise the per-block partial write
+  const int npair = d * (d + 1) / 2;
+  const int dp = (d + 3) & ~3;
   int rows_per_block = npair > 1000 ? 160 : 128;
-  int b = (n + rows_per_block - 1) / rows_per_block;
-  return b < 1 ? 1 : (b > 148 ? 148 : b);
-}
-
-static size_t partial_smem(int d) {
-  int npair = d * (d + 1) / 2, nent = npair + d;
-  size_t s = static_cast<size_t>(nent + kTileRows * d + d) * 8 + 2 * static_cast<size_t>(npair) + 16;
-  return s;
+  const int rows_max = 96 * 1024 / (dp * 4);  // the CTA's rows stay in shared memory
+  if (rows_per_block > rows_max) rows_per_block = rows_max;
+  const int b = (n + rows_per_block - 1) / rows_per_block;
+  return b < 1 ? 1 : b;
 }
 
 void launch_metric(const RunDev &r, double metric_reg, int width_rule, double width_param, int end_of_iteration,
-                   double *partials, int n_blocks, const LaunchCtx &lc) {
-  size_t s1 = partial_smem(r.d);
-  size_t s2 = static_cast<size_t>(r.d) * r.d * 8 + static_cast<size_t>(r.d) * 8 * 2 + 64;
+                   double *partials, unsigned *ticket, int n_blocks, const LaunchCtx &lc) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_cov_partial, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_cov_final, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_metric, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  k_cov_partial<<<n_blocks, kPartialThreads, s1, lc.stream>>>(r, partials, end_of_iteration);
-  k_cov_final<<<1, 1024, s2, lc.stream>>>(r, partials, n_blocks, metric_reg, width_rule, width_param,
-                                          end_of_iteration);
-  *lc.launch_counter += 2;
+  NSS_PIN_CARVEOUT(k_metric);
+  k_metric<<<n_blocks, kThreads, metric_smem(r.n, r.d, n_blocks), lc.stream>>>(r, partials, ticket, n_blocks, metric_reg,
+                                                                 width_rule, width_param, end_of_iteration);
+  ++*lc.launch_counter;
 }
 
 }  // namespace nss

@@ -131,6 +131,7 @@ __global__ void __launch_bounds__(1024) k_normalise(long long N, double *logw) {
 }  // namespace
 
 void launch_evidence_summary(const RunDev &r, double *out, const LaunchCtx &lc) {
+  NSS_PIN_CARVEOUT(k_evidence_summary);
   k_evidence_summary<<<1, 128, 0, lc.stream>>>(r, out);
   ++*lc.launch_counter;
 }

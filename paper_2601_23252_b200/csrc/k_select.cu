@@ -1,28 +1,34 @@
 // A2 delete + A3 record dead + A4 resample for one outer iteration, and the
-// finalisation sort (R-18).  One CTA of 1024 threads: at n <= 2e4 the keys fit
-// in L1/L2 and the select is latency-bound, so one SM doing a radix select is
-// cheaper than a multi-CTA scheme plus a grid barrier.
+// finalisation sort (R-18).  One CTA: at n <= 2e4 the whole key set fits in
+// one SM's shared memory and the select is latency-bound, so one SM doing a
+// radix select beats a multi-CTA scheme plus a grid barrier.
 //
 // Keys: key = (ord(E) << 32) | gid -- unique, so "the k largest keys" is the
 // set of the k worst energies with ties broken towards the larger gid (R-1).
+// The radix passes start at the highest bit where the keys differ (a min/max
+// reduction first), so a live set whose energies share exponent and leading
+// mantissa bits needs only 2-3 passes of 8 bits.
 #include "nss_internal.cuh"
 
 namespace nss {
 
 namespace {
 
-constexpr int kThreads = 1024;
-constexpr int kSmemSortMax = 16384;  // keys sorted in shared memory (128 KB)
+constexpr int kThreads = 512;
+constexpr int kWarps = kThreads / 32;
+constexpr int kSmemKeysMax = 12288;   // keys cached in shared memory (96 KB)
+constexpr int kSmemSortMax = 8192;    // selected keys sorted in shared memory (64 KB)
+constexpr int kRankSortMax = 1024;    // rank sort (k^2/T compares) up to this k
 
 // Descending bitonic sort of P (power of two) keys at `buf` (shared or global).
 __device__ void bitonic_desc(unsigned long long *buf, int P) {
   for (int size = 2; size <= P; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       for (int i = threadIdx.x; i < (P >> 1); i += blockDim.x) {
-        int lo = 2 * stride * (i / stride) + (i % stride);
-        int hi = lo + stride;
-        bool desc = (lo & size) == 0;
-        unsigned long long a = buf[lo], b = buf[hi];
+        const int lo = 2 * stride * (i / stride) + (i % stride);
+        const int hi = lo + stride;
+        const bool desc = (lo & size) == 0;
+        const unsigned long long a = buf[lo], b = buf[hi];
         if (desc ? (a < b) : (a > b)) {
           buf[lo] = b;
           buf[hi] = a;
@@ -33,38 +39,51 @@ __device__ void bitonic_desc(unsigned long long *buf, int P) {
   }
 }
 
-// Block-wide exclusive scan of one int per thread (blockDim.x == 1024).
-__device__ int block_exclusive_scan(int v, int *warp_tot, int *total) {
+// Block-wide exclusive scan of one int per thread.
+__device__ int block_exclusive_scan(int v, int *warp_tot) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int incl = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    int t = __shfl_up_sync(0xffffffffu, incl, o);
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += t;
   }
   if (lane == 31) warp_tot[wid] = incl;
   __syncthreads();
-  if (wid == 0) {
-    int t = warp_tot[lane];
-    int s = t;
+  int off = 0;
+  for (int w = 0; w < wid; ++w) off += warp_tot[w];
+  __syncthreads();
+  return off + incl - v;
+}
+
+__device__ void block_minmax(unsigned long long &mn, unsigned long long &mx, unsigned long long *red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int u = __shfl_up_sync(0xffffffffu, s, o);
-      if (lane >= o) s += u;
-    }
-    warp_tot[lane] = s - t;  // exclusive warp offsets
-    if (lane == 31) *total = s;
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
+    mn = a < mn ? a : mn;
+    mx = b > mx ? b : mx;
+  }
+  if (lane == 0) {
+    red[wid] = mn;
+    red[kWarps + wid] = mx;
   }
   __syncthreads();
-  return warp_tot[wid] + incl - v;
+  mn = red[0];
+  mx = red[kWarps];
+  for (int w = 1; w < kWarps; ++w) {
+    mn = red[w] < mn ? red[w] : mn;
+    mx = red[kWarps + w] > mx ? red[kWarps + w] : mx;
+  }
+  __syncthreads();
 }
 
 // Writes the dead records (R-14 birth, P:1197-1201 n_live) and copies rows.
 __device__ void write_dead(const RunDev &r, const unsigned long long *sorted, int cnt, int n_for_nlive,
                            long long nd, int it) {
   for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
-    int g = static_cast<int>(sorted[j] & 0xffffffffu);
-    long long q = nd + j;
+    const int g = static_cast<int>(sorted[j] & 0xffffffffu);
+    const long long q = nd + j;
     r.dE[q] = r.E[g];
     r.dbirth[q] = r.birth[g];
     r.dnlive[q] = n_for_nlive - j;
@@ -72,43 +91,93 @@ __device__ void write_dead(const RunDev &r, const unsigned long long *sorted, in
     r.dord[q] = j;
     r.diter[q] = it;
   }
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int j = wid; j < cnt; j += nw) {
-    int g = static_cast<int>(sorted[j] & 0xffffffffu);
-    const float *src = r.X + static_cast<long long>(g) * r.dp;
-    float *dst = r.dX + (nd + j) * r.dp;
-    for (int i = lane; i < r.dp; i += 32) dst[i] = src[i];
+  // rows: one thread per float, consecutive threads on consecutive columns
+  const long long tot = static_cast<long long>(cnt) * r.dp;
+  for (long long e = threadIdx.x; e < tot; e += blockDim.x) {
+    const int j = static_cast<int>(e / r.dp), i = static_cast<int>(e - static_cast<long long>(j) * r.dp);
+    const int g = static_cast<int>(sorted[j] & 0xffffffffu);
+    r.dX[(nd + j) * r.dp + i] = r.X[static_cast<long long>(g) * r.dp + i];
   }
 }
 
-__global__ void __launch_bounds__(kThreads) k_select(RunDev r, unsigned long long *gscratch) {
-  extern __shared__ unsigned long long sbuf[];
+// Sort `cnt` distinct keys descending into out[] (shared or global).
+__device__ void sort_desc(const unsigned long long *in, int cnt, unsigned long long *out,
+                          unsigned long long *gscratch, unsigned long long *sbuf) {
+  if (cnt <= kRankSortMax) {
+    // rank sort: position = number of larger keys (keys are unique); the keys
+    // are staged in shared memory and read as broadcasts
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) sbuf[i] = in[i];
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+      const unsigned long long ki = sbuf[i];
+      int rank = 0;
+      for (int j = 0; j < cnt; ++j) rank += sbuf[j] > ki;
+      out[rank] = ki;
+    }
+    __syncthreads();
+    return;
+  }
+  int P = 1;
+  while (P < cnt) P <<= 1;
+  unsigned long long *buf = (P <= kSmemSortMax) ? sbuf : gscratch;
+  for (int i = threadIdx.x; i < P; i += blockDim.x) buf[i] = (i < cnt) ? in[i] : 0ull;
+  __syncthreads();
+  bitonic_desc(buf, P);
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) out[i] = buf[i];
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kThreads) k_select(RunDev r, unsigned long long *gscratch,
+                                                     unsigned long long *gsel) {
+  extern __shared__ unsigned long long sm[];
   __shared__ unsigned hist[256];
-  __shared__ int warp_tot[32];
-  __shared__ int sh_total, sh_flag;
+  __shared__ int warp_tot[kWarps];
+  __shared__ unsigned long long red[2 * kWarps];
+  __shared__ int sh_flag;
   __shared__ unsigned long long sh_prefix;
   __shared__ int sh_kk, sh_done;
   DevState *st = r.st;
   if (threadIdx.x == 0) sh_flag = (st->terminated || st->error || st->finalised) ? 1 : 0;
   __syncthreads();
   if (sh_flag) return;
-  const int n = r.n, k = r.k, tid = threadIdx.x;
+  const int n = r.n, k = r.k, tid = threadIdx.x, lane = tid & 31;
   const long long nd = st->n_dead;
   const int it = st->iter + 1;
   if (nd + k + n > r.max_dead) {  // R-26
     if (tid == 0) raise_error(st, NSS_ERR_CAPACITY);
     return;
   }
+  // ---- keys (cached in shared memory when they fit) ----
+  const bool cached = n <= kSmemKeysMax;
+  unsigned long long *keys = cached ? sm : gscratch;
+  unsigned long long *sbuf = cached ? sm + kSmemKeysMax : sm;  // sort buffer after the key cache
+  unsigned long long mn = ~0ull, mx = 0ull;
+  for (int g = tid; g < n; g += blockDim.x) {
+    const unsigned long long key = key_of(r.E[g], g);
+    keys[g] = key;
+    mn = key < mn ? key : mn;
+    mx = key > mx ? key : mx;
+  }
+  block_minmax(mn, mx, red);  // contains a barrier: keys[] is visible
+  // highest differing bit: all keys agree above it
+  const int hb = 63 - __clzll(mn ^ mx);
+  const unsigned long long common = hb >= 63 ? 0ull : (mn >> (hb + 1)) << (hb + 1);
 
-  // ---- radix select of the k-th largest key, 8 bits per pass, MSB first ----
-  unsigned long long prefix = 0, mask = 0;
+  // ---- radix select of the k-th largest key, 8 bits per pass from bit hb down ----
+  unsigned long long prefix = common, mask = hb >= 63 ? 0ull : ~((1ull << (hb + 1)) - 1ull);
   int kk = k;
-  for (int shift = 56; shift >= 0; shift -= 8) {
+  for (int top = hb; top >= 0; top -= 8) {
+    const int shift = top >= 7 ? top - 7 : 0;
+    const int width = top - shift + 1;
+    const unsigned dmask = (1u << width) - 1u;
     for (int i = tid; i < 256; i += blockDim.x) hist[i] = 0;
     __syncthreads();
     for (int g = tid; g < n; g += blockDim.x) {
-      unsigned long long key = key_of(r.E[g], g);
-      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+      const unsigned long long key = keys[g];
+      const bool m = (key & mask) == prefix;
+      const unsigned dig = m ? static_cast<unsigned>((key >> shift) & dmask) : 0xffffffffu;
+      const unsigned peers = __match_any_sync(__activemask(), dig);
+      if (m && lane == __ffs(peers) - 1) atomicAdd(&hist[dig], static_cast<unsigned>(__popc(peers)));
     }
     __syncthreads();
     if (tid < 32) {
@@ -122,19 +191,18 @@ __global__ void __launch_bounds__(kThreads) k_select(RunDev r, unsigned long lon
       unsigned incl = tot;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+        const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
         if (tid >= o) incl += t;
       }
-      unsigned excl = incl - tot;
-      bool mine = excl < static_cast<unsigned>(kk) && static_cast<unsigned>(kk) <= incl;
-      if (mine) {
+      const unsigned excl = incl - tot;
+      if (excl < static_cast<unsigned>(kk) && static_cast<unsigned>(kk) <= incl) {
         unsigned cum = excl;
         int j = 0;
         for (; j < 8; ++j) {
           if (cum + c[j] >= static_cast<unsigned>(kk)) break;
           cum += c[j];
         }
-        unsigned D = 255u - 8u * tid - j;
+        const unsigned D = 255u - 8u * tid - j;
         sh_kk = kk - static_cast<int>(cum);
         sh_prefix = prefix | (static_cast<unsigned long long>(D) << shift);
         sh_done = (c[j] == static_cast<unsigned>(kk) - cum) ? 1 : 0;
@@ -143,9 +211,8 @@ __global__ void __launch_bounds__(kThreads) k_select(RunDev r, unsigned long lon
     __syncthreads();
     kk = sh_kk;
     prefix = sh_prefix;
-    mask |= 0xFFull << shift;
+    mask |= static_cast<unsigned long long>(dmask) << shift;
     if (sh_done) break;
-    __syncthreads();
   }
   // selected  <=>  (key & mask) >= prefix
 
@@ -153,36 +220,37 @@ __global__ void __launch_bounds__(kThreads) k_select(RunDev r, unsigned long lon
   const int chunk = (n + blockDim.x - 1) / blockDim.x;
   const int g0 = min(n, tid * chunk), g1 = min(n, g0 + chunk);
   int nsel = 0;
-  for (int g = g0; g < g1; ++g) nsel += ((key_of(r.E[g], g) & mask) >= prefix) ? 1 : 0;
-  int off = block_exclusive_scan(nsel, warp_tot, &sh_total);
+  for (int g = g0; g < g1; ++g) nsel += ((keys[g] & mask) >= prefix) ? 1 : 0;
+  int off = block_exclusive_scan(nsel, warp_tot);
   int soff = g0 - off;
   for (int g = g0; g < g1; ++g) {
-    if ((key_of(r.E[g], g) & mask) >= prefix) r.dest_gid[off++] = g;
-    else r.surv[soff++] = g;
+    const unsigned long long key = keys[g];
+    if ((key & mask) >= prefix) {
+      r.dest_gid[off] = g;
+      gsel[off] = key;
+      ++off;
+    } else {
+      r.surv[soff++] = g;
+    }
   }
   __syncthreads();
 
   // ---- dead order: the k selected keys sorted descending ----
-  int P = 1;
-  while (P < k) P <<= 1;
-  unsigned long long *buf = (P <= kSmemSortMax) ? sbuf : gscratch;
-  for (int i = tid; i < P; i += blockDim.x)
-    buf[i] = (i < k) ? key_of(r.E[r.dest_gid[i]], r.dest_gid[i]) : 0ull;
-  __syncthreads();
-  bitonic_desc(buf, P);
-  for (int j = tid; j < k; j += blockDim.x) r.dead_gid[j] = static_cast<int>(buf[j] & 0xffffffffu);
-  const float e_star = r.E[static_cast<int>(buf[k - 1] & 0xffffffffu)];
+  unsigned long long *sorted = gsel + k;
+  sort_desc(gsel, k, sorted, gscratch + (cached ? 0 : n), sbuf);
+  for (int j = tid; j < k; j += blockDim.x) r.dead_gid[j] = static_cast<int>(sorted[j] & 0xffffffffu);
+  const float e_star = r.E[static_cast<int>(sorted[k - 1] & 0xffffffffu)];
 
   // ---- parents: S[floor(u32 (n-k) / 2^32)] (R-4) ----
   for (int c = tid; c < k; c += blockDim.x) {
-    int s = r.dest_gid[c];
-    uint4 b = philox_block(r, it, s, kPhaseResample, 0, 0);
-    unsigned long long rank = (static_cast<unsigned long long>(b.x) * static_cast<unsigned>(n - k)) >> 32;
+    const int s = r.dest_gid[c];
+    const uint4 b = philox_block(r, it, s, kPhaseResample, 0, 0);
+    const unsigned long long rank = (static_cast<unsigned long long>(b.x) * static_cast<unsigned>(n - k)) >> 32;
     r.parent_gid[c] = r.surv[rank];
   }
 
   // ---- dead records: n_live = n - j in key-descending order ----
-  write_dead(r, buf, k, n, nd, it);
+  write_dead(r, sorted, k, n, nd, it);
   __syncthreads();
   if (tid == 0) {
     st->dead_base = nd;
@@ -191,9 +259,193 @@ __global__ void __launch_bounds__(kThreads) k_select(RunDev r, unsigned long lon
   }
 }
 
+__device__ __forceinline__ float energy_of_key(unsigned long long key) {  // inverse of ord_f32
+  const uint32_t u = static_cast<uint32_t>(key >> 32);
+  return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+
+// Shared-memory-resident variant (the common case, n <= kSmemKeysMax): keys,
+// selected keys, the sorted dead order, survivors and destinations all stay on
+// chip, and E* and the dead energies are decoded from the keys, so the only
+// global traffic is the energy load, the row gather and the outputs.
+__global__ void __launch_bounds__(kThreads) k_select_smem(RunDev r) {
+  extern __shared__ unsigned long long sm[];
+  __shared__ unsigned hist[256];
+  __shared__ int warp_tot[kWarps];
+  __shared__ unsigned long long red[2 * kWarps];
+  __shared__ unsigned long long sh_prefix;
+  __shared__ int sh_kk, sh_done;
+  DevState *st = r.st;
+  const int n = r.n, k = r.k, tid = threadIdx.x, lane = tid & 31;
+  unsigned long long *keys = sm;              // n
+  unsigned long long *sel = keys + n;         // k (gid order)
+  unsigned long long *sorted = sel + k;       // k (descending)
+  int *surv = reinterpret_cast<int *>(sorted + k);  // n - k
+  int *dest = surv + (n - k);                        // k
+  if (tid == 0) st->stamp[0] = global_ns();
+  // independent global loads first, flags checked afterwards
+  unsigned long long mn = ~0ull, mx = 0ull;
+  for (int g = tid; g < n; g += blockDim.x) {
+    const unsigned long long key = key_of(r.E[g], g);
+    keys[g] = key;
+    mn = key < mn ? key : mn;
+    mx = key > mx ? key : mx;
+  }
+  const int flags = st->terminated | st->error | st->finalised;
+  const long long nd = st->n_dead;
+  const int it = st->iter + 1;
+  if (flags) return;  // uniform: written only by other kernels
+  if (tid == 0) st->stamp[1] = global_ns();
+  if (nd + k + n > r.max_dead) {  // R-26
+    if (tid == 0) raise_error(st, NSS_ERR_CAPACITY);
+    return;
+  }
+  block_minmax(mn, mx, red);
+  if (tid == 0) st->stamp[2] = global_ns();
+  const int hb = 63 - __clzll(mn ^ mx);
+  const unsigned long long common = hb >= 63 ? 0ull : (mn >> (hb + 1)) << (hb + 1);
+  unsigned long long prefix = common, mask = hb >= 63 ? 0ull : ~((1ull << (hb + 1)) - 1ull);
+  int kk = k;
+  for (int top = hb; top >= 0; top -= 8) {
+    const int shift = top >= 7 ? top - 7 : 0;
+    const unsigned dmask = (1u << (top - shift + 1)) - 1u;
+    for (int i = tid; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    for (int g = tid; g < n; g += blockDim.x) {
+      const unsigned long long key = keys[g];
+      const bool m = (key & mask) == prefix;
+      const unsigned dig = m ? static_cast<unsigned>((key >> shift) & dmask) : 0xffffffffu;
+      const unsigned peers = __match_any_sync(__activemask(), dig);
+      if (m && lane == __ffs(peers) - 1) atomicAdd(&hist[dig], static_cast<unsigned>(__popc(peers)));
+    }
+    __syncthreads();
+    if (tid < 32) {
+      unsigned c[8], tot = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        c[j] = hist[255 - 8 * tid - j];
+        tot += c[j];
+      }
+      unsigned incl = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (tid >= o) incl += t;
+      }
+      const unsigned excl = incl - tot;
+      if (excl < static_cast<unsigned>(kk) && static_cast<unsigned>(kk) <= incl) {
+        unsigned cum = excl;
+        int j = 0;
+        for (; j < 8; ++j) {
+          if (cum + c[j] >= static_cast<unsigned>(kk)) break;
+          cum += c[j];
+        }
+        sh_kk = kk - static_cast<int>(cum);
+        sh_prefix = prefix | (static_cast<unsigned long long>(255u - 8u * tid - j) << shift);
+        sh_done = (c[j] == static_cast<unsigned>(kk) - cum) ? 1 : 0;
+      }
+    }
+    __syncthreads();
+    kk = sh_kk;
+    prefix = sh_prefix;
+    mask |= static_cast<unsigned long long>(dmask) << shift;
+    if (sh_done) break;
+  }
+  if (tid == 0) st->stamp[3] = global_ns();
+  // compaction in ascending gid order (shared memory only)
+  const int chunk = (n + blockDim.x - 1) / blockDim.x;
+  const int g0 = min(n, tid * chunk), g1 = min(n, g0 + chunk);
+  int nsel = 0;
+  for (int g = g0; g < g1; ++g) nsel += ((keys[g] & mask) >= prefix) ? 1 : 0;
+  int off = block_exclusive_scan(nsel, warp_tot);
+  int soff = g0 - off;
+  for (int g = g0; g < g1; ++g) {
+    const unsigned long long key = keys[g];
+    if ((key & mask) >= prefix) {
+      dest[off] = g;
+      sel[off++] = key;
+    } else {
+      surv[soff++] = g;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) st->stamp[4] = global_ns();
+  // dead order: rank sort (k <= kRankSortMax) or bitonic in place
+  if (k <= kRankSortMax) {
+    for (int i = tid; i < k; i += blockDim.x) {
+      const unsigned long long ki = sel[i];
+      int rank = 0;
+      for (int j = 0; j < k; ++j) rank += sel[j] > ki;
+      sorted[rank] = ki;
+    }
+    __syncthreads();
+  } else {
+    int P = 1;
+    while (P < k) P <<= 1;
+    unsigned long long *buf = keys;  // keys are no longer needed: reuse (n >= P checked on host)
+    for (int i = tid; i < P; i += blockDim.x) buf[i] = i < k ? sel[i] : 0ull;
+    __syncthreads();
+    bitonic_desc(buf, P);
+    for (int i = tid; i < k; i += blockDim.x) sorted[i] = buf[i];
+    __syncthreads();
+  }
+  if (tid == 0) st->stamp[5] = global_ns();
+  // outputs: destinations, dead order, parents (R-4), dead records
+  for (int c = tid; c < k; c += blockDim.x) {
+    const int s = dest[c];
+    r.dest_gid[c] = s;
+    r.dead_gid[c] = static_cast<int>(sorted[c] & 0xffffffffu);
+    const uint4 b = philox_block(r, it, s, kPhaseResample, 0, 0);
+    const unsigned long long rank = (static_cast<unsigned long long>(b.x) * static_cast<unsigned>(n - k)) >> 32;
+    r.parent_gid[c] = surv[rank];
+    const unsigned long long key = sorted[c];
+    const int g = static_cast<int>(key & 0xffffffffu);
+    const long long q = nd + c;
+    r.dE[q] = energy_of_key(key);
+    r.dbirth[q] = r.birth[g];
+    r.dnlive[q] = n - c;
+    r.dgid[q] = g;
+    r.dord[q] = c;
+    r.diter[q] = it;
+  }
+  {
+    // dead rows: float4 granules, four loads in flight per thread before the stores
+    const int dp4 = r.dp >> 2, tot = k * dp4, T = blockDim.x;
+    const float4 *X4 = reinterpret_cast<const float4 *>(r.X);
+    float4 *D4 = reinterpret_cast<float4 *>(r.dX) + nd * dp4;
+    for (int q0 = tid; q0 < tot; q0 += 4 * T) {
+      float4 v[4];
+      int dst[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int q = q0 + u * T;
+        dst[u] = q;
+        if (q < tot) {
+          const int j = q / dp4, i = q - j * dp4;
+          v[u] = X4[static_cast<long long>(sorted[j] & 0xffffffffu) * dp4 + i];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (dst[u] < tot) D4[dst[u]] = v[u];
+    }
+  }
+  if (tid == 0) st->stamp[6] = global_ns();
+  if (tid == 0) {
+    st->dead_base = nd;
+    st->n_dead = nd + k;
+    st->e_star = energy_of_key(sorted[k - 1]);
+  }
+}
+
+size_t select_smem_fused(int n, int k) {
+  return static_cast<size_t>(n + 2 * k) * 8 + static_cast<size_t>(n) * 4 + 16;
+}
+
 // Finalisation: every live point dies, key-descending, n_live = n..1 (R-18).
-__global__ void __launch_bounds__(kThreads) k_finalise_sort(RunDev r, unsigned long long *gscratch) {
-  extern __shared__ unsigned long long sbuf[];
+__global__ void __launch_bounds__(kThreads) k_finalise_sort(RunDev r, unsigned long long *gscratch,
+                                                            unsigned long long *gsel) {
+  extern __shared__ unsigned long long sm[];
   DevState *st = r.st;
   __shared__ int sh_flag;
   if (threadIdx.x == 0) sh_flag = (st->error || st->finalised) ? 1 : 0;
@@ -207,7 +459,7 @@ __global__ void __launch_bounds__(kThreads) k_finalise_sort(RunDev r, unsigned l
   }
   int P = 1;
   while (P < n) P <<= 1;
-  unsigned long long *buf = (P <= kSmemSortMax) ? sbuf : gscratch;
+  unsigned long long *buf = (P <= kSmemSortMax) ? sm : gscratch;
   for (int i = threadIdx.x; i < P; i += blockDim.x) buf[i] = (i < n) ? key_of(r.E[i], i) : 0ull;
   __syncthreads();
   bitonic_desc(buf, P);
@@ -217,32 +469,50 @@ __global__ void __launch_bounds__(kThreads) k_finalise_sort(RunDev r, unsigned l
     st->dead_base = nd;
     st->n_dead = nd + n;
   }
+  (void)gsel;
 }
 
-size_t sort_smem(int cnt) {
-  int P = 1;
-  while (P < cnt) P <<= 1;
-  return P <= kSmemSortMax ? static_cast<size_t>(P) * 8 : 0;
+size_t select_smem(int n) {
+  if (n <= kSmemKeysMax) return static_cast<size_t>(kSmemKeysMax + kSmemSortMax) * 8;
+  return static_cast<size_t>(kSmemSortMax) * 8;
 }
 
 }  // namespace
 
+// scratch layout (device, sized by the host): sort_scratch holds max(n, k)
+// rounded up to a power of two plus n; sel_scratch 2k keys.
 void launch_select(const RunDev &r, const LaunchCtx &lc) {
-  size_t smem = sort_smem(r.k);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSortMax * 8);
+    cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (kSmemKeysMax + kSmemSortMax) * 8);
     cudaFuncSetAttribute(k_finalise_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSortMax * 8);
     attr = true;
   }
-  k_select<<<1, kThreads, smem, lc.stream>>>(r, r.sort_scratch);
+  const size_t fused = select_smem_fused(r.n, r.k);
+  int P = 1;
+  while (P < r.k) P <<= 1;
+  if (fused <= 200 * 1024 && P <= r.n) {
+    static bool attr2 = false;
+    if (!attr2) {
+      cudaFuncSetAttribute(k_select_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr2 = true;
+    }
+    NSS_PIN_CARVEOUT(k_select_smem);
+    k_select_smem<<<1, kThreads, fused, lc.stream>>>(r);
+  } else {
+    NSS_PIN_CARVEOUT(k_select);
+    k_select<<<1, kThreads, select_smem(r.n), lc.stream>>>(r, r.sort_scratch, r.sel_scratch);
+  }
   ++*lc.launch_counter;
 }
 
 void launch_finalise_sort(const RunDev &r, const LaunchCtx &lc) {
-  size_t smem = sort_smem(r.n);
   cudaFuncSetAttribute(k_finalise_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSortMax * 8);
-  k_finalise_sort<<<1, kThreads, smem, lc.stream>>>(r, r.sort_scratch);
+  int P = 1;
+  while (P < r.n) P <<= 1;
+  const size_t smem = P <= kSmemSortMax ? static_cast<size_t>(P) * 8 : 0;
+  NSS_PIN_CARVEOUT(k_finalise_sort);
+  k_finalise_sort<<<1, kThreads, smem, lc.stream>>>(r, r.sort_scratch, r.sel_scratch);
   ++*lc.launch_counter;
 }
 

@@ -32,6 +32,9 @@ struct nss_ctx {
   EnergyDev en{};
   std::vector<void *> allocs;
   double *partials = nullptr;
+  unsigned *ticket = nullptr;   // last-block-done counter of k_metric
+  cudaStream_t side = nullptr;  // evidence runs here, concurrently with HRSS
+  cudaEvent_t ev_sel = nullptr, ev_evid = nullptr;
   int nblk = 1;
   double *summary = nullptr;  // device: [mean, std, closed lz_0..R]
   DevState *h_st = nullptr;   // pinned mirror of the device state
@@ -40,10 +43,21 @@ struct nss_ctx {
   std::string err;
   long long launches = 0;
   bool timing = false;
-  std::vector<cudaEvent_t> ev_free, ev_pending;
-  double time_ms = 0.0;
-  long long timed = 0;
+  bool serial_evidence = false;  // run A8 on the main stream (no overlap)
+  struct Timed {
+    int phase;  // 0 hrss, 1 select, 2 evidence, 3 metric
+    cudaEvent_t a, b;
+  };
+  std::vector<cudaEvent_t> ev_free;
+  std::vector<Timed> ev_pending;
+  double time_ms[4] = {0, 0, 0, 0};
+  long long timed[4] = {0, 0, 0, 0};
   int host_finalised = 0;
+  // one iteration captured as a CUDA graph (about 1 us per kernel node
+  // instead of about 3.4 us per stream launch on B200)
+  bool use_graph = true;
+  cudaGraphExec_t graph = nullptr;
+  long long graph_launches = 0;
 };
 
 namespace {
@@ -159,13 +173,13 @@ void fill_info(nss_ctx *c, nss_step_info *info) {
 }
 
 nss_status collect_timing(nss_ctx *c) {
-  for (size_t i = 0; i + 1 < c->ev_pending.size(); i += 2) {
+  for (const auto &t : c->ev_pending) {
     float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, c->ev_pending[i], c->ev_pending[i + 1]));
-    c->time_ms += ms;
-    c->timed += 1;
-    c->ev_free.push_back(c->ev_pending[i]);
-    c->ev_free.push_back(c->ev_pending[i + 1]);
+    CK(cudaEventElapsedTime(&ms, t.a, t.b));
+    c->time_ms[t.phase] += ms;
+    c->timed[t.phase] += 1;
+    c->ev_free.push_back(t.a);
+    c->ev_free.push_back(t.b);
   }
   c->ev_pending.clear();
   return NSS_OK;
@@ -182,22 +196,80 @@ cudaEvent_t take_event(nss_ctx *c) {
   return e;
 }
 
-nss_status enqueue_iteration(nss_ctx *c) {
-  LaunchCtx lc = lctx(c);
-  launch_select(c->r, lc);
-  launch_evidence(c->r, 0, lc);
-  if (c->timing) {
-    cudaEvent_t a = take_event(c), b = take_event(c);
-    CK(cudaEventRecord(a, c->stream));
-    launch_hrss(c->r, c->pr, c->en, lc);
-    CK(cudaEventRecord(b, c->stream));
-    c->ev_pending.push_back(a);
-    c->ev_pending.push_back(b);
-  } else {
-    launch_hrss(c->r, c->pr, c->en, lc);
+// Runs `launch` on `stream`, bracketed by timing events in timing mode.
+template <class F>
+nss_status timed_launch(nss_ctx *c, int phase, cudaStream_t stream, F &&launch) {
+  if (!c->timing) {
+    launch();
+    return NSS_OK;
   }
-  launch_metric(c->r, c->cfg.metric_reg, c->cfg.width_rule, c->cfg.width, 1, c->partials, c->nblk, lc);
+  cudaEvent_t a = take_event(c), b = take_event(c);
+  CK(cudaEventRecord(a, stream));
+  launch();
+  CK(cudaEventRecord(b, stream));
+  c->ev_pending.push_back({phase, a, b});
+  return NSS_OK;
+}
+
+nss_status enqueue_iteration_eager(nss_ctx *c) {
+  LaunchCtx lc = lctx(c);
+  nss_status s;
+  if ((s = timed_launch(c, 1, c->stream, [&] { launch_select(c->r, lc); }))) return s;
+  if (c->serial_evidence) {
+    if ((s = timed_launch(c, 2, c->stream, [&] { launch_evidence(c->r, 0, lc); }))) return s;
+  } else {
+    // A8 only needs this iteration's dead records: fork it onto the side
+    // stream so it overlaps HRSS; the metric kernel (termination test) joins it.
+    CK(cudaEventRecord(c->ev_sel, c->stream));
+    CK(cudaStreamWaitEvent(c->side, c->ev_sel, 0));
+    LaunchCtx ls{c->side, &c->launches};
+    if ((s = timed_launch(c, 2, c->side, [&] { launch_evidence(c->r, 0, ls); }))) return s;
+    CK(cudaEventRecord(c->ev_evid, c->side));
+  }
+  if ((s = timed_launch(c, 0, c->stream, [&] { launch_hrss(c->r, c->pr, c->en, lc); }))) return s;
+  if (!c->serial_evidence) CK(cudaStreamWaitEvent(c->stream, c->ev_evid, 0));
+  if ((s = timed_launch(c, 3, c->stream, [&] {
+         launch_metric(c->r, c->cfg.metric_reg, c->cfg.width_rule, c->cfg.width, 1, c->partials, c->ticket,
+                       c->nblk, lc);
+       })))
+    return s;
   CK(cudaGetLastError());
+  return NSS_OK;
+}
+
+void drop_graph(nss_ctx *c) {
+  if (c->graph) {
+    cudaGraphExecDestroy(c->graph);
+    c->graph = nullptr;
+  }
+}
+
+// One outer iteration: replayed from a captured graph, or launched eagerly in
+// timing mode (events bracket each kernel) or when graphs are disabled.
+nss_status enqueue_iteration(nss_ctx *c) {
+  if (c->timing || !c->use_graph) return enqueue_iteration_eager(c);
+  if (!c->graph) {
+    const long long before = c->launches;
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    const nss_status s = enqueue_iteration_eager(c);
+    const cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+    if (s != NSS_OK) return s;
+    if (e != cudaSuccess) {
+      c->poisoned = true;
+      return fail(c, NSS_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    }
+    const cudaError_t e2 = cudaGraphInstantiate(&c->graph, g, 0);
+    cudaGraphDestroy(g);
+    if (e2 != cudaSuccess) {
+      c->poisoned = true;
+      return fail(c, NSS_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e2));
+    }
+    c->graph_launches = c->launches - before;
+    c->launches = before;
+  }
+  CK(cudaGraphLaunch(c->graph, c->stream));
+  c->launches += c->graph_launches;
   return NSS_OK;
 }
 
@@ -240,6 +312,9 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
   }
   if (cudaMallocHost(&c->h_st, sizeof(DevState)) != cudaSuccess) return bail(NSS_ERR_CUDA);
   if (cudaMallocHost(&c->h_one, sizeof(int)) != cudaSuccess) return bail(NSS_ERR_CUDA);
+  if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess) return bail(NSS_ERR_CUDA);
+  if (cudaEventCreateWithFlags(&c->ev_sel, cudaEventDisableTiming) != cudaSuccess) return bail(NSS_ERR_CUDA);
+  if (cudaEventCreateWithFlags(&c->ev_evid, cudaEventDisableTiming) != cudaSuccess) return bail(NSS_ERR_CUDA);
   *c->h_one = 1;
 
   // ---- energy parameters (fp64 host -> fp32 device) ----
@@ -321,6 +396,33 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
     pr.sd = tmp;
   }
 
+  // ---- padded tables of the one-probe-per-lane engine (k_hrss_lane.cu) ----
+  {
+    const int K = (en.kind == NSS_E_MOG) ? en.n_comp : 1;
+    std::vector<double> ab(static_cast<size_t>(K) * 64, 0.0), pab(64, 0.0);
+    if (en.kind == NSS_E_MOG || en.kind == NSS_E_GAUSS) {
+      for (int j = 0; j < K; ++j)
+        for (int i = 0; i < d && i < 32; ++i) {
+          const double is = 1.0 / energy->sigma[j * d + i];
+          ab[j * 64 + i] = is;
+          ab[j * 64 + 32 + i] = -energy->mu[j * d + i] * is;
+        }
+    }
+    for (int i = 0; i < 32; ++i) {
+      if (pr.kind == NSS_PRIOR_BOX) {
+        pab[i] = i < d ? prior->lo[i] : -INFINITY;
+        pab[32 + i] = i < d ? prior->hi[i] : INFINITY;
+      } else {
+        pab[i] = i < d ? prior->mean[i] : 0.0;
+        pab[32 + i] = i < d ? 1.0 / prior->sd[i] : 0.0;
+      }
+    }
+    if ((s = upload_f32(c, &tmp, ab.data(), ab.size()))) return bail(s);
+    en.lane_ab = tmp;
+    if ((s = upload_f32(c, &tmp, pab.data(), pab.size()))) return bail(s);
+    pr.lane_pab = tmp;
+  }
+
   // ---- live set, dead store, scratch ----
   RunDev &r = c->r;
   r.n = static_cast<int>(n);
@@ -357,7 +459,8 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
   if ((s = dalloc(c, &r.counts, static_cast<size_t>(k) * (cfg->steps > 0 ? cfg->steps : 1)))) return bail(s);
   size_t P = 1;
   while (P < static_cast<size_t>(n)) P <<= 1;
-  if ((s = dalloc(c, &r.sort_scratch, P))) return bail(s);
+  if ((s = dalloc(c, &r.sort_scratch, P + static_cast<size_t>(n)))) return bail(s);
+  if ((s = dalloc(c, &r.sel_scratch, 2 * static_cast<size_t>(k)))) return bail(s);
   if ((s = dalloc(c, &r.lx_prev, R + 1))) return bail(s);
   if ((s = dalloc(c, &r.lx_cur, R + 1))) return bail(s);
   if ((s = dalloc(c, &r.lz, R + 1))) return bail(s);
@@ -366,6 +469,7 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
   c->nblk = metric_blocks(r.n, d);
   const int nent = d * (d + 1) / 2 + d + 1;
   if ((s = dalloc(c, &c->partials, static_cast<size_t>(c->nblk) * nent))) return bail(s);
+  if ((s = dalloc(c, &c->ticket, 1))) return bail(s);
   {
     std::vector<double> ninf(R + 1, -INFINITY);
     if (cudaMemcpy(r.lz, ninf.data(), (R + 1) * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
@@ -374,7 +478,7 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
   // ---- init: prior draws (R-20), then the first metric ----
   LaunchCtx lc = lctx(c);
   launch_init(r, pr, en, lc);
-  launch_metric(r, cfg->metric_reg, cfg->width_rule, cfg->width, 0, c->partials, c->nblk, lc);
+  launch_metric(r, cfg->metric_reg, cfg->width_rule, cfg->width, 0, c->partials, c->ticket, c->nblk, lc);
   if (cudaGetLastError() != cudaSuccess) return bail(NSS_ERR_CUDA);
   if ((s = pull_state(c))) return bail(s);
   if ((s = device_error(c))) return bail(s);
@@ -523,11 +627,18 @@ NSS_API nss_status nss_sync(nss_ctx *c) {
 NSS_API nss_status nss_destroy(nss_ctx *c) {
   if (!c) return NSS_ERR_INVALID_ARG;
   if (c->stream) cudaStreamSynchronize(c->stream);
+  drop_graph(c);
   for (void *p : c->allocs) cudaFree(p);
   for (auto e : c->ev_free) cudaEventDestroy(e);
-  for (auto e : c->ev_pending) cudaEventDestroy(e);
+  for (auto &t : c->ev_pending) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
   if (c->h_st) cudaFreeHost(c->h_st);
   if (c->h_one) cudaFreeHost(c->h_one);
+  if (c->side) { cudaStreamSynchronize(c->side); cudaStreamDestroy(c->side); }
+  if (c->ev_sel) cudaEventDestroy(c->ev_sel);
+  if (c->ev_evid) cudaEventDestroy(c->ev_evid);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return NSS_OK;
@@ -551,7 +662,7 @@ NSS_API nss_status nss_set_live(nss_ctx *c, const float *x, const float *e, int6
   c->h_st->iter = static_cast<int>(next_iteration - 1);
   c->h_st->terminated = 0;
   CK(cudaMemcpyAsync(c->r.st, c->h_st, sizeof(DevState), cudaMemcpyHostToDevice, c->stream));
-  launch_metric(c->r, c->cfg.metric_reg, c->cfg.width_rule, c->cfg.width, 0, c->partials, c->nblk, lctx(c));
+  launch_metric(c->r, c->cfg.metric_reg, c->cfg.width_rule, c->cfg.width, 0, c->partials, c->ticket, c->nblk, lctx(c));
   CK(cudaGetLastError());
   if ((s = pull_state(c))) return s;
   return NSS_OK;
@@ -642,8 +753,10 @@ NSS_API nss_status nss_set_kernel_timing(nss_ctx *c, int32_t enable) {
   CK(cudaStreamSynchronize(c->stream));
   if ((s = collect_timing(c))) return s;
   c->timing = enable != 0;
-  c->time_ms = 0.0;
-  c->timed = 0;
+  for (int i = 0; i < 4; ++i) {
+    c->time_ms[i] = 0.0;
+    c->timed[i] = 0;
+  }
   return NSS_OK;
 }
 
@@ -652,8 +765,8 @@ NSS_API nss_status nss_kernel_time(nss_ctx *c, double *ms, int64_t *launches) {
   if (s) return s;
   CK(cudaStreamSynchronize(c->stream));
   if ((s = collect_timing(c))) return s;
-  if (ms) *ms = c->time_ms;
-  if (launches) *launches = c->timed;
+  if (ms) *ms = c->time_ms[0];
+  if (launches) *launches = c->timed[0];
   return NSS_OK;
 }
 
@@ -661,6 +774,7 @@ NSS_API nss_status nss_set_hrss_engine(nss_ctx *c, int32_t engine) {
   nss_status s = check_usable(c);
   if (s) return s;
   if (engine < NSS_ENGINE_AUTO || engine > NSS_ENGINE_LANE) return NSS_ERR_INVALID_ARG;
+  drop_graph(c);
   c->r.engine = engine;
   return NSS_OK;
 }
@@ -670,6 +784,47 @@ NSS_API nss_status nss_get_hrss_engine(nss_ctx *c, int32_t *engine) {
   if (s) return s;
   if (!engine) return NSS_ERR_INVALID_ARG;
   *engine = hrss_engine(c->r, c->en) == 1 ? NSS_ENGINE_LANE : NSS_ENGINE_WARP;
+  return NSS_OK;
+}
+
+NSS_API nss_status nss_phase_times(nss_ctx *c, double *ms, int64_t *launches) {
+  nss_status s = check_usable(c);
+  if (s) return s;
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaStreamSynchronize(c->side));
+  if ((s = collect_timing(c))) return s;
+  for (int i = 0; i < 4; ++i) {
+    if (ms) ms[i] = c->time_ms[i];
+    if (launches) launches[i] = c->timed[i];
+  }
+  return NSS_OK;
+}
+
+NSS_API nss_status nss_set_overlap(nss_ctx *c, int32_t overlap) {
+  nss_status s = check_usable(c);
+  if (s) return s;
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaStreamSynchronize(c->side));
+  drop_graph(c);
+  c->serial_evidence = overlap == 0;
+  return NSS_OK;
+}
+
+NSS_API nss_status nss_set_graph(nss_ctx *c, int32_t enable) {
+  nss_status s = check_usable(c);
+  if (s) return s;
+  CK(cudaStreamSynchronize(c->stream));
+  drop_graph(c);
+  c->use_graph = enable != 0;
+  return NSS_OK;
+}
+
+NSS_API nss_status nss_debug_stamps(nss_ctx *c, uint64_t *stamps) {
+  nss_status s = check_usable(c);
+  if (s) return s;
+  if (!stamps) return NSS_ERR_INVALID_ARG;
+  if ((s = pull_state(c))) return s;
+  for (int i = 0; i < 16; ++i) stamps[i] = c->h_st->stamp[i];
   return NSS_OK;
 }
 

@@ -30,6 +30,7 @@ struct DevState {
   double log_z_live;
   unsigned long long probes, evals, expansions, shrinks, nulls;
   unsigned long long init_evals, init_attempts;
+  unsigned long long stamp[16];  // %globaltimer stamps (ns) for latency profiling
 };
 
 // Energy parameters laid out for the kernels (device pointers, fp32).
@@ -48,6 +49,9 @@ struct EnergyDev {
   const float *prec;    // CORR: d*d
   const float *data_x;  // LOGREG: N*d; GP: N*d_in
   const float *data_y;  // LOGREG / GP: N
+  // one-probe-per-lane engine tables, padded to 32 coordinates with neutral
+  // values: [K][2][32] = {1/sigma, -mu/sigma} per component (GAUSS: K = 1)
+  const float *lane_ab;
 };
 
 struct PriorDev {
@@ -55,6 +59,8 @@ struct PriorDev {
   const float *lo, *hi;       // BOX
   const float *mean, *isd, *sd;  // GAUSS_DIAG (isd = 1/sd)
   float log_norm;             // BOX: -sum log(hi-lo); GAUSS: -sum log sd - d/2 log 2pi
+  // [2][32] padded: BOX {lo (-inf), hi (+inf)}; GAUSS {mean (0), 1/sd (0)}
+  const float *lane_pab;
 };
 
 // Everything a kernel needs about the live set and the run.
@@ -76,7 +82,8 @@ struct RunDev {
   // per-iteration scratch
   int *dead_gid, *dest_gid, *parent_gid, *surv;
   uint32_t *counts;           // k*p packed {nL, nR, nS, acc}
-  unsigned long long *sort_scratch;  // max(n, k) rounded to a power of two
+  unsigned long long *sort_scratch;  // n + pow2(max(n, k)) keys
+  unsigned long long *sel_scratch;   // 2k keys: selected (gid order), sorted
   // evidence replicas
   double *lx_prev, *lx_cur, *lz;
   DevState *st;
@@ -133,11 +140,31 @@ __device__ __forceinline__ unsigned long long key_of(float e, int gid) {
   return (static_cast<unsigned long long>(ord_f32(e)) << 32) | static_cast<uint32_t>(gid);
 }
 
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ void raise_error(DevState *st, int code) { atomicCAS(&st->error, 0, code); }
 
 // ----------------------------------------------------------------------------
 // Launchers (host side, one per kernel file)
 // ----------------------------------------------------------------------------
+// Every kernel of the library runs with the same (maximum) shared-memory
+// carveout: a different carveout per kernel forces the SM to reconfigure its
+// L1/shared split between consecutive launches.
+template <class Kern>
+inline bool pin_carveout(Kern *kernel) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  return true;
+}
+#define NSS_PIN_CARVEOUT(kern)                       \
+  do {                                               \
+    static const bool pinned_ = pin_carveout(kern); \
+    (void)pinned_;                                   \
+  } while (0)
+
 struct LaunchCtx {
   cudaStream_t stream;
   long long *launch_counter;
@@ -160,7 +187,7 @@ bool lane_engine_ok(const RunDev &r, const EnergyDev &en);
 void launch_hrss_lane(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc);
 // k_metric.cu: A5 metric (+ A9 termination when iterating)
 void launch_metric(const RunDev &r, double metric_reg, int width_rule, double width_param,
-                   int end_of_iteration, double *partials, int n_blocks, const LaunchCtx &lc);
+                   int end_of_iteration, double *partials, unsigned *ticket, int n_blocks, const LaunchCtx &lc);
 int metric_blocks(int n, int d);
 
 }  // namespace nss

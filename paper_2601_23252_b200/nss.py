@@ -71,7 +71,9 @@ EXPORTS = ["nss_get_unique_id", "nss_init", "nss_step", "nss_steps", "nss_run", 
            "nss_evidence", "nss_evidence_reps", "nss_samples", "nss_info", "nss_sync", "nss_destroy",
            "nss_last_error", "nss_set_live", "nss_get_live", "nss_get_metric", "nss_get_trace",
            "nss_dead", "nss_volume_reps", "nss_set_kernel_timing", "nss_kernel_time",
-           "nss_launch_count", "nss_set_hrss_engine", "nss_get_hrss_engine"]
+           "nss_launch_count", "nss_set_hrss_engine", "nss_get_hrss_engine",
+           "nss_phase_times", "nss_set_overlap", "nss_set_graph",
+           "nss_debug_stamps"]
 
 _lib = None
 
@@ -112,6 +114,10 @@ def lib():
     L.nss_launch_count.argtypes = [vp, P(C.c_int64)]
     L.nss_set_hrss_engine.argtypes = [vp, C.c_int32]
     L.nss_get_hrss_engine.argtypes = [vp, P(C.c_int32)]
+    L.nss_phase_times.argtypes = [vp, P(C.c_double), P(C.c_int64)]
+    L.nss_set_overlap.argtypes = [vp, C.c_int32]
+    L.nss_set_graph.argtypes = [vp, C.c_int32]
+    L.nss_debug_stamps.argtypes = [vp, P(C.c_uint64)]
     _lib = L
     return L
 
@@ -292,6 +298,26 @@ class Sampler:
         e = C.c_int32()
         self._check(lib().nss_get_hrss_engine(self._h, C.byref(e)), "nss_get_hrss_engine")
         return {1: "warp", 2: "lane"}[e.value]
+
+    def phase_times(self) -> Dict:
+        """Summed ms and launches per phase since timing was enabled."""
+        ms = (C.c_double * 4)()
+        n = (C.c_int64 * 4)()
+        self._check(lib().nss_phase_times(self._h, ms, n), "nss_phase_times")
+        names = ("hrss", "select", "evidence", "metric")
+        return {nm: (ms[i], n[i]) for i, nm in enumerate(names)}
+
+    def set_overlap(self, on: bool):
+        self._check(lib().nss_set_overlap(self._h, 1 if on else 0), "nss_set_overlap")
+
+    def set_graph(self, on: bool):
+        self._check(lib().nss_set_graph(self._h, 1 if on else 0), "nss_set_graph")
+
+    def debug_stamps(self) -> np.ndarray:
+        out = np.zeros(16, np.uint64)
+        self._check(lib().nss_debug_stamps(self._h, out.ctypes.data_as(C.POINTER(C.c_uint64))),
+                    "nss_debug_stamps")
+        return out
 
     def launch_count(self) -> int:
         n = C.c_int64()
