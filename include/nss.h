@@ -182,14 +182,26 @@ nss_status nss_dead(nss_ctx *ctx, float *e, int32_t *n_live, float *birth, int32
                     int64_t cap, int64_t *n_out);
 nss_status nss_volume_reps(nss_ctx *ctx, double *log_x /* R+1 */);
 
-/* HRSS engine.  AUTO picks LANE (one probe per lane,
- * speculative rounds) when d <= 32 and the energy is cheap, WARP (warp-
- * cooperative energy, one probe at a time) otherwise; forcing LANE where it
- * does not apply falls back to WARP.  Both compute the same algorithm. */
-typedef enum { NSS_ENGINE_AUTO = 0, NSS_ENGINE_WARP = 1, NSS_ENGINE_LANE = 2 } nss_hrss_engine;
+/* HRSS engine.  AUTO picks BATCH (round-synchronous
+ * chains feeding one batched energy kernel: tensor cores for logistic
+ * regression with bf16-exact data, batched Cholesky for GP) for the
+ * expensive energies, LANE (one probe per lane, speculative rounds) when
+ * d <= 32 and the energy is cheap, WARP (warp-cooperative energy, one probe at
+ * a time) otherwise.  Forcing an engine that does not apply falls back to WARP
+ * (LANE) or to a generic warp-per-probe batched energy (BATCH).  All engines
+ * compute the same algorithm with the same draws. */
+typedef enum { NSS_ENGINE_AUTO = 0, NSS_ENGINE_WARP = 1, NSS_ENGINE_LANE = 2, NSS_ENGINE_BATCH = 3 } nss_hrss_engine;
 nss_status nss_set_hrss_engine(nss_ctx *ctx, int32_t engine);
-/* The engine the next iteration will use (resolved: WARP or LANE). */
+/* The engine the next iteration will use (resolved: WARP, LANE or BATCH). */
 nss_status nss_get_hrss_engine(nss_ctx *ctx, int32_t *engine);
+
+/* Kernel check: logistic-regression energies E(theta_p) = sum_r softplus(a_rp)
+ * - y_r a_rp, a = X theta (P:466 shape), for P probe points theta (P*d
+ * row-major), computed by the tcgen05 tensor-core kernel the sampler uses.
+ * X (N*d) must be bf16-exact, else NSS_ERR_UNSUPPORTED.
+ * E_out: P values. */
+nss_status nss_lr_energy_batch(const double *X, const double *y, int64_t N, int32_t d, const double *theta,
+                               int64_t P, double *E_out);
 
 /* ---- measurement hooks ---- */
 /* When enabled, the HRSS kernel launch of every iteration is bracketed by CUDA

@@ -1,0 +1,36 @@
+// Round-synchronous batched HRSS engine (k_batch.cu) for energies that are too
+// expensive for one warp: every round, each chain advances its HRSS state
+// machine until it needs an energy, writes that probe point into a shared
+// probe buffer, and one batched energy kernel evaluates all probes at once
+// (tensor cores for logistic regression, batched Cholesky for GP).
+#pragma once
+#include <cuda_bf16.h>
+
+#include "nss_internal.cuh"
+
+namespace nss {
+
+enum BatchPhase : int { kPhDir = 0, kPhStepOut = 1, kPhShrink = 2, kPhDone = 3 };
+
+struct BatchDev {
+  int k, dp, max_rows, n_splits, p_stride;
+  // per-chain state (k each)
+  int *phase, *step, *nl, *nr, *ns, *ldone, *rdone, *row0, *row1;
+  float *l0, *r0, *lft, *rgt, *log_y, *e, *lp, *t0, *t1, *lp0, *lp1;
+  unsigned *cnt;              // [5][k]: probes, evals, expansions, shrinks, nulls
+  float *x, *v;               // [k][dp]
+  // probe buffers, double-buffered by round parity
+  float *P[2];                // [max_rows][dp] probe points (fp32)
+  int *n_probe;               // [2] rows issued in the round of that parity
+  float *partial[2];          // [n_splits][p_stride] energy partial sums per row
+  __nv_bfloat16 *A[2];        // logistic regression: [3][p_stride][128] bf16 splits, else null
+};
+
+// k_batch.cu
+void batch_begin(const RunDev &r, const PriorDev &pr, const BatchDev &b, const LaunchCtx &lc);
+void batch_advance(const RunDev &r, const PriorDev &pr, const BatchDev &b, int parity, const LaunchCtx &lc);
+void batch_energy_generic(const RunDev &r, const EnergyDev &en, const BatchDev &b, int parity, const LaunchCtx &lc);
+void batch_finish(const RunDev &r, const BatchDev &b, const LaunchCtx &lc);
+bool batch_generic_ok(const EnergyDev &en);
+
+}  // namespace nss

@@ -73,4 +73,134 @@ __device__ __forceinline__ void load_prior_lane(const PriorDev &pr, int lane, in
   }
 }
 
+// Warp-cooperative energy E(x); the result is identical in every lane.
+// `wbuf` is a per-warp shared buffer of NPL*32 floats.
+template <int NPL, int KIND>
+__device__ __forceinline__ float warp_energy(const float (&x)[NPL], const EnergyDev &en, const ESm &es,
+                                             float *wbuf, int lane) {
+  const int d = en.d;
+  if constexpr (KIND == NSS_E_FLAT) {
+    return en.c;
+  } else if constexpr (KIND == NSS_E_GAUSS) {
+    float s = 0.f;
+#pragma unroll
+    for (int t = 0; t < NPL; ++t) {
+      const int i = lane + 32 * t;
+      if (i < d) {
+        float u = (x[t] - es.mu[i]) * es.isig[i];
+        s = fmaf(u, u, s);
+      }
+    }
+    return 0.5f * warp_sum(s) + en.c;
+  } else if constexpr (KIND == NSS_E_MOG) {
+    // online log-sum-exp over components; unrolling lets the K independent
+    // butterfly reductions overlap
+    float m = -INFINITY, acc = 0.f;
+#pragma unroll 4
+    for (int j = 0; j < en.n_comp; ++j) {
+      float s = 0.f;
+#pragma unroll
+      for (int t = 0; t < NPL; ++t) {
+        const int i = lane + 32 * t;
+        if (i < d) {
+          float u = (x[t] - es.mu[j * d + i]) * es.isig[j * d + i];
+          s = fmaf(u, u, s);
+        }
+      }
+      s = warp_sum(s);
+      const float l = es.logc[j] - 0.5f * s;
+      if (l > m) {
+        acc = acc * __expf(m - l) + 1.f;
+        m = l;
+      } else {
+        acc += __expf(l - m);
+      }
+    }
+    return -(m + __logf(acc));
+  } else if constexpr (KIND == NSS_E_CORR_GAUSS) {
+#pragma unroll
+    for (int t = 0; t < NPL; ++t) {
+      const int i = lane + 32 * t;
+      if (i < d) wbuf[i] = x[t] - es.mu[i];
+    }
+    __syncwarp();
+    float q = 0.f;
+#pragma unroll
+    for (int t = 0; t < NPL; ++t) {
+      const int i = lane + 32 * t;
+      if (i < d) {
+        const float *row = es.prec + i * es.ldp;
+        float py = 0.f;
+        for (int m = 0; m < d; ++m) py = fmaf(row[m], wbuf[m], py);
+        q = fmaf(wbuf[i], py, q);
+      }
+    }
+    q = warp_sum(q);
+    __syncwarp();
+    return 0.5f * q + en.c;
+  } else if constexpr (KIND == NSS_E_FUNNEL) {
+    // P:885 (R-23): x_0 = y ~ N(0, sy^2), x_n ~ N(0, e^y)
+    const float y = __shfl_sync(kFull, x[0], 0);
+    float s = 0.f;
+#pragma unroll
+    for (int t = 0; t < NPL; ++t) {
+      const int i = lane + 32 * t;
+      if (i >= 1 && i < d) s = fmaf(x[t], x[t], s);
+    }
+    s = warp_sum(s);
+    const float sy = en.sigma_y;
+    const float yy = y / sy;
+    return 0.5f * yy * yy + logf(sy) + 0.5f * kLn2Pi + 0.5f * s * expf(-y) +
+           static_cast<float>(d - 1) * 0.5f * (y + kLn2Pi);
+  } else if constexpr (KIND == NSS_E_LOGREG) {
+    // naive warp path (lanes over data rows); the batched tensor-core engine is
+    // the production path for large N
+#pragma unroll
+    for (int t = 0; t < NPL; ++t) {
+      const int i = lane + 32 * t;
+      if (i < d) wbuf[i] = x[t];
+    }
+    __syncwarp();
+    float acc = 0.f;
+    for (long long rr = lane; rr < en.n_data; rr += 32) {
+      const float *row = en.data_x + rr * d;
+      float a = 0.f;
+      for (int m = 0; m < d; ++m) a = fmaf(row[m], wbuf[m], a);
+      acc += softplusf(a) - en.data_y[rr] * a;
+    }
+    acc = warp_sum(acc);
+    __syncwarp();
+    return acc;
+  } else {
+    return NAN;
+  }
+}
+
+// log Pi(x) and support test (box: all lanes inside; Gaussian: always inside).
+template <int NPL>
+__device__ __forceinline__ float prior_logp(const float (&x)[NPL], const PriorDev &pr, const float (&pa)[NPL],
+                                            const float (&pb)[NPL], int lane, int d, bool &inside) {
+  if (pr.kind == NSS_PRIOR_BOX) {
+    bool ok = true;
+#pragma unroll
+    for (int t = 0; t < NPL; ++t) {
+      const int i = lane + 32 * t;
+      if (i < d) ok = ok && (x[t] >= pa[t]) && (x[t] <= pb[t]);
+    }
+    inside = __all_sync(kFull, ok);
+    return pr.log_norm;
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int t = 0; t < NPL; ++t) {
+    const int i = lane + 32 * t;
+    if (i < d) {
+      float u = (x[t] - pa[t]) * pb[t];
+      s = fmaf(u, u, s);
+    }
+  }
+  inside = true;
+  return -0.5f * warp_sum(s) + pr.log_norm;
+}
+
 }  // namespace nss

@@ -11,6 +11,8 @@
 #include <string>
 #include <vector>
 
+#include "batch.cuh"
+#include "lr_engine.cuh"
 #include "nss_internal.cuh"
 
 #define NSS_API extern "C" __attribute__((visibility("default")))
@@ -58,7 +60,19 @@ struct nss_ctx {
   bool use_graph = true;
   cudaGraphExec_t graph = nullptr;
   long long graph_launches = 0;
+  // round-synchronous batch engine (k_batch.cu) and its energy backends
+  BatchDev bd{};
+  bool batch_alloc = false;
+  int batch_backend = 0;  // 1 generic warp-per-probe energy, 2 tensor-core logistic regression
+  LrEngine lr{};
+  bool lr_ok = false;     // logistic-regression data are bf16-exact and d <= 112
+  std::vector<double> lr_x, lr_y;
+  cudaGraphExec_t round_graph = nullptr;
+  long long round_graph_launches = 0;
+  int *h_nprobe = nullptr;  // pinned
 };
+
+static const int kRoundsPerChunk = 32;
 
 namespace {
 
@@ -237,16 +251,162 @@ nss_status enqueue_iteration_eager(nss_ctx *c) {
   return NSS_OK;
 }
 
+// 0 warp, 1 lane, 2 batch
+int resolve_engine(const nss_ctx *c) {
+  const int want = c->r.engine;
+  const bool expensive = c->en.kind == NSS_E_LOGREG && c->lr_ok;
+  if (want == NSS_ENGINE_BATCH) return 2;
+  if (want == NSS_ENGINE_AUTO && expensive) return 2;
+  return hrss_engine(c->r, c->en);
+}
+
+nss_status ensure_batch(nss_ctx *c) {
+  const int backend = (c->en.kind == NSS_E_LOGREG && c->lr_ok) ? 2 : 1;
+  if (c->batch_alloc && c->batch_backend == backend) return NSS_OK;
+  if (backend == 1 && !batch_generic_ok(c->en)) return fail(c, NSS_ERR_UNSUPPORTED, "no batched energy for this kind");
+  BatchDev &b = c->bd;
+  const int k = c->r.k;
+  if (!c->batch_alloc) {
+    b.k = k;
+    b.dp = c->dp;
+    b.max_rows = 2 * k;
+    nss_status s;
+    int **ints[] = {&b.phase, &b.step, &b.nl, &b.nr, &b.ns, &b.ldone, &b.rdone, &b.row0, &b.row1};
+    for (int **q : ints)
+      if ((s = dalloc(c, q, k))) return s;
+    float **flts[] = {&b.l0, &b.r0, &b.lft, &b.rgt, &b.log_y, &b.e, &b.lp, &b.t0, &b.t1, &b.lp0, &b.lp1};
+    for (float **q : flts)
+      if ((s = dalloc(c, q, k))) return s;
+    if ((s = dalloc(c, &b.cnt, 5 * static_cast<size_t>(k)))) return s;
+    if ((s = dalloc(c, &b.x, static_cast<size_t>(k) * c->dp))) return s;
+    if ((s = dalloc(c, &b.v, static_cast<size_t>(k) * c->dp))) return s;
+    for (int q = 0; q < 2; ++q)
+      if ((s = dalloc(c, &b.P[q], static_cast<size_t>(b.max_rows) * c->dp))) return s;
+    if ((s = dalloc(c, &b.n_probe, 2))) return s;
+    if (cudaMallocHost(&c->h_nprobe, sizeof(int)) != cudaSuccess) return fail(c, NSS_ERR_CUDA, "cudaMallocHost");
+    c->batch_alloc = true;
+  }
+  if (backend == 2) {
+    if (!c->lr.Xb) {
+      if (lr_setup(c->lr, c->lr_x.data(), c->lr_y.data(), c->en.n_data, c->d, b.max_rows) != cudaSuccess)
+        return fail(c, NSS_ERR_CUDA, "tensor-core logistic-regression setup failed");
+    }
+    b.n_splits = c->lr.n_splits;
+    b.p_stride = c->lr.p_stride;
+    for (int q = 0; q < 2; ++q) {
+      b.partial[q] = c->lr.partial[q];
+      b.A[q] = c->lr.A[q];
+    }
+  } else {
+    b.n_splits = 1;
+    b.p_stride = b.max_rows;
+    for (int q = 0; q < 2; ++q) {
+      nss_status s;
+      if ((s = dalloc(c, &b.partial[q], static_cast<size_t>(b.max_rows)))) return s;
+      b.A[q] = nullptr;
+    }
+  }
+  c->batch_backend = backend;
+  return NSS_OK;
+}
+
+void enqueue_rounds(nss_ctx *c, int count) {
+  LaunchCtx lc = lctx(c);
+  for (int i = 0; i < count; ++i) {
+    const int par = i & 1;
+    batch_advance(c->r, c->pr, c->bd, par, lc);
+    if (c->batch_backend == 2)
+      lr_energy_pass(c->lr, par, c->bd.n_probe + par, c->bd.n_probe + (par ^ 1), lc);
+    else
+      batch_energy_generic(c->r, c->en, c->bd, par, lc);
+  }
+}
+
 void drop_graph(nss_ctx *c) {
   if (c->graph) {
     cudaGraphExecDestroy(c->graph);
     c->graph = nullptr;
   }
+  if (c->round_graph) {
+    cudaGraphExecDestroy(c->round_graph);
+    c->round_graph = nullptr;
+  }
+}
+
+// One iteration with the batch engine: the HRSS part is a data-dependent
+// number of rounds, replayed in chunks from a captured graph; the host polls
+// the last round's probe count after each chunk (zero: every chain is done).
+nss_status enqueue_iteration_batch(nss_ctx *c) {
+  nss_status s;
+  if ((s = ensure_batch(c))) return s;
+  LaunchCtx lc = lctx(c);
+  if ((s = timed_launch(c, 1, c->stream, [&] { launch_select(c->r, lc); }))) return s;
+  CK(cudaEventRecord(c->ev_sel, c->stream));
+  CK(cudaStreamWaitEvent(c->side, c->ev_sel, 0));
+  LaunchCtx ls{c->side, &c->launches};
+  if ((s = timed_launch(c, 2, c->side, [&] { launch_evidence(c->r, 0, ls); }))) return s;
+  CK(cudaEventRecord(c->ev_evid, c->side));
+  auto rounds = [&]() -> nss_status {
+    batch_begin(c->r, c->pr, c->bd, lc);
+    const long long max_rounds =
+        static_cast<long long>(c->r.p) * (c->r.max_stepout + 2 + c->r.max_shrink) + kRoundsPerChunk;
+    for (long long done = 0; done < max_rounds; done += kRoundsPerChunk) {
+      if (c->use_graph && !c->timing) {
+        if (!c->round_graph) {
+          const long long before = c->launches;
+          cudaGraph_t g = nullptr;
+          CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+          enqueue_rounds(c, kRoundsPerChunk);
+          const cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+          if (e != cudaSuccess) {
+            c->poisoned = true;
+            return fail(c, NSS_ERR_CUDA, std::string("round graph capture: ") + cudaGetErrorString(e));
+          }
+          const cudaError_t e2 = cudaGraphInstantiate(&c->round_graph, g, 0);
+          cudaGraphDestroy(g);
+          if (e2 != cudaSuccess) {
+            c->poisoned = true;
+            return fail(c, NSS_ERR_CUDA, std::string("round graph: ") + cudaGetErrorString(e2));
+          }
+          c->round_graph_launches = c->launches - before;
+          c->launches = before;
+        }
+        CK(cudaGraphLaunch(c->round_graph, c->stream));
+        c->launches += c->round_graph_launches;
+      } else {
+        enqueue_rounds(c, kRoundsPerChunk);
+      }
+      CK(cudaMemcpyAsync(c->h_nprobe, c->bd.n_probe + ((kRoundsPerChunk - 1) & 1), sizeof(int),
+                         cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      if (*c->h_nprobe == 0) break;
+    }
+    batch_finish(c->r, c->bd, lc);
+    return NSS_OK;
+  };
+  if (c->timing) {
+    cudaEvent_t a = take_event(c), b = take_event(c);
+    CK(cudaEventRecord(a, c->stream));
+    if ((s = rounds())) return s;
+    CK(cudaEventRecord(b, c->stream));
+    c->ev_pending.push_back({0, a, b});
+  } else if ((s = rounds())) {
+    return s;
+  }
+  CK(cudaStreamWaitEvent(c->stream, c->ev_evid, 0));
+  if ((s = timed_launch(c, 3, c->stream, [&] {
+         launch_metric(c->r, c->cfg.metric_reg, c->cfg.width_rule, c->cfg.width, 1, c->partials, c->ticket,
+                       c->nblk, lc);
+       })))
+    return s;
+  CK(cudaGetLastError());
+  return NSS_OK;
 }
 
 // One outer iteration: replayed from a captured graph, or launched eagerly in
 // timing mode (events bracket each kernel) or when graphs are disabled.
 nss_status enqueue_iteration(nss_ctx *c) {
+  if (resolve_engine(c) == 2) return enqueue_iteration_batch(c);
   if (c->timing || !c->use_graph) return enqueue_iteration_eager(c);
   if (!c->graph) {
     const long long before = c->launches;
@@ -363,7 +523,13 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
     if ((s = upload_f32(c, &tmp, energy->prec, static_cast<size_t>(d) * d))) return bail(s);
     en.prec = tmp;
   } else if (en.kind == NSS_E_LOGREG) {
-    if ((s = upload_f32(c, &tmp, energy->data_x, static_cast<size_t>(energy->n_data) * d))) return bail(s);
+    const size_t nx = static_cast<size_t>(energy->n_data) * d;
+    c->lr_ok = d <= 112 && lr_data_bf16_exact(energy->data_x, static_cast<long long>(nx));
+    if (c->lr_ok) {
+      c->lr_x.assign(energy->data_x, energy->data_x + nx);
+      c->lr_y.assign(energy->data_y, energy->data_y + energy->n_data);
+    }
+    if ((s = upload_f32(c, &tmp, energy->data_x, nx))) return bail(s);
     en.data_x = tmp;
     if ((s = upload_f32(c, &tmp, energy->data_y, energy->n_data))) return bail(s);
     en.data_y = tmp;
@@ -628,6 +794,8 @@ NSS_API nss_status nss_destroy(nss_ctx *c) {
   if (!c) return NSS_ERR_INVALID_ARG;
   if (c->stream) cudaStreamSynchronize(c->stream);
   drop_graph(c);
+  if (c->lr.Xb) lr_free(c->lr);
+  if (c->h_nprobe) cudaFreeHost(c->h_nprobe);
   for (void *p : c->allocs) cudaFree(p);
   for (auto e : c->ev_free) cudaEventDestroy(e);
   for (auto &t : c->ev_pending) {
@@ -773,7 +941,7 @@ NSS_API nss_status nss_kernel_time(nss_ctx *c, double *ms, int64_t *launches) {
 NSS_API nss_status nss_set_hrss_engine(nss_ctx *c, int32_t engine) {
   nss_status s = check_usable(c);
   if (s) return s;
-  if (engine < NSS_ENGINE_AUTO || engine > NSS_ENGINE_LANE) return NSS_ERR_INVALID_ARG;
+  if (engine < NSS_ENGINE_AUTO || engine > NSS_ENGINE_BATCH) return NSS_ERR_INVALID_ARG;
   drop_graph(c);
   c->r.engine = engine;
   return NSS_OK;
@@ -783,7 +951,8 @@ NSS_API nss_status nss_get_hrss_engine(nss_ctx *c, int32_t *engine) {
   nss_status s = check_usable(c);
   if (s) return s;
   if (!engine) return NSS_ERR_INVALID_ARG;
-  *engine = hrss_engine(c->r, c->en) == 1 ? NSS_ENGINE_LANE : NSS_ENGINE_WARP;
+  const int e = resolve_engine(c);
+  *engine = e == 2 ? NSS_ENGINE_BATCH : (e == 1 ? NSS_ENGINE_LANE : NSS_ENGINE_WARP);
   return NSS_OK;
 }
 
@@ -826,6 +995,44 @@ NSS_API nss_status nss_debug_stamps(nss_ctx *c, uint64_t *stamps) {
   if ((s = pull_state(c))) return s;
   for (int i = 0; i < 16; ++i) stamps[i] = c->h_st->stamp[i];
   return NSS_OK;
+}
+
+NSS_API nss_status nss_lr_energy_batch(const double *X, const double *y, int64_t N, int32_t d, const double *theta,
+                                       int64_t P, double *E_out) {
+  if (!X || !y || !theta || !E_out || N < 1 || d < 1 || d > 112 || P < 1) return NSS_ERR_INVALID_ARG;
+  if (!lr_data_bf16_exact(X, N * d)) return NSS_ERR_UNSUPPORTED;
+  LrEngine L;
+  if (lr_setup(L, X, y, N, d, static_cast<int>(P)) != cudaSuccess) {
+    lr_free(L);
+    return NSS_ERR_CUDA;
+  }
+  std::vector<float> pt(static_cast<size_t>(P) * d);
+  for (size_t i = 0; i < pt.size(); ++i) pt[i] = static_cast<float>(theta[i]);
+  float *dP = nullptr, *dE = nullptr;
+  int *dn = nullptr;
+  const int np = static_cast<int>(P);
+  long long launches = 0;
+  cudaStream_t st;
+  cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  cudaError_t e = cudaMalloc(&dP, pt.size() * sizeof(float));
+  if (!e) e = cudaMalloc(&dE, P * sizeof(float));
+  if (!e) e = cudaMalloc(&dn, sizeof(int));
+  if (!e) e = cudaMemcpy(dP, pt.data(), pt.size() * sizeof(float), cudaMemcpyHostToDevice);
+  if (!e) e = cudaMemcpy(dn, &np, sizeof(int), cudaMemcpyHostToDevice);
+  if (!e) {
+    lr_energies(L, dP, d, dn, dE, LaunchCtx{st, &launches});
+    e = cudaGetLastError();
+  }
+  std::vector<float> Ef(P);
+  if (!e) e = cudaStreamSynchronize(st);
+  if (!e) e = cudaMemcpy(Ef.data(), dE, P * sizeof(float), cudaMemcpyDeviceToHost);
+  for (int64_t i = 0; i < P; ++i) E_out[i] = Ef[i];
+  cudaFree(dP);
+  cudaFree(dE);
+  cudaFree(dn);
+  cudaStreamDestroy(st);
+  lr_free(L);
+  return e ? NSS_ERR_CUDA : NSS_OK;
 }
 
 NSS_API nss_status nss_launch_count(nss_ctx *c, int64_t *launches) {

@@ -73,7 +73,7 @@ EXPORTS = ["nss_get_unique_id", "nss_init", "nss_step", "nss_steps", "nss_run", 
            "nss_dead", "nss_volume_reps", "nss_set_kernel_timing", "nss_kernel_time",
            "nss_launch_count", "nss_set_hrss_engine", "nss_get_hrss_engine",
            "nss_phase_times", "nss_set_overlap", "nss_set_graph",
-           "nss_debug_stamps"]
+           "nss_debug_stamps", "nss_lr_energy_batch"]
 
 _lib = None
 
@@ -118,6 +118,8 @@ def lib():
     L.nss_set_overlap.argtypes = [vp, C.c_int32]
     L.nss_set_graph.argtypes = [vp, C.c_int32]
     L.nss_debug_stamps.argtypes = [vp, P(C.c_uint64)]
+    L.nss_lr_energy_batch.argtypes = [P(C.c_double), P(C.c_double), C.c_int64, C.c_int32, P(C.c_double),
+                                      C.c_int64, P(C.c_double)]
     _lib = L
     return L
 
@@ -138,6 +140,19 @@ def _fp(a):
 
 def _ip(a):
     return None if a is None else a.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+def lr_energy_batch(data_x: np.ndarray, data_y: np.ndarray, theta: np.ndarray) -> np.ndarray:
+    """Logistic-regression energies of the probe rows `theta` from the tcgen05
+    kernel (include/nss.h nss_lr_energy_batch)."""
+    X = _f64(data_x)
+    y = _f64(data_y)
+    th = np.ascontiguousarray(np.atleast_2d(np.asarray(theta, dtype=np.float64)))
+    out = np.zeros(th.shape[0])
+    st = lib().nss_lr_energy_batch(_dp(X), _dp(y), X.shape[0], X.shape[1], _dp(th), th.shape[0], _dp(out))
+    if st != 0:
+        raise NssError(st, "nss_lr_energy_batch")
+    return out
 
 
 class Sampler:
@@ -290,14 +305,14 @@ class Sampler:
         return ms.value, n.value
 
     def set_engine(self, engine: str):
-        """'auto', 'warp' or 'lane' (include/nss.h nss_hrss_engine)."""
-        code = {"auto": 0, "warp": 1, "lane": 2}[engine]
+        """"auto", "warp", "lane" or "batch" (include/nss.h nss_hrss_engine)."""
+        code = {"auto": 0, "warp": 1, "lane": 2, "batch": 3}[engine]
         self._check(lib().nss_set_hrss_engine(self._h, code), "nss_set_hrss_engine")
 
     def engine(self) -> str:
         e = C.c_int32()
         self._check(lib().nss_get_hrss_engine(self._h, C.byref(e)), "nss_get_hrss_engine")
-        return {1: "warp", 2: "lane"}[e.value]
+        return {1: "warp", 2: "lane", 3: "batch"}[e.value]
 
     def phase_times(self) -> Dict:
         """Summed ms and launches per phase since timing was enabled."""

@@ -53,15 +53,15 @@ CASES = {
 }
 
 
-@pytest.mark.parametrize("engine", ["warp", "lane"])
+@pytest.mark.parametrize("engine", ["warp", "lane", "batch"])
 @pytest.mark.parametrize("name", sorted(CASES))
 def test_single_iteration_parity(name, engine):
     make, kw, warm = CASES[name]
     prob = make()
     cfg = W.config(seed=11, **kw)
     gpu, ref = inject_pair(prob, cfg, warm_iters=warm, engine=engine)
-    if engine == "lane" and gpu.engine() != "lane":
-        pytest.skip("lane engine does not apply to this case")
+    if engine != "warp" and gpu.engine() != engine:
+        pytest.skip(f"{engine} engine does not apply to this case")
     # metric from the same injected cloud
     Lg, wg = gpu.metric()
     Lr, wr = ref.metric()
@@ -267,3 +267,42 @@ def test_errors():
     with pytest.raises(nss.NssError) as ei:
         g2.step()
     assert ei.value.code == 7
+
+
+def test_c4_full_size_iteration_subset():
+    """C4 at full size (n=2e4, k=1e4, p=100, N=1e4, d=100) through the tensor-core
+    batch engine; the oracle replays 6 chains of the same iteration."""
+    import numpy as np
+    from oracle import nsso
+    from paper_2601_23252_b200 import nss
+    prob, cfg = W.workload("C4", seed=3)
+    gpu = nss.Sampler(prob, cfg)
+    assert gpu.engine() == "batch"
+    x0, _ = gpu.get_live()
+    a = x0.astype(np.float64) @ prob.data_x.T
+    e32 = np.sum(np.logaddexp(0.0, a) - prob.data_y * a, axis=1).astype(np.float32)
+    gpu.set_live(x0, e32, 1)
+    ref = nsso.Oracle(prob, dict(cfg, n_live=cfg["n_live"]))
+    ref.set_live(x0.astype(np.float64), e32.astype(np.float64), 1)
+    chains = [0, 1, 777, 5000, 9998, 9999]
+    ref.set_chain_subset(chains)
+    gpu.step()
+    ref.step()
+    tg, tr = gpu.trace(), ref.trace()
+    for key in ("dead_gid", "dest_gid", "parent_gid"):
+        assert np.array_equal(tg[key], tr[key]), key
+    xg, eg = gpu.get_live()
+    xr, er = ref.get_live()
+    good = 0
+    for c in chains:
+        diff = np.nonzero(np.any(tg["counts"][c] != tr["counts"][c], axis=1))[0]
+        if diff.size:
+            assert np.min(tr["min_margin"][c, : diff[0] + 1]) < 1e-5, (c, diff[0])
+            continue
+        good += 1
+        s = tg["dest_gid"][c]
+        assert np.allclose(xg[s], xr[s], rtol=1e-5, atol=1e-5)
+        assert abs(eg[s] - er[s]) <= 1e-5 * abs(er[s])
+    assert good >= 5
+    info = gpu.info()
+    assert info["null_moves"] == 0 and info["energy_evals"] > 1e6
