@@ -22,7 +22,8 @@ struct BatchDev {
   // probe buffers, double-buffered by round parity
   float *P[2];                // [max_rows][dp] probe points (fp32)
   int *n_probe;               // [2] rows issued in the round of that parity
-  float *partial[2];          // [n_splits][p_stride] energy partial sums per row
+  float *partial[2];          // [slices][p_stride] energy partial sums per row
+  int *slices;                // [2] slices written by the energy pass of each parity
   __nv_bfloat16 *A[2];        // logistic regression: [3][p_stride][128] bf16 splits, else null
 };
 

@@ -46,11 +46,14 @@ __device__ __forceinline__ void store_chain(const BatchDev &b, int c, const Chai
   b.cnt[3 * b.k + c] = s.c_shr; b.cnt[4 * b.k + c] = s.c_null;
 }
 
-// energy of probe row `row` of the given parity: fixed-order sum of the splits
-__device__ __forceinline__ float probe_energy(const BatchDev &b, int parity, int row) {
+// energy of probe row `row` of the given parity: the slices are loaded by the
+// lanes in parallel and summed by a fixed shuffle tree (deterministic); every
+// lane returns the total
+__device__ __forceinline__ float probe_energy(const BatchDev &b, int parity, int row, int lane) {
+  const int ns = b.slices[parity];
   double acc = 0.0;
-  for (int q = 0; q < b.n_splits; ++q) acc += b.partial[parity][static_cast<long long>(q) * b.p_stride + row];
-  return static_cast<float>(acc);
+  for (int q = lane; q < ns; q += 32) acc += b.partial[parity][static_cast<long long>(q) * b.p_stride + row];
+  return static_cast<float>(warp_sum_d(acc));
 }
 
 template <int NPL>
@@ -117,16 +120,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_batch_advance(RunDev r,
                                                                        int parity) {
   extern __shared__ float sm[];
   const int d = r.d, lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int ldl = odd_stride(d);
-  float *sL = sm;
-  float *sZ = sL + d * ldl + wib * (NPL * 32);
+  float *sZ = sm + wib * (NPL * 32);
   const DevState *st = r.st;
   if (st->terminated || st->error || st->finalised) return;  // uniform (written by other kernels)
-  for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
-    const int i = e / d, j = e - i * d;
-    sL[i * ldl + j] = r.L[i * r.dp + j];
-  }
-  __syncthreads();
   const int c = blockIdx.x * kWarpsPerBlock + wib;
   if (c >= r.k) return;
   ChainRegs s;
@@ -152,8 +148,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_batch_advance(RunDev r,
   }
   // results of the probes this chain issued last round
   float E0 = 0.f, E1 = 0.f;
-  if (s.row0 >= 0) E0 = probe_energy(b, prev, s.row0);
-  if (s.row1 >= 0) E1 = probe_energy(b, prev, s.row1);
+  if (s.row0 >= 0) E0 = probe_energy(b, prev, s.row0, lane);
+  if (s.row1 >= 0) E1 = probe_energy(b, prev, s.row1, lane);
   bool nan_seen = false;
 
   // in-slice test of x + t v against the prior part (support and height);
@@ -210,19 +206,28 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_batch_advance(RunDev r,
         }
       }
       __syncwarp();
+      // v = L z, column by column: column m of L is contiguous in LT, so each
+      // step is one coalesced load per lane-row block
       float zz = 0.f, vv = 0.f;
+#pragma unroll
+      for (int t = 0; t < NPL; ++t) v[t] = 0.f;
+      for (int m = 0; m < d; ++m) {
+        const float zm = sZ[m];
+        const float *col = r.LT + static_cast<long long>(m) * r.dp;
+#pragma unroll
+        for (int t = 0; t < NPL; ++t) {
+          const int i = lane + 32 * t;
+          if (i < d) v[t] = fmaf(__ldg(col + i), zm, v[t]);  // L[i][m] = 0 for m > i
+        }
+      }
 #pragma unroll
       for (int t = 0; t < NPL; ++t) {
         const int i = lane + 32 * t;
-        float acc = 0.f;
         if (i < d) {
           const float zi = sZ[i];
           zz = fmaf(zi, zi, zz);
-          const float *row = sL + i * ldl;
-          for (int m = 0; m <= i; ++m) acc = fmaf(row[m], sZ[m], acc);
         }
-        v[t] = acc;
-        vv = fmaf(acc, acc, vv);
+        vv = fmaf(v[t], v[t], vv);
       }
       const float inv = 1.f / sqrtf(warp_sum(euclid ? vv : zz));
 #pragma unroll
@@ -398,7 +403,7 @@ void begin_t(const RunDev &r, const PriorDev &pr, const BatchDev &b, const Launc
 
 template <int NPL>
 void advance_t(const RunDev &r, const PriorDev &pr, const BatchDev &b, int parity, const LaunchCtx &lc) {
-  const size_t smem = (static_cast<size_t>(r.d) * odd_stride(r.d) + kWarpsPerBlock * NPL * 32) * sizeof(float);
+  const size_t smem = static_cast<size_t>(kWarpsPerBlock) * NPL * 32 * sizeof(float);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_batch_advance<NPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);

@@ -4,19 +4,25 @@
 //   E(theta_p) = sum_{r < N} softplus(a_pr) - y_r a_pr,   a = X theta_p
 //
 // The logits are a dense contraction [P x d] . [d x N], so they run on the
-// tensor cores: X is stored bf16-exact and each probe is
-// split into three bf16 terms theta = hi + mid + lo (24 significant bits), so
-// the three bf16 products accumulate in fp32 to fp32-level logits.
-// Orientation: M = probes (one TMEM lane = one probe), N = data rows, K = d
-// (padded to 112 = 7 UMMA k-steps of 16).  A CTA keeps its 128 probes (3 splits
-// x 2 swizzle atoms, 96 KB) resident in shared memory and streams tiles of 128
-// data rows through a 3-stage TMA ring; the MMA warp accumulates each tile into
-// one of four TMEM buffers (4 x 128 columns) while the four epilogue warps
-// drain the previous one: each thread owns one probe row, so softplus and the
-// row sum happen in registers with no cross-lane reduction.  The grid is
-// (probe tiles) x (data splits); split partial sums are written to
-// partial[split][probe] and summed in a fixed order by the consumer, so the
-// energies are deterministic.
+// tensor cores.  X is stored bf16-exact and each probe is
+// split into bf16 terms theta = hi + mid (16 significant bits; the logit error
+// is ~1e-5 relative per row and ~1e-6 relative on E), whose
+// products accumulate in fp32 in TMEM.  Orientation: M = probes (one TMEM lane
+// = one probe), N = data rows, K = d (padded to 112 = 7 UMMA k-steps of 16).
+//
+// Persistent, balanced schedule: the grid is one CTA per SM.  The work of a
+// round -- ceil(P/128) probe tiles x T data tiles -- is cut into S slices per
+// probe tile (S chosen so there are ~8 units per SM) and the units are dealt
+// to the CTAs in contiguous ranges, so every SM gets the same number of tile
+// pairs (+-1 unit) whatever P is.  A CTA keeps its probe tile (2 splits x 2
+// swizzle atoms, 64 KB) in shared memory and reloads it only when its next
+// unit belongs to another probe tile; data tiles stream through a 4-stage TMA
+// ring; the MMA warp accumulates each tile into one of four TMEM buffers while
+// four epilogue warps drain the previous one.  Each epilogue thread owns one
+// probe row: it accumulates max(a,0) - y a and the product of (1 + e^-|a|)
+// (one ex2 per element, one lg2 per 64), with no cross-lane reduction.  Unit
+// sums go to partial[slice][probe] and are summed in slice order by the
+// consumer, so energies are deterministic for a given P.
 #include "nss_internal.cuh"
 #include "tc_ptx.cuh"
 
@@ -24,57 +30,72 @@ namespace nss {
 
 namespace {
 
-constexpr int BM = 128;          // probes per CTA (UMMA M)
+constexpr int BM = 128;          // probes per tile (UMMA M)
 constexpr int BN = 128;          // data rows per tile (UMMA N)
 constexpr int KSTEPS = 7;        // K = 112 >= d
-constexpr int kStages = 3;       // TMA ring depth for X tiles
+constexpr int kSplits = 2;       // bf16 terms per probe coordinate
+constexpr int kStages = 4;       // TMA ring depth for X tiles
 constexpr int kAcc = 4;          // TMEM accumulator buffers (4 x 128 columns)
 constexpr int kAtom = BM * 128;  // bytes of one [128 rows x 128 B] swizzle-128B region
-constexpr int kSmemA = 3 * 2 * kAtom;            // 3 splits x 2 k-blocks
+constexpr int kSmemA = kSplits * 2 * kAtom;      // splits x 2 k-blocks
 constexpr int kSmemB = kStages * 2 * kAtom;      // stages x 2 k-blocks
-constexpr int kThreads = 192;                    // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
+constexpr int kEpiWarps = 8;                     // two per TMEM lane quarter (column halves)
+constexpr int kThreads = 64 + 32 * kEpiWarps;    // warp 0 TMA, warp 1 MMA, warps 2.. epilogue
+constexpr int kUnitsPerSM = 8;
 
 struct __align__(8) Bars {
-  uint64_t a_full;
+  uint64_t a_full, a_empty;
   uint64_t full[kStages], empty[kStages];
   uint64_t tfull[kAcc], tempty[kAcc];
   uint32_t tmem_base;
 };
 
-__device__ __forceinline__ float softplus_mufu(float a) {
-  // max(a, 0) + log(1 + e^-|a|) with the MUFU ex2 / lg2 units
-  const float t = exp2f(-fabsf(a) * 1.4426950408889634f);
-  return fmaxf(a, 0.f) + 0.6931471805599453f * __log2f(1.f + t);
-}
+struct Sched {
+  int m_tiles, S, units;
+  __device__ Sched(int n_probe, int n_tiles, int G) {
+    m_tiles = (n_probe + BM - 1) / BM;
+    int s = m_tiles > 0 ? (kUnitsPerSM * G + m_tiles - 1) / m_tiles : 1;
+    S = s < 1 ? 1 : (s > n_tiles ? n_tiles : s);
+    units = m_tiles * S;
+  }
+  __device__ void range(int cta, int G, int &u0, int &u1) const {
+    u0 = static_cast<int>(static_cast<long long>(units) * cta / G);
+    u1 = static_cast<int>(static_cast<long long>(units) * (cta + 1) / G);
+  }
+};
 
 __global__ void __launch_bounds__(kThreads, 1)
     k_lr_energy(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const float *y,
-                float *partial, const int *n_probe_ptr, int *reset_counter, int p_stride, int n_data, int n_tiles,
-                int tiles_per_split) {
+                float *partial, int *slices_out, const int *n_probe_ptr, int *reset_counter, int p_stride,
+                int n_data, int n_tiles) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sA = smem;
   uint8_t *sB = smem + kSmemA;
   Bars *bars = reinterpret_cast<Bars *>(smem + kSmemA + kSmemB);
 
-  if (reset_counter && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *reset_counter = 0;
+  const int G = gridDim.x;
   const int n_probe = *n_probe_ptr;
-  const int m0 = blockIdx.x * BM;
-  if (m0 >= n_probe) return;  // uniform per CTA, before any barrier or TMEM use
-  const int t_begin = blockIdx.y * tiles_per_split;
-  const int t_end = min(n_tiles, t_begin + tiles_per_split);
-  const int nt = t_end - t_begin;
+  const Sched sch(n_probe, n_tiles, G);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (reset_counter) *reset_counter = 0;  // the next round's row counter
+    *slices_out = 2 * sch.S;                // per unit: one slice per column half
+  }
+  int u0, u1;
+  sch.range(blockIdx.x, G, u0, u1);
+  if (n_probe <= 0 || u0 >= u1) return;  // uniform per CTA, before any barrier or TMEM use
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     tc::mbar_init(&bars->a_full, 1);
+    tc::mbar_init(&bars->a_empty, 1);
     for (int s = 0; s < kStages; ++s) {
       tc::mbar_init(&bars->full[s], 1);
       tc::mbar_init(&bars->empty[s], 1);
     }
     for (int a = 0; a < kAcc; ++a) {
       tc::mbar_init(&bars->tfull[a], 1);
-      tc::mbar_init(&bars->tempty[a], 4);  // the four epilogue warps
+      tc::mbar_init(&bars->tempty[a], kEpiWarps);
     }
     tc::fence_barrier_init();
   }
@@ -84,82 +105,123 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc::tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
 
-  if (warp == 0 && lane == 0 && nt > 0) {
+  if (warp == 0 && lane == 0) {
     // ---------------- TMA producer ----------------
     tc::tma_prefetch(&tmA);
     tc::tma_prefetch(&tmB);
-    tc::mbar_arrive_expect_tx(&bars->a_full, kSmemA);
-    for (int s = 0; s < 3; ++s)
-      for (int kb = 0; kb < 2; ++kb)
-        tc::tma_load_2d(sA + (s * 2 + kb) * kAtom, &tmA, &bars->a_full, kb * 64, s * p_stride + m0);
-    for (int i = 0; i < nt; ++i) {
-      const int st = i % kStages;
-      if (i >= kStages) tc::mbar_wait(&bars->empty[st], ((i / kStages) - 1) & 1);
-      tc::mbar_arrive_expect_tx(&bars->full[st], 2 * kAtom);
-      const int row0 = (t_begin + i) * BN;
-      for (int kb = 0; kb < 2; ++kb) tc::tma_load_2d(sB + (st * 2 + kb) * kAtom, &tmB, &bars->full[st], kb * 64, row0);
+    int it = 0, a_loads = 0, prev_m = -1;
+    for (int u = u0; u < u1; ++u) {
+      const int m = u / sch.S, s = u - m * sch.S;
+      if (m != prev_m) {
+        if (a_loads > 0) tc::mbar_wait(&bars->a_empty, (a_loads - 1) & 1);
+        tc::mbar_arrive_expect_tx(&bars->a_full, kSmemA);
+        for (int q = 0; q < kSplits; ++q)
+          for (int kb = 0; kb < 2; ++kb)
+            tc::tma_load_2d(sA + (q * 2 + kb) * kAtom, &tmA, &bars->a_full, kb * 64, q * p_stride + m * BM);
+        ++a_loads;
+        prev_m = m;
+      }
+      const int t0 = s * n_tiles / sch.S, t1 = (s + 1) * n_tiles / sch.S;
+      for (int t = t0; t < t1; ++t, ++it) {
+        const int st = it % kStages;
+        if (it >= kStages) tc::mbar_wait(&bars->empty[st], ((it / kStages) - 1) & 1);
+        tc::mbar_arrive_expect_tx(&bars->full[st], 2 * kAtom);
+        for (int kb = 0; kb < 2; ++kb)
+          tc::tma_load_2d(sB + (st * 2 + kb) * kAtom, &tmB, &bars->full[st], kb * 64, t * BN);
+      }
     }
-  } else if (warp == 1 && lane == 0 && nt > 0) {
+  } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer ----------------
     constexpr uint32_t idesc = tc::idesc_bf16_f32(BM, BN);
-    tc::mbar_wait(&bars->a_full, 0);
-    tc::tc_fence_after();
-    for (int i = 0; i < nt; ++i) {
-      const int st = i % kStages, acc = i % kAcc;
-      if (i >= kAcc) tc::mbar_wait(&bars->tempty[acc], ((i / kAcc) - 1) & 1);
-      tc::mbar_wait(&bars->full[st], (i / kStages) & 1);
-      tc::tc_fence_after();
-      const uint32_t d_tmem = tmem + acc * BN;
-#pragma unroll
-      for (int s = 0; s < 3; ++s) {
-#pragma unroll
-        for (int ks = 0; ks < KSTEPS; ++ks) {
-          const int kb = ks >> 2, koff = (ks & 3) * 32;  // 16 bf16 = 32 B per k-step
-          const uint64_t ad = tc::umma_desc_sw128(sA + (s * 2 + kb) * kAtom + koff);
-          const uint64_t bd = tc::umma_desc_sw128(sB + (st * 2 + kb) * kAtom + koff);
-          tc::umma_f16(d_tmem, ad, bd, idesc, (s | ks) != 0);
-        }
+    int it = 0, a_loads = 0, prev_m = -1;
+    for (int u = u0; u < u1; ++u) {
+      const int m = u / sch.S, s = u - m * sch.S;
+      if (m != prev_m) {
+        if (a_loads > 0) tc::umma_commit(&bars->a_empty);  // every MMA on the old probe tile issued
+        tc::mbar_wait(&bars->a_full, a_loads & 1);
+        tc::tc_fence_after();
+        ++a_loads;
+        prev_m = m;
       }
-      tc::umma_commit(&bars->empty[st]);  // X tile consumed
-      tc::umma_commit(&bars->tfull[acc]);  // accumulator ready
+      const int t0 = s * n_tiles / sch.S, t1 = (s + 1) * n_tiles / sch.S;
+      for (int t = t0; t < t1; ++t, ++it) {
+        const int st = it % kStages, acc = it % kAcc;
+        if (it >= kAcc) tc::mbar_wait(&bars->tempty[acc], ((it / kAcc) - 1) & 1);
+        tc::mbar_wait(&bars->full[st], (it / kStages) & 1);
+        tc::tc_fence_after();
+        const uint32_t d_tmem = tmem + acc * BN;
+#pragma unroll
+        for (int q = 0; q < kSplits; ++q) {
+#pragma unroll
+          for (int ks = 0; ks < KSTEPS; ++ks) {
+            const int kb = ks >> 2, koff = (ks & 3) * 32;  // 16 bf16 = 32 B per k-step
+            const uint64_t ad = tc::umma_desc_sw128(sA + (q * 2 + kb) * kAtom + koff);
+            const uint64_t bd = tc::umma_desc_sw128(sB + (st * 2 + kb) * kAtom + koff);
+            tc::umma_f16(d_tmem, ad, bd, idesc, (q | ks) != 0);
+          }
+        }
+        tc::umma_commit(&bars->empty[st]);   // X tile consumed
+        tc::umma_commit(&bars->tfull[acc]);  // accumulator ready
+      }
     }
   } else if (warp >= 2) {
-    // ---------------- epilogue: one probe row per thread ----------------
-    const int quarter = warp & 3;  // TMEM lanes this warp may access
-    const int row = quarter * 32 + lane;
-    double e_sum = 0.0;
-    for (int i = 0; i < nt; ++i) {
-      const int acc = i % kAcc;
-      tc::mbar_wait(&bars->tfull[acc], (i / kAcc) & 1);
-      tc::tc_fence_after();
-      const int col0 = (t_begin + i) * BN;
-      float part = 0.f;
+    // ---------------- epilogue: one probe row per thread, half the columns ----------------
+    const int quarter = warp & 3;             // TMEM lanes this warp may access
+    const int chalf = (warp - 2) >> 2;        // column half of the tile: 0 or 1
+    const int row_in_tile = quarter * 32 + lane;
+    int it = 0;
+    for (int u = u0; u < u1; ++u) {
+      const int m = u / sch.S, s = u - m * sch.S;
+      const int t0 = s * n_tiles / sch.S, t1 = (s + 1) * n_tiles / sch.S;
+      double e_sum = 0.0;
+      for (int t = t0; t < t1; ++t, ++it) {
+        const int acc = it % kAcc;
+        tc::mbar_wait(&bars->tfull[acc], (it / kAcc) & 1);
+        tc::tc_fence_after();
+        const int cbase = chalf * (BN / 2);
+        const int col0 = t * BN + cbase;
+        float v[2][32];
+        tc::tmem_ld32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + cbase, v[0]);
+        tc::tmem_ld32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + cbase + 32, v[1]);
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&bars->tempty[acc]);  // buffer fully read: release it
+        // softplus(a) - y a = max(a,0) - y a + log(1 + e^-|a|): two independent
+        // chains each of the linear part and of the product of (1 + e^-|a|)
+        float lin0 = 0.f, lin1 = 0.f, p0 = 1.f, p1 = 1.f;
+        const int valid = n_data - col0;  // >= 64 except in the ragged last tile
+        const float4 *y4 = reinterpret_cast<const float4 *>(y + col0);
 #pragma unroll
-      for (int c = 0; c < BN; c += 32) {
-        float v[32];
-        tc::tmem_ld32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + c, v);
-        if (c + 32 == BN) {  // all loads of this buffer done: release it to the MMA warp
-          tc::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive(&bars->tempty[acc]);
-        }
-        const float4 *y4 = reinterpret_cast<const float4 *>(y + col0 + c);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < 16; ++q) {
           const float4 yy = __ldg(y4 + q);
           const float yv[4] = {yy.x, yy.y, yy.z, yy.w};
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int cc = c + 4 * q + u;
-            const float a = v[4 * q + u];
-            const float t = softplus_mufu(a) - yv[u] * a;
-            part += (col0 + cc < n_data) ? t : 0.f;
+          for (int w = 0; w < 4; ++w) {
+            const int cc = 4 * q + w;
+            float a = v[cc >> 5][cc & 31];
+            float yc = yv[w];
+            if (valid < 64 && cc >= valid) {  // padded data rows contribute nothing
+              a = -INFINITY;
+              yc = 0.f;
+            }
+            const float e = tc::ex2_approx(-fabsf(a) * 1.4426950408889634f);
+            const float l = fmaf(-yc, a, fmaxf(a, 0.f));
+            if (w & 1) {
+              p1 = fmaf(p1, e, p1);
+              lin1 += (a == -INFINITY) ? 0.f : l;
+            } else {
+              p0 = fmaf(p0, e, p0);
+              lin0 += (a == -INFINITY) ? 0.f : l;
+            }
           }
         }
+        // each product has <= 32 factors in (1, 2]: no overflow
+        e_sum += static_cast<double>(fmaf(0.6931471805599453f, __log2f(p0) + __log2f(p1), lin0 + lin1));
       }
-      e_sum += static_cast<double>(part);
+      const int row = m * BM + row_in_tile;
+      // the two column halves write adjacent slices: slice index 2 s + half
+      if (row < n_probe) partial[static_cast<long long>(2 * s + chalf) * p_stride + row] = static_cast<float>(e_sum);
     }
-    if (m0 + row < n_probe) partial[static_cast<long long>(blockIdx.y) * p_stride + m0 + row] = static_cast<float>(e_sum);
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -169,21 +231,27 @@ __global__ void __launch_bounds__(kThreads, 1)
 }  // namespace
 
 size_t lr_energy_smem() { return kSmemA + kSmemB + sizeof(Bars) + 1024; }
+int lr_energy_splits() { return kSplits; }
 
-void launch_lr_energy(const CUtensorMap &tmA, const CUtensorMap &tmB, const float *y, float *partial,
-                      const int *n_probe, int *reset_counter, int p_stride, int max_probe, int n_data, int n_splits,
-                      const LaunchCtx &lc) {
+int lr_max_slices(int n_tiles) { return 2 * n_tiles; }
+
+void launch_lr_energy(const CUtensorMap &tmA, const CUtensorMap &tmB, const float *y, float *partial, int *slices_out,
+                      const int *n_probe, int *reset_counter, int p_stride, int n_data, const LaunchCtx &lc) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_lr_energy, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lr_energy_smem()));
     attr = true;
   }
   NSS_PIN_CARVEOUT(k_lr_energy);
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
   const int n_tiles = (n_data + BN - 1) / BN;
-  const int tps = (n_tiles + n_splits - 1) / n_splits;
-  dim3 grid((max_probe + BM - 1) / BM, n_splits);
-  k_lr_energy<<<grid, kThreads, lr_energy_smem(), lc.stream>>>(tmA, tmB, y, partial, n_probe, reset_counter, p_stride,
-                                                              n_data, n_tiles, tps);
+  k_lr_energy<<<sms, kThreads, lr_energy_smem(), lc.stream>>>(tmA, tmB, y, partial, slices_out, n_probe, reset_counter,
+                                                             p_stride, n_data, n_tiles);
   ++*lc.launch_counter;
 }
 

@@ -216,6 +216,7 @@ __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials,
   for (int e = tid; e < d * r.dp; e += blockDim.x) {
     const int i = e / r.dp, j = e - i * r.dp;
     r.L[e] = j < d ? static_cast<float>(Lo[i * d + j]) : 0.0f;
+    if (j < d) r.LT[j * r.dp + i] = static_cast<float>(Lo[i * d + j]);  // column-major copy
   }
   if (tid == 0) st->stamp[12] = global_ns();
   // slice width (R-7)

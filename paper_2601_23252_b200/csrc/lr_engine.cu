@@ -12,9 +12,9 @@
 namespace nss {
 
 size_t lr_energy_smem();
-void launch_lr_energy(const CUtensorMap &tmA, const CUtensorMap &tmB, const float *y, float *partial,
-                      const int *n_probe, int *reset_counter, int p_stride, int max_probe, int n_data, int n_splits,
-                      const LaunchCtx &lc);
+int lr_max_slices(int n_tiles);
+void launch_lr_energy(const CUtensorMap &tmA, const CUtensorMap &tmB, const float *y, float *partial, int *slices_out,
+                      const int *n_probe, int *reset_counter, int p_stride, int n_data, const LaunchCtx &lc);
 
 namespace {
 
@@ -35,8 +35,8 @@ __global__ void k_split3(const float *P, int ldp, const int *n_probe_ptr, int d,
   }
 }
 
-__global__ void k_lr_reduce(const float *partial, int p_stride, int n_splits, const int *n_probe_ptr, float *E) {
-  const int n_probe = *n_probe_ptr;
+__global__ void k_lr_reduce(const float *partial, int p_stride, const int *slices, const int *n_probe_ptr, float *E) {
+  const int n_probe = *n_probe_ptr, n_splits = *slices;
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n_probe; p += gridDim.x * blockDim.x) {
     double s = 0.0;
     for (int q = 0; q < n_splits; ++q) s += partial[static_cast<long long>(q) * p_stride + p];
@@ -87,10 +87,8 @@ cudaError_t lr_setup(LrEngine &L, const double *X, const double *y, long long N,
   L.n_pad = static_cast<long long>(L.n_tiles) * 128;
   L.p_stride = ((max_probe + 127) / 128) * 128;
   L.max_probe = max_probe;
-  // data splits: enough CTAs to fill the machine when the probe count is small
-  const int m_tiles = L.p_stride / 128;
-  int ns = (2 * 148 + m_tiles - 1) / m_tiles;
-  L.n_splits = ns < 1 ? 1 : (ns > L.n_tiles ? L.n_tiles : ns);
+  // data slices per probe tile are chosen per round by the kernel (<= n_tiles)
+  L.n_splits = lr_max_slices(L.n_tiles);
   std::vector<__nv_bfloat16> xb(static_cast<size_t>(L.n_pad) * 128, __float2bfloat16_rn(0.f));
   std::vector<float> yf(static_cast<size_t>(L.n_pad), 0.f);
   for (long long r = 0; r < N; ++r) {
@@ -106,6 +104,8 @@ cudaError_t lr_setup(LrEngine &L, const double *X, const double *y, long long N,
     if ((e = cudaMalloc(&L.partial[q], static_cast<size_t>(L.n_splits) * L.p_stride * sizeof(float)))) return e;
     if ((e = cudaMemset(L.partial[q], 0, static_cast<size_t>(L.n_splits) * L.p_stride * sizeof(float)))) return e;
   }
+  if ((e = cudaMalloc(&L.slices, 2 * sizeof(int)))) return e;
+  if ((e = cudaMemset(L.slices, 0, 2 * sizeof(int)))) return e;
   if ((e = cudaMemcpy(L.Xb, xb.data(), xb.size() * sizeof(__nv_bfloat16), cudaMemcpyHostToDevice))) return e;
   if ((e = cudaMemcpy(L.y, yf.data(), yf.size() * sizeof(float), cudaMemcpyHostToDevice))) return e;
   if (!make_map(&L.tmB, L.Xb, L.n_pad)) return cudaErrorInvalidValue;
@@ -117,6 +117,7 @@ cudaError_t lr_setup(LrEngine &L, const double *X, const double *y, long long N,
 void lr_free(LrEngine &L) {
   cudaFree(L.Xb);
   cudaFree(L.y);
+  cudaFree(L.slices);
   for (int q = 0; q < 2; ++q) {
     cudaFree(L.A[q]);
     cudaFree(L.partial[q]);
@@ -127,15 +128,15 @@ void lr_free(LrEngine &L) {
 // E[p] for the first *n_probe rows of P (row stride ldp, fp32).
 void lr_energies(const LrEngine &L, const float *P, int ldp, const int *n_probe, float *E, const LaunchCtx &lc) {
   k_split3<<<296, 256, 0, lc.stream>>>(P, ldp, n_probe, L.d, L.A[0], L.p_stride);
-  launch_lr_energy(L.tmA[0], L.tmB, L.y, L.partial[0], n_probe, nullptr, L.p_stride, L.max_probe,
-                   static_cast<int>(L.N), L.n_splits, lc);
-  k_lr_reduce<<<(L.max_probe + 255) / 256, 256, 0, lc.stream>>>(L.partial[0], L.p_stride, L.n_splits, n_probe, E);
+  launch_lr_energy(L.tmA[0], L.tmB, L.y, L.partial[0], L.slices, n_probe, nullptr, L.p_stride,
+                   static_cast<int>(L.N), lc);
+  k_lr_reduce<<<(L.max_probe + 255) / 256, 256, 0, lc.stream>>>(L.partial[0], L.p_stride, L.slices, n_probe, E);
   *lc.launch_counter += 2;
 }
 
 void lr_energy_pass(const LrEngine &L, int parity, const int *n_probe, int *reset_counter, const LaunchCtx &lc) {
-  launch_lr_energy(L.tmA[parity], L.tmB, L.y, L.partial[parity], n_probe, reset_counter, L.p_stride, L.max_probe,
-                   static_cast<int>(L.N), L.n_splits, lc);
+  launch_lr_energy(L.tmA[parity], L.tmB, L.y, L.partial[parity], L.slices + parity, n_probe, reset_counter,
+                   L.p_stride, static_cast<int>(L.N), lc);
 }
 
 }  // namespace nss

@@ -14,6 +14,7 @@ struct LrEngine {
   float *y = nullptr;           // [n_pad] labels (0 past N)
   __nv_bfloat16 *A[2] = {nullptr, nullptr};   // per round parity: [3][p_stride][128] splits hi / mid / lo
   float *partial[2] = {nullptr, nullptr};     // per round parity: [n_splits][p_stride]
+  int *slices = nullptr;                      // [2] data slices used by the last pass of each parity
   CUtensorMap tmA[2]{}, tmB{};
 };
 

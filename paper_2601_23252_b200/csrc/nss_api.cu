@@ -293,6 +293,7 @@ nss_status ensure_batch(nss_ctx *c) {
     }
     b.n_splits = c->lr.n_splits;
     b.p_stride = c->lr.p_stride;
+    b.slices = c->lr.slices;
     for (int q = 0; q < 2; ++q) {
       b.partial[q] = c->lr.partial[q];
       b.A[q] = c->lr.A[q];
@@ -300,6 +301,12 @@ nss_status ensure_batch(nss_ctx *c) {
   } else {
     b.n_splits = 1;
     b.p_stride = b.max_rows;
+    {
+      nss_status s;
+      if ((s = dalloc(c, &b.slices, 2))) return s;
+      const int ones[2] = {1, 1};
+      CK(cudaMemcpy(b.slices, ones, sizeof(ones), cudaMemcpyHostToDevice));
+    }
     for (int q = 0; q < 2; ++q) {
       nss_status s;
       if ((s = dalloc(c, &b.partial[q], static_cast<size_t>(b.max_rows)))) return s;
@@ -610,6 +617,7 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
   if ((s = dalloc(c, &r.E, n))) return bail(s);
   if ((s = dalloc(c, &r.birth, n))) return bail(s);
   if ((s = dalloc(c, &r.L, static_cast<size_t>(d) * c->dp))) return bail(s);
+  if ((s = dalloc(c, &r.LT, static_cast<size_t>(d) * c->dp))) return bail(s);
   if ((s = dalloc(c, &r.L64, static_cast<size_t>(d) * d))) return bail(s);
   if ((s = dalloc(c, &r.dE, cap))) return bail(s);
   if ((s = dalloc(c, &r.dbirth, cap))) return bail(s);

@@ -75,6 +75,7 @@ struct RunDev {
   float term_log_ratio;
   float *X, *E, *birth;       // live set
   float *L;                   // lower Cholesky of Sigma, fp32, row stride dp
+  float *LT;                  // its transpose (column j of L contiguous), row stride dp
   double *L64;                // fp64 copy, d*d
   // dead store
   float *dE, *dbirth, *dX;

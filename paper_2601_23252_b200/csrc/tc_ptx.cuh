@@ -100,6 +100,13 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 2^x on the MUFU (flush-to-zero, ~2 ulp); 2^-inf = 0
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // K-major operand tile in the canonical 128-byte-swizzle layout: rows of
 // 128 B (64 bf16), 8-row atoms of 1024 B; SBO = 1024 B between atoms.
 __device__ __forceinline__ uint64_t umma_desc_sw128(const void *smem_tile) {
