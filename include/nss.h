@@ -203,6 +203,15 @@ nss_status nss_get_hrss_engine(nss_ctx *ctx, int32_t *engine);
 nss_status nss_lr_energy_batch(const double *X, const double *y, int64_t N, int32_t d, const double *theta,
                                int64_t P, double *E_out);
 
+/* Kernel check: GP ARD-RBF negative log marginal likelihoods (P:935-962
+ * shape; DESIGN R-22) for P hyperparameter points phi (P*(d_in+2) row-major,
+ * phi = log l_1..l_{d_in}, log sigma_f, log sigma_n), computed in fp64 by the
+ * batched-Cholesky kernel the sampler uses (phi is rounded to fp32 first, as
+ * in the sampler's state).  X: N*d_in, y: N.  E_out: P values, +inf where K
+ * is not numerically positive definite. */
+nss_status nss_gp_energy_batch(const double *X, const double *y, int64_t N, int32_t d_in, double jitter,
+                               const double *phi, int64_t P, double *E_out);
+
 /* ---- measurement hooks ---- */
 /* When enabled, the HRSS kernel launch of every iteration is bracketed by CUDA
  * events on the context's stream; nss_kernel_time returns the summed elapsed

@@ -559,6 +559,11 @@ static int validate(const nsso_prior *p, const nsso_energy *e, const nsso_config
 }
 
 int nsso_init(const nsso_prior *p, const nsso_energy *e, const nsso_config *cfg, nsso_ctx **out) {
+  return nsso_init_ex(p, e, cfg, 1, out);
+}
+
+int nsso_init_ex(const nsso_prior *p, const nsso_energy *e, const nsso_config *cfg, int draw_live,
+                 nsso_ctx **out) {
   if (!out) return NSSO_ERR_INVALID_ARG;
   *out = NULL;
   if (!validate(p, e, cfg)) return NSSO_ERR_INVALID_ARG;
@@ -611,7 +616,7 @@ int nsso_init(const nsso_prior *p, const nsso_energy *e, const nsso_config *cfg,
   c->e_star = INFINITY;
   /* prior draws with rejection, budget 100 n attempts in total */
   int64_t budget = 100 * n, used = 0;
-  for (int64_t g = 0; g < n; ++g) {
+  for (int64_t g = 0; g < (draw_live ? n : 0); ++g) {
     uint32_t a = 0;
     for (;;) {
       if (used >= budget) { nsso_destroy(c); return NSSO_ERR_PRIOR_SUPPORT; }

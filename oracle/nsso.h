@@ -103,6 +103,11 @@ typedef struct nsso_ctx nsso_ctx;
 /* ---- sampler (same call set as include/nss.h, prefix nsso_) ---- */
 int nsso_init(const nsso_prior *prior, const nsso_energy *energy,
               const nsso_config *cfg, nsso_ctx **out);
+/* Same, but draw_live = 0 skips the prior draws: the live set is all zeros
+ * until nsso_set_live (for full-size parity cases whose energies are too
+ * slow to draw n of in the oracle). */
+int nsso_init_ex(const nsso_prior *prior, const nsso_energy *energy,
+                 const nsso_config *cfg, int draw_live, nsso_ctx **out);
 int nsso_step(nsso_ctx *ctx, nsso_step_info *info);
 int nsso_run(nsso_ctx *ctx, int64_t max_iters, nsso_step_info *info);
 int nsso_finalise(nsso_ctx *ctx);

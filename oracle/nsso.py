@@ -75,6 +75,7 @@ def lib():
         P = C.POINTER
         vp = C.c_void_p
         L.nsso_init.argtypes = [P(Prior), P(Energy), P(Config), P(vp)]
+        L.nsso_init_ex.argtypes = [P(Prior), P(Energy), P(Config), C.c_int, P(vp)]
         for name in ("nsso_step", "nsso_info"):
             getattr(L, name).argtypes = [vp, P(StepInfo)]
         L.nsso_run.argtypes = [vp, C.c_int64, P(StepInfo)]
@@ -168,7 +169,7 @@ def draw_normals(seed, it, gid, phase, sub, d) -> np.ndarray:
 class Oracle:
     """One oracle NSS run (nsso_ctx)."""
 
-    def __init__(self, problem, cfg: Dict):
+    def __init__(self, problem, cfg: Dict, draw_live: bool = True):
         self.problem = problem
         self.cfg = dict(cfg)
         d = problem.d
@@ -189,7 +190,7 @@ class Oracle:
                     c=problem.c, sigma_y=problem.sigma_y, jitter=problem.jitter)
         cf = Config(**self.cfg)
         h = C.c_void_p()
-        _check(lib().nsso_init(C.byref(pr), C.byref(en), C.byref(cf), C.byref(h)), "nsso_init")
+        _check(lib().nsso_init_ex(C.byref(pr), C.byref(en), C.byref(cf), int(draw_live), C.byref(h)), "nsso_init")
         self._h = h
         self.d = d
         self.n = self.cfg["n_live"]

@@ -33,5 +33,15 @@ void batch_advance(const RunDev &r, const PriorDev &pr, const BatchDev &b, int p
 void batch_energy_generic(const RunDev &r, const EnergyDev &en, const BatchDev &b, int parity, const LaunchCtx &lc);
 void batch_finish(const RunDev &r, const BatchDev &b, const LaunchCtx &lc);
 bool batch_generic_ok(const EnergyDev &en);
+void batch_init_draw(const RunDev &r, const PriorDev &pr, const BatchDev &b, const int *pending, int *map,
+                     uint32_t attempt, const LaunchCtx &lc);
+void batch_init_accept(const RunDev &r, const BatchDev &b, const int *map, int *pending, int *n_pending,
+                       const LaunchCtx &lc);
+
+// k_gp.cu: fp64 batched GP marginal likelihood (one CTA per probe matrix)
+bool gp_setup(void **handle, const double *X, const double *y, int N, int D, double jitter);
+void gp_free(void *handle);
+void gp_set_out64(void *handle, double *e64);  // also write fp64 energies (kernel checks)
+void gp_energy_pass(void *handle, const BatchDev &b, int parity, const LaunchCtx &lc);
 
 }  // namespace nss

@@ -73,6 +73,34 @@ __device__ __forceinline__ void load_prior_lane(const PriorDev &pr, int lane, in
   }
 }
 
+// Attempt `a` of the prior draw of live point g (R-20, phase INIT): box
+// coordinates u (hi - lo) + lo, Gaussian ones by Box-Muller pairs (2m, 2m+1).
+template <int NPL>
+__device__ __forceinline__ void prior_draw(const RunDev &r, const PriorDev &pr, int g, uint32_t a, int lane,
+                                           const float (&pa)[NPL], const float (&pb)[NPL], float (&x)[NPL]) {
+  const int d = r.d;
+#pragma unroll
+  for (int t = 0; t < NPL; ++t) {
+    const int i = lane + 32 * t;
+    x[t] = 0.f;
+    if (i < d) {
+      if (pr.kind == NSS_PRIOR_BOX) {
+        uint4 b = philox_block(r, 0, g, kPhaseInit, a, i >> 2);
+        x[t] = fmaf(u01(word(b, i & 3)), pb[t] - pa[t], pa[t]);
+      } else {
+        const int m = i >> 1;  // Box-Muller pair (2m, 2m+1)
+        uint4 b = philox_block(r, 0, g, kPhaseInit, a, (2 * m) >> 2);
+        const float u1 = u01(word(b, (2 * m) & 3)), u2 = u01(word(b, (2 * m + 1) & 3));
+        const float rr = sqrtf(-2.f * logf(u1));
+        float sn, cs;
+        sincospif(2.f * u2, &sn, &cs);
+        const float z = (i & 1) ? rr * sn : rr * cs;
+        x[t] = fmaf(z, pr.sd[i], pa[t]);
+      }
+    }
+  }
+}
+
 // Warp-cooperative energy E(x); the result is identical in every lane.
 // `wbuf` is a per-warp shared buffer of NPL*32 floats.
 template <int NPL, int KIND>

@@ -370,6 +370,60 @@ __global__ void __launch_bounds__(256) k_batch_energy(RunDev r, EnergyDev en, Ba
   if (lane == 0) b.partial[parity][row] = e;
 }
 
+// Batched prior draws (R-20) for energies that only have a batched
+// implementation (GP): attempt `a` of every still-pending live point goes to
+// the probe buffer of parity 0 (row ticket, map row -> gid), the energy pass
+// evaluates them, and k_binit_accept keeps the finite ones.  Draws, budget
+// and error rules are those of k_init (k_hrss.cu).
+template <int NPL>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32) k_binit_draw(RunDev r, PriorDev pr, BatchDev b,
+                                                                     const int *pending, int *map, uint32_t a) {
+  const int lane = threadIdx.x & 31;
+  const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  DevState *st = r.st;
+  if (g >= r.n || st->error || !pending[g]) return;
+  unsigned long long used = 0;
+  if (lane == 0) used = atomicAdd(&st->init_attempts, 1ull);
+  used = __shfl_sync(kFull, used, 0);
+  if (used >= 100ull * static_cast<unsigned long long>(r.n)) {
+    if (lane == 0) raise_error(st, NSS_ERR_PRIOR_SUPPORT);
+    return;
+  }
+  float pa[NPL], pb[NPL], x[NPL];
+  load_prior_lane<NPL>(pr, lane, r.d, pa, pb);
+  prior_draw<NPL>(r, pr, g, a, lane, pa, pb, x);
+  int row = 0;
+  if (lane == 0) row = atomicAdd(&b.n_probe[0], 1);
+  row = __shfl_sync(kFull, row, 0);
+#pragma unroll
+  for (int t = 0; t < NPL; ++t) {
+    const int i = lane + 32 * t;
+    if (i < r.d) {
+      b.P[0][static_cast<long long>(row) * b.dp + i] = x[t];
+      r.X[static_cast<long long>(g) * r.dp + i] = x[t];
+    }
+  }
+  if (lane == 0) map[row] = g;
+}
+
+__global__ void k_binit_accept(RunDev r, BatchDev b, const int *map, int *pending, int *n_pending) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  DevState *st = r.st;
+  if (row >= b.n_probe[0] || st->error) return;
+  const int g = map[row];
+  const float e = b.partial[0][row];
+  atomicAdd(&st->init_evals, 1ull);
+  if (isnan(e)) {
+    raise_error(st, NSS_ERR_NAN);
+  } else if (isfinite(e)) {
+    r.E[g] = e;
+    r.birth[g] = INFINITY;
+    pending[g] = 0;
+  } else {
+    atomicAdd(n_pending, 1);
+  }
+}
+
 __global__ void k_batch_finish(RunDev r, BatchDev b) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   DevState *st = r.st;
@@ -412,6 +466,14 @@ void advance_t(const RunDev &r, const PriorDev &pr, const BatchDev &b, int parit
   NSS_PIN_CARVEOUT(k_batch_advance<NPL>);
   k_batch_advance<NPL><<<(r.k + kWarpsPerBlock - 1) / kWarpsPerBlock, kWarpsPerBlock * 32, smem, lc.stream>>>(
       r, pr, b, parity);
+  ++*lc.launch_counter;
+}
+
+template <int NPL>
+void binit_draw_t(const RunDev &r, const PriorDev &pr, const BatchDev &b, const int *pending, int *map, uint32_t a,
+                  const LaunchCtx &lc) {
+  k_binit_draw<NPL><<<(r.n + kWarpsPerBlock - 1) / kWarpsPerBlock, kWarpsPerBlock * 32, 0, lc.stream>>>(
+      r, pr, b, pending, map, a);
   ++*lc.launch_counter;
 }
 
@@ -478,6 +540,22 @@ void batch_energy_generic(const RunDev &r, const EnergyDev &en, const BatchDev &
     case NSS_E_LOGREG: energy_kind<NSS_E_LOGREG>(r, en, b, parity, lc); break;
     default: break;
   }
+}
+
+void batch_init_draw(const RunDev &r, const PriorDev &pr, const BatchDev &b, const int *pending, int *map,
+                     uint32_t attempt, const LaunchCtx &lc) {
+  switch ((r.d + 31) / 32) {
+    case 1: binit_draw_t<1>(r, pr, b, pending, map, attempt, lc); break;
+    case 2: binit_draw_t<2>(r, pr, b, pending, map, attempt, lc); break;
+    case 3: binit_draw_t<3>(r, pr, b, pending, map, attempt, lc); break;
+    default: binit_draw_t<4>(r, pr, b, pending, map, attempt, lc); break;
+  }
+}
+
+void batch_init_accept(const RunDev &r, const BatchDev &b, const int *map, int *pending, int *n_pending,
+                       const LaunchCtx &lc) {
+  k_binit_accept<<<(r.n + 255) / 256, 256, 0, lc.stream>>>(r, b, map, pending, n_pending);
+  ++*lc.launch_counter;
 }
 
 void batch_finish(const RunDev &r, const BatchDev &b, const LaunchCtx &lc) {

@@ -219,26 +219,7 @@ __global__ void __launch_bounds__(256) k_init(RunDev r, PriorDev pr, EnergyDev e
       return;
     }
     float x[NPL];
-#pragma unroll
-    for (int t = 0; t < NPL; ++t) {
-      const int i = lane + 32 * t;
-      x[t] = 0.f;
-      if (i < d) {
-        if (pr.kind == NSS_PRIOR_BOX) {
-          uint4 b = philox_block(r, 0, g, kPhaseInit, a, i >> 2);
-          x[t] = fmaf(u01(word(b, i & 3)), pb[t] - pa[t], pa[t]);
-        } else {
-          const int m = i >> 1;  // Box-Muller pair (2m, 2m+1)
-          uint4 b = philox_block(r, 0, g, kPhaseInit, a, (2 * m) >> 2);
-          const float u1 = u01(word(b, (2 * m) & 3)), u2 = u01(word(b, (2 * m + 1) & 3));
-          const float rr = sqrtf(-2.f * logf(u1));
-          float sn, cs;
-          sincospif(2.f * u2, &sn, &cs);
-          const float z = (i & 1) ? rr * sn : rr * cs;
-          x[t] = fmaf(z, pr.sd[i], pa[t]);
-        }
-      }
-    }
+    prior_draw<NPL>(r, pr, g, a, lane, pa, pb, x);
     float e = warp_energy<NPL, KIND>(x, en, es, sY, lane);
     if (lane == 0) atomicAdd(&st->init_evals, 1ull);
     if (isnan(e)) {

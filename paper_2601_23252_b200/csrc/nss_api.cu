@@ -63,13 +63,14 @@ struct nss_ctx {
   // round-synchronous batch engine (k_batch.cu) and its energy backends
   BatchDev bd{};
   bool batch_alloc = false;
-  int batch_backend = 0;  // 1 generic warp-per-probe energy, 2 tensor-core logistic regression
+  int batch_backend = 0;  // 1 generic warp-per-probe energy, 2 tensor-core logistic regression, 3 GP
   LrEngine lr{};
   bool lr_ok = false;     // logistic-regression data are bf16-exact and d <= 112
   std::vector<double> lr_x, lr_y;
   cudaGraphExec_t round_graph = nullptr;
   long long round_graph_launches = 0;
   int *h_nprobe = nullptr;  // pinned
+  void *gp = nullptr;       // fp64 batched GP marginal likelihood (k_gp.cu)
 };
 
 static const int kRoundsPerChunk = 32;
@@ -254,6 +255,7 @@ nss_status enqueue_iteration_eager(nss_ctx *c) {
 // 0 warp, 1 lane, 2 batch
 int resolve_engine(const nss_ctx *c) {
   const int want = c->r.engine;
+  if (c->en.kind == NSS_E_GP_ARD) return 2;  // no per-warp GP energy
   const bool expensive = c->en.kind == NSS_E_LOGREG && c->lr_ok;
   if (want == NSS_ENGINE_BATCH) return 2;
   if (want == NSS_ENGINE_AUTO && expensive) return 2;
@@ -261,7 +263,7 @@ int resolve_engine(const nss_ctx *c) {
 }
 
 nss_status ensure_batch(nss_ctx *c) {
-  const int backend = (c->en.kind == NSS_E_LOGREG && c->lr_ok) ? 2 : 1;
+  const int backend = c->en.kind == NSS_E_GP_ARD ? 3 : (c->en.kind == NSS_E_LOGREG && c->lr_ok) ? 2 : 1;
   if (c->batch_alloc && c->batch_backend == backend) return NSS_OK;
   if (backend == 1 && !batch_generic_ok(c->en)) return fail(c, NSS_ERR_UNSUPPORTED, "no batched energy for this kind");
   BatchDev &b = c->bd;
@@ -269,7 +271,7 @@ nss_status ensure_batch(nss_ctx *c) {
   if (!c->batch_alloc) {
     b.k = k;
     b.dp = c->dp;
-    b.max_rows = 2 * k;
+    b.max_rows = backend == 3 ? std::max(2 * k, c->r.n) : 2 * k;  // GP also draws the n initial points
     nss_status s;
     int **ints[] = {&b.phase, &b.step, &b.nl, &b.nr, &b.ns, &b.ldone, &b.rdone, &b.row0, &b.row1};
     for (int **q : ints)
@@ -324,6 +326,8 @@ void enqueue_rounds(nss_ctx *c, int count) {
     batch_advance(c->r, c->pr, c->bd, par, lc);
     if (c->batch_backend == 2)
       lr_energy_pass(c->lr, par, c->bd.n_probe + par, c->bd.n_probe + (par ^ 1), lc);
+    else if (c->batch_backend == 3)
+      gp_energy_pass(c->gp, c->bd, par, lc);
     else
       batch_energy_generic(c->r, c->en, c->bd, par, lc);
   }
@@ -440,6 +444,34 @@ nss_status enqueue_iteration(nss_ctx *c) {
   return NSS_OK;
 }
 
+// R-20 for energies with only a batched implementation: every attempt draws
+// the still-pending live points into the probe buffer, one energy pass
+// evaluates them, and the accept pass keeps the finite ones.
+nss_status init_batched(nss_ctx *c) {
+  nss_status s;
+  if ((s = ensure_batch(c))) return s;
+  int *pending = nullptr, *map = nullptr, *npend = nullptr;
+  if ((s = dalloc(c, &pending, c->r.n))) return s;
+  if ((s = dalloc(c, &map, c->r.n))) return s;
+  if ((s = dalloc(c, &npend, 1))) return s;
+  std::vector<int> ones(c->r.n, 1);
+  CK(cudaMemcpyAsync(pending, ones.data(), ones.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  LaunchCtx lc = lctx(c);
+  for (uint32_t a = 0;; ++a) {
+    CK(cudaMemsetAsync(c->bd.n_probe, 0, 2 * sizeof(int), c->stream));
+    CK(cudaMemsetAsync(npend, 0, sizeof(int), c->stream));
+    batch_init_draw(c->r, c->pr, c->bd, pending, map, a, lc);
+    gp_energy_pass(c->gp, c->bd, 0, lc);
+    batch_init_accept(c->r, c->bd, map, pending, npend, lc);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(c->h_nprobe, npend, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    if ((s = pull_state(c))) return s;  // synchronises the stream
+    if (c->h_st->error || *c->h_nprobe == 0) break;
+  }
+  CK(cudaMemsetAsync(c->bd.n_probe, 0, 2 * sizeof(int), c->stream));
+  return NSS_OK;
+}
+
 nss_status check_usable(nss_ctx *c) {
   if (!c) return NSS_ERR_INVALID_ARG;
   if (c->poisoned) return fail(c, NSS_ERR_CUDA, "context poisoned by an earlier CUDA failure");
@@ -494,7 +526,7 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
   en.c = static_cast<float>(energy->c);
   en.sigma_y = static_cast<float>(energy->sigma_y);
   en.jitter = static_cast<float>(energy->jitter);
-  if (!energy_supported(en)) {
+  if (en.kind != NSS_E_GP_ARD && !energy_supported(en)) {
     nss_destroy(c);
     return NSS_ERR_UNSUPPORTED;
   }
@@ -540,6 +572,10 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
     en.data_x = tmp;
     if ((s = upload_f32(c, &tmp, energy->data_y, energy->n_data))) return bail(s);
     en.data_y = tmp;
+  } else if (en.kind == NSS_E_GP_ARD) {
+    if (!gp_setup(&c->gp, energy->data_x, energy->data_y, static_cast<int>(energy->n_data), energy->d_in,
+                  energy->jitter))
+      return bail(c->gp ? NSS_ERR_UNSUPPORTED : NSS_ERR_OOM);
   }
 
   // ---- prior ----
@@ -651,7 +687,11 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
   }
   // ---- init: prior draws (R-20), then the first metric ----
   LaunchCtx lc = lctx(c);
-  launch_init(r, pr, en, lc);
+  if (en.kind == NSS_E_GP_ARD) {
+    if ((s = init_batched(c))) return bail(s);
+  } else {
+    launch_init(r, pr, en, lc);
+  }
   launch_metric(r, cfg->metric_reg, cfg->width_rule, cfg->width, 0, c->partials, c->ticket, c->nblk, lc);
   if (cudaGetLastError() != cudaSuccess) return bail(NSS_ERR_CUDA);
   if ((s = pull_state(c))) return bail(s);
@@ -803,6 +843,7 @@ NSS_API nss_status nss_destroy(nss_ctx *c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   drop_graph(c);
   if (c->lr.Xb) lr_free(c->lr);
+  if (c->gp) gp_free(c->gp);
   if (c->h_nprobe) cudaFreeHost(c->h_nprobe);
   for (void *p : c->allocs) cudaFree(p);
   for (auto e : c->ev_free) cudaEventDestroy(e);
@@ -1040,6 +1081,54 @@ NSS_API nss_status nss_lr_energy_batch(const double *X, const double *y, int64_t
   cudaFree(dn);
   cudaStreamDestroy(st);
   lr_free(L);
+  return e ? NSS_ERR_CUDA : NSS_OK;
+}
+
+NSS_API nss_status nss_gp_energy_batch(const double *X, const double *y, int64_t N, int32_t d_in, double jitter,
+                                       const double *phi, int64_t P, double *E_out) {
+  if (!X || !y || !phi || !E_out || N < 1 || d_in < 1 || d_in + 2 > NSS_MAX_DIM || P < 1 || P > (1 << 24))
+    return NSS_ERR_INVALID_ARG;
+  void *gp = nullptr;
+  if (!gp_setup(&gp, X, y, static_cast<int>(N), d_in, jitter)) {
+    gp_free(gp);
+    return gp ? NSS_ERR_UNSUPPORTED : NSS_ERR_OOM;
+  }
+  const int d = d_in + 2, dp = (d + 3) & ~3, np = static_cast<int>(P);
+  std::vector<float> pt(static_cast<size_t>(P) * dp, 0.f);
+  for (int64_t i = 0; i < P; ++i)
+    for (int j = 0; j < d; ++j) pt[i * dp + j] = static_cast<float>(phi[i * d + j]);
+  BatchDev b{};
+  b.dp = dp;
+  b.max_rows = np;
+  b.p_stride = np;
+  float *dP = nullptr, *dE = nullptr;
+  double *dE64 = nullptr;
+  int *dn = nullptr;
+  long long launches = 0;
+  cudaStream_t st;
+  cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  cudaError_t e = cudaMalloc(&dP, pt.size() * sizeof(float));
+  if (!e) e = cudaMalloc(&dE, P * sizeof(float));
+  if (!e) e = cudaMalloc(&dE64, P * sizeof(double));
+  if (!e) e = cudaMalloc(&dn, 2 * sizeof(int));
+  if (!e) e = cudaMemcpy(dP, pt.data(), pt.size() * sizeof(float), cudaMemcpyHostToDevice);
+  if (!e) e = cudaMemcpy(dn, &np, sizeof(int), cudaMemcpyHostToDevice);
+  if (!e) {
+    b.P[0] = b.P[1] = dP;
+    b.partial[0] = b.partial[1] = dE;
+    b.n_probe = dn;
+    gp_set_out64(gp, dE64);
+    gp_energy_pass(gp, b, 0, LaunchCtx{st, &launches});
+    e = cudaGetLastError();
+  }
+  if (!e) e = cudaStreamSynchronize(st);
+  if (!e) e = cudaMemcpy(E_out, dE64, P * sizeof(double), cudaMemcpyDeviceToHost);
+  cudaFree(dP);
+  cudaFree(dE);
+  cudaFree(dE64);
+  cudaFree(dn);
+  cudaStreamDestroy(st);
+  gp_free(gp);
   return e ? NSS_ERR_CUDA : NSS_OK;
 }
 

@@ -73,7 +73,7 @@ EXPORTS = ["nss_get_unique_id", "nss_init", "nss_step", "nss_steps", "nss_run", 
            "nss_dead", "nss_volume_reps", "nss_set_kernel_timing", "nss_kernel_time",
            "nss_launch_count", "nss_set_hrss_engine", "nss_get_hrss_engine",
            "nss_phase_times", "nss_set_overlap", "nss_set_graph",
-           "nss_debug_stamps", "nss_lr_energy_batch"]
+           "nss_debug_stamps", "nss_lr_energy_batch", "nss_gp_energy_batch"]
 
 _lib = None
 
@@ -120,6 +120,8 @@ def lib():
     L.nss_debug_stamps.argtypes = [vp, P(C.c_uint64)]
     L.nss_lr_energy_batch.argtypes = [P(C.c_double), P(C.c_double), C.c_int64, C.c_int32, P(C.c_double),
                                       C.c_int64, P(C.c_double)]
+    L.nss_gp_energy_batch.argtypes = [P(C.c_double), P(C.c_double), C.c_int64, C.c_int32, C.c_double,
+                                      P(C.c_double), C.c_int64, P(C.c_double)]
     _lib = L
     return L
 
@@ -152,6 +154,20 @@ def lr_energy_batch(data_x: np.ndarray, data_y: np.ndarray, theta: np.ndarray) -
     st = lib().nss_lr_energy_batch(_dp(X), _dp(y), X.shape[0], X.shape[1], _dp(th), th.shape[0], _dp(out))
     if st != 0:
         raise NssError(st, "nss_lr_energy_batch")
+    return out
+
+
+def gp_energy_batch(data_x: np.ndarray, data_y: np.ndarray, jitter: float, phi: np.ndarray) -> np.ndarray:
+    """fp64 GP marginal-likelihood energies of the hyperparameter rows `phi`
+    from the batched-Cholesky kernel (include/nss.h nss_gp_energy_batch)."""
+    X = _f64(np.atleast_2d(data_x))
+    y = _f64(data_y)
+    ph = np.ascontiguousarray(np.atleast_2d(np.asarray(phi, dtype=np.float64)))
+    out = np.zeros(ph.shape[0])
+    st = lib().nss_gp_energy_batch(_dp(X), _dp(y), X.shape[0], X.shape[1], float(jitter), _dp(ph), ph.shape[0],
+                                   _dp(out))
+    if st != 0:
+        raise NssError(st, "nss_gp_energy_batch")
     return out
 
 

@@ -278,11 +278,12 @@ def test_c4_full_size_iteration_subset():
     prob, cfg = W.workload("C4", seed=3)
     gpu = nss.Sampler(prob, cfg)
     assert gpu.engine() == "batch"
-    x0, _ = gpu.get_live()
+    rng = np.random.default_rng(44)  # seeded prior draws, energies by numpy (not the GPU)
+    x0 = (prob.mean + prob.sd * rng.standard_normal((cfg["n_live"], prob.d))).astype(np.float32)
     a = x0.astype(np.float64) @ prob.data_x.T
     e32 = np.sum(np.logaddexp(0.0, a) - prob.data_y * a, axis=1).astype(np.float32)
     gpu.set_live(x0, e32, 1)
-    ref = nsso.Oracle(prob, dict(cfg, n_live=cfg["n_live"]))
+    ref = nsso.Oracle(prob, cfg, draw_live=False)
     ref.set_live(x0.astype(np.float64), e32.astype(np.float64), 1)
     chains = [0, 1, 777, 5000, 9998, 9999]
     ref.set_chain_subset(chains)
