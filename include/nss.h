@@ -100,8 +100,16 @@ typedef struct {
   uint64_t seed;         /* Philox key                          */
 } nss_config;
 
-/* Multi-GPU: one process per GPU, live set sharded by gid blocks (DESIGN 9).
- * Pass NULL for a single GPU. */
+/* Multi-GPU: one process per GPU.  The HRSS chains of an
+ * iteration are split in contiguous blocks of ceil(k / world) chains per rank;
+ * the live set and dead store are replicated, and thresholding, resampling,
+ * metric and evidence run redundantly on every rank from identical state.
+ * After its chains finish, each rank's new rows reach every rank through one
+ * NCCL all-gather on the context's stream, so a multi-GPU run is bit-identical
+ * to a one-GPU run with the same seed.  nss_info counters (probes, evals, ...)
+ * are this rank's; sum them over ranks for job totals.  All ranks must call
+ * nss_step / nss_steps / nss_run the same number of times.
+ * Pass NULL for a single GPU.  nccl_uid NULL: no communicator (single GPU). */
 typedef struct {
   int32_t rank, world;
   const uint8_t *nccl_uid; /* 128 bytes from nss_get_unique_id on rank 0      */
@@ -125,7 +133,8 @@ typedef struct {
 
 typedef struct nss_ctx nss_ctx;
 
-/* Rank 0 of a multi-GPU run: fills 128 bytes to broadcast to the other ranks. */
+/* Rank 0 of a multi-GPU run: fills 128 bytes (an NCCL unique id) to
+ * broadcast to the other ranks.  UNSUPPORTED if NCCL cannot be loaded. */
 nss_status nss_get_unique_id(uint8_t out[128]);
 
 /* Validate, allocate, upload prior/energy data, draw the n initial live points
@@ -194,6 +203,12 @@ typedef enum { NSS_ENGINE_AUTO = 0, NSS_ENGINE_WARP = 1, NSS_ENGINE_LANE = 2, NS
 nss_status nss_set_hrss_engine(nss_ctx *ctx, int32_t engine);
 /* The engine the next iteration will use (resolved: WARP, LANE or BATCH). */
 nss_status nss_get_hrss_engine(nss_ctx *ctx, int32_t *engine);
+
+/* Parity hook: run only HRSS chains [c0, c1) (ordinals into the ascending
+ * destination list) from the next iteration on, without a communicator --
+ * what rank r of a multi-GPU run computes.  STATE if the
+ * context has an NCCL communicator. */
+nss_status nss_set_chain_range(nss_ctx *ctx, int32_t c0, int32_t c1);
 
 /* Kernel check: logistic-regression energies E(theta_p) = sum_r softplus(a_rp)
  * - y_r a_rp, a = X theta (P:466 shape), for P probe points theta (P*d

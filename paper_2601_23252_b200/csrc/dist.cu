@@ -1,0 +1,133 @@
+// Multi-GPU NSS: one process per GPU, HRSS chains split in
+// contiguous blocks of kc = ceil(k / W) chains per rank, live set and dead
+// store replicated.  Thresholding, resampling, metric and evidence are
+// computed redundantly on every rank from identical state (same kernels, same
+// inputs, same Philox draws), so they need no collective; after its chains
+// finish, each rank packs its kc new rows (x, E) and one NCCL all-gather
+// over NVLink hands every rank all k rows, which are written to their
+// destination slots.  A W-GPU run is therefore bit-identical to a 1-GPU run
+// with the same seed (chains are independent given the iteration's state).
+//
+// NCCL is loaded with dlopen (the copy PyTorch already mapped, when present),
+// so libnss has no link-time dependency on it.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "nss_internal.cuh"
+
+namespace nss {
+
+struct NcclApi {
+  ncclResult_t (*get_unique_id)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*all_gather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  const char *(*error_string)(ncclResult_t) = nullptr;
+};
+
+const NcclApi *nccl_api() {
+  static NcclApi api;
+  static int state = 0;  // 0 untried, 1 ok, -1 unavailable
+  if (state) return state > 0 ? &api : nullptr;
+  const char *env = getenv("NSS_NCCL_LIB");
+  const char *names[] = {env, "libnccl.so.2", "libnccl.so"};
+  void *h = nullptr;
+  for (const char *nm : names)
+    if (nm && (h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL))) break;
+  if (!h) {
+    state = -1;
+    return nullptr;
+  }
+  api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+  api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+  api.all_gather = reinterpret_cast<decltype(api.all_gather)>(dlsym(h, "ncclAllGather"));
+  api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+  api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
+  state = (api.get_unique_id && api.comm_init_rank && api.all_gather && api.comm_destroy) ? 1 : -1;
+  return state > 0 ? &api : nullptr;
+}
+
+namespace {
+
+// row of chain c: x (dp floats, zero past d) then E
+__global__ void k_pack_chains(RunDev r, float *buf, int row) {
+  const int c = r.c0 + blockIdx.x;
+  if (c >= r.c1) return;
+  const int s = r.dest_gid[c];
+  float *o = buf + static_cast<long long>(c - r.c0) * row;
+  for (int i = threadIdx.x; i < row; i += blockDim.x)
+    o[i] = i < r.dp ? r.X[static_cast<long long>(s) * r.dp + i] : r.E[s];
+}
+
+__global__ void k_unpack_chains(RunDev r, const float *all, int row) {
+  const int c = blockIdx.x;
+  if (c >= r.k || (c >= r.c0 && c < r.c1)) return;  // own rows are already in place
+  const DevState *st = r.st;
+  const int s = r.dest_gid[c];
+  const float *in = all + static_cast<long long>(c) * row;
+  for (int i = threadIdx.x; i < row; i += blockDim.x) {
+    if (i < r.dp)
+      r.X[static_cast<long long>(s) * r.dp + i] = in[i];
+    else
+      r.E[s] = in[i];
+  }
+  if (threadIdx.x == 0 && !(st->terminated || st->error || st->finalised)) r.birth[s] = st->e_star;
+}
+
+}  // namespace
+
+bool nccl_unique_id(uint8_t out[128]) {
+  const NcclApi *api = nccl_api();
+  if (!api) return false;
+  ncclUniqueId id;
+  if (api->get_unique_id(&id) != ncclSuccess) return false;
+  static_assert(sizeof(id.internal) == 128, "NCCL unique id size");
+  memcpy(out, id.internal, 128);
+  return true;
+}
+
+bool nccl_comm_init(void **comm, int world, const uint8_t uid[128], int rank, std::string *err) {
+  const NcclApi *api = nccl_api();
+  if (!api) {
+    *err = "NCCL library not found (set NSS_NCCL_LIB)";
+    return false;
+  }
+  ncclUniqueId id;
+  memcpy(id.internal, uid, 128);
+  ncclComm_t c = nullptr;
+  const ncclResult_t rc = api->comm_init_rank(&c, world, id, rank);
+  if (rc != ncclSuccess) {
+    *err = std::string("ncclCommInitRank: ") + (api->error_string ? api->error_string(rc) : "error");
+    return false;
+  }
+  *comm = c;
+  return true;
+}
+
+void nccl_comm_free(void *comm) {
+  const NcclApi *api = nccl_api();
+  if (api && comm) api->comm_destroy(static_cast<ncclComm_t>(comm));
+}
+
+// pack this rank's chain rows, all-gather kc rows per rank, scatter all k rows
+bool exchange_chains(const RunDev &r, void *comm, float *buf, float *all, int kc, const LaunchCtx &lc,
+                     std::string *err) {
+  const int row = r.dp + 1;
+  k_pack_chains<<<kc > 0 ? kc : 1, 128, 0, lc.stream>>>(r, buf, row);
+  ++*lc.launch_counter;
+  const ncclResult_t rc = nccl_api()->all_gather(buf, all, static_cast<size_t>(kc) * row, ncclFloat32,
+                                                 static_cast<ncclComm_t>(comm), lc.stream);
+  if (rc != ncclSuccess) {
+    *err = std::string("ncclAllGather: ") + (nccl_api()->error_string ? nccl_api()->error_string(rc) : "error");
+    return false;
+  }
+  k_unpack_chains<<<r.k, 128, 0, lc.stream>>>(r, all, row);
+  ++*lc.launch_counter;
+  return true;
+}
+
+}  // namespace nss

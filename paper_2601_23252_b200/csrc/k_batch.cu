@@ -86,12 +86,12 @@ __device__ __forceinline__ void emit_probe(const BatchDev &b, int parity, int ro
 template <int NPL>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_batch_begin(RunDev r, PriorDev pr, BatchDev b) {
   const int lane = threadIdx.x & 31;
-  const int c = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  const int c = r.c0 + blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     b.n_probe[0] = 0;
     b.n_probe[1] = 0;
   }
-  if (c >= r.k) return;
+  if (c >= r.c1) return;
   const DevState *st = r.st;
   const bool off = st->terminated || st->error || st->finalised;
   const int d = r.d, par = r.parent_gid[c];
@@ -123,8 +123,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_batch_advance(RunDev r,
   float *sZ = sm + wib * (NPL * 32);
   const DevState *st = r.st;
   if (st->terminated || st->error || st->finalised) return;  // uniform (written by other kernels)
-  const int c = blockIdx.x * kWarpsPerBlock + wib;
-  if (c >= r.k) return;
+  const int c = r.c0 + blockIdx.x * kWarpsPerBlock + wib;
+  if (c >= r.c1) return;
   ChainRegs s;
   load_chain(b, c, s);
   if (s.phase == kPhDone) return;
@@ -425,13 +425,13 @@ __global__ void k_binit_accept(RunDev r, BatchDev b, const int *map, int *pendin
 }
 
 __global__ void k_batch_finish(RunDev r, BatchDev b) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = r.c0 + blockIdx.x * blockDim.x + threadIdx.x;
   DevState *st = r.st;
   if (st->terminated || st->error || st->finalised) return;
   __shared__ unsigned long long acc[5];
   if (threadIdx.x < 5) acc[threadIdx.x] = 0;
   __syncthreads();
-  if (c < r.k) {
+  if (c < r.c1) {
     const int s = r.dest_gid[c];
     for (int i = 0; i < r.d; ++i) r.X[static_cast<long long>(s) * r.dp + i] = b.x[static_cast<long long>(c) * b.dp + i];
     r.E[s] = b.e[c];
@@ -448,10 +448,16 @@ __global__ void k_batch_finish(RunDev r, BatchDev b) {
   }
 }
 
+// blocks for this GPU's chains; at least one (block 0 resets the row counters)
+int chain_blocks(const RunDev &r, int per_block) {
+  const int nc = r.c1 - r.c0;
+  return nc > 0 ? (nc + per_block - 1) / per_block : 1;
+}
+
 template <int NPL>
 void begin_t(const RunDev &r, const PriorDev &pr, const BatchDev &b, const LaunchCtx &lc) {
   NSS_PIN_CARVEOUT(k_batch_begin<NPL>);
-  k_batch_begin<NPL><<<(r.k + kWarpsPerBlock - 1) / kWarpsPerBlock, kWarpsPerBlock * 32, 0, lc.stream>>>(r, pr, b);
+  k_batch_begin<NPL><<<chain_blocks(r, kWarpsPerBlock), kWarpsPerBlock * 32, 0, lc.stream>>>(r, pr, b);
   ++*lc.launch_counter;
 }
 
@@ -464,7 +470,7 @@ void advance_t(const RunDev &r, const PriorDev &pr, const BatchDev &b, int parit
     attr = true;
   }
   NSS_PIN_CARVEOUT(k_batch_advance<NPL>);
-  k_batch_advance<NPL><<<(r.k + kWarpsPerBlock - 1) / kWarpsPerBlock, kWarpsPerBlock * 32, smem, lc.stream>>>(
+  k_batch_advance<NPL><<<chain_blocks(r, kWarpsPerBlock), kWarpsPerBlock * 32, smem, lc.stream>>>(
       r, pr, b, parity);
   ++*lc.launch_counter;
 }
@@ -560,7 +566,7 @@ void batch_init_accept(const RunDev &r, const BatchDev &b, const int *map, int *
 
 void batch_finish(const RunDev &r, const BatchDev &b, const LaunchCtx &lc) {
   NSS_PIN_CARVEOUT(k_batch_finish);
-  k_batch_finish<<<(r.k + 255) / 256, 256, 0, lc.stream>>>(r, b);
+  k_batch_finish<<<chain_blocks(r, 256), 256, 0, lc.stream>>>(r, b);
   ++*lc.launch_counter;
 }
 

@@ -42,8 +42,8 @@ __global__ void __launch_bounds__(256) k_hrss(RunDev r, PriorDev pr, EnergyDev e
   stage_energy(en, sP, es);
   __syncthreads();
   if (sh_flag) return;
-  const int c = blockIdx.x * wpb + wib;
-  if (c >= r.k) return;
+  const int c = r.c0 + blockIdx.x * wpb + wib;
+  if (c >= r.c1) return;
 
   DevState *st = r.st;
   const uint32_t it = static_cast<uint32_t>(st->iter + 1);
@@ -244,7 +244,9 @@ __global__ void __launch_bounds__(256) k_init(RunDev r, PriorDev pr, EnergyDev e
 template <int NPL, int KIND>
 void launch_hrss_t(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc) {
   const int ldl = odd_stride(r.d);
-  int wpb = r.k / 296;
+  const int nc = r.c1 - r.c0;
+  if (nc <= 0) return;
+  int wpb = nc / 296;
   wpb = wpb < 1 ? 1 : (wpb > 8 ? 8 : wpb);
   const size_t smem = (static_cast<size_t>(r.d) * ldl + energy_param_floats(KIND, r.d, en.n_comp) +
                        static_cast<size_t>(wpb) * 2 * NPL * 32) * sizeof(float);
@@ -253,7 +255,7 @@ void launch_hrss_t(const RunDev &r, const PriorDev &pr, const EnergyDev &en, con
     cudaFuncSetAttribute(k_hrss<NPL, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     attr = smem;
   }
-  const int blocks = (r.k + wpb - 1) / wpb;
+  const int blocks = (nc + wpb - 1) / wpb;
   NSS_PIN_CARVEOUT((k_hrss<NPL, KIND>));
   k_hrss<NPL, KIND><<<blocks, wpb * 32, smem, lc.stream>>>(r, pr, en);
   ++*lc.launch_counter;

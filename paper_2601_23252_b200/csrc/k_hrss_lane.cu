@@ -210,8 +210,8 @@ __global__ void __launch_bounds__(256) k_hrss_lane(RunDev r, PriorDev pr, Energy
     }
   }
   if constexpr (kSmemTables) __syncthreads();
-  const int c = blockIdx.x * wpb + wib;
-  if (c >= r.k) return;
+  const int c = r.c0 + blockIdx.x * wpb + wib;
+  if (c >= r.c1) return;
 
   DevState *st = r.st;
   // issue the independent loads first; the flags are checked after
@@ -430,13 +430,15 @@ __global__ void __launch_bounds__(256) k_hrss_lane(RunDev r, PriorDev pr, Energy
 template <int D, int KIND, int K>
 void launch_lane_t(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc) {
   constexpr int ldD = D | 1;
-  int wpb = r.k / (148 * 4);
+  const int nc = r.c1 - r.c0;
+  if (nc <= 0) return;
+  int wpb = nc / (148 * 4);
   wpb = wpb < 1 ? 1 : (wpb > 8 ? 8 : wpb);
   size_t floats = 1;
   if (KIND == NSS_E_MOG) floats += 2 * kMaxComp * D + kMaxComp;
   if (KIND == NSS_E_CORR_GAUSS) floats += D + static_cast<size_t>(D) * ldD;
   const size_t smem = floats * sizeof(float);
-  const int blocks = (r.k + wpb - 1) / wpb;
+  const int blocks = (nc + wpb - 1) / wpb;
   NSS_PIN_CARVEOUT((k_hrss_lane<D, KIND, K>));
   k_hrss_lane<D, KIND, K><<<blocks, wpb * 32, smem, lc.stream>>>(r, pr, en);
   ++*lc.launch_counter;

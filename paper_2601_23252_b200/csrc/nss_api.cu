@@ -20,6 +20,11 @@
 using namespace nss;
 
 namespace nss {
+bool nccl_unique_id(uint8_t out[128]);
+bool nccl_comm_init(void **comm, int world, const uint8_t uid[128], int rank, std::string *err);
+void nccl_comm_free(void *comm);
+bool exchange_chains(const RunDev &r, void *comm, float *buf, float *all, int kc, const LaunchCtx &lc,
+                     std::string *err);
 void launch_evidence_summary(const RunDev &r, double *out, const LaunchCtx &lc);
 void launch_samples(const RunDev &r, long long N, double *logw, double *scratch, int chunk, const LaunchCtx &lc);
 }  // namespace nss
@@ -71,6 +76,10 @@ struct nss_ctx {
   long long round_graph_launches = 0;
   int *h_nprobe = nullptr;  // pinned
   void *gp = nullptr;       // fp64 batched GP marginal likelihood (k_gp.cu)
+  // multi-GPU (dist.cu): chain block [r.c0, r.c1) of kc chains, NCCL all-gather of new rows
+  void *comm = nullptr;
+  int rank = 0, world = 1, kc = 0;
+  float *xbuf = nullptr, *xall = nullptr;
 };
 
 static const int kRoundsPerChunk = 32;
@@ -81,6 +90,8 @@ nss_status fail(nss_ctx *c, nss_status s, const std::string &msg) {
   if (c) c->err = msg;
   return s;
 }
+
+nss_status exchange(nss_ctx *c);
 
 #define CK(call)                                                                   \
   do {                                                                             \
@@ -242,6 +253,7 @@ nss_status enqueue_iteration_eager(nss_ctx *c) {
     CK(cudaEventRecord(c->ev_evid, c->side));
   }
   if ((s = timed_launch(c, 0, c->stream, [&] { launch_hrss(c->r, c->pr, c->en, lc); }))) return s;
+  if ((s = exchange(c))) return s;
   if (!c->serial_evidence) CK(cudaStreamWaitEvent(c->stream, c->ev_evid, 0));
   if ((s = timed_launch(c, 3, c->stream, [&] {
          launch_metric(c->r, c->cfg.metric_reg, c->cfg.width_rule, c->cfg.width, 1, c->partials, c->ticket,
@@ -249,6 +261,17 @@ nss_status enqueue_iteration_eager(nss_ctx *c) {
        })))
     return s;
   CK(cudaGetLastError());
+  return NSS_OK;
+}
+
+// Multi-GPU: every rank's new chain rows to every rank.
+nss_status exchange(nss_ctx *c) {
+  if (!c->comm) return NSS_OK;
+  std::string err;
+  if (!exchange_chains(c->r, c->comm, c->xbuf, c->xall, c->kc, lctx(c), &err)) {
+    c->poisoned = true;
+    return fail(c, NSS_ERR_CUDA, err);
+  }
   return NSS_OK;
 }
 
@@ -404,6 +427,7 @@ nss_status enqueue_iteration_batch(nss_ctx *c) {
   } else if ((s = rounds())) {
     return s;
   }
+  if ((s = exchange(c))) return s;
   CK(cudaStreamWaitEvent(c->stream, c->ev_evid, 0));
   if ((s = timed_launch(c, 3, c->stream, [&] {
          launch_metric(c->r, c->cfg.metric_reg, c->cfg.width_rule, c->cfg.width, 1, c->partials, c->ticket,
@@ -483,7 +507,7 @@ nss_status check_usable(nss_ctx *c) {
 NSS_API nss_status nss_get_unique_id(uint8_t out[128]) {
   if (!out) return NSS_ERR_INVALID_ARG;
   std::memset(out, 0, 128);
-  return NSS_ERR_UNSUPPORTED;  // multi-GPU build: see DESIGN section 9
+  return nccl_unique_id(out) ? NSS_OK : NSS_ERR_UNSUPPORTED;
 }
 
 NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, const nss_config *cfg,
@@ -491,7 +515,9 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
   if (!out) return NSS_ERR_INVALID_ARG;
   *out = nullptr;
   if (!validate(prior, energy, cfg)) return NSS_ERR_INVALID_ARG;
-  if (dist && dist->world > 1) return NSS_ERR_UNSUPPORTED;
+  if (dist && (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world ||
+               (dist->world > 1 && !dist->nccl_uid)))
+    return NSS_ERR_INVALID_ARG;
   nss_ctx *c = new nss_ctx();
   c->cfg = *cfg;
   const int d = prior->d;
@@ -645,6 +671,8 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
   r.quadrature = cfg->quadrature;
   r.R = R;
   r.max_dead = cfg->max_dead;
+  r.c0 = 0;
+  r.c1 = static_cast<int>(k);
   r.seed_lo = static_cast<uint32_t>(cfg->seed);
   r.seed_hi = static_cast<uint32_t>(cfg->seed >> 32);
   r.term_log_ratio = static_cast<float>(cfg->term_log_ratio);
@@ -684,6 +712,22 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
     std::vector<double> ninf(R + 1, -INFINITY);
     if (cudaMemcpy(r.lz, ninf.data(), (R + 1) * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
       return bail(NSS_ERR_CUDA);
+  }
+  // ---- multi-GPU: this rank's chain block and the NCCL communicator ----
+  if (dist && dist->nccl_uid) {
+    c->rank = dist->rank;
+    c->world = dist->world;
+    c->kc = static_cast<int>((k + c->world - 1) / c->world);
+    r.c0 = static_cast<int>(std::min<long long>(k, static_cast<long long>(c->rank) * c->kc));
+    r.c1 = static_cast<int>(std::min<long long>(k, r.c0 + static_cast<long long>(c->kc)));
+    const size_t row = static_cast<size_t>(c->dp) + 1;
+    if ((s = dalloc(c, &c->xbuf, static_cast<size_t>(c->kc) * row))) return bail(s);
+    if ((s = dalloc(c, &c->xall, static_cast<size_t>(c->world) * c->kc * row))) return bail(s);
+    std::string err;
+    if (!nccl_comm_init(&c->comm, c->world, dist->nccl_uid, c->rank, &err)) {
+      c->err = err;
+      return bail(NSS_ERR_CUDA);
+    }
   }
   // ---- init: prior draws (R-20), then the first metric ----
   LaunchCtx lc = lctx(c);
@@ -844,6 +888,7 @@ NSS_API nss_status nss_destroy(nss_ctx *c) {
   drop_graph(c);
   if (c->lr.Xb) lr_free(c->lr);
   if (c->gp) gp_free(c->gp);
+  if (c->comm) nccl_comm_free(c->comm);
   if (c->h_nprobe) cudaFreeHost(c->h_nprobe);
   for (void *p : c->allocs) cudaFree(p);
   for (auto e : c->ev_free) cudaEventDestroy(e);
@@ -1130,6 +1175,18 @@ NSS_API nss_status nss_gp_energy_batch(const double *X, const double *y, int64_t
   cudaStreamDestroy(st);
   gp_free(gp);
   return e ? NSS_ERR_CUDA : NSS_OK;
+}
+
+NSS_API nss_status nss_set_chain_range(nss_ctx *c, int32_t c0, int32_t c1) {
+  nss_status s = check_usable(c);
+  if (s) return s;
+  if (c->comm) return fail(c, NSS_ERR_STATE, "chain range is fixed by the NCCL rank");
+  if (c0 < 0 || c1 < c0 || c1 > c->r.k) return NSS_ERR_INVALID_ARG;
+  CK(cudaStreamSynchronize(c->stream));
+  drop_graph(c);
+  c->r.c0 = c0;
+  c->r.c1 = c1;
+  return NSS_OK;
 }
 
 NSS_API nss_status nss_launch_count(nss_ctx *c, int64_t *launches) {

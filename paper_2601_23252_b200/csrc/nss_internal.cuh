@@ -70,6 +70,7 @@ struct RunDev {
   int dir_norm, quadrature;
   int R;
   int engine;                 // nss_hrss_engine (host-side choice)
+  int c0, c1;                 // HRSS chains [c0, c1) run here (all k on one GPU)
   long long max_dead;
   uint32_t seed_lo, seed_hi;
   float term_log_ratio;

@@ -73,7 +73,7 @@ EXPORTS = ["nss_get_unique_id", "nss_init", "nss_step", "nss_steps", "nss_run", 
            "nss_dead", "nss_volume_reps", "nss_set_kernel_timing", "nss_kernel_time",
            "nss_launch_count", "nss_set_hrss_engine", "nss_get_hrss_engine",
            "nss_phase_times", "nss_set_overlap", "nss_set_graph",
-           "nss_debug_stamps", "nss_lr_energy_batch", "nss_gp_energy_batch"]
+           "nss_debug_stamps", "nss_lr_energy_batch", "nss_gp_energy_batch", "nss_set_chain_range"]
 
 _lib = None
 
@@ -120,6 +120,7 @@ def lib():
     L.nss_debug_stamps.argtypes = [vp, P(C.c_uint64)]
     L.nss_lr_energy_batch.argtypes = [P(C.c_double), P(C.c_double), C.c_int64, C.c_int32, P(C.c_double),
                                       C.c_int64, P(C.c_double)]
+    L.nss_set_chain_range.argtypes = [vp, C.c_int32, C.c_int32]
     L.nss_gp_energy_batch.argtypes = [P(C.c_double), P(C.c_double), C.c_int64, C.c_int32, C.c_double,
                                       P(C.c_double), C.c_int64, P(C.c_double)]
     _lib = L
@@ -175,7 +176,9 @@ class Sampler:
     """One NSS run on one GPU (nss_ctx).  `problem` is a workloads.Problem and
     `cfg` a workloads.config() dict."""
 
-    def __init__(self, problem, cfg: Dict, stream: Optional[int] = None):
+    def __init__(self, problem, cfg: Dict, stream: Optional[int] = None, dist=None):
+        """dist: None (one GPU) or (rank, world, nccl_uid bytes) -- see
+        paper_2601_23252_b200.dist.sharded_sampler."""
         self.problem = problem
         self.cfg = dict(cfg)
         self._keep = []
@@ -196,11 +199,21 @@ class Sampler:
                         data_x=_dp(keep(problem.data_x)), data_y=_dp(keep(problem.data_y)),
                         c=problem.c, sigma_y=problem.sigma_y, jitter=problem.jitter)
         cf = nss_config(**self.cfg)
-        dist = None
-        if stream is not None:
-            dist = nss_dist(rank=0, world=1, nccl_uid=None, cuda_stream=C.c_void_p(stream))
+        dd = None
+        self.rank, self.world = 0, 1
+        if stream is not None or dist is not None:
+            uid = None
+            if dist is not None:
+                self.rank, self.world, raw = int(dist[0]), int(dist[1]), bytes(dist[2])
+                if len(raw) != 128:
+                    raise ValueError("nccl uid must be 128 bytes")
+                uid = (C.c_uint8 * 128).from_buffer_copy(raw)
+                self._keep.append(uid)
+            dd = nss_dist(rank=self.rank, world=self.world,
+                          nccl_uid=C.cast(uid, C.POINTER(C.c_uint8)) if uid is not None else None,
+                          cuda_stream=C.c_void_p(stream) if stream is not None else None)
         st = lib().nss_init(C.byref(pr), C.byref(en), C.byref(cf),
-                            C.byref(dist) if dist is not None else None, C.byref(self._h))
+                            C.byref(dd) if dd is not None else None, C.byref(self._h))
         if st != 0:
             raise NssError(st, "nss_init")
         self.d, self.n, self.k = d, self.cfg["n_live"], self.cfg["k"]
@@ -210,6 +223,10 @@ class Sampler:
         if st != 0:
             msg = lib().nss_last_error(self._h) if self._h else b""
             raise NssError(st, where, (msg or b"").decode())
+
+    def set_chain_range(self, c0: int, c1: int):
+        """Run only HRSS chains [c0, c1) (what one rank of a sharded run does)."""
+        self._check(lib().nss_set_chain_range(self._h, int(c0), int(c1)), "nss_set_chain_range")
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:

@@ -242,9 +242,13 @@ def test_errors():
     with pytest.raises(nss.NssError) as ei:
         nss.Sampler(W.gauss(2), W.config(n_live=10, k=10, steps=1))
     assert ei.value.code == 1
-    with pytest.raises(nss.NssError) as ei:
-        nss.Sampler(W.gp_ard(2, n_data=8), W.config(n_live=10, k=1, steps=1))
-    assert ei.value.code in (9,)
+    with pytest.raises(nss.NssError) as ei:  # rank outside the world
+        nss.Sampler(W.gauss(2), W.config(n_live=10, k=1, steps=1), dist=(2, 2, bytes(128)))
+    assert ei.value.code == 1
+    g0 = nss.Sampler(W.gauss(2), W.config(n_live=10, k=3, steps=1))
+    with pytest.raises(nss.NssError) as ei:  # chain range outside [0, k]
+        g0.set_chain_range(1, 4)
+    assert ei.value.code == 1
     p = W.gauss(2, half_width=1.0)
     p.c = float("inf")
     with pytest.raises(nss.NssError) as ei:
