@@ -18,6 +18,7 @@ constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr int kSmemKeysMax = 12288;   // keys cached in shared memory (96 KB)
 constexpr int kSmemSortMax = 8192;    // selected keys sorted in shared memory (64 KB)
+constexpr int kSmemOrdMax = 28672;    // 32-bit energy ordinals cached next to the sort buffer (112 KB)
 constexpr int kRankSortMax = 1024;    // rank sort (k^2/T compares) up to this k
 
 // Descending bitonic sort of P (power of two) keys at `buf` (shared or global).
@@ -80,7 +81,7 @@ __device__ void block_minmax(unsigned long long &mn, unsigned long long &mx, uns
 
 // Writes the dead records (R-14 birth, P:1197-1201 n_live) and copies rows.
 __device__ void write_dead(const RunDev &r, const unsigned long long *sorted, int cnt, int n_for_nlive,
-                           long long nd, int it) {
+                           long long nd, int it, bool rows) {
   for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
     const int g = static_cast<int>(sorted[j] & 0xffffffffu);
     const long long q = nd + j;
@@ -91,12 +92,69 @@ __device__ void write_dead(const RunDev &r, const unsigned long long *sorted, in
     r.dord[q] = j;
     r.diter[q] = it;
   }
+  if (!rows) return;  // copied by the grid-wide k_dead_rows
   // rows: one thread per float, consecutive threads on consecutive columns
   const long long tot = static_cast<long long>(cnt) * r.dp;
   for (long long e = threadIdx.x; e < tot; e += blockDim.x) {
     const int j = static_cast<int>(e / r.dp), i = static_cast<int>(e - static_cast<long long>(j) * r.dp);
     const int g = static_cast<int>(sorted[j] & 0xffffffffu);
     r.dX[(nd + j) * r.dp + i] = r.X[static_cast<long long>(g) * r.dp + i];
+  }
+}
+
+// Bitonic stages of one chunk of C keys (staged in shared memory at sbuf)
+// whose first element has global index `base`: sizes size_lo..size_hi with
+// strides below C, directions taken from the global index (the network of
+// bitonic_desc over the whole array).
+__device__ void bitonic_chunk(unsigned long long *sbuf, int C, int base, int size_first, int size_last,
+                              int stride_first) {
+  for (int size = size_first; size <= size_last; size <<= 1) {
+    for (int stride = (size == size_first ? stride_first : size >> 1); stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < (C >> 1); i += blockDim.x) {
+        const int lo = 2 * stride * (i / stride) + (i % stride);
+        const int hi = lo + stride;
+        const bool desc = ((base + lo) & size) == 0;
+        const unsigned long long a = sbuf[lo], b = sbuf[hi];
+        if (desc ? (a < b) : (a > b)) {
+          sbuf[lo] = b;
+          sbuf[hi] = a;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Descending bitonic sort of P (power of two) > C keys in global memory:
+// every stage with stride < C runs chunk by chunk in shared memory, only the
+// strides >= C stream through global memory (log2(P/C) (log2(P/C)+1)/2
+// passes instead of log2(P)(log2(P)+1)/2).
+__device__ void bitonic_desc_chunked(unsigned long long *g, int P, unsigned long long *sbuf, int C) {
+  auto chunk_pass = [&](int size_first, int size_last, int stride_first) {
+    for (int base = 0; base < P; base += C) {
+      for (int i = threadIdx.x; i < C; i += blockDim.x) sbuf[i] = g[base + i];
+      __syncthreads();
+      bitonic_chunk(sbuf, C, base, size_first, size_last, stride_first);
+      for (int i = threadIdx.x; i < C; i += blockDim.x) g[base + i] = sbuf[i];
+      __syncthreads();
+    }
+  };
+  chunk_pass(2, C, 1);  // sizes 2..C entirely on chip
+  for (int size = 2 * C; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride >= C; stride >>= 1) {
+      for (int i = threadIdx.x; i < (P >> 1); i += blockDim.x) {
+        const int lo = 2 * stride * (i / stride) + (i % stride);
+        const int hi = lo + stride;
+        const bool desc = (lo & size) == 0;
+        const unsigned long long a = g[lo], b = g[hi];
+        if (desc ? (a < b) : (a > b)) {
+          g[lo] = b;
+          g[hi] = a;
+        }
+      }
+      __syncthreads();
+    }
+    chunk_pass(size, size, C >> 1);  // the remaining strides C/2..1 of this size
   }
 }
 
@@ -122,13 +180,16 @@ __device__ void sort_desc(const unsigned long long *in, int cnt, unsigned long l
   unsigned long long *buf = (P <= kSmemSortMax) ? sbuf : gscratch;
   for (int i = threadIdx.x; i < P; i += blockDim.x) buf[i] = (i < cnt) ? in[i] : 0ull;
   __syncthreads();
-  bitonic_desc(buf, P);
+  if (P <= kSmemSortMax)
+    bitonic_desc(buf, P);
+  else
+    bitonic_desc_chunked(buf, P, sbuf, kSmemSortMax);
   for (int i = threadIdx.x; i < cnt; i += blockDim.x) out[i] = buf[i];
   __syncthreads();
 }
 
 __global__ void __launch_bounds__(kThreads) k_select(RunDev r, unsigned long long *gscratch,
-                                                     unsigned long long *gsel) {
+                                                     unsigned long long *gsel, bool rows) {
   extern __shared__ unsigned long long sm[];
   __shared__ unsigned hist[256];
   __shared__ int warp_tot[kWarps];
@@ -147,14 +208,23 @@ __global__ void __launch_bounds__(kThreads) k_select(RunDev r, unsigned long lon
     if (tid == 0) raise_error(st, NSS_ERR_CAPACITY);
     return;
   }
-  // ---- keys (cached in shared memory when they fit) ----
+  // ---- keys: 64-bit in shared memory (n <= kSmemKeysMax), else the 32-bit
+  //      energy ordinals in shared memory (the gid is the index), else global
   const bool cached = n <= kSmemKeysMax;
+  const bool ord32 = !cached && n <= kSmemOrdMax;
   unsigned long long *keys = cached ? sm : gscratch;
-  unsigned long long *sbuf = cached ? sm + kSmemKeysMax : sm;  // sort buffer after the key cache
+  uint32_t *ords = reinterpret_cast<uint32_t *>(sm + kSmemSortMax);
+  unsigned long long *sbuf = cached ? sm + kSmemKeysMax : sm;  // sort buffer next to the key cache
+  auto key_at = [&](int g) -> unsigned long long {
+    return ord32 ? ((static_cast<unsigned long long>(ords[g]) << 32) | static_cast<unsigned>(g)) : keys[g];
+  };
   unsigned long long mn = ~0ull, mx = 0ull;
   for (int g = tid; g < n; g += blockDim.x) {
     const unsigned long long key = key_of(r.E[g], g);
-    keys[g] = key;
+    if (ord32)
+      ords[g] = static_cast<uint32_t>(key >> 32);
+    else
+      keys[g] = key;
     mn = key < mn ? key : mn;
     mx = key > mx ? key : mx;
   }
@@ -173,7 +243,7 @@ __global__ void __launch_bounds__(kThreads) k_select(RunDev r, unsigned long lon
     for (int i = tid; i < 256; i += blockDim.x) hist[i] = 0;
     __syncthreads();
     for (int g = tid; g < n; g += blockDim.x) {
-      const unsigned long long key = keys[g];
+      const unsigned long long key = key_at(g);
       const bool m = (key & mask) == prefix;
       const unsigned dig = m ? static_cast<unsigned>((key >> shift) & dmask) : 0xffffffffu;
       const unsigned peers = __match_any_sync(__activemask(), dig);
@@ -220,11 +290,11 @@ __global__ void __launch_bounds__(kThreads) k_select(RunDev r, unsigned long lon
   const int chunk = (n + blockDim.x - 1) / blockDim.x;
   const int g0 = min(n, tid * chunk), g1 = min(n, g0 + chunk);
   int nsel = 0;
-  for (int g = g0; g < g1; ++g) nsel += ((keys[g] & mask) >= prefix) ? 1 : 0;
+  for (int g = g0; g < g1; ++g) nsel += ((key_at(g) & mask) >= prefix) ? 1 : 0;
   int off = block_exclusive_scan(nsel, warp_tot);
   int soff = g0 - off;
   for (int g = g0; g < g1; ++g) {
-    const unsigned long long key = keys[g];
+    const unsigned long long key = key_at(g);
     if ((key & mask) >= prefix) {
       r.dest_gid[off] = g;
       gsel[off] = key;
@@ -250,7 +320,7 @@ __global__ void __launch_bounds__(kThreads) k_select(RunDev r, unsigned long lon
   }
 
   // ---- dead records: n_live = n - j in key-descending order ----
-  write_dead(r, sorted, k, n, nd, it);
+  write_dead(r, sorted, k, n, nd, it, rows);
   __syncthreads();
   if (tid == 0) {
     st->dead_base = nd;
@@ -268,7 +338,7 @@ __device__ __forceinline__ float energy_of_key(unsigned long long key) {  // inv
 // selected keys, the sorted dead order, survivors and destinations all stay on
 // chip, and E* and the dead energies are decoded from the keys, so the only
 // global traffic is the energy load, the row gather and the outputs.
-__global__ void __launch_bounds__(kThreads) k_select_smem(RunDev r) {
+__global__ void __launch_bounds__(kThreads) k_select_smem(RunDev r, bool rows) {
   extern __shared__ unsigned long long sm[];
   __shared__ unsigned hist[256];
   __shared__ int warp_tot[kWarps];
@@ -408,7 +478,7 @@ __global__ void __launch_bounds__(kThreads) k_select_smem(RunDev r) {
     r.dord[q] = c;
     r.diter[q] = it;
   }
-  {
+  if (rows) {
     // dead rows: float4 granules, four loads in flight per thread before the stores
     const int dp4 = r.dp >> 2, tot = k * dp4, T = blockDim.x;
     const float4 *X4 = reinterpret_cast<const float4 *>(r.X);
@@ -462,8 +532,11 @@ __global__ void __launch_bounds__(kThreads) k_finalise_sort(RunDev r, unsigned l
   unsigned long long *buf = (P <= kSmemSortMax) ? sm : gscratch;
   for (int i = threadIdx.x; i < P; i += blockDim.x) buf[i] = (i < n) ? key_of(r.E[i], i) : 0ull;
   __syncthreads();
-  bitonic_desc(buf, P);
-  write_dead(r, buf, n, n, nd, st->iter + 1);
+  if (P <= kSmemSortMax)
+    bitonic_desc(buf, P);
+  else
+    bitonic_desc_chunked(buf, P, sm, kSmemSortMax);
+  write_dead(r, buf, n, n, nd, st->iter + 1, true);
   __syncthreads();
   if (threadIdx.x == 0) {
     st->dead_base = nd;
@@ -472,8 +545,26 @@ __global__ void __launch_bounds__(kThreads) k_finalise_sort(RunDev r, unsigned l
   (void)gsel;
 }
 
+// Dead rows of the iteration just selected, copied by the whole grid (large
+// k * d: one CTA would be bound by its own load latency).
+__global__ void k_dead_rows(RunDev r) {
+  const DevState *st = r.st;
+  if (st->terminated || st->error || st->finalised) return;  // select did not run
+  const long long nd = st->dead_base;
+  const int dp4 = r.dp >> 2;
+  const long long tot = static_cast<long long>(r.k) * dp4;
+  const float4 *X4 = reinterpret_cast<const float4 *>(r.X);
+  float4 *D4 = reinterpret_cast<float4 *>(r.dX) + nd * dp4;
+  for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < tot;
+       q += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long j = q / dp4, i = q - j * dp4;
+    D4[q] = X4[static_cast<long long>(r.dgid[nd + j]) * dp4 + i];
+  }
+}
+
 size_t select_smem(int n) {
   if (n <= kSmemKeysMax) return static_cast<size_t>(kSmemKeysMax + kSmemSortMax) * 8;
+  if (n <= kSmemOrdMax) return static_cast<size_t>(kSmemSortMax) * 8 + static_cast<size_t>(n) * 4;
   return static_cast<size_t>(kSmemSortMax) * 8;
 }
 
@@ -484,11 +575,13 @@ size_t select_smem(int n) {
 void launch_select(const RunDev &r, const LaunchCtx &lc) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (kSmemKeysMax + kSmemSortMax) * 8);
+    cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kSmemSortMax * 8 + kSmemOrdMax * 4);
     cudaFuncSetAttribute(k_finalise_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSortMax * 8);
     attr = true;
   }
   const size_t fused = select_smem_fused(r.n, r.k);
+  const bool separate_rows = static_cast<long long>(r.k) * r.dp >= 16384;
   int P = 1;
   while (P < r.k) P <<= 1;
   if (fused <= 200 * 1024 && P <= r.n) {
@@ -498,19 +591,28 @@ void launch_select(const RunDev &r, const LaunchCtx &lc) {
       attr2 = true;
     }
     NSS_PIN_CARVEOUT(k_select_smem);
-    k_select_smem<<<1, kThreads, fused, lc.stream>>>(r);
+    k_select_smem<<<1, kThreads, fused, lc.stream>>>(r, !separate_rows);
   } else {
     NSS_PIN_CARVEOUT(k_select);
-    k_select<<<1, kThreads, select_smem(r.n), lc.stream>>>(r, r.sort_scratch, r.sel_scratch);
+    k_select<<<1, kThreads, select_smem(r.n), lc.stream>>>(r, r.sort_scratch, r.sel_scratch, !separate_rows);
   }
   ++*lc.launch_counter;
+  if (separate_rows) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long long tot = static_cast<long long>(r.k) * (r.dp >> 2);
+    const long long want = (tot + 255) / 256;
+    k_dead_rows<<<static_cast<int>(want < 2 * sms ? want : 2 * sms), 256, 0, lc.stream>>>(r);
+    ++*lc.launch_counter;
+  }
 }
 
 void launch_finalise_sort(const RunDev &r, const LaunchCtx &lc) {
   cudaFuncSetAttribute(k_finalise_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSortMax * 8);
   int P = 1;
   while (P < r.n) P <<= 1;
-  const size_t smem = P <= kSmemSortMax ? static_cast<size_t>(P) * 8 : 0;
+  const size_t smem = static_cast<size_t>(P <= kSmemSortMax ? P : kSmemSortMax) * 8;
   NSS_PIN_CARVEOUT(k_finalise_sort);
   k_finalise_sort<<<1, kThreads, smem, lc.stream>>>(r, r.sort_scratch, r.sel_scratch);
   ++*lc.launch_counter;

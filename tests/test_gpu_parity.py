@@ -50,6 +50,10 @@ CASES = {
     "stepout_cap": (lambda: W.gauss(2, half_width=50.0, sigma=20.0),
                     dict(n_live=100, k=10, steps=4, width_rule=W.W_FIXED, width=0.05, max_stepout=3), 0),
     "shrink_cap": (lambda: W.gauss(4), dict(n_live=100, k=10, steps=4, max_shrink=2), 2),
+    # large-n thresholding paths of k_select: 32-bit ordinals on chip + chunked
+    # bitonic dead-order sort; keys in global memory
+    "select_ord32": (lambda: W.gauss(3), dict(n_live=20_000, k=9_000, steps=2), 0),
+    "select_global": (lambda: W.gauss(2), dict(n_live=30_000, k=10_000, steps=1), 0),
 }
 
 
