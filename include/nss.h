@@ -233,9 +233,11 @@ nss_status nss_gp_energy_batch(const double *X, const double *y, int64_t N, int3
  * milliseconds and the number of launches since the last reset. */
 nss_status nss_set_kernel_timing(nss_ctx *ctx, int32_t enable);
 nss_status nss_kernel_time(nss_ctx *ctx, double *ms, int64_t *launches);
-/* Per-phase totals of the same timing mode: ms[4] and launches[4] for
- * {HRSS, select/dead/resample, evidence, metric+termination}. */
-nss_status nss_phase_times(nss_ctx *ctx, double *ms /* 4 */, int64_t *launches /* 4 */);
+/* Per-phase totals of the same timing mode: ms[5] and launches[5] for
+ * {HRSS, select/dead/resample, evidence, metric+termination, batched energy
+ * passes}.  The last is the batch engine's energy kernels alone (also
+ * counted inside HRSS); zero for the warp and lane engines. */
+nss_status nss_phase_times(nss_ctx *ctx, double *ms /* 5 */, int64_t *launches /* 5 */);
 /* overlap != 0 (default): the evidence kernel runs on a side stream
  * concurrently with HRSS; 0: all kernels in sequence on one stream. */
 nss_status nss_set_overlap(nss_ctx *ctx, int32_t overlap);

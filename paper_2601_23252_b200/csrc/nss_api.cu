@@ -29,6 +29,8 @@ void launch_evidence_summary(const RunDev &r, double *out, const LaunchCtx &lc);
 void launch_samples(const RunDev &r, long long N, double *logw, double *scratch, int chunk, const LaunchCtx &lc);
 }  // namespace nss
 
+static const int kPhases = 5;
+
 struct nss_ctx {
   nss_config cfg{};
   int d = 0, dp = 0;
@@ -52,13 +54,13 @@ struct nss_ctx {
   bool timing = false;
   bool serial_evidence = false;  // run A8 on the main stream (no overlap)
   struct Timed {
-    int phase;  // 0 hrss, 1 select, 2 evidence, 3 metric
+    int phase;  // 0 hrss, 1 select, 2 evidence, 3 metric, 4 batched energy passes (inside 0)
     cudaEvent_t a, b;
   };
   std::vector<cudaEvent_t> ev_free;
   std::vector<Timed> ev_pending;
-  double time_ms[4] = {0, 0, 0, 0};
-  long long timed[4] = {0, 0, 0, 0};
+  double time_ms[kPhases] = {0, 0, 0, 0, 0};
+  long long timed[kPhases] = {0, 0, 0, 0, 0};
   int host_finalised = 0;
   // one iteration captured as a CUDA graph (about 1 us per kernel node
   // instead of about 3.4 us per stream launch on B200)
@@ -347,12 +349,18 @@ void enqueue_rounds(nss_ctx *c, int count) {
   for (int i = 0; i < count; ++i) {
     const int par = i & 1;
     batch_advance(c->r, c->pr, c->bd, par, lc);
-    if (c->batch_backend == 2)
-      lr_energy_pass(c->lr, par, c->bd.n_probe + par, c->bd.n_probe + (par ^ 1), lc);
-    else if (c->batch_backend == 3)
-      gp_energy_pass(c->gp, c->bd, par, lc);
+    auto energy = [&] {
+      if (c->batch_backend == 2)
+        lr_energy_pass(c->lr, par, c->bd.n_probe + par, c->bd.n_probe + (par ^ 1), lc);
+      else if (c->batch_backend == 3)
+        gp_energy_pass(c->gp, c->bd, par, lc);
+      else
+        batch_energy_generic(c->r, c->en, c->bd, par, lc);
+    };
+    if (c->timing)
+      (void)timed_launch(c, 4, c->stream, energy);  // per-launch energy timing (nss_phase_times)
     else
-      batch_energy_generic(c->r, c->en, c->bd, par, lc);
+      energy();
   }
 }
 
@@ -1015,7 +1023,7 @@ NSS_API nss_status nss_set_kernel_timing(nss_ctx *c, int32_t enable) {
   CK(cudaStreamSynchronize(c->stream));
   if ((s = collect_timing(c))) return s;
   c->timing = enable != 0;
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < kPhases; ++i) {
     c->time_ms[i] = 0.0;
     c->timed[i] = 0;
   }
@@ -1056,7 +1064,7 @@ NSS_API nss_status nss_phase_times(nss_ctx *c, double *ms, int64_t *launches) {
   CK(cudaStreamSynchronize(c->stream));
   CK(cudaStreamSynchronize(c->side));
   if ((s = collect_timing(c))) return s;
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < kPhases; ++i) {
     if (ms) ms[i] = c->time_ms[i];
     if (launches) launches[i] = c->timed[i];
   }

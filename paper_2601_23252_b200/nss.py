@@ -349,10 +349,10 @@ class Sampler:
 
     def phase_times(self) -> Dict:
         """Summed ms and launches per phase since timing was enabled."""
-        ms = (C.c_double * 4)()
-        n = (C.c_int64 * 4)()
+        ms = (C.c_double * 5)()
+        n = (C.c_int64 * 5)()
         self._check(lib().nss_phase_times(self._h, ms, n), "nss_phase_times")
-        names = ("hrss", "select", "evidence", "metric")
+        names = ("hrss", "select", "evidence", "metric", "energy")
         return {nm: (ms[i], n[i]) for i, nm in enumerate(names)}
 
     def set_overlap(self, on: bool):
