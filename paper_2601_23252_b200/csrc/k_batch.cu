@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_batch_advance(RunDev r,
   load_chain(b, c, s);
   if (s.phase == kPhDone) return;
 
-  const uint32_t it = static_cast<uint32_t>(st->iter + 1);
+  const uint32_t it = static_cast<uint32_t>(st->iter)  /* set by the select kernel */;
   const int dest = r.dest_gid[c];
   const float e_star = st->e_star, w = st->width;
   const int p = r.p, cap = r.max_stepout, maxs = r.max_shrink;

@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(256) k_hrss(RunDev r, PriorDev pr, EnergyDev e
   if (c >= r.c1) return;
 
   DevState *st = r.st;
-  const uint32_t it = static_cast<uint32_t>(st->iter + 1);
+  const uint32_t it = static_cast<uint32_t>(st->iter)  /* set by the select kernel */;
   const int s = r.dest_gid[c];
   const int par = r.parent_gid[c];
   const float e_star = st->e_star;

@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(256) k_hrss_lane(RunDev r, PriorDev pr, Energy
   for (int i = 0; i < D; ++i) x[i] = i < d ? r.X[static_cast<long long>(par) * r.dp + i] : 0.f;
   float e = r.E[par];
   if (st->terminated || st->error || st->finalised) return;
-  const uint32_t it = static_cast<uint32_t>(st->iter + 1);
+  const uint32_t it = static_cast<uint32_t>(st->iter)  /* set by the select kernel */;
   const float e_star = st->e_star;
   const float w = st->width;
   const int p = r.p, cap = r.max_stepout, maxs = r.max_shrink;

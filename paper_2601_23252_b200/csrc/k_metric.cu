@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials,
                                                      int end_of_iter) {
   DevState *st = r.st;
   if (st->error) return;
-  if (end_of_iter && (st->terminated || st->finalised)) return;
+  if (end_of_iter && st->finalised) return;
   extern __shared__ double sm[];
   const int d = r.d, n = r.n, tid = threadIdx.x;
   const int npair = d * (d + 1) / 2;
@@ -252,18 +252,26 @@ __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials,
     *ticket = 0u;  // re-arm for the next launch
     st->stamp[13] = global_ns();
     st->width = static_cast<float>(w);
-    if (end_of_iter) {
-      const float emin2 = sh_emin;
-      st->emin = emin2;
-      // A9 / R-19: stop when the live bound is below e^{term} of the total
-      const double lz_live = -static_cast<double>(emin2) + r.lx_cur[0];
-      const double lz0 = r.lz[0];
-      const double mm = fmax(lz0, lz_live);
-      const double tot = (mm == -INFINITY) ? -INFINITY : mm + log(exp(lz0 - mm) + exp(lz_live - mm));
-      st->log_z_live = lz_live;
-      if (st->n_dead > 0 && (lz_live - tot) < static_cast<double>(r.term_log_ratio)) st->terminated = 1;
-      st->iter += 1;
-    }
+    (void)sh_emin;  // termination (A9) is evaluated by the select kernels and k_term_probe
+  }
+}
+
+// A9 / R-19 on demand (the host asks for the run's state between
+// iterations): minimum live energy, then the same test the next select
+// kernel would make.
+__global__ void __launch_bounds__(kThreads) k_term_probe(RunDev r) {
+  DevState *st = r.st;
+  if (st->error || st->finalised || st->terminated) return;
+  __shared__ float red[kThreads / 32];
+  float emin = INFINITY;
+  for (int g = threadIdx.x; g < r.n; g += blockDim.x) emin = fminf(emin, r.E[g]);
+  for (int o = 16; o > 0; o >>= 1) emin = fminf(emin, __shfl_xor_sync(0xffffffffu, emin, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = emin;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < kThreads / 32; ++w) emin = fminf(emin, red[w]);
+    emin = fminf(emin, red[0]);
+    term_check(r, st, emin);
   }
 }
 
@@ -287,6 +295,11 @@ int metric_blocks(int n, int d) {
   if (rows_per_block > rows_max) rows_per_block = rows_max;
   const int b = (n + rows_per_block - 1) / rows_per_block;
   return b < 1 ? 1 : b;
+}
+
+void launch_term_probe(const RunDev &r, const LaunchCtx &lc) {
+  k_term_probe<<<1, kThreads, 0, lc.stream>>>(r);
+  ++*lc.launch_counter;
 }
 
 void launch_metric(const RunDev &r, double metric_reg, int width_rule, double width_param, int end_of_iteration,

@@ -188,6 +188,11 @@ __device__ void sort_desc(const unsigned long long *in, int cnt, unsigned long l
   __syncthreads();
 }
 
+__device__ __forceinline__ float energy_of_key(unsigned long long key) {  // inverse of ord_f32
+  const uint32_t u = static_cast<uint32_t>(key >> 32);
+  return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+
 __global__ void __launch_bounds__(kThreads) k_select(RunDev r, unsigned long long *gscratch,
                                                      unsigned long long *gsel, bool rows) {
   extern __shared__ unsigned long long sm[];
@@ -204,10 +209,6 @@ __global__ void __launch_bounds__(kThreads) k_select(RunDev r, unsigned long lon
   const int n = r.n, k = r.k, tid = threadIdx.x, lane = tid & 31;
   const long long nd = st->n_dead;
   const int it = st->iter + 1;
-  if (nd + k + n > r.max_dead) {  // R-26
-    if (tid == 0) raise_error(st, NSS_ERR_CAPACITY);
-    return;
-  }
   // ---- keys: 64-bit in shared memory (n <= kSmemKeysMax), else the 32-bit
   //      energy ordinals in shared memory (the gid is the index), else global
   const bool cached = n <= kSmemKeysMax;
@@ -229,6 +230,13 @@ __global__ void __launch_bounds__(kThreads) k_select(RunDev r, unsigned long lon
     mx = key > mx ? key : mx;
   }
   block_minmax(mn, mx, red);  // contains a barrier: keys[] is visible
+  // A9 before the iteration (R-19), then the capacity rule (R-26)
+  if (tid == 0) sh_flag = term_check(r, st, energy_of_key(mn)) ? 1 : (nd + k + n > r.max_dead ? 2 : 0);
+  __syncthreads();
+  if (sh_flag) {
+    if (sh_flag == 2 && tid == 0) raise_error(st, NSS_ERR_CAPACITY);
+    return;
+  }
   // highest differing bit: all keys agree above it
   const int hb = 63 - __clzll(mn ^ mx);
   const unsigned long long common = hb >= 63 ? 0ull : (mn >> (hb + 1)) << (hb + 1);
@@ -326,13 +334,10 @@ __global__ void __launch_bounds__(kThreads) k_select(RunDev r, unsigned long lon
     st->dead_base = nd;
     st->n_dead = nd + k;
     st->e_star = e_star;
+    st->iter = it;  // iteration `it` is under way: HRSS and evidence read it
   }
 }
 
-__device__ __forceinline__ float energy_of_key(unsigned long long key) {  // inverse of ord_f32
-  const uint32_t u = static_cast<uint32_t>(key >> 32);
-  return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
-}
 
 // Shared-memory-resident variant (the common case, n <= kSmemKeysMax): keys,
 // selected keys, the sorted dead order, survivors and destinations all stay on
@@ -366,11 +371,14 @@ __global__ void __launch_bounds__(kThreads) k_select_smem(RunDev r, bool rows) {
   const int it = st->iter + 1;
   if (flags) return;  // uniform: written only by other kernels
   if (tid == 0) st->stamp[1] = global_ns();
-  if (nd + k + n > r.max_dead) {  // R-26
-    if (tid == 0) raise_error(st, NSS_ERR_CAPACITY);
+  block_minmax(mn, mx, red);
+  // A9 before the iteration (R-19), then the capacity rule (R-26)
+  if (tid == 0) sh_kk = term_check(r, st, energy_of_key(mn)) ? 1 : (nd + k + n > r.max_dead ? 2 : 0);
+  __syncthreads();
+  if (sh_kk) {
+    if (sh_kk == 2 && tid == 0) raise_error(st, NSS_ERR_CAPACITY);
     return;
   }
-  block_minmax(mn, mx, red);
   if (tid == 0) st->stamp[2] = global_ns();
   const int hb = 63 - __clzll(mn ^ mx);
   const unsigned long long common = hb >= 63 ? 0ull : (mn >> (hb + 1)) << (hb + 1);
@@ -505,6 +513,7 @@ __global__ void __launch_bounds__(kThreads) k_select_smem(RunDev r, bool rows) {
     st->dead_base = nd;
     st->n_dead = nd + k;
     st->e_star = energy_of_key(sorted[k - 1]);
+    st->iter = it;  // iteration `it` is under way: HRSS and evidence read it
   }
 }
 

@@ -43,7 +43,14 @@ struct nss_ctx {
   double *partials = nullptr;
   unsigned *ticket = nullptr;   // last-block-done counter of k_metric
   cudaStream_t side = nullptr;  // evidence runs here, concurrently with HRSS
-  cudaEvent_t ev_sel = nullptr, ev_evid = nullptr;
+  cudaStream_t side2 = nullptr;  // the previous iteration's metric, concurrently with the select
+  cudaEvent_t ev_sel = nullptr, ev_evid = nullptr, ev_fork = nullptr, ev_met = nullptr;
+  // A5 of iteration i only feeds HRSS of iteration i+1, so it is deferred into
+  // the next iteration (overlapping its select) and computed on demand when the
+  // host asks for the metric; A9 is evaluated by the select kernel, and on
+  // demand (k_term_probe) when the host reads the state.
+  bool metric_pending = false;
+  bool term_stale = false;
   int nblk = 1;
   double *summary = nullptr;  // device: [mean, std, closed lz_0..R]
   DevState *h_st = nullptr;   // pinned mirror of the device state
@@ -65,8 +72,8 @@ struct nss_ctx {
   // one iteration captured as a CUDA graph (about 1 us per kernel node
   // instead of about 3.4 us per stream launch on B200)
   bool use_graph = true;
-  cudaGraphExec_t graph = nullptr;
-  long long graph_launches = 0;
+  cudaGraphExec_t graph = nullptr, graph0 = nullptr;  // with / without the deferred metric
+  long long graph_launches = 0, graph0_launches = 0;
   // round-synchronous batch engine (k_batch.cu) and its energy backends
   BatchDev bd{};
   bool batch_alloc = false;
@@ -177,6 +184,11 @@ nss_status device_error(nss_ctx *c) {
 }
 
 nss_status pull_state(nss_ctx *c) {
+  if (c->term_stale) {  // A9 at the end of the last enqueued iteration (R-19)
+    LaunchCtx lc{c->stream, &c->launches};
+    launch_term_probe(c->r, lc);
+    c->term_stale = false;
+  }
   CK(cudaMemcpyAsync(c->h_st, c->r.st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   return NSS_OK;
@@ -239,29 +251,45 @@ nss_status timed_launch(nss_ctx *c, int phase, cudaStream_t stream, F &&launch) 
   return NSS_OK;
 }
 
-nss_status enqueue_iteration_eager(nss_ctx *c) {
+nss_status launch_metric_on(nss_ctx *c, cudaStream_t stream, int end_of_iter) {
+  LaunchCtx l{stream, &c->launches};
+  return timed_launch(c, 3, stream, [&] {
+    launch_metric(c->r, c->cfg.metric_reg, c->cfg.width_rule, c->cfg.width, end_of_iter, c->partials, c->ticket,
+                  c->nblk, l);
+  });
+}
+
+// One iteration: [deferred A5 of the previous iteration || A2-A4 select] ->
+// [A8 evidence on the side stream || A6 HRSS] (-> multi-GPU exchange).
+nss_status enqueue_iteration_eager(nss_ctx *c, bool with_metric) {
   LaunchCtx lc = lctx(c);
   nss_status s;
+  if (with_metric) {
+    if (c->serial_evidence) {
+      if ((s = launch_metric_on(c, c->stream, 1))) return s;
+    } else {
+      CK(cudaEventRecord(c->ev_fork, c->stream));
+      CK(cudaStreamWaitEvent(c->side2, c->ev_fork, 0));
+      if ((s = launch_metric_on(c, c->side2, 1))) return s;
+      CK(cudaEventRecord(c->ev_met, c->side2));
+    }
+  }
   if ((s = timed_launch(c, 1, c->stream, [&] { launch_select(c->r, lc); }))) return s;
   if (c->serial_evidence) {
     if ((s = timed_launch(c, 2, c->stream, [&] { launch_evidence(c->r, 0, lc); }))) return s;
   } else {
     // A8 only needs this iteration's dead records: fork it onto the side
-    // stream so it overlaps HRSS; the metric kernel (termination test) joins it.
+    // stream so it overlaps HRSS; joined at the end of the iteration.
     CK(cudaEventRecord(c->ev_sel, c->stream));
     CK(cudaStreamWaitEvent(c->side, c->ev_sel, 0));
     LaunchCtx ls{c->side, &c->launches};
     if ((s = timed_launch(c, 2, c->side, [&] { launch_evidence(c->r, 0, ls); }))) return s;
     CK(cudaEventRecord(c->ev_evid, c->side));
   }
+  if (with_metric && !c->serial_evidence) CK(cudaStreamWaitEvent(c->stream, c->ev_met, 0));
   if ((s = timed_launch(c, 0, c->stream, [&] { launch_hrss(c->r, c->pr, c->en, lc); }))) return s;
   if ((s = exchange(c))) return s;
   if (!c->serial_evidence) CK(cudaStreamWaitEvent(c->stream, c->ev_evid, 0));
-  if ((s = timed_launch(c, 3, c->stream, [&] {
-         launch_metric(c->r, c->cfg.metric_reg, c->cfg.width_rule, c->cfg.width, 1, c->partials, c->ticket,
-                       c->nblk, lc);
-       })))
-    return s;
   CK(cudaGetLastError());
   return NSS_OK;
 }
@@ -369,6 +397,10 @@ void drop_graph(nss_ctx *c) {
     cudaGraphExecDestroy(c->graph);
     c->graph = nullptr;
   }
+  if (c->graph0) {
+    cudaGraphExecDestroy(c->graph0);
+    c->graph0 = nullptr;
+  }
   if (c->round_graph) {
     cudaGraphExecDestroy(c->round_graph);
     c->round_graph = nullptr;
@@ -382,6 +414,7 @@ nss_status enqueue_iteration_batch(nss_ctx *c) {
   nss_status s;
   if ((s = ensure_batch(c))) return s;
   LaunchCtx lc = lctx(c);
+  if (c->metric_pending && (s = launch_metric_on(c, c->stream, 1))) return s;
   if ((s = timed_launch(c, 1, c->stream, [&] { launch_select(c->r, lc); }))) return s;
   CK(cudaEventRecord(c->ev_sel, c->stream));
   CK(cudaStreamWaitEvent(c->side, c->ev_sel, 0));
@@ -437,11 +470,6 @@ nss_status enqueue_iteration_batch(nss_ctx *c) {
   }
   if ((s = exchange(c))) return s;
   CK(cudaStreamWaitEvent(c->stream, c->ev_evid, 0));
-  if ((s = timed_launch(c, 3, c->stream, [&] {
-         launch_metric(c->r, c->cfg.metric_reg, c->cfg.width_rule, c->cfg.width, 1, c->partials, c->ticket,
-                       c->nblk, lc);
-       })))
-    return s;
   CK(cudaGetLastError());
   return NSS_OK;
 }
@@ -449,30 +477,40 @@ nss_status enqueue_iteration_batch(nss_ctx *c) {
 // One outer iteration: replayed from a captured graph, or launched eagerly in
 // timing mode (events bracket each kernel) or when graphs are disabled.
 nss_status enqueue_iteration(nss_ctx *c) {
-  if (resolve_engine(c) == 2) return enqueue_iteration_batch(c);
-  if (c->timing || !c->use_graph) return enqueue_iteration_eager(c);
-  if (!c->graph) {
+  const bool wm = c->metric_pending;
+  c->term_stale = true;
+  c->metric_pending = true;
+  if (resolve_engine(c) == 2) {
+    c->metric_pending = wm;  // the batch path launches the deferred metric itself
+    const nss_status s = enqueue_iteration_batch(c);
+    c->metric_pending = true;
+    return s;
+  }
+  if (c->timing || !c->use_graph) return enqueue_iteration_eager(c, wm);
+  cudaGraphExec_t &g = wm ? c->graph : c->graph0;
+  long long &gl = wm ? c->graph_launches : c->graph0_launches;
+  if (!g) {
     const long long before = c->launches;
-    cudaGraph_t g = nullptr;
+    cudaGraph_t cg = nullptr;
     CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-    const nss_status s = enqueue_iteration_eager(c);
-    const cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+    const nss_status s = enqueue_iteration_eager(c, wm);
+    const cudaError_t e = cudaStreamEndCapture(c->stream, &cg);
     if (s != NSS_OK) return s;
     if (e != cudaSuccess) {
       c->poisoned = true;
       return fail(c, NSS_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
     }
-    const cudaError_t e2 = cudaGraphInstantiate(&c->graph, g, 0);
-    cudaGraphDestroy(g);
+    const cudaError_t e2 = cudaGraphInstantiate(&g, cg, 0);
+    cudaGraphDestroy(cg);
     if (e2 != cudaSuccess) {
       c->poisoned = true;
       return fail(c, NSS_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e2));
     }
-    c->graph_launches = c->launches - before;
+    gl = c->launches - before;
     c->launches = before;
   }
-  CK(cudaGraphLaunch(c->graph, c->stream));
-  c->launches += c->graph_launches;
+  CK(cudaGraphLaunch(g, c->stream));
+  c->launches += gl;
   return NSS_OK;
 }
 
@@ -548,6 +586,9 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
   if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess) return bail(NSS_ERR_CUDA);
   if (cudaEventCreateWithFlags(&c->ev_sel, cudaEventDisableTiming) != cudaSuccess) return bail(NSS_ERR_CUDA);
   if (cudaEventCreateWithFlags(&c->ev_evid, cudaEventDisableTiming) != cudaSuccess) return bail(NSS_ERR_CUDA);
+  if (cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess) return bail(NSS_ERR_CUDA);
+  if (cudaEventCreateWithFlags(&c->ev_met, cudaEventDisableTiming) != cudaSuccess) return bail(NSS_ERR_CUDA);
+  if (cudaStreamCreateWithFlags(&c->side2, cudaStreamNonBlocking) != cudaSuccess) return bail(NSS_ERR_CUDA);
   *c->h_one = 1;
 
   // ---- energy parameters (fp64 host -> fp32 device) ----
@@ -909,6 +950,9 @@ NSS_API nss_status nss_destroy(nss_ctx *c) {
   if (c->side) { cudaStreamSynchronize(c->side); cudaStreamDestroy(c->side); }
   if (c->ev_sel) cudaEventDestroy(c->ev_sel);
   if (c->ev_evid) cudaEventDestroy(c->ev_evid);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_met) cudaEventDestroy(c->ev_met);
+  if (c->side2) { cudaStreamSynchronize(c->side2); cudaStreamDestroy(c->side2); }
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return NSS_OK;
@@ -933,6 +977,8 @@ NSS_API nss_status nss_set_live(nss_ctx *c, const float *x, const float *e, int6
   c->h_st->terminated = 0;
   CK(cudaMemcpyAsync(c->r.st, c->h_st, sizeof(DevState), cudaMemcpyHostToDevice, c->stream));
   launch_metric(c->r, c->cfg.metric_reg, c->cfg.width_rule, c->cfg.width, 0, c->partials, c->ticket, c->nblk, lctx(c));
+  c->metric_pending = false;
+  c->term_stale = false;
   CK(cudaGetLastError());
   if ((s = pull_state(c))) return s;
   return NSS_OK;
@@ -956,6 +1002,11 @@ NSS_API nss_status nss_get_live(nss_ctx *c, float *x, float *e) {
 NSS_API nss_status nss_get_metric(nss_ctx *c, double *chol, double *width) {
   nss_status s = check_usable(c);
   if (s) return s;
+  if (c->metric_pending) {  // the deferred A5 of the last iteration
+    launch_metric(c->r, c->cfg.metric_reg, c->cfg.width_rule, c->cfg.width, 0, c->partials, c->ticket, c->nblk,
+                  lctx(c));
+    c->metric_pending = false;
+  }
   CK(cudaStreamSynchronize(c->stream));
   if (chol) CK(cudaMemcpy(chol, c->r.L64, static_cast<size_t>(c->d) * c->d * sizeof(double), cudaMemcpyDeviceToHost));
   if (width) {

@@ -150,6 +150,22 @@ __device__ __forceinline__ unsigned long long global_ns() {
 
 __device__ __forceinline__ void raise_error(DevState *st, int code) { atomicCAS(&st->error, 0, code); }
 
+// A9 / R-19: the run stops when the live bound log Z_live = -min E_live +
+// log X (replica 0) is below e^{term} of log Z_0 + Z_live.  Evaluated before
+// each iteration by the select kernel (one thread) and by k_term_probe when
+// the host asks; records E_min and log Z_live; returns the decision.
+__device__ inline bool term_check(const RunDev &r, DevState *st, float emin) {
+  const double lz_live = -static_cast<double>(emin) + r.lx_cur[0];
+  const double lz0 = r.lz[0];
+  const double mm = fmax(lz0, lz_live);
+  const double tot = (mm == -INFINITY) ? -INFINITY : mm + log(exp(lz0 - mm) + exp(lz_live - mm));
+  const bool stop = st->n_dead > 0 && (lz_live - tot) < static_cast<double>(r.term_log_ratio);
+  st->emin = emin;
+  st->log_z_live = lz_live;
+  if (stop) st->terminated = 1;
+  return stop;
+}
+
 // ----------------------------------------------------------------------------
 // Launchers (host side, one per kernel file)
 // ----------------------------------------------------------------------------
@@ -188,6 +204,7 @@ int hrss_engine(const RunDev &r, const EnergyDev &en);  // 0 warp-cooperative, 1
 bool lane_engine_ok(const RunDev &r, const EnergyDev &en);
 void launch_hrss_lane(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc);
 // k_metric.cu: A5 metric (+ A9 termination when iterating)
+void launch_term_probe(const RunDev &r, const LaunchCtx &lc);
 void launch_metric(const RunDev &r, double metric_reg, int width_rule, double width_param,
                    int end_of_iteration, double *partials, unsigned *ticket, int n_blocks, const LaunchCtx &lc);
 int metric_blocks(int n, int d);
