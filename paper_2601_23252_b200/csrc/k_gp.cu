@@ -11,8 +11,9 @@
 // panels: the diagonal block is factorised in shared memory by one warp, the
 // panel below it is solved row by row (the extra row y^T becomes alpha =
 // L^-1 y on the way), and the trailing lower trapezoid receives the rank-64
-// update in 64 x 64 tiles: panel rows staged column-major in shared memory,
-// 4 x 4 fp64 outputs per thread.  E then needs only
+// update in 64 x 64 tiles: panel rows staged row-major in shared memory and
+// contracted on the fp64 tensor cores (mma.sync m8n8k4 DMMA, 8 per warp per
+// k-step).  E then needs only
 // the pivots (log det) and |alpha|^2.  A non-positive pivot gives E = +inf (K
 // not positive definite), as in the oracle.  fp64 throughout: the paper runs
 // its GP experiments in double precision.
@@ -26,7 +27,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int PB = 64;       // panel width = trailing-update tile edge
 constexpr int LDK = PB + 1;  // diagonal block row stride (doubles)
-constexpr int LDC = PB + 2;  // column-major panel tile stride (even: 16-B aligned double2 loads)
+constexpr int LDR = PB + 4;  // row-major panel tile stride: 68 = 4 mod 16 -> conflict-free DMMA fragments
 constexpr double kLn2Pi = 1.8378770664093454836;
 
 struct GpDev {
@@ -49,34 +50,56 @@ __device__ __forceinline__ double block_sum(double v, double *red) {
   return s;
 }
 
-// rows [r0, r0+rows) x panel columns [k0, k0+kb) of A -> column-major tile T[c][r]
-__device__ __forceinline__ void load_panel_tile(double *T, const double *A, int N, int r0, int rows, int k0,
+// rows [r0, r0+rows) x panel columns [k0, k0+kb) of A -> row-major tile T[r][c]
+// with asynchronous 16-B copies (zero-filled past the edges); the caller
+// commits and waits (cp.async.commit_group / wait_group).
+__device__ __forceinline__ void load_panel_tile(double *T, const double *A, int lda, int r0, int rows, int k0,
                                                 int kb) {
-  for (int e = threadIdx.x; e < PB * PB; e += kThreads) {
-    const int r = e / PB, c = e - r * PB;
-    T[c * LDC + r] = (r < rows && c < kb) ? A[static_cast<long long>(r0 + r) * N + k0 + c] : 0.0;
+  constexpr int G = PB / 2;  // 16-B granules per tile row
+  for (int e = threadIdx.x; e < PB * G; e += kThreads) {
+    const int r = e / G, c = 2 * (e - r * G);
+    const int valid = (r < rows) ? max(0, min(2, kb - c)) : 0;
+    const double *src = valid ? A + static_cast<long long>(r0 + r) * lda + k0 + c : A;
+    const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(T + r * LDR + c));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid * 8)
+                 : "memory");
   }
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// D(8x8) += A(8x4) B(4x8) on the fp64 tensor cores: a = A[lane/4][lane%4],
+// b = B[lane%4][lane/4], d = D[lane/4][2 (lane%4) + {0, 1}]
+__device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
 }
 
 __global__ void __launch_bounds__(kThreads, 1) k_gp_energy(GpDev g, BatchDev b, int parity, int dp) {
   extern __shared__ double sm[];
   const int N = g.N, D = g.D, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int lda = (N + 1) & ~1;  // even row stride: 16-B aligned panel granules for cp.async
   if (blockIdx.x == 0 && tid == 0) b.n_probe[parity ^ 1] = 0;  // the next round's row counter
   const int n = b.n_probe[parity];
   if (static_cast<int>(blockIdx.x) >= n) return;
   double *sX = sm;                // N x D
   double *Lkk = sX + ((N * D + 1) & ~1);  // PB x LDK
-  double *Ti = Lkk + PB * LDK;            // PB x LDC (column-major: [c][r]); 16-B aligned (PB * LDK even)
-  double *Tj = Ti + PB * LDC;     // PB x LDC
-  double *inv = Tj + PB * LDC;    // PB: 1 / L_cc
+  double *Ti = Lkk + PB * LDK;            // PB x LDR (row-major panel rows)
+  double *Tj = Ti + PB * LDR;     // 2 x PB x LDR (double buffer)
+  double *inv = Tj + 2 * PB * LDR;  // PB: 1 / L_cc
   double *diag = inv + PB;        // PB: L_cc
   double *red = diag + PB;        // 8
   __shared__ double sh_par[NSS_MAX_DIM + 2];
   __shared__ int sh_fail;
   for (int e = tid; e < N * D; e += kThreads) sX[e] = g.X[e];
-  double *A = g.scratch + static_cast<long long>(blockIdx.x) * (N + 1) * N;
+  double *A = g.scratch + static_cast<long long>(blockIdx.x) * (N + 1) * lda;
   __syncthreads();
-  const int ty = tid >> 4, tx = tid & 15;  // 4 x 4 outputs per thread in a 64 x 64 tile
+  const int ty = tid >> 4, tx = tid & 15;  // diagonal-block owner map
+  // trailing update: warp (wr, wc) owns rows 32 wr .. +32, columns 16 wc .. +16
+  // of the 64 x 64 tile as 4 x 2 DMMA 8x8 tiles
+  const int m_base = (wid >> 2) * 32, n_base = (wid & 3) * 16, gq = lane >> 2, tq = lane & 3;
 
   for (int p = blockIdx.x; p < n; p += gridDim.x) {
     if (tid < D + 2) {
@@ -88,7 +111,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gp_energy(GpDev g, BatchDev b, 
     const double sf2 = sh_par[D], diag_add = sh_par[D + 1] + g.jitter;
     // ---- build [K; y^T] (lower trapezoid) ----
     for (int i = wid; i <= N; i += kThreads / 32) {
-      double *row = A + static_cast<long long>(i) * N;
+      double *row = A + static_cast<long long>(i) * lda;
       if (i == N) {
         for (int j = lane; j < N; j += 32) row[j] = g.y[j];
         continue;
@@ -110,7 +133,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gp_energy(GpDev g, BatchDev b, 
       //    (lane owns rows lane and lane + 32)
       for (int e = tid; e < kb * kb; e += kThreads) {
         const int r = e / kb, c = e - r * kb;
-        Lkk[r * LDK + c] = c <= r ? A[static_cast<long long>(k0 + r) * N + k0 + c] : 0.0;
+        Lkk[r * LDK + c] = c <= r ? A[static_cast<long long>(k0 + r) * lda + k0 + c] : 0.0;
       }
       __syncthreads();
       // All threads, one barrier per column: column j updates the trailing
@@ -168,7 +191,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gp_energy(GpDev g, BatchDev b, 
       // 2. panel solve x L_kk^T = a for the rows below the block and the y row
       const int r0 = k0 + kb;
       for (int i = r0 + tid; i <= N; i += kThreads) {
-        double *row = A + static_cast<long long>(i) * N + k0;
+        double *row = A + static_cast<long long>(i) * lda + k0;
         double a[PB];
 #pragma unroll
         for (int c = 0; c < PB; ++c) a[c] = c < kb ? row[c] : 0.0;
@@ -194,57 +217,70 @@ __global__ void __launch_bounds__(kThreads, 1) k_gp_energy(GpDev g, BatchDev b, 
       }
       __syncthreads();
       // 3. trailing update A[i][j] -= sum_c L[i][c] L[j][c] over rows r0..N,
-      //    columns r0..min(i, N-1), in 64 x 64 tiles (4 x 4 per thread)
+      //    columns r0..min(i, N-1), in 64 x 64 tiles on the fp64 tensor cores
       const int nrb = (N + 1 - r0 + PB - 1) / PB, ncb = (N - r0 + PB - 1) / PB;
       for (int bi = 0; bi < nrb; ++bi) {
         const int i0 = r0 + bi * PB;
         const int rows = min(PB, N + 1 - i0);
-        load_panel_tile(Ti, A, N, i0, rows, k0, kb);
-        for (int bj = 0; bj <= bi && bj < ncb; ++bj) {
+        // Ti, then Tj(0) in flight; Tj(bj+1) is fetched while Tj(bj) is used
+        load_panel_tile(Ti, A, lda, i0, rows, k0, kb);
+        cp_async_commit();
+        const int nbj = min(bi + 1, ncb);
+        auto fetch = [&](int bj) {
+          if (bj < nbj && bj != bi)
+            load_panel_tile(Tj + (bj & 1) * PB * LDR, A, lda, r0 + bj * PB, min(PB, N - (r0 + bj * PB)), k0, kb);
+          cp_async_commit();  // possibly empty group: keeps the wait count uniform
+        };
+        fetch(0);
+        for (int bj = 0; bj < nbj; ++bj) {
           const int j0 = r0 + bj * PB;
           const int cols = min(PB, N - j0);
+          fetch(bj + 1);
+          cp_async_wait<1>();  // all but the newest group: Ti and Tj(bj) have landed
           __syncthreads();
-          if (bj != bi) load_panel_tile(Tj, A, N, j0, cols, k0, kb);
-          __syncthreads();
-          const double *Tb = bj == bi ? Ti : Tj;
+          const double *Tj_cur = Tj + (bj & 1) * PB * LDR;
+          const double *Tb = bj == bi ? Ti : Tj_cur;
           // prefetch the 16 outputs (their latency hides behind the rank-kb product)
-          double cur[4][4];
+          double cur[4][2][2], acc[4][2][2];
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
+          for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              const int r = ty * 4 + u, cc = tx * 4 + v;
-              cur[u][v] = (r < rows && cc < cols && j0 + cc <= i0 + r)
-                              ? A[static_cast<long long>(i0 + r) * N + j0 + cc]
-                              : 0.0;
-            }
-          double acc[4][4];
+            for (int ni = 0; ni < 2; ++ni)
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-#pragma unroll
-            for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+              for (int h = 0; h < 2; ++h) {
+                const int r = m_base + 8 * mi + gq, cc = n_base + 8 * ni + 2 * tq + h;
+                cur[mi][ni][h] = (r < rows && cc < cols && j0 + cc <= i0 + r)
+                                     ? A[static_cast<long long>(i0 + r) * lda + j0 + cc]
+                                     : 0.0;
+                acc[mi][ni][h] = 0.0;
+              }
+          const double *pa = Ti + (m_base + gq) * LDR + tq;
+          const double *pb = Tb + (n_base + gq) * LDR + tq;
 #pragma unroll 4
-          for (int c = 0; c < kb; ++c) {
-            const double2 a01 = *reinterpret_cast<const double2 *>(Ti + c * LDC + ty * 4);
-            const double2 a23 = *reinterpret_cast<const double2 *>(Ti + c * LDC + ty * 4 + 2);
-            const double2 b01 = *reinterpret_cast<const double2 *>(Tb + c * LDC + tx * 4);
-            const double2 b23 = *reinterpret_cast<const double2 *>(Tb + c * LDC + tx * 4 + 2);
-            const double av[4] = {a01.x, a01.y, a23.x, a23.y};
-            const double bv[4] = {b01.x, b01.y, b23.x, b23.y};
+          for (int c = 0; c < kb; c += 4) {
+            double av[4], bv[2];
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+            for (int mi = 0; mi < 4; ++mi) av[mi] = pa[8 * mi * LDR + c];
 #pragma unroll
-              for (int v = 0; v < 4; ++v) acc[u][v] = fma(av[u], bv[v], acc[u][v]);
+            for (int ni = 0; ni < 2; ++ni) bv[ni] = pb[8 * ni * LDR + c];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+              for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], av[mi], bv[ni]);
           }
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
+          for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              const int r = ty * 4 + u, cc = tx * 4 + v;
-              if (r < rows && cc < cols && j0 + cc <= i0 + r)
-                A[static_cast<long long>(i0 + r) * N + j0 + cc] = cur[u][v] - acc[u][v];
-            }
+            for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int r = m_base + 8 * mi + gq, cc = n_base + 8 * ni + 2 * tq + h;
+                if (r < rows && cc < cols && j0 + cc <= i0 + r)
+                  A[static_cast<long long>(i0 + r) * lda + j0 + cc] = cur[mi][ni][h] - acc[mi][ni][h];
+              }
+          __syncthreads();  // Tj(bj) is refilled by the fetch of iteration bj + 1
         }
+        cp_async_wait<0>();
         __syncthreads();
       }
     }
@@ -252,7 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gp_energy(GpDev g, BatchDev b, 
     double q = 0.0;
     if (!sh_fail)
       for (int j = tid; j < N; j += kThreads) {
-        const double al = A[static_cast<long long>(N) * N + j];
+        const double al = A[static_cast<long long>(N) * lda + j];
         q = fma(al, al, q);
       }
     const double qs = block_sum(q, red);
@@ -285,7 +321,7 @@ bool gp_setup(void **handle, const double *X, const double *y, int N, int D, dou
   E->g.jitter = jitter;
   double *dX = nullptr, *dy = nullptr, *sc = nullptr;
   if (cudaMalloc(&dX, sizeof(double) * N * D) || cudaMalloc(&dy, sizeof(double) * N) ||
-      cudaMalloc(&sc, sizeof(double) * static_cast<size_t>(sms) * (N + 1) * N)) {
+      cudaMalloc(&sc, sizeof(double) * static_cast<size_t>(sms) * (N + 1) * ((N + 1) & ~1))) {
     cudaFree(dX);
     cudaFree(dy);
     cudaFree(sc);
@@ -297,7 +333,7 @@ bool gp_setup(void **handle, const double *X, const double *y, int N, int D, dou
   E->g.X = dX;
   E->g.y = dy;
   E->g.scratch = sc;
-  E->smem = (static_cast<size_t>(N) * D + 1 + PB * LDK + 1 + 2 * PB * LDC + 2 * PB + 16) * sizeof(double);
+  E->smem = (static_cast<size_t>(N) * D + 1 + PB * LDK + 3 * PB * LDR + 2 * PB + 16) * sizeof(double);
   cudaFuncSetAttribute(k_gp_energy, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(E->smem));
   *handle = E;
   return E->smem <= 200 * 1024;
