@@ -21,7 +21,7 @@
 /* kappa_infinity as printed in the paper, P:2125 ("kappa_infty ~ 1.3035"). */
 #define KAPPA_INF_PAPER 1.3035
 
-enum { PH_INIT = 1, PH_RESAMPLE = 2, PH_HRSS = 3, PH_VOLUME = 4 };
+enum { PH_INIT = 1, PH_RESAMPLE = 2, PH_HRSS = 3, PH_VOLUME = 4, PH_POSTERIOR = 5 };
 
 /* ------------------------------------------------------------------------ */
 /* Counter-based RNG: Philox4x32-10 (Salmon et al. 2011). */
@@ -894,6 +894,103 @@ int nsso_samples(nsso_ctx *c, double *x, double *log_w, int64_t cap, int64_t *n_
   for (int64_t i = 0; i < N; ++i) log_w[i] -= lz;
   free(acc);
   free(lx);
+  return NSSO_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Posterior products at inverse temperature beta (F2; P:123-132 reweighting, */
+/* P:1225-1255 weights, geometric-mean collapse and Kish ESS).                */
+/* ------------------------------------------------------------------------ */
+/* w_i^(r)(beta) = exp(-beta E_i) dX_i^(r) over the dead points in death order,
+ * Z^(r)(beta) = sum_i w_i^(r)(beta); log Z reported as mean and
+ * std (ddof 1) over r = 1..R; geometric-mean weights
+ * w~_i = exp(mean_r log w_i^(r)), normalised; Kish
+ * ESS = (sum w~)^2 / sum w~^2.  Before finalisation the last
+ * dead point closes with X_{N+1} = 0, as nsso_samples does (R-27). */
+int nsso_posterior(nsso_ctx *c, double beta, double *log_z, double *log_z_err, double *ess, double *log_w,
+                   int64_t cap) {
+  if (!c) return NSSO_ERR_INVALID_ARG;
+  if (c->n_dead == 0) return NSSO_ERR_STATE;
+  int64_t N = c->n_dead;
+  if (log_w && cap < N) return NSSO_ERR_CAPACITY;
+  double *acc = (double *)xcalloc((size_t)N, sizeof(double));
+  double *lx = (double *)xcalloc((size_t)N + 2, sizeof(double));
+  double *term = (double *)xcalloc((size_t)N, sizeof(double));
+  double *lzr = (double *)xcalloc((size_t)c->R + 1, sizeof(double));
+  for (int r = 1; r <= c->R; ++r) {
+    lx[0] = 0.0;
+    for (int64_t i = 0; i < N; ++i)
+      lx[i + 1] = lx[i] + dlogx(c, r, c->dnlive[i], (uint32_t)c->diter[i], (uint32_t)c->dord[i]);
+    double m = -INFINITY;
+    for (int64_t i = 1; i <= N; ++i) {
+      double ldx;
+      if (c->cfg.quadrature == NSSO_Q_RECTANGLE)
+        ldx = lx[i - 1] + log1mexp(lx[i] - lx[i - 1]);
+      else if (i < N)
+        ldx = lx[i - 1] + log1mexp(lx[i + 1] - lx[i - 1]) - log(2.0);
+      else
+        ldx = lx[i - 1] - log(2.0);
+      acc[i - 1] += ldx;
+      term[i - 1] = -beta * c->dE[i - 1] + ldx; /* log w_i^(r)(beta) */
+      if (term[i - 1] > m) m = term[i - 1];
+    }
+    double s = 0.0;
+    for (int64_t i = 0; i < N; ++i) s += exp(term[i] - m);
+    lzr[r] = m + log(s);
+  }
+  double mean = 0.0;
+  for (int r = 1; r <= c->R; ++r) mean += lzr[r];
+  mean /= c->R;
+  double var = 0.0;
+  for (int r = 1; r <= c->R; ++r) var += (lzr[r] - mean) * (lzr[r] - mean);
+  if (log_z) *log_z = mean;
+  if (log_z_err) *log_z_err = sqrt(var / (c->R - 1));
+  /* geometric-mean weights, normalised in log space */
+  double m = -INFINITY;
+  for (int64_t i = 0; i < N; ++i) {
+    term[i] = acc[i] / c->R - beta * c->dE[i];
+    if (term[i] > m) m = term[i];
+  }
+  double s = 0.0;
+  for (int64_t i = 0; i < N; ++i) s += exp(term[i] - m);
+  double lse = m + log(s);
+  double s2 = 0.0;
+  for (int64_t i = 0; i < N; ++i) {
+    term[i] -= lse;
+    s2 += exp(2.0 * term[i]);
+  }
+  if (ess) *ess = 1.0 / s2;
+  if (log_w) memcpy(log_w, term, sizeof(double) * (size_t)N);
+  free(acc); free(lx); free(term); free(lzr);
+  return NSSO_OK;
+}
+
+/* Equal-weight posterior samples (F2; "resampling"):
+ * m multinomial draws from the normalised weights w_bar(beta): draw j takes
+ * u_j = uniform 0 of stream (iteration 0, j, POSTERIOR, 0) under key `seed`
+ * and returns the first dead point i with u_j < sum_{l <= i} w_bar_l
+ * (the last point if rounding leaves u_j above the total). */
+int nsso_resample(nsso_ctx *c, double beta, int64_t m, uint64_t seed, int64_t *idx, double *x) {
+  if (!c || m < 1 || (!idx && !x)) return NSSO_ERR_INVALID_ARG;
+  if (c->n_dead == 0) return NSSO_ERR_STATE;
+  int64_t N = c->n_dead;
+  double *lw = (double *)xcalloc((size_t)N, sizeof(double));
+  double *cum = (double *)xcalloc((size_t)N, sizeof(double));
+  int st = nsso_posterior(c, beta, NULL, NULL, NULL, lw, N);
+  if (st) { free(lw); free(cum); return st; }
+  double run = 0.0;
+  for (int64_t i = 0; i < N; ++i) { run += exp(lw[i]); cum[i] = run; }
+  for (int64_t j = 0; j < m; ++j) {
+    double u = nsso_draw_uniform(seed, 0, (uint32_t)j, PH_POSTERIOR, 0, 0);
+    int64_t lo = 0, hi = N - 1; /* first i with u < cum[i] */
+    while (lo < hi) {
+      int64_t mid = (lo + hi) / 2;
+      if (u < cum[mid]) hi = mid; else lo = mid + 1;
+    }
+    if (idx) idx[j] = lo;
+    if (x) memcpy(x + j * c->d, c->dX + lo * c->d, sizeof(double) * (size_t)c->d);
+  }
+  free(lw); free(cum);
   return NSSO_OK;
 }
 

@@ -114,6 +114,13 @@ int nsso_finalise(nsso_ctx *ctx);
 int nsso_evidence(nsso_ctx *ctx, double *log_z, double *log_z_err);
 int nsso_evidence_reps(nsso_ctx *ctx, double *log_z_reps /* R+1 */);
 int nsso_samples(nsso_ctx *ctx, double *x, double *log_w, int64_t cap, int64_t *n_out);
+/* F2 posterior products at inverse temperature beta: log Z(beta) mean/std over
+ * the R replicas, Kish ESS of the geometric-mean weights, normalised log
+ * weights (nullable, cap >= n_dead). */
+int nsso_posterior(nsso_ctx *ctx, double beta, double *log_z, double *log_z_err, double *ess,
+                   double *log_w, int64_t cap);
+/* m equal-weight multinomial draws from the beta-weights; idx and/or x (m*d). */
+int nsso_resample(nsso_ctx *ctx, double beta, int64_t m, uint64_t seed, int64_t *idx, double *x);
 int nsso_info(nsso_ctx *ctx, nsso_step_info *info);
 int nsso_should_terminate(nsso_ctx *ctx, int32_t *flag);
 void nsso_destroy(nsso_ctx *ctx);

@@ -83,6 +83,9 @@ def lib():
         L.nsso_evidence.argtypes = [vp, P(C.c_double), P(C.c_double)]
         L.nsso_evidence_reps.argtypes = [vp, P(C.c_double)]
         L.nsso_samples.argtypes = [vp, P(C.c_double), P(C.c_double), C.c_int64, P(C.c_int64)]
+        L.nsso_posterior.argtypes = [vp, C.c_double, P(C.c_double), P(C.c_double), P(C.c_double),
+                                     P(C.c_double), C.c_int64]
+        L.nsso_resample.argtypes = [vp, C.c_double, C.c_int64, C.c_uint64, P(C.c_int64), P(C.c_double)]
         L.nsso_should_terminate.argtypes = [vp, P(C.c_int32)]
         L.nsso_destroy.argtypes = [vp]
         L.nsso_destroy.restype = None
@@ -250,6 +253,27 @@ class Oracle:
         lw = np.zeros(n.value)
         _check(lib().nsso_samples(self._h, _dp(x), _dp(lw), n.value, C.byref(n)), "nsso_samples")
         return x, lw
+
+    def posterior(self, beta: float = 1.0, weights: bool = False):
+        """F2: (log Z(beta) mean, std over replicas, Kish ESS[, normalised log weights])."""
+        lz, err, ess = C.c_double(), C.c_double(), C.c_double()
+        lw = None
+        if weights:
+            n = C.c_int64()
+            _check(lib().nsso_samples(self._h, None, None, 0, C.byref(n)), "nsso_samples")
+            lw = np.zeros(n.value)
+        _check(lib().nsso_posterior(self._h, float(beta), C.byref(lz), C.byref(err), C.byref(ess), _dp(lw),
+                                    0 if lw is None else lw.size), "nsso_posterior")
+        out = (lz.value, err.value, ess.value)
+        return out + (lw,) if weights else out
+
+    def resample(self, m: int, seed: int, beta: float = 1.0):
+        """F2: m equal-weight draws: (dead indices, positions)."""
+        idx = np.zeros(m, np.int64)
+        x = np.zeros((m, self.d))
+        _check(lib().nsso_resample(self._h, float(beta), int(m), int(seed),
+                                   idx.ctypes.data_as(C.POINTER(C.c_int64)), _dp(x)), "nsso_resample")
+        return idx, x
 
     def dead(self):
         n = C.c_int64()

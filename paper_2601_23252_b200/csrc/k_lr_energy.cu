@@ -191,27 +191,47 @@ __global__ void __launch_bounds__(kThreads, 1)
         float lin0 = 0.f, lin1 = 0.f, p0 = 1.f, p1 = 1.f;
         const int valid = n_data - col0;  // >= 64 except in the ragged last tile
         const float4 *y4 = reinterpret_cast<const float4 *>(y + col0);
+        if (valid >= 64) {
+          // full tile (all but the last): no masks
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const float4 yy = __ldg(y4 + q);
-          const float yv[4] = {yy.x, yy.y, yy.z, yy.w};
+          for (int q = 0; q < 16; ++q) {
+            const float4 yy = __ldg(y4 + q);
+            const float yv[4] = {yy.x, yy.y, yy.z, yy.w};
 #pragma unroll
-          for (int w = 0; w < 4; ++w) {
-            const int cc = 4 * q + w;
-            float a = v[cc >> 5][cc & 31];
-            float yc = yv[w];
-            if (valid < 64 && cc >= valid) {  // padded data rows contribute nothing
-              a = -INFINITY;
-              yc = 0.f;
+            for (int w = 0; w < 4; ++w) {
+              const int cc = 4 * q + w;
+              const float a = v[cc >> 5][cc & 31];
+              const float e = tc::ex2_approx(-fabsf(a) * 1.4426950408889634f);
+              const float l = fmaf(-yv[w], a, fmaxf(a, 0.f));
+              if (w & 1) {
+                p1 = fmaf(p1, e, p1);
+                lin1 += l;
+              } else {
+                p0 = fmaf(p0, e, p0);
+                lin0 += l;
+              }
             }
-            const float e = tc::ex2_approx(-fabsf(a) * 1.4426950408889634f);
-            const float l = fmaf(-yc, a, fmaxf(a, 0.f));
-            if (w & 1) {
-              p1 = fmaf(p1, e, p1);
-              lin1 += (a == -INFINITY) ? 0.f : l;
-            } else {
-              p0 = fmaf(p0, e, p0);
-              lin0 += (a == -INFINITY) ? 0.f : l;
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const float4 yy = __ldg(y4 + q);
+            const float yv[4] = {yy.x, yy.y, yy.z, yy.w};
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+              const int cc = 4 * q + w;
+              if (cc < valid) {  // padded data rows contribute nothing
+                const float a = v[cc >> 5][cc & 31];
+                const float e = tc::ex2_approx(-fabsf(a) * 1.4426950408889634f);
+                const float l = fmaf(-yv[w], a, fmaxf(a, 0.f));
+                if (w & 1) {
+                  p1 = fmaf(p1, e, p1);
+                  lin1 += l;
+                } else {
+                  p0 = fmaf(p0, e, p0);
+                  lin0 += l;
+                }
+              }
             }
           }
         }
