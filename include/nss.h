@@ -179,6 +179,23 @@ const char *nss_last_error(const nss_ctx *ctx);
 /* ---- parity hooks (exported for the tests; not on the user path) ---- */
 /* Inject a live set (n*d fp32 positions, n fp32 energies); the next nss_step
  * is iteration `next_iteration`.  Recomputes the metric from x. */
+/* F2 posterior products at inverse temperature beta >= 0 (the
+ * same dead points reweighted, w_i^(r)(beta) = exp(-beta E_i) dX_i^(r);
+ * log Z(beta) mean and std (ddof 1) over the R volume replicas,
+ * geometric-mean weights w~_i = exp(mean_r log w_i^(r)), Kish
+ * ESS = (sum w~)^2 / sum w~^2).  log_w (nullable, cap >= n_dead) receives
+ * the normalised log w~_i in death order.  beta = 1 reproduces
+ * nss_evidence and nss_samples.  Errors: INVALID_ARG (beta < 0 or not
+ * finite), STATE (no dead points), CAPACITY. */
+nss_status nss_posterior(nss_ctx *ctx, double beta, double *log_z, double *log_z_err, double *ess,
+                         double *log_w, int64_t cap);
+/* Equal-weight posterior samples: m multinomial draws from the
+ * normalised beta-weights; draw j uses uniform 0 of the Philox stream
+ * (iteration 0, j, POSTERIOR = 5, 0) under key `seed` and takes the first dead
+ * point whose cumulative weight exceeds it.  idx (m dead-store indices)
+ * and/or x (m*d positions) may be NULL, not both. */
+nss_status nss_resample(nss_ctx *ctx, double beta, int64_t m, uint64_t seed, int64_t *idx, double *x);
+
 nss_status nss_set_live(nss_ctx *ctx, const float *x, const float *e, int64_t next_iteration);
 nss_status nss_get_live(nss_ctx *ctx, float *x, float *e);
 nss_status nss_get_metric(nss_ctx *ctx, double *chol /* d*d lower, fp64 */, double *width);

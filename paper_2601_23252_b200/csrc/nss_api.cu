@@ -26,7 +26,10 @@ void nccl_comm_free(void *comm);
 bool exchange_chains(const RunDev &r, void *comm, float *buf, float *all, int kc, const LaunchCtx &lc,
                      std::string *err);
 void launch_evidence_summary(const RunDev &r, double *out, const LaunchCtx &lc);
-void launch_samples(const RunDev &r, long long N, double *logw, double *scratch, int chunk, const LaunchCtx &lc);
+void launch_samples(const RunDev &r, long long N, double *logw, double *scratch, int chunk, const LaunchCtx &lc,
+                    double beta, double *zacc);
+void launch_resample(const RunDev &r, long long N, const double *logw, double *cum, long long m, uint64_t seed,
+                     long long *idx, double *x, const LaunchCtx &lc);
 }  // namespace nss
 
 static const int kPhases = 5;
@@ -901,7 +904,7 @@ NSS_API nss_status nss_samples(nss_ctx *c, double *x, double *log_w, int64_t cap
     double *logw = nullptr, *scratch = nullptr;
     CK(cudaMalloc(&logw, N * sizeof(double)));
     CK(cudaMalloc(&scratch, (static_cast<size_t>(c->r.R) * (chunk + 3)) * sizeof(double)));
-    launch_samples(c->r, N, logw, scratch, chunk, lctx(c));
+    launch_samples(c->r, N, logw, scratch, chunk, lctx(c), 1.0, nullptr);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaMemcpyAsync(log_w, logw, N * sizeof(double), cudaMemcpyDeviceToHost, c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
@@ -913,6 +916,64 @@ NSS_API nss_status nss_samples(nss_ctx *c, double *x, double *log_w, int64_t cap
     }
   }
   return NSS_OK;
+}
+
+// F2 posterior products: weights at inverse
+// temperature beta re-simulated on the device; optional equal-weight draws.
+static nss_status posterior_impl(nss_ctx *c, double beta, double *log_z, double *log_z_err, double *ess,
+                                 double *log_w, int64_t cap, int64_t m, uint64_t seed, int64_t *idx, double *x) {
+  nss_status s = check_usable(c);
+  if (s) return s;
+  if (!std::isfinite(beta) || beta < 0.0) return NSS_ERR_INVALID_ARG;
+  if ((s = pull_state(c))) return s;
+  const long long N = c->h_st->n_dead;
+  if (N == 0) return fail(c, NSS_ERR_STATE, "no dead points yet");
+  if (log_w && cap < N) return fail(c, NSS_ERR_CAPACITY, "output buffer smaller than the dead store");
+  const int chunk = 1 << 16, R = c->r.R;
+  double *logw = nullptr, *scratch = nullptr, *zacc = nullptr, *cum = nullptr, *xd = nullptr;
+  long long *idxd = nullptr;
+  cudaError_t e = cudaMalloc(&logw, N * sizeof(double));
+  if (!e) e = cudaMalloc(&scratch, (static_cast<size_t>(R) * (chunk + 3)) * sizeof(double));
+  if (!e) e = cudaMalloc(&zacc, (2 * static_cast<size_t>(R) + 4) * sizeof(double));
+  if (!e && m > 0) e = cudaMalloc(&cum, N * sizeof(double));
+  if (!e && m > 0) e = cudaMalloc(&idxd, m * sizeof(long long));
+  if (!e && m > 0) e = cudaMalloc(&xd, static_cast<size_t>(m) * c->d * sizeof(double));
+  double summary[3] = {0, 0, 0};
+  if (!e) {
+    launch_samples(c->r, N, logw, scratch, chunk, lctx(c), beta, zacc);
+    if (m > 0) launch_resample(c->r, N, logw, cum, m, seed, idxd, xd, lctx(c));
+    e = cudaGetLastError();
+  }
+  if (!e) e = cudaMemcpyAsync(summary, zacc + 2 * R, 3 * sizeof(double), cudaMemcpyDeviceToHost, c->stream);
+  if (!e && log_w) e = cudaMemcpyAsync(log_w, logw, N * sizeof(double), cudaMemcpyDeviceToHost, c->stream);
+  if (!e && idx) e = cudaMemcpyAsync(idx, idxd, m * sizeof(long long), cudaMemcpyDeviceToHost, c->stream);
+  if (!e && x) e = cudaMemcpyAsync(x, xd, static_cast<size_t>(m) * c->d * sizeof(double), cudaMemcpyDeviceToHost,
+                                   c->stream);
+  if (!e) e = cudaStreamSynchronize(c->stream);
+  cudaFree(logw);
+  cudaFree(scratch);
+  cudaFree(zacc);
+  cudaFree(cum);
+  cudaFree(idxd);
+  cudaFree(xd);
+  if (e != cudaSuccess) {
+    c->poisoned = true;
+    return fail(c, NSS_ERR_CUDA, cudaGetErrorString(e));
+  }
+  if (log_z) *log_z = summary[0];
+  if (log_z_err) *log_z_err = summary[1];
+  if (ess) *ess = summary[2];
+  return NSS_OK;
+}
+
+NSS_API nss_status nss_posterior(nss_ctx *c, double beta, double *log_z, double *log_z_err, double *ess,
+                                 double *log_w, int64_t cap) {
+  return posterior_impl(c, beta, log_z, log_z_err, ess, log_w, cap, 0, 0, nullptr, nullptr);
+}
+
+NSS_API nss_status nss_resample(nss_ctx *c, double beta, int64_t m, uint64_t seed, int64_t *idx, double *x) {
+  if (!c || m < 1 || (!idx && !x)) return NSS_ERR_INVALID_ARG;
+  return posterior_impl(c, beta, nullptr, nullptr, nullptr, nullptr, 0, m, seed, idx, x);
 }
 
 NSS_API nss_status nss_info(nss_ctx *c, nss_step_info *info) {

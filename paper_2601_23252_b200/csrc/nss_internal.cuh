@@ -10,7 +10,7 @@ namespace nss {
 
 constexpr int kMaxDim = NSS_MAX_DIM;
 constexpr int kMaxComp = 16;
-constexpr uint32_t kPhaseInit = 1, kPhaseResample = 2, kPhaseHrss = 3, kPhaseVolume = 4;
+constexpr uint32_t kPhaseInit = 1, kPhaseResample = 2, kPhaseHrss = 3, kPhaseVolume = 4, kPhasePosterior = 5;
 
 // ----------------------------------------------------------------------------
 // Device-resident run state (one small struct, read by every kernel).

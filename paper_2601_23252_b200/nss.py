@@ -73,7 +73,7 @@ EXPORTS = ["nss_get_unique_id", "nss_init", "nss_step", "nss_steps", "nss_run", 
            "nss_dead", "nss_volume_reps", "nss_set_kernel_timing", "nss_kernel_time",
            "nss_launch_count", "nss_set_hrss_engine", "nss_get_hrss_engine",
            "nss_phase_times", "nss_set_overlap", "nss_set_graph",
-           "nss_debug_stamps", "nss_lr_energy_batch", "nss_gp_energy_batch", "nss_set_chain_range"]
+           "nss_debug_stamps", "nss_lr_energy_batch", "nss_gp_energy_batch", "nss_set_chain_range", "nss_posterior", "nss_resample"]
 
 _lib = None
 
@@ -121,6 +121,9 @@ def lib():
     L.nss_lr_energy_batch.argtypes = [P(C.c_double), P(C.c_double), C.c_int64, C.c_int32, P(C.c_double),
                                       C.c_int64, P(C.c_double)]
     L.nss_set_chain_range.argtypes = [vp, C.c_int32, C.c_int32]
+    L.nss_posterior.argtypes = [vp, C.c_double, P(C.c_double), P(C.c_double), P(C.c_double), P(C.c_double),
+                                C.c_int64]
+    L.nss_resample.argtypes = [vp, C.c_double, C.c_int64, C.c_uint64, P(C.c_int64), P(C.c_double)]
     L.nss_gp_energy_batch.argtypes = [P(C.c_double), P(C.c_double), C.c_int64, C.c_int32, C.c_double,
                                       P(C.c_double), C.c_int64, P(C.c_double)]
     _lib = L
@@ -223,6 +226,27 @@ class Sampler:
         if st != 0:
             msg = lib().nss_last_error(self._h) if self._h else b""
             raise NssError(st, where, (msg or b"").decode())
+
+    def posterior(self, beta: float = 1.0, weights: bool = False):
+        """F2: (log Z(beta) mean, std over replicas, Kish ESS[, normalised log weights])."""
+        lz, err, ess = C.c_double(), C.c_double(), C.c_double()
+        lw = None
+        if weights:
+            n = C.c_int64()
+            self._check(lib().nss_samples(self._h, None, None, 0, C.byref(n)), "nss_samples")
+            lw = np.zeros(n.value)
+        self._check(lib().nss_posterior(self._h, float(beta), C.byref(lz), C.byref(err), C.byref(ess), _dp(lw),
+                                        0 if lw is None else lw.size), "nss_posterior")
+        out = (lz.value, err.value, ess.value)
+        return out + (lw,) if weights else out
+
+    def resample(self, m: int, seed: int, beta: float = 1.0):
+        """F2: m equal-weight posterior draws: (dead-store indices, positions)."""
+        idx = np.zeros(m, np.int64)
+        x = np.zeros((m, self.d))
+        self._check(lib().nss_resample(self._h, float(beta), int(m), int(seed),
+                                       idx.ctypes.data_as(C.POINTER(C.c_int64)), _dp(x)), "nss_resample")
+        return idx, x
 
     def set_chain_range(self, c0: int, c1: int):
         """Run only HRSS chains [c0, c1) (what one rank of a sharded run does)."""
