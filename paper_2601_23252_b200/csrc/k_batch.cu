@@ -211,7 +211,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_batch_advance(RunDev r,
       float zz = 0.f, vv = 0.f;
 #pragma unroll
       for (int t = 0; t < NPL; ++t) v[t] = 0.f;
-      for (int m = 0; m < d; ++m) {
+#pragma unroll 8
+      for (int m = 0; m < d; ++m) {  // unrolled: 8 columns of loads in flight
         const float zm = sZ[m];
         const float *col = r.LT + static_cast<long long>(m) * r.dp;
 #pragma unroll

@@ -26,7 +26,6 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int PB = 64;       // panel width = trailing-update tile edge
-constexpr int LDK = PB + 1;  // diagonal block row stride (doubles)
 constexpr int LDR = PB + 4;  // row-major panel tile stride: 68 = 4 mod 16 -> conflict-free DMMA fragments
 constexpr double kLn2Pi = 1.8378770664093454836;
 
@@ -77,28 +76,44 @@ __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(kThreads, 1) k_gp_energy(GpDev g, BatchDev b, int parity, int dp) {
+// acc(32 x 16 per warp) += Ta(rows) . Tb(rows)^T over k < kb: 4 x 2 DMMA
+// 8x8 tiles, operand rows at m_base / n_base of the row-major tiles
+__device__ __forceinline__ void mma_rows(const double *Ta, const double *Tb, int kb, int m_base, int n_base, int gq,
+                                         int tq, double (&acc)[4][2][2]) {
+  const double *pa = Ta + (m_base + gq) * LDR + tq;
+  const double *pb = Tb + (n_base + gq) * LDR + tq;
+#pragma unroll 4
+  for (int c = 0; c < kb; c += 4) {
+    double av[4], bv[2];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) av[mi] = pa[8 * mi * LDR + c];
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni) bv[ni] = pb[8 * ni * LDR + c];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], av[mi], bv[ni]);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 2) k_gp_energy(GpDev g, BatchDev b, int parity, int dp) {
   extern __shared__ double sm[];
   const int N = g.N, D = g.D, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int lda = (N + 1) & ~1;  // even row stride: 16-B aligned panel granules for cp.async
   if (blockIdx.x == 0 && tid == 0) b.n_probe[parity ^ 1] = 0;  // the next round's row counter
   const int n = b.n_probe[parity];
   if (static_cast<int>(blockIdx.x) >= n) return;
-  double *sX = sm;                // N x D
-  double *Lkk = sX + ((N * D + 1) & ~1);  // PB x LDK
-  double *Ti = Lkk + PB * LDK;            // PB x LDR (row-major panel rows)
-  double *Tj = Ti + PB * LDR;     // 2 x PB x LDR (double buffer)
-  double *inv = Tj + 2 * PB * LDR;  // PB: 1 / L_cc
-  double *diag = inv + PB;        // PB: L_cc
+  double *Ti = sm;                // PB x LDR: panel rows of the current row block (then its X rows)
+  double *Tj = Ti + PB * LDR;     // PB x LDR: X rows of an earlier row block; the diagonal block first
+  double *W = Tj + PB * LDR;      // PB x LDR: L_kk^-1 (lower), zero above the diagonal and past kb
+  double *diag = W + PB * LDR;    // PB: L_cc
   double *red = diag + PB;        // 8
   __shared__ double sh_par[NSS_MAX_DIM + 2];
   __shared__ int sh_fail;
-  for (int e = tid; e < N * D; e += kThreads) sX[e] = g.X[e];
   double *A = g.scratch + static_cast<long long>(blockIdx.x) * (N + 1) * lda;
-  __syncthreads();
+  double *Lkk = Tj;
   const int ty = tid >> 4, tx = tid & 15;  // diagonal-block owner map
-  // trailing update: warp (wr, wc) owns rows 32 wr .. +32, columns 16 wc .. +16
-  // of the 64 x 64 tile as 4 x 2 DMMA 8x8 tiles
+  // DMMA warp tiles: warp (wr, wc) owns rows 32 wr .. +32, columns 16 wc .. +16
   const int m_base = (wid >> 2) * 32, n_base = (wid & 3) * 16, gq = lane >> 2, tq = lane & 3;
 
   for (int p = blockIdx.x; p < n; p += gridDim.x) {
@@ -119,7 +134,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gp_energy(GpDev g, BatchDev b, 
       for (int j = lane; j <= i; j += 32) {
         double s = 0.0;
         for (int q = 0; q < D; ++q) {
-          const double t = (sX[i * D + q] - sX[j * D + q]) * sh_par[q];
+          const double t = (__ldg(g.X + i * D + q) - __ldg(g.X + j * D + q)) * sh_par[q];
           s = fma(t, t, s);
         }
         row[j] = sf2 * exp(-0.5 * s) + (i == j ? diag_add : 0.0);
@@ -129,20 +144,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_gp_energy(GpDev g, BatchDev b, 
     double logdet_part = 0.0;  // lane-held sums of log pivots (warp 0)
     for (int k0 = 0; k0 < N; k0 += PB) {
       const int kb = min(PB, N - k0);
-      // 1. diagonal block -> shared memory; row-owner Cholesky in warp 0
-      //    (lane owns rows lane and lane + 32)
-      for (int e = tid; e < kb * kb; e += kThreads) {
-        const int r = e / kb, c = e - r * kb;
-        Lkk[r * LDK + c] = c <= r ? A[static_cast<long long>(k0 + r) * lda + k0 + c] : 0.0;
+      // 1. diagonal block -> shared memory; all threads, one barrier per
+      //    column: column j updates the block with its unscaled values
+      //    (A_rl -= A_rj A_lj / A_jj) while column j-1 is scaled by 1/L_{j-1,j-1};
+      //    thread (ty, tx) owns rows ty + 16 u and columns tx + 16 v
+      for (int e = tid; e < PB * PB; e += kThreads) {
+        const int r = e / PB, c = e - r * PB;
+        Lkk[r * LDR + c] = (r < kb && c <= r) ? A[static_cast<long long>(k0 + r) * lda + k0 + c] : 0.0;
       }
       __syncthreads();
-      // All threads, one barrier per column: column j updates the trailing
-      // block with its unscaled values (A_rl -= A_rj A_lj / A_jj) while
-      // column j-1 is scaled by 1/L_{j-1,j-1}; thread (ty, tx) owns rows
-      // ty + 16 u and columns tx + 16 v of the block.
       bool bad = false;  // uniform: every thread reads the same pivot
       for (int j = 0; j < kb; ++j) {
-        const double ajj = Lkk[j * LDK + j];
+        const double ajj = Lkk[j * LDR + j];
         if (!(ajj > 0.0)) {
           bad = true;
           if (tid == 0) sh_fail = 1;
@@ -150,36 +163,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_gp_energy(GpDev g, BatchDev b, 
         }
         const double iajj = 1.0 / ajj;
         if (j > 0) {
-          const double ipm = inv[j - 1];
-          for (int r = j + tid; r < kb; r += kThreads) Lkk[r * LDK + j - 1] *= ipm;
+          const double ipm = 1.0 / diag[j - 1];
+          for (int r = j + tid; r < kb; r += kThreads) Lkk[r * LDR + j - 1] *= ipm;
         }
-        if (tid == 0) {
-          const double piv = sqrt(ajj);
-          inv[j] = 1.0 / piv;
-          diag[j] = piv;
-        }
+        if (tid == 0) diag[j] = sqrt(ajj);
         double cj[4];
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
           const int l = tx + 16 * v;
-          cj[v] = (l > j && l < kb) ? Lkk[l * LDK + j] * iajj : 0.0;
+          cj[v] = (l > j && l < kb) ? Lkk[l * LDR + j] * iajj : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int r = ty + 16 * u;
           if (r > j && r < kb) {
-            const double arj = Lkk[r * LDK + j];
+            const double arj = Lkk[r * LDR + j];
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
               const int l = tx + 16 * v;
-              if (l > j && l <= r) Lkk[r * LDK + l] = fma(-arj, cj[v], Lkk[r * LDK + l]);
+              if (l > j && l <= r) Lkk[r * LDR + l] = fma(-arj, cj[v], Lkk[r * LDR + l]);
             }
           }
         }
         __syncthreads();
       }
       if (!bad) {
-        for (int c = tid; c < kb; c += kThreads) Lkk[c * LDK + c] = diag[c];
+        for (int c = tid; c < kb; c += kThreads) Lkk[c * LDR + c] = diag[c];
         if (tid < 32) {
           double lg = 0.0;
           for (int c = lane; c < kb; c += 32) lg += log(diag[c]);
@@ -188,60 +197,49 @@ __global__ void __launch_bounds__(kThreads, 1) k_gp_energy(GpDev g, BatchDev b, 
       }
       __syncthreads();
       if (sh_fail) break;
-      // 2. panel solve x L_kk^T = a for the rows below the block and the y row
-      const int r0 = k0 + kb;
-      for (int i = r0 + tid; i <= N; i += kThreads) {
-        double *row = A + static_cast<long long>(i) * lda + k0;
-        double a[PB];
-#pragma unroll
-        for (int c = 0; c < PB; ++c) a[c] = c < kb ? row[c] : 0.0;
-#pragma unroll
-        for (int c = 0; c < PB; ++c) {
-          if (c < kb) {
-            double s0 = a[c], s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-            for (int j = 0; j + 3 < c; j += 4) {
-              s0 = fma(-a[j], Lkk[c * LDK + j], s0);
-              s1 = fma(-a[j + 1], Lkk[c * LDK + j + 1], s1);
-              s2 = fma(-a[j + 2], Lkk[c * LDK + j + 2], s2);
-              s3 = fma(-a[j + 3], Lkk[c * LDK + j + 3], s3);
-            }
-#pragma unroll
-            for (int j = c & ~3; j < c; ++j) s0 = fma(-a[j], Lkk[c * LDK + j], s0);
-            a[c] = ((s0 + s1) + (s2 + s3)) * inv[c];
-          }
+      // 2. W = L_kk^-1 by forward substitution, column c by the 4 lanes
+      //    4c'..4c'+3 of a warp (partial sums over l split 4 ways):
+      //    W_cc = 1 / L_cc, W_ic = -(sum_{c <= l < i} L_il W_lc) / L_ii
+      {
+        const int c = tid >> 2, part = tid & 3;  // 64 columns x 4 parts, warp-uniform loop bounds
+        for (int e = tid; e < PB * PB; e += kThreads) W[(e / PB) * LDR + (e % PB)] = 0.0;
+        __syncthreads();
+        if (c < kb && part == 0) W[c * LDR + c] = 1.0 / diag[c];
+        __syncwarp();
+        for (int i = 1; i < kb; ++i) {
+          const bool act = c < i;  // (c < kb follows)
+          double s = 0.0;
+          if (act)
+            for (int l = c + part; l < i; l += 4) s = fma(Lkk[i * LDR + l], W[l * LDR + c], s);
+          s += __shfl_xor_sync(0xffffffffu, s, 1);
+          s += __shfl_xor_sync(0xffffffffu, s, 2);
+          if (act && part == 0) W[i * LDR + c] = -s / diag[i];
+          __syncwarp();
         }
-#pragma unroll
-        for (int c = 0; c < PB; ++c)
-          if (c < kb) row[c] = a[c];
       }
       __syncthreads();
-      // 3. trailing update A[i][j] -= sum_c L[i][c] L[j][c] over rows r0..N,
-      //    columns r0..min(i, N-1), in 64 x 64 tiles on the fp64 tensor cores
+      // 3. row blocks of [r0, N] (the y row included): X = A_panel W^T on the
+      //    fp64 tensor cores, written back to A and kept in Ti, then the
+      //    trailing update A[i][j] -= sum_c X[i][c] X[j][c] for the tiles
+      //    (bi, bj <= bi), columns r0..min(i, N-1)
+      const int r0 = k0 + kb;
       const int nrb = (N + 1 - r0 + PB - 1) / PB, ncb = (N - r0 + PB - 1) / PB;
+      const int kr = (kb + 3) & ~3;  // DMMA k range (W and Ti zero past kb)
       for (int bi = 0; bi < nrb; ++bi) {
         const int i0 = r0 + bi * PB;
         const int rows = min(PB, N + 1 - i0);
-        // Ti, then Tj(0) in flight; Tj(bj+1) is fetched while Tj(bj) is used
         load_panel_tile(Ti, A, lda, i0, rows, k0, kb);
         cp_async_commit();
-        const int nbj = min(bi + 1, ncb);
-        auto fetch = [&](int bj) {
-          if (bj < nbj && bj != bi)
-            load_panel_tile(Tj + (bj & 1) * PB * LDR, A, lda, r0 + bj * PB, min(PB, N - (r0 + bj * PB)), k0, kb);
-          cp_async_commit();  // possibly empty group: keeps the wait count uniform
-        };
-        fetch(0);
-        for (int bj = 0; bj < nbj; ++bj) {
-          const int j0 = r0 + bj * PB;
-          const int cols = min(PB, N - j0);
-          fetch(bj + 1);
-          cp_async_wait<1>();  // all but the newest group: Ti and Tj(bj) have landed
-          __syncthreads();
-          const double *Tj_cur = Tj + (bj & 1) * PB * LDR;
-          const double *Tb = bj == bi ? Ti : Tj_cur;
-          // prefetch the 16 outputs (their latency hides behind the rank-kb product)
-          double cur[4][2][2], acc[4][2][2];
+        cp_async_wait<0>();
+        __syncthreads();
+        {
+          double acc[4][2][2];
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < 2; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+          mma_rows(Ti, W, kr, m_base, n_base, gq, tq, acc);
+          __syncthreads();  // every warp is done reading Ti
 #pragma unroll
           for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
@@ -249,39 +247,73 @@ __global__ void __launch_bounds__(kThreads, 1) k_gp_energy(GpDev g, BatchDev b, 
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
                 const int r = m_base + 8 * mi + gq, cc = n_base + 8 * ni + 2 * tq + h;
-                cur[mi][ni][h] = (r < rows && cc < cols && j0 + cc <= i0 + r)
-                                     ? A[static_cast<long long>(i0 + r) * lda + j0 + cc]
-                                     : 0.0;
-                acc[mi][ni][h] = 0.0;
+                Ti[r * LDR + cc] = acc[mi][ni][h];  // zero past rows / kb
+                if (r < rows && cc < kb) A[static_cast<long long>(i0 + r) * lda + k0 + cc] = acc[mi][ni][h];
               }
-          const double *pa = Ti + (m_base + gq) * LDR + tq;
-          const double *pb = Tb + (n_base + gq) * LDR + tq;
-#pragma unroll 4
-          for (int c = 0; c < kb; c += 4) {
-            double av[4], bv[2];
-#pragma unroll
-            for (int mi = 0; mi < 4; ++mi) av[mi] = pa[8 * mi * LDR + c];
-#pragma unroll
-            for (int ni = 0; ni < 2; ++ni) bv[ni] = pb[8 * ni * LDR + c];
+          __syncthreads();
+        }
+        const int nbj = min(bi + 1, ncb);
+        for (int bj = 0; bj < nbj; ++bj) {
+          const int j0 = r0 + bj * PB;
+          const int cols = min(PB, N - j0);
+          if (bj != bi) {
+            load_panel_tile(Tj, A, lda, j0, cols, k0, kb);
+            cp_async_commit();
+          }
+          // prefetch the 16 outputs (their latency hides behind the tile loads
+          // and the product); interior tiles (full, strictly below the
+          // diagonal) need no masks and use 16-B accesses
+          const bool interior = bj < bi && rows == PB && cols == PB;
+          double *Ot = A + static_cast<long long>(i0 + m_base + gq) * lda + j0 + n_base + 2 * tq;
+          double cur[4][2][2], acc[4][2][2];
+          if (interior) {
 #pragma unroll
             for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-              for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], av[mi], bv[ni]);
+              for (int ni = 0; ni < 2; ++ni) {
+                const double2 v = *reinterpret_cast<const double2 *>(Ot + 8 * mi * lda + 8 * ni);
+                cur[mi][ni][0] = v.x;
+                cur[mi][ni][1] = v.y;
+              }
+          } else {
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+              for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                  const int r = m_base + 8 * mi + gq, cc = n_base + 8 * ni + 2 * tq + h;
+                  cur[mi][ni][h] = (r < rows && cc < cols && j0 + cc <= i0 + r) ? Ot[8 * mi * lda + 8 * ni + h] : 0.0;
+                }
           }
 #pragma unroll
           for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-            for (int ni = 0; ni < 2; ++ni)
+            for (int ni = 0; ni < 2; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+          if (bj != bi) cp_async_wait<0>();
+          __syncthreads();
+          mma_rows(Ti, bj == bi ? Ti : Tj, kr, m_base, n_base, gq, tq, acc);
+          if (interior) {
 #pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                const int r = m_base + 8 * mi + gq, cc = n_base + 8 * ni + 2 * tq + h;
-                if (r < rows && cc < cols && j0 + cc <= i0 + r)
-                  A[static_cast<long long>(i0 + r) * lda + j0 + cc] = cur[mi][ni][h] - acc[mi][ni][h];
-              }
-          __syncthreads();  // Tj(bj) is refilled by the fetch of iteration bj + 1
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+              for (int ni = 0; ni < 2; ++ni)
+                *reinterpret_cast<double2 *>(Ot + 8 * mi * lda + 8 * ni) =
+                    make_double2(cur[mi][ni][0] - acc[mi][ni][0], cur[mi][ni][1] - acc[mi][ni][1]);
+          } else {
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+              for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                  const int r = m_base + 8 * mi + gq, cc = n_base + 8 * ni + 2 * tq + h;
+                  if (r < rows && cc < cols && j0 + cc <= i0 + r)
+                    Ot[8 * mi * lda + 8 * ni + h] = cur[mi][ni][h] - acc[mi][ni][h];
+                }
+          }
+          __syncthreads();  // Tj is refilled by the next tile
         }
-        cp_async_wait<0>();
-        __syncthreads();
       }
     }
     // ---- E = 1/2 |alpha|^2 + sum log L_ii + N/2 log 2 pi ----
@@ -315,6 +347,7 @@ bool gp_setup(void **handle, const double *X, const double *y, int N, int D, dou
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  sms *= 2;  // two CTAs (two probe matrices) per SM
   E->grid = sms;
   E->g.N = N;
   E->g.D = D;
@@ -333,7 +366,7 @@ bool gp_setup(void **handle, const double *X, const double *y, int N, int D, dou
   E->g.X = dX;
   E->g.y = dy;
   E->g.scratch = sc;
-  E->smem = (static_cast<size_t>(N) * D + 1 + PB * LDK + 3 * PB * LDR + 2 * PB + 16) * sizeof(double);
+  E->smem = (3 * static_cast<size_t>(PB) * LDR + PB + 16) * sizeof(double);
   cudaFuncSetAttribute(k_gp_energy, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(E->smem));
   *handle = E;
   return E->smem <= 200 * 1024;
