@@ -98,6 +98,9 @@ typedef struct {
   int32_t n_volume_sims; /* R volume replicas, >= 2                       */
   int64_t max_dead;      /* dead-store capacity in records, >= n_live (R-26)       */
   uint64_t seed;         /* Philox key                          */
+  int32_t update_all;    /* F4: 1 = every live point runs p HRSS steps each
+                            iteration (deleted slots from their parent, survivors
+                            from themselves); 0 = the k replacements only          */
 } nss_config;
 
 /* Multi-GPU: one process per GPU.  The HRSS chains of an

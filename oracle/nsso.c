@@ -608,10 +608,11 @@ int nsso_init_ex(const nsso_prior *p, const nsso_energy *e, const nsso_config *c
   c->lz = (double *)xcalloc((size_t)c->R + 1, sizeof(double));
   for (int r = 0; r <= c->R; ++r) c->lz[r] = -INFINITY;
   c->t_dead = (int32_t *)xcalloc((size_t)k, sizeof(int32_t));
-  c->t_dest = (int32_t *)xcalloc((size_t)k, sizeof(int32_t));
-  c->t_parent = (int32_t *)xcalloc((size_t)k, sizeof(int32_t));
-  c->t_counts = (uint8_t *)xcalloc((size_t)(k * (cfg->steps > 0 ? cfg->steps : 1) * 4), 1);
-  c->t_margin = (double *)xcalloc((size_t)(k * (cfg->steps > 0 ? cfg->steps : 1)), sizeof(double));
+  int64_t nch = cfg->update_all ? n : k; /* chains per iteration */
+  c->t_dest = (int32_t *)xcalloc((size_t)nch, sizeof(int32_t));
+  c->t_parent = (int32_t *)xcalloc((size_t)nch, sizeof(int32_t));
+  c->t_counts = (uint8_t *)xcalloc((size_t)(nch * (cfg->steps > 0 ? cfg->steps : 1) * 4), 1);
+  c->t_margin = (double *)xcalloc((size_t)(nch * (cfg->steps > 0 ? cfg->steps : 1)), sizeof(double));
   c->n_subset = -1;
   c->e_star = INFINITY;
   /* prior draws with rejection, budget 100 n attempts in total */
@@ -727,6 +728,21 @@ int nsso_step(nsso_ctx *c, nsso_step_info *info) {
     uint64_t rank = ((uint64_t)u32 * (uint64_t)(n - k)) >> 32;
     c->t_parent[cidx] = S[rank];
   }
+  /* F4 "applying updates to all m particles": every live slot runs a
+   * chain, in ascending gid order; a deleted slot starts from its resampled
+   * parent, a surviving slot from its own point; all start from the
+   * pre-mutation live set and use the destination-keyed RNG stream. */
+  if (c->cfg.update_all) {
+    int32_t *par_of = (int32_t *)xcalloc((size_t)n, sizeof(int32_t));
+    for (int64_t g = 0; g < n; ++g) par_of[g] = (int32_t)g;
+    for (int64_t cidx = 0; cidx < k; ++cidx) par_of[c->t_dest[cidx]] = c->t_parent[cidx];
+    for (int64_t g = 0; g < n; ++g) {
+      c->t_dest[g] = (int32_t)g;
+      c->t_parent[g] = par_of[g];
+    }
+    free(par_of);
+    k = n; /* chains below */
+  }
 
   /* (iii) mutate: p HRSS steps from each duplicated parent;
    * (iv) replace: write into the destination slot */
@@ -768,7 +784,7 @@ int nsso_step(nsso_ctx *c, nsso_step_info *info) {
     int32_t s = c->t_dest[cidx];
     memcpy(&c->X[(int64_t)s * d], &Xnew[cidx * d], sizeof(double) * (size_t)d);
     c->E[s] = Enew[cidx];
-    c->birth[s] = e_star;
+    if (c->t_parent[cidx] != s) c->birth[s] = e_star; /* a moved survivor keeps its birth level */
   }
   free(Xnew); free(Enew);
   free(x); free(xn); free(z); free(v); free(run); free(is_dead); free(S); free(order);
@@ -1061,13 +1077,13 @@ int nsso_set_chain_subset(nsso_ctx *c, const int32_t *chains, int64_t count) {
 int nsso_get_trace(nsso_ctx *c, int32_t *dead_gid, int32_t *dest_gid, int32_t *parent_gid,
                    uint8_t *counts, double *min_margin, double *e_star) {
   if (!c) return NSSO_ERR_INVALID_ARG;
-  int64_t k = c->k;
+  int64_t k = c->k, nch = c->cfg.update_all ? c->n : c->k;
   int p = c->cfg.steps > 0 ? c->cfg.steps : 1;
   if (dead_gid) memcpy(dead_gid, c->t_dead, sizeof(int32_t) * (size_t)k);
-  if (dest_gid) memcpy(dest_gid, c->t_dest, sizeof(int32_t) * (size_t)k);
-  if (parent_gid) memcpy(parent_gid, c->t_parent, sizeof(int32_t) * (size_t)k);
-  if (counts) memcpy(counts, c->t_counts, (size_t)(k * p * 4));
-  if (min_margin) memcpy(min_margin, c->t_margin, sizeof(double) * (size_t)(k * p));
+  if (dest_gid) memcpy(dest_gid, c->t_dest, sizeof(int32_t) * (size_t)nch);
+  if (parent_gid) memcpy(parent_gid, c->t_parent, sizeof(int32_t) * (size_t)nch);
+  if (counts) memcpy(counts, c->t_counts, (size_t)(nch * p * 4));
+  if (min_margin) memcpy(min_margin, c->t_margin, sizeof(double) * (size_t)(nch * p));
   if (e_star) *e_star = c->e_star;
   return NSSO_OK;
 }

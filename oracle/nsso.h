@@ -86,6 +86,7 @@ typedef struct {
   int32_t n_volume_sims;   /* R = 100                           */
   int64_t max_dead;        /* dead-store capacity                        */
   uint64_t seed;
+  int32_t update_all;      /* F4: 1 = mutate all n live points each iteration */
 } nsso_config;
 
 typedef struct {
@@ -133,7 +134,8 @@ int nsso_get_metric(nsso_ctx *ctx, double *chol /* d*d lower */, double *width);
  * ascending destination list); count < 0 restores "all chains". */
 int nsso_set_chain_subset(nsso_ctx *ctx, const int32_t *chains, int64_t count);
 /* Trace of the last iteration: dead gids (key-descending), destinations
- * (ascending gid), parent gid per destination, per (chain, step) counts
+ * (ascending gid; all n gids when update_all), parent gid per destination
+ * (itself for a surviving slot), per (chain, step) counts
  * packed as {n_left, n_right, n_shrink, accepted} and the smallest relative
  * decision margin seen in that step. Any pointer may be NULL. */
 int nsso_get_trace(nsso_ctx *ctx, int32_t *dead_gid, int32_t *dest_gid, int32_t *parent_gid,

@@ -51,7 +51,7 @@ class Config(C.Structure):
                 ("max_stepout", C.c_int32), ("max_shrink", C.c_int32),
                 ("quadrature", C.c_int32), ("metric_reg", C.c_double),
                 ("term_log_ratio", C.c_double), ("n_volume_sims", C.c_int32),
-                ("max_dead", C.c_int64), ("seed", C.c_uint64)]
+                ("max_dead", C.c_int64), ("seed", C.c_uint64), ("update_all", C.c_int32)]
 
 
 class StepInfo(C.Structure):
@@ -324,11 +324,12 @@ class Oracle:
 
     def trace(self) -> Dict:
         k, p = self.k, max(self.p, 1)
+        nch = self.n if self.cfg.get("update_all", 0) else k  # chains per iteration (F4: all n)
         dead = np.zeros(k, np.int32)
-        dest = np.zeros(k, np.int32)
-        par = np.zeros(k, np.int32)
-        counts = np.zeros((k, p, 4), np.uint8)
-        margin = np.zeros((k, p))
+        dest = np.zeros(nch, np.int32)
+        par = np.zeros(nch, np.int32)
+        counts = np.zeros((nch, p, 4), np.uint8)
+        margin = np.zeros((nch, p))
         es = C.c_double()
         i32 = lambda a: a.ctypes.data_as(C.POINTER(C.c_int32))
         _check(lib().nsso_get_trace(self._h, i32(dead), i32(dest), i32(par),
