@@ -57,7 +57,7 @@ namespace {
 __global__ void k_pack_chains(RunDev r, float *buf, int row) {
   const int c = r.c0 + blockIdx.x;
   if (c >= r.c1) return;
-  const int s = r.dest_gid[c];
+  const int s = r.cdest[c];
   float *o = buf + static_cast<long long>(c - r.c0) * row;
   for (int i = threadIdx.x; i < row; i += blockDim.x)
     o[i] = i < r.dp ? r.X[static_cast<long long>(s) * r.dp + i] : r.E[s];
@@ -65,9 +65,9 @@ __global__ void k_pack_chains(RunDev r, float *buf, int row) {
 
 __global__ void k_unpack_chains(RunDev r, const float *all, int row) {
   const int c = blockIdx.x;
-  if (c >= r.k || (c >= r.c0 && c < r.c1)) return;  // own rows are already in place
+  if (c >= r.nch || (c >= r.c0 && c < r.c1)) return;  // own rows are already in place
   const DevState *st = r.st;
-  const int s = r.dest_gid[c];
+  const int s = r.cdest[c];
   const float *in = all + static_cast<long long>(c) * row;
   for (int i = threadIdx.x; i < row; i += blockDim.x) {
     if (i < r.dp)
@@ -75,7 +75,7 @@ __global__ void k_unpack_chains(RunDev r, const float *all, int row) {
     else
       r.E[s] = in[i];
   }
-  if (threadIdx.x == 0 && !(st->terminated || st->error || st->finalised)) r.birth[s] = st->e_star;
+  if (threadIdx.x == 0 && !(st->terminated || st->error || st->finalised) && r.cpar[c] != s) r.birth[s] = st->e_star;
 }
 
 }  // namespace
@@ -125,7 +125,7 @@ bool exchange_chains(const RunDev &r, void *comm, float *buf, float *all, int kc
     *err = std::string("ncclAllGather: ") + (nccl_api()->error_string ? nccl_api()->error_string(rc) : "error");
     return false;
   }
-  k_unpack_chains<<<r.k, 128, 0, lc.stream>>>(r, all, row);
+  k_unpack_chains<<<r.nch, 128, 0, lc.stream>>>(r, all, row);
   ++*lc.launch_counter;
   return true;
 }

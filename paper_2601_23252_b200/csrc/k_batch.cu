@@ -94,13 +94,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_batch_begin(RunDev r, P
   if (c >= r.c1) return;
   const DevState *st = r.st;
   const bool off = st->terminated || st->error || st->finalised;
-  const int d = r.d, par = r.parent_gid[c];
+  const int d = r.d, par = r.cpar[c];
   float pa[NPL], pb[NPL], x[NPL];
   load_prior_lane<NPL>(pr, lane, d, pa, pb);
 #pragma unroll
   for (int t = 0; t < NPL; ++t) {
     const int i = lane + 32 * t;
-    x[t] = i < d ? r.X[static_cast<long long>(par) * r.dp + i] : 0.f;
+    x[t] = i < d ? r.Xs[static_cast<long long>(par) * r.dp + i] : 0.f;
     if (i < r.dp) b.x[static_cast<long long>(c) * b.dp + i] = x[t];
   }
   bool dummy;
@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_batch_begin(RunDev r, P
     ChainRegs s{};
     s.phase = off ? kPhDone : kPhDir;
     s.row0 = s.row1 = -1;
-    s.e = r.E[par];
+    s.e = r.Es[par];
     s.lp = lp;
     store_chain(b, c, s);
   }
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_batch_advance(RunDev r,
   if (s.phase == kPhDone) return;
 
   const uint32_t it = static_cast<uint32_t>(st->iter)  /* set by the select kernel */;
-  const int dest = r.dest_gid[c];
+  const int dest = r.cdest[c];
   const float e_star = st->e_star, w = st->width;
   const int p = r.p, cap = r.max_stepout, maxs = r.max_shrink;
   const bool euclid = r.dir_norm == NSS_DIR_EUCLIDEAN;
@@ -433,10 +433,10 @@ __global__ void k_batch_finish(RunDev r, BatchDev b) {
   if (threadIdx.x < 5) acc[threadIdx.x] = 0;
   __syncthreads();
   if (c < r.c1) {
-    const int s = r.dest_gid[c];
+    const int s = r.cdest[c];
     for (int i = 0; i < r.d; ++i) r.X[static_cast<long long>(s) * r.dp + i] = b.x[static_cast<long long>(c) * b.dp + i];
     r.E[s] = b.e[c];
-    r.birth[s] = st->e_star;
+    if (r.cpar[c] != s) r.birth[s] = st->e_star;  // a moved survivor (F4) keeps its birth level
     for (int q = 0; q < 5; ++q) atomicAdd(&acc[q], static_cast<unsigned long long>(b.cnt[q * b.k + c]));
   }
   __syncthreads();

@@ -47,8 +47,8 @@ __global__ void __launch_bounds__(256) k_hrss(RunDev r, PriorDev pr, EnergyDev e
 
   DevState *st = r.st;
   const uint32_t it = static_cast<uint32_t>(st->iter)  /* set by the select kernel */;
-  const int s = r.dest_gid[c];
-  const int par = r.parent_gid[c];
+  const int s = r.cdest[c];
+  const int par = r.cpar[c];
   const float e_star = st->e_star;
   const float w = st->width;
   const int p = r.p;
@@ -63,9 +63,9 @@ __global__ void __launch_bounds__(256) k_hrss(RunDev r, PriorDev pr, EnergyDev e
 #pragma unroll
   for (int t = 0; t < NPL; ++t) {
     const int i = lane + 32 * t;
-    x[t] = i < d ? r.X[static_cast<long long>(par) * r.dp + i] : 0.f;
+    x[t] = i < d ? r.Xs[static_cast<long long>(par) * r.dp + i] : 0.f;
   }
-  float e = r.E[par];
+  float e = r.Es[par];
   bool dummy;
   float lp = prior_logp<NPL>(x, pr, pa, pb, lane, d, dummy);
 
@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(256) k_hrss(RunDev r, PriorDev pr, EnergyDev e
   }
   if (lane == 0) {
     r.E[s] = e;
-    r.birth[s] = e_star;
+    if (par != s) r.birth[s] = e_star;  // a moved survivor (F4) keeps its birth level
     atomicAdd(&st->probes, n_probe);
     atomicAdd(&st->evals, n_eval);
     atomicAdd(&st->expansions, n_exp);

@@ -215,8 +215,8 @@ __global__ void __launch_bounds__(256) k_hrss_lane(RunDev r, PriorDev pr, Energy
 
   DevState *st = r.st;
   // issue the independent loads first; the flags are checked after
-  const int s = r.dest_gid[c];
-  const int par = r.parent_gid[c];
+  const int s = r.cdest[c];
+  const int par = r.cpar[c];
   LaneParams<D, KIND, K> P;
   load_params<D, KIND, K>(P, en);
   // row `lane` of L (zeros past d), held in registers for the whole chain
@@ -235,8 +235,8 @@ __global__ void __launch_bounds__(256) k_hrss_lane(RunDev r, PriorDev pr, Energy
   }
   float x[D], v[D];
 #pragma unroll
-  for (int i = 0; i < D; ++i) x[i] = i < d ? r.X[static_cast<long long>(par) * r.dp + i] : 0.f;
-  float e = r.E[par];
+  for (int i = 0; i < D; ++i) x[i] = i < d ? r.Xs[static_cast<long long>(par) * r.dp + i] : 0.f;
+  float e = r.Es[par];
   if (st->terminated || st->error || st->finalised) return;
   const uint32_t it = static_cast<uint32_t>(st->iter)  /* set by the select kernel */;
   const float e_star = st->e_star;
@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(256) k_hrss_lane(RunDev r, PriorDev pr, Energy
   if (lane < d) r.X[static_cast<long long>(s) * r.dp + lane] = xv;
   if (lane == 0) {
     r.E[s] = e;
-    r.birth[s] = e_star;
+    if (par != s) r.birth[s] = e_star;  // a moved survivor (F4) keeps its birth level
     if (nan_seen) raise_error(st, NSS_ERR_NAN);
     atomicAdd(&st->probes, n_probe);
     atomicAdd(&st->evals, n_eval);

@@ -571,6 +571,31 @@ __global__ void k_dead_rows(RunDev r) {
   }
 }
 
+// F4 update-all: chain c = slot c; a deleted slot starts from its
+// resampled parent (binary search in the ascending destinations), a survivor
+// from itself; all start from a snapshot of the pre-mutation live set.
+__global__ void k_chains_all(RunDev r, int *cdest, int *cpar, float *Xs, float *Es) {
+  const DevState *st = r.st;
+  if (st->terminated || st->error || st->finalised) return;
+  const long long tid = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long gg = tid; gg < r.n; gg += stride) {
+    const int g = static_cast<int>(gg);
+    int lo = 0, hi = r.k;  // first destination >= g
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (r.dest_gid[mid] < g) lo = mid + 1; else hi = mid;
+    }
+    cdest[g] = g;
+    cpar[g] = (lo < r.k && r.dest_gid[lo] == g) ? r.parent_gid[lo] : g;
+    Es[g] = r.E[g];
+  }
+  const long long tot = static_cast<long long>(r.n) * (r.dp >> 2);
+  const float4 *X4 = reinterpret_cast<const float4 *>(r.X);
+  float4 *S4 = reinterpret_cast<float4 *>(Xs);
+  for (long long q = tid; q < tot; q += stride) S4[q] = X4[q];
+}
+
 size_t select_smem(int n) {
   if (n <= kSmemKeysMax) return static_cast<size_t>(kSmemKeysMax + kSmemSortMax) * 8;
   if (n <= kSmemOrdMax) return static_cast<size_t>(kSmemSortMax) * 8 + static_cast<size_t>(n) * 4;
@@ -615,6 +640,13 @@ void launch_select(const RunDev &r, const LaunchCtx &lc) {
     k_dead_rows<<<static_cast<int>(want < 2 * sms ? want : 2 * sms), 256, 0, lc.stream>>>(r);
     ++*lc.launch_counter;
   }
+}
+
+void launch_chains_all(const RunDev &r, int *cdest, int *cpar, float *Xs, float *Es, const LaunchCtx &lc) {
+  const long long work = static_cast<long long>(r.n) * (r.dp >> 2);
+  const long long want = ((work > r.n ? work : r.n) + 255) / 256;
+  k_chains_all<<<static_cast<int>(want < 1184 ? want : 1184), 256, 0, lc.stream>>>(r, cdest, cpar, Xs, Es);
+  ++*lc.launch_counter;
 }
 
 void launch_finalise_sort(const RunDev &r, const LaunchCtx &lc) {

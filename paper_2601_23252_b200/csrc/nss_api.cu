@@ -147,6 +147,7 @@ bool validate(const nss_prior *p, const nss_energy *e, const nss_config *cfg) {
       cfg->max_shrink > 255)
     return false;
   if (cfg->n_volume_sims < 2 || !(cfg->width > 0.0) || cfg->max_dead < cfg->n_live) return false;
+  if (cfg->update_all != 0 && cfg->update_all != 1) return false;
   if (cfg->width_rule != NSS_W_OPTIMAL && cfg->width_rule != NSS_W_FIXED) return false;
   if (cfg->dir_norm != NSS_DIR_MAHALANOBIS && cfg->dir_norm != NSS_DIR_EUCLIDEAN) return false;
   if (cfg->quadrature != NSS_Q_TRAPEZOID && cfg->quadrature != NSS_Q_RECTANGLE) return false;
@@ -277,7 +278,12 @@ nss_status enqueue_iteration_eager(nss_ctx *c, bool with_metric) {
       CK(cudaEventRecord(c->ev_met, c->side2));
     }
   }
-  if ((s = timed_launch(c, 1, c->stream, [&] { launch_select(c->r, lc); }))) return s;
+  if ((s = timed_launch(c, 1, c->stream, [&] {
+         launch_select(c->r, lc);
+         if (c->cfg.update_all) launch_chains_all(c->r, c->r.cdest, c->r.cpar, const_cast<float *>(c->r.Xs),
+                                                  const_cast<float *>(c->r.Es), lc);
+       })))
+    return s;
   if (c->serial_evidence) {
     if ((s = timed_launch(c, 2, c->stream, [&] { launch_evidence(c->r, 0, lc); }))) return s;
   } else {
@@ -323,7 +329,7 @@ nss_status ensure_batch(nss_ctx *c) {
   if (c->batch_alloc && c->batch_backend == backend) return NSS_OK;
   if (backend == 1 && !batch_generic_ok(c->en)) return fail(c, NSS_ERR_UNSUPPORTED, "no batched energy for this kind");
   BatchDev &b = c->bd;
-  const int k = c->r.k;
+  const int k = c->r.nch;  // chains per iteration
   if (!c->batch_alloc) {
     b.k = k;
     b.dp = c->dp;
@@ -418,7 +424,12 @@ nss_status enqueue_iteration_batch(nss_ctx *c) {
   if ((s = ensure_batch(c))) return s;
   LaunchCtx lc = lctx(c);
   if (c->metric_pending && (s = launch_metric_on(c, c->stream, 1))) return s;
-  if ((s = timed_launch(c, 1, c->stream, [&] { launch_select(c->r, lc); }))) return s;
+  if ((s = timed_launch(c, 1, c->stream, [&] {
+         launch_select(c->r, lc);
+         if (c->cfg.update_all) launch_chains_all(c->r, c->r.cdest, c->r.cpar, const_cast<float *>(c->r.Xs),
+                                                  const_cast<float *>(c->r.Es), lc);
+       })))
+    return s;
   CK(cudaEventRecord(c->ev_sel, c->stream));
   CK(cudaStreamWaitEvent(c->side, c->ev_sel, 0));
   LaunchCtx ls{c->side, &c->launches};
@@ -723,8 +734,10 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
   r.quadrature = cfg->quadrature;
   r.R = R;
   r.max_dead = cfg->max_dead;
+  const long long nch = cfg->update_all ? n : k;
+  r.nch = static_cast<int>(nch);
   r.c0 = 0;
-  r.c1 = static_cast<int>(k);
+  r.c1 = static_cast<int>(nch);
   r.seed_lo = static_cast<uint32_t>(cfg->seed);
   r.seed_hi = static_cast<uint32_t>(cfg->seed >> 32);
   r.term_log_ratio = static_cast<float>(cfg->term_log_ratio);
@@ -746,7 +759,21 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
   if ((s = dalloc(c, &r.dest_gid, k))) return bail(s);
   if ((s = dalloc(c, &r.parent_gid, k))) return bail(s);
   if ((s = dalloc(c, &r.surv, n))) return bail(s);
-  if ((s = dalloc(c, &r.counts, static_cast<size_t>(k) * (cfg->steps > 0 ? cfg->steps : 1)))) return bail(s);
+  if ((s = dalloc(c, &r.counts, static_cast<size_t>(nch) * (cfg->steps > 0 ? cfg->steps : 1)))) return bail(s);
+  if (cfg->update_all) {  // F4: chains over every slot, started from a snapshot
+    float *xs = nullptr, *es = nullptr;
+    if ((s = dalloc(c, &r.cdest, n))) return bail(s);
+    if ((s = dalloc(c, &r.cpar, n))) return bail(s);
+    if ((s = dalloc(c, &xs, static_cast<size_t>(n) * c->dp))) return bail(s);
+    if ((s = dalloc(c, &es, n))) return bail(s);
+    r.Xs = xs;
+    r.Es = es;
+  } else {
+    r.cdest = r.dest_gid;
+    r.cpar = r.parent_gid;
+    r.Xs = r.X;
+    r.Es = r.E;
+  }
   size_t P = 1;
   while (P < static_cast<size_t>(n)) P <<= 1;
   if ((s = dalloc(c, &r.sort_scratch, P + static_cast<size_t>(n)))) return bail(s);
@@ -769,9 +796,9 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
   if (dist && dist->nccl_uid) {
     c->rank = dist->rank;
     c->world = dist->world;
-    c->kc = static_cast<int>((k + c->world - 1) / c->world);
-    r.c0 = static_cast<int>(std::min<long long>(k, static_cast<long long>(c->rank) * c->kc));
-    r.c1 = static_cast<int>(std::min<long long>(k, r.c0 + static_cast<long long>(c->kc)));
+    c->kc = static_cast<int>((nch + c->world - 1) / c->world);
+    r.c0 = static_cast<int>(std::min<long long>(nch, static_cast<long long>(c->rank) * c->kc));
+    r.c1 = static_cast<int>(std::min<long long>(nch, r.c0 + static_cast<long long>(c->kc)));
     const size_t row = static_cast<size_t>(c->dp) + 1;
     if ((s = dalloc(c, &c->xbuf, static_cast<size_t>(c->kc) * row))) return bail(s);
     if ((s = dalloc(c, &c->xall, static_cast<size_t>(c->world) * c->kc * row))) return bail(s);
@@ -1082,13 +1109,13 @@ NSS_API nss_status nss_get_trace(nss_ctx *c, int32_t *dead_gid, int32_t *dest_gi
   nss_status s = check_usable(c);
   if (s) return s;
   CK(cudaStreamSynchronize(c->stream));
-  const size_t k = c->r.k;
+  const size_t k = c->r.k, nch = c->r.nch;
   if (dead_gid) CK(cudaMemcpy(dead_gid, c->r.dead_gid, k * sizeof(int), cudaMemcpyDeviceToHost));
-  if (dest_gid) CK(cudaMemcpy(dest_gid, c->r.dest_gid, k * sizeof(int), cudaMemcpyDeviceToHost));
-  if (parent_gid) CK(cudaMemcpy(parent_gid, c->r.parent_gid, k * sizeof(int), cudaMemcpyDeviceToHost));
+  if (dest_gid) CK(cudaMemcpy(dest_gid, c->r.cdest, nch * sizeof(int), cudaMemcpyDeviceToHost));
+  if (parent_gid) CK(cudaMemcpy(parent_gid, c->r.cpar, nch * sizeof(int), cudaMemcpyDeviceToHost));
   if (counts) {
     const size_t p = c->cfg.steps > 0 ? c->cfg.steps : 1;
-    CK(cudaMemcpy(counts, c->r.counts, k * p * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(counts, c->r.counts, nch * p * sizeof(uint32_t), cudaMemcpyDeviceToHost));
   }
   if (e_star) {
     if ((s = pull_state(c))) return s;
@@ -1301,7 +1328,7 @@ NSS_API nss_status nss_set_chain_range(nss_ctx *c, int32_t c0, int32_t c1) {
   nss_status s = check_usable(c);
   if (s) return s;
   if (c->comm) return fail(c, NSS_ERR_STATE, "chain range is fixed by the NCCL rank");
-  if (c0 < 0 || c1 < c0 || c1 > c->r.k) return NSS_ERR_INVALID_ARG;
+  if (c0 < 0 || c1 < c0 || c1 > c->r.nch) return NSS_ERR_INVALID_ARG;
   CK(cudaStreamSynchronize(c->stream));
   drop_graph(c);
   c->r.c0 = c0;

@@ -70,7 +70,14 @@ struct RunDev {
   int dir_norm, quadrature;
   int R;
   int engine;                 // nss_hrss_engine (host-side choice)
-  int c0, c1;                 // HRSS chains [c0, c1) run here (all k on one GPU)
+  int c0, c1;                 // HRSS chains [c0, c1) run here (all on one GPU)
+  // HRSS chains of the iteration: nch = k (destinations = deleted slots) or n
+  // (F4 update-all: every slot); chain c writes slot cdest[c] starting from
+  // row cpar[c] of the start arrays Xs/Es (X/E themselves, or a snapshot of
+  // the pre-mutation live set when survivors move too)
+  int nch;
+  int *cdest, *cpar;
+  const float *Xs, *Es;
   long long max_dead;
   uint32_t seed_lo, seed_hi;
   float term_log_ratio;
@@ -205,6 +212,7 @@ bool lane_engine_ok(const RunDev &r, const EnergyDev &en);
 void launch_hrss_lane(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc);
 // k_metric.cu: A5 metric (+ A9 termination when iterating)
 void launch_term_probe(const RunDev &r, const LaunchCtx &lc);
+void launch_chains_all(const RunDev &r, int *cdest, int *cpar, float *Xs, float *Es, const LaunchCtx &lc);
 void launch_metric(const RunDev &r, double metric_reg, int width_rule, double width_param,
                    int end_of_iteration, double *partials, unsigned *ticket, int n_blocks, const LaunchCtx &lc);
 int metric_blocks(int n, int d);

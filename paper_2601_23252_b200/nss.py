@@ -339,8 +339,10 @@ class Sampler:
 
     def trace(self) -> Dict:
         k, p = self.k, max(self.p, 1)
-        dead, dest, par = (np.zeros(k, np.int32) for _ in range(3))
-        counts = np.zeros((k, p, 4), np.uint8)
+        nch = self.n if self.cfg.get("update_all", 0) else k  # chains per iteration (F4: all n)
+        dead = np.zeros(k, np.int32)
+        dest, par = np.zeros(nch, np.int32), np.zeros(nch, np.int32)
+        counts = np.zeros((nch, p, 4), np.uint8)
         es = C.c_float()
         self._check(lib().nss_get_trace(self._h, _ip(dead), _ip(dest), _ip(par),
                                         counts.ctypes.data_as(C.POINTER(C.c_uint8)), C.byref(es)),

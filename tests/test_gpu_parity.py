@@ -315,3 +315,27 @@ def test_c4_full_size_iteration_subset():
     assert good >= 5
     info = gpu.info()
     assert info["null_moves"] == 0 and info["energy_evals"] > 1e6
+
+
+UPDATE_ALL_CASES = {
+    "lane_mog": (lambda: W.mog(4, n_comp=2, seed=4, mean_box=3.0, min_sep=3.0), dict(n_live=150, k=15, steps=4),
+                 "lane"),
+    "warp_corr": (lambda: W.corr_gauss(12, seed=2), dict(n_live=200, k=20, steps=3), "warp"),
+    "batch_logreg": (lambda: W.logreg(5, n_data=300, seed=3), dict(n_live=120, k=12, steps=2), "batch"),
+}
+
+
+@pytest.mark.parametrize("name", sorted(UPDATE_ALL_CASES))
+def test_update_all_single_iteration_parity(name):
+    """F4: every live slot runs a chain; same bar as the standard iteration."""
+    make, kw, engine = UPDATE_ALL_CASES[name]
+    prob = make()
+    cfg = W.config(seed=11, update_all=1, **kw)
+    gpu, ref = inject_pair(prob, cfg, warm_iters=1, engine=engine)
+    if gpu.engine() != engine:
+        pytest.skip(f"{engine} engine does not apply")
+    st = compare_iteration(gpu, ref, prob)
+    tg = gpu.trace()
+    assert tg["dest_gid"].size == kw["n_live"]
+    dg, dr = gpu.dead(), ref.dead()
+    assert np.array_equal(dg["gid"], dr["gid"])
