@@ -101,7 +101,14 @@ typedef struct {
   int32_t update_all;    /* F4: 1 = every live point runs p HRSS steps each
                             iteration (deleted slots from their parent, survivors
                             from themselves); 0 = the k replacements only          */
+  int32_t mutation;      /* F1: NSS_MUT_HRSS (the paper's method) or NSS_MUT_RW, the
+                            constrained Gaussian random walk baseline (P:301-302,
+                            P:765): `steps` proposals x + c 2.38/sqrt(d) L z per
+                            replacement, c = `width`; Metropolis on the prior,
+                            rejected outside E < E*                                 */
 } nss_config;
+
+typedef enum { NSS_MUT_HRSS = 0, NSS_MUT_RW = 1 } nss_mutation;
 
 /* Multi-GPU: one process per GPU.  The HRSS chains of an
  * iteration are split in contiguous blocks of ceil(k / world) chains per rank;

@@ -21,7 +21,7 @@
 /* kappa_infinity as printed in the paper, P:2125 ("kappa_infty ~ 1.3035"). */
 #define KAPPA_INF_PAPER 1.3035
 
-enum { PH_INIT = 1, PH_RESAMPLE = 2, PH_HRSS = 3, PH_VOLUME = 4, PH_POSTERIOR = 5 };
+enum { PH_INIT = 1, PH_RESAMPLE = 2, PH_HRSS = 3, PH_VOLUME = 4, PH_POSTERIOR = 5, PH_RW = 6 };
 
 /* ------------------------------------------------------------------------ */
 /* Counter-based RNG: Philox4x32-10 (Salmon et al. 2011). */
@@ -436,6 +436,72 @@ static int slice_step(nsso_ctx *c, const double *x0, double e0, const double *v,
   return NSSO_OK;
 }
 
+/* F1 constrained random walk ("constrained Gaussian random-walk
+ * baseline"; "Gaussian proposal with covariance matched to the target
+ * and scaled optimally, rejecting proposals that violate the constraint"):
+ * proposal covariance (c 2.38)^2/d Sigma_hat (Roberts-Gelman-Gilks scaling
+ * with the live-set covariance as the matched covariance), Metropolis
+ * acceptance for the prior restricted to E < E*. */
+static int rw_step(nsso_ctx *c, const double *x0, double e0, double e_star, uint32_t iter, uint32_t gid,
+                   uint32_t step, double *x_out, double *e_out, int32_t counts[4], double *min_margin) {
+  int d = c->d;
+  uint32_t h = (uint32_t)(2 * ((d + 1) / 2));
+  double *z = (double *)xcalloc((size_t)d + 1, sizeof(double));
+  double *xp = (double *)xcalloc((size_t)d, sizeof(double));
+  nsso_draw_normals(c->cfg.seed, iter, gid, PH_RW, step, d, z);
+  double u = nsso_draw_uniform(c->cfg.seed, iter, gid, PH_RW, step, h);
+  double sigma = c->cfg.width * 2.38 / sqrt((double)d);
+  for (int i = 0; i < d; ++i) {
+    double s = 0.0;
+    for (int j = 0; j <= i; ++j) s += c->L[i * d + j] * z[j];
+    xp[i] = x0[i] + sigma * s;
+  }
+  c->probes++;
+  double lp0 = log_prior(c, x0), lpp = log_prior(c, xp);
+  double mm = INFINITY;
+  int evaluated = 0, accepted = 0;
+  double en = NAN;
+  if (c->prior_kind == NSSO_PRIOR_BOX) {
+    for (int i = 0; i < d; ++i) {
+      double span = c->hi[i] - c->lo[i];
+      double m = fmin(xp[i] - c->lo[i], c->hi[i] - xp[i]) / span;
+      if (fabs(m) < mm) mm = fabs(m);
+    }
+  } else {
+    double m = (lpp - lp0 - log(u)) / fabs_max1(lp0);
+    if (fabs(m) < mm) mm = fabs(m);
+  }
+  if (lpp > -INFINITY && log(u) < lpp - lp0) {
+    en = energy(c, xp);
+    evaluated = 1;
+    c->evals++;
+    if (isnan(en)) c->nan_seen = 1;
+    else {
+      double m = (e_star - en) / fabs_max1(e_star);
+      if (fabs(m) < mm) mm = fabs(m);
+      accepted = en < e_star;
+    }
+  }
+  if (accepted) {
+    memcpy(x_out, xp, sizeof(double) * (size_t)d);
+    *e_out = en;
+  } else {
+    memcpy(x_out, x0, sizeof(double) * (size_t)d);
+    *e_out = e0;
+    c->nulls++;
+  }
+  counts[0] = 0; counts[1] = 0; counts[2] = evaluated; counts[3] = accepted;
+  if (min_margin) *min_margin = mm;
+  free(z); free(xp);
+  return NSSO_OK;
+}
+
+int nsso_rw_step(nsso_ctx *c, const double *x0, double e0, double e_star, uint32_t iter, uint32_t gid,
+                 uint32_t step, double *x_out, double *e_out, int32_t counts[4]) {
+  if (!c) return NSSO_ERR_INVALID_ARG;
+  return rw_step(c, x0, e0, e_star, iter, gid, step, x_out, e_out, counts, NULL);
+}
+
 int nsso_slice_step(nsso_ctx *c, const double *x0, double e0, const double *v, double w,
                     double e_star, uint32_t iter, uint32_t gid, uint32_t step,
                     double *x_out, double *e_out, int32_t counts[4]) {
@@ -535,6 +601,8 @@ static int validate(const nsso_prior *p, const nsso_energy *e, const nsso_config
   if (cfg->n_volume_sims < 2) return 0;
   if (!(cfg->width > 0.0)) return 0;
   if (cfg->max_dead < cfg->n_live) return 0;
+  if (cfg->update_all != 0 && cfg->update_all != 1) return 0;
+  if (cfg->mutation != NSSO_MUT_HRSS && cfg->mutation != NSSO_MUT_RW) return 0;
   if (p->kind == NSSO_PRIOR_BOX) {
     if (!p->lo || !p->hi) return 0;
     for (int i = 0; i < d; ++i) if (!(p->lo[i] < p->hi[i])) return 0;
@@ -765,11 +833,15 @@ int nsso_step(nsso_ctx *c, nsso_step_info *info) {
     memcpy(x, &c->X[(int64_t)par * d], sizeof(double) * (size_t)d);
     double e = c->E[par];
     for (int j = 0; j < p; ++j) {
-      direction(c, it, s, (uint32_t)j, z, v);
       int32_t cnt[4];
       double mm;
       double en;
-      slice_step(c, x, e, v, c->w, e_star, it, s, (uint32_t)j, xn, &en, cnt, &mm);
+      if (c->cfg.mutation == NSSO_MUT_RW) {
+        rw_step(c, x, e, e_star, it, s, (uint32_t)j, xn, &en, cnt, &mm);
+      } else {
+        direction(c, it, s, (uint32_t)j, z, v);
+        slice_step(c, x, e, v, c->w, e_star, it, s, (uint32_t)j, xn, &en, cnt, &mm);
+      }
       memcpy(x, xn, sizeof(double) * (size_t)d);
       e = en;
       uint8_t *tc = &c->t_counts[(cidx * p + j) * 4];

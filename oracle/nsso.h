@@ -87,7 +87,10 @@ typedef struct {
   int64_t max_dead;        /* dead-store capacity                        */
   uint64_t seed;
   int32_t update_all;      /* F4: 1 = mutate all n live points each iteration */
+  int32_t mutation;        /* F1: NSSO_MUT_HRSS (default) or NSSO_MUT_RW */
 } nsso_config;
+
+enum { NSSO_MUT_HRSS = 0, NSSO_MUT_RW = 1 };
 
 typedef struct {
   int64_t iteration;       /* iterations completed                       */
@@ -160,6 +163,14 @@ double nsso_log_prior_at(nsso_ctx *ctx, const double *x);
 /* One HRSS step from x0 along the given direction v with width w
  * under threshold e_star, drawing u_h, u_b and shrink uniforms from stream
  * (iter, gid, HRSS, step).  counts = {n_left, n_right, n_shrink, accepted}. */
+/* One constrained Gaussian random-walk proposal (F1):
+ * x' = x0 + sigma L z with sigma = c 2.38 / sqrt(d) (c = cfg.width), z from
+ * the normals of stream (iter, gid, RW = 6, step); accepted iff x' is in the
+ * prior support, ln u < log Pi(x') - log Pi(x0) (u = draw h = 2 ceil(d/2))
+ * and E(x') < E*; the energy is evaluated only if the prior test passes.
+ * counts = {0, 0, evaluated, accepted}. */
+int nsso_rw_step(nsso_ctx *ctx, const double *x0, double e0, double e_star, uint32_t iter, uint32_t gid,
+                 uint32_t step, double *x_out, double *e_out, int32_t counts[4]);
 int nsso_slice_step(nsso_ctx *ctx, const double *x0, double e0, const double *v, double w,
                     double e_star, uint32_t iter, uint32_t gid, uint32_t step,
                     double *x_out, double *e_out, int32_t counts[4]);

@@ -51,7 +51,8 @@ class Config(C.Structure):
                 ("max_stepout", C.c_int32), ("max_shrink", C.c_int32),
                 ("quadrature", C.c_int32), ("metric_reg", C.c_double),
                 ("term_log_ratio", C.c_double), ("n_volume_sims", C.c_int32),
-                ("max_dead", C.c_int64), ("seed", C.c_uint64), ("update_all", C.c_int32)]
+                ("max_dead", C.c_int64), ("seed", C.c_uint64), ("update_all", C.c_int32),
+                ("mutation", C.c_int32)]
 
 
 class StepInfo(C.Structure):
@@ -83,6 +84,8 @@ def lib():
         L.nsso_evidence.argtypes = [vp, P(C.c_double), P(C.c_double)]
         L.nsso_evidence_reps.argtypes = [vp, P(C.c_double)]
         L.nsso_samples.argtypes = [vp, P(C.c_double), P(C.c_double), C.c_int64, P(C.c_int64)]
+        L.nsso_rw_step.argtypes = [vp, P(C.c_double), C.c_double, C.c_double, C.c_uint32, C.c_uint32, C.c_uint32,
+                                    P(C.c_double), P(C.c_double), P(C.c_int32)]
         L.nsso_posterior.argtypes = [vp, C.c_double, P(C.c_double), P(C.c_double), P(C.c_double),
                                      P(C.c_double), C.c_int64]
         L.nsso_resample.argtypes = [vp, C.c_double, C.c_int64, C.c_uint64, P(C.c_int64), P(C.c_double)]
@@ -346,6 +349,16 @@ class Oracle:
     def log_prior(self, x) -> float:
         x = _f64(x)
         return lib().nsso_log_prior_at(self._h, _dp(x))
+
+    def rw_step(self, x0, e0: float, e_star: float, it: int, gid: int, step: int):
+        """F1: one constrained random-walk proposal (nsso_rw_step)."""
+        x0 = _f64(x0)
+        xo = np.zeros(self.d)
+        eo = C.c_double()
+        cnt = (C.c_int32 * 4)()
+        _check(lib().nsso_rw_step(self._h, _dp(x0), e0, e_star, it, gid, step, _dp(xo), C.byref(eo), cnt),
+               "nsso_rw_step")
+        return xo, eo.value, list(cnt)
 
     def slice_step(self, x0, e0: float, v, w: float, e_star: float, it: int, gid: int, step: int):
         x0, v = _f64(x0), _f64(v)

@@ -48,7 +48,8 @@ class nss_config(C.Structure):
                 ("max_stepout", C.c_int32), ("max_shrink", C.c_int32),
                 ("quadrature", C.c_int32), ("metric_reg", C.c_double),
                 ("term_log_ratio", C.c_double), ("n_volume_sims", C.c_int32),
-                ("max_dead", C.c_int64), ("seed", C.c_uint64), ("update_all", C.c_int32)]
+                ("max_dead", C.c_int64), ("seed", C.c_uint64), ("update_all", C.c_int32),
+                ("mutation", C.c_int32)]
 
 
 class nss_dist(C.Structure):

@@ -37,6 +37,8 @@ DIR_MAHALANOBIS = 0
 DIR_EUCLIDEAN = 1
 Q_TRAPEZOID = 0
 Q_RECTANGLE = 1
+MUT_HRSS = 0
+MUT_RW = 1
 
 LN2PI = math.log(2.0 * math.pi)
 
@@ -75,7 +77,7 @@ def config(n_live: int, k: int, steps: int, *, seed: int = 1, width_rule: int = 
            width: float = 1.0, dir_norm: int = DIR_MAHALANOBIS, max_stepout: int = 10,
            max_shrink: int = 100, quadrature: int = Q_TRAPEZOID, metric_reg: float = 1e-6,
            term_log_ratio: float = -3.0, n_volume_sims: int = 100,
-           max_dead: Optional[int] = None, update_all: int = 0) -> Dict:
+           max_dead: Optional[int] = None, update_all: int = 0, mutation: int = 0) -> Dict:
     """Run configuration (P:684-686 defaults)."""
     if max_dead is None:
         max_dead = n_live + k * 1000
@@ -84,7 +86,7 @@ def config(n_live: int, k: int, steps: int, *, seed: int = 1, width_rule: int = 
                 max_shrink=int(max_shrink), quadrature=int(quadrature),
                 metric_reg=float(metric_reg), term_log_ratio=float(term_log_ratio),
                 n_volume_sims=int(n_volume_sims), max_dead=int(max_dead), seed=int(seed),
-                update_all=int(update_all))
+                update_all=int(update_all), mutation=int(mutation))
 
 
 # --------------------------------------------------------------------------
