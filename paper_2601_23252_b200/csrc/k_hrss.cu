@@ -193,6 +193,122 @@ __global__ void __launch_bounds__(256) k_hrss(RunDev r, PriorDev pr, EnergyDev e
   }
 }
 
+// F1 constrained Gaussian random walk: one warp per
+// chain, p proposals x' = x + sigma L z (sigma = c 2.38 / sqrt(d), z from the
+// normals of stream (iter, s, RW, j), Metropolis on the prior with the
+// uniform draw h = 2 ceil(d/2)), rejected outside E < E*; the energy is
+// evaluated only when the prior test passes.  counts = {0, 0, evaluated,
+// accepted}.
+template <int NPL, int KIND>
+__global__ void __launch_bounds__(256) k_rw(RunDev r, PriorDev pr, EnergyDev en) {
+  extern __shared__ float sm[];
+  __shared__ int sh_flag;
+  const int d = r.d, lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  const int ldl = odd_stride(d);
+  float *sL = sm;
+  float *sP = sL + d * ldl;
+  const int npar = energy_param_floats(KIND, d, en.n_comp);
+  float *sZ = sP + npar + wib * (2 * NPL * 32);
+  float *sY = sZ + NPL * 32;
+  if (threadIdx.x == 0) sh_flag = (r.st->terminated || r.st->error || r.st->finalised) ? 1 : 0;
+  for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
+    int i = e / d, j = e - i * d;
+    sL[i * ldl + j] = r.L[i * r.dp + j];
+  }
+  ESm es;
+  stage_energy(en, sP, es);
+  __syncthreads();
+  if (sh_flag) return;
+  const int c = r.c0 + blockIdx.x * wpb + wib;
+  if (c >= r.c1) return;
+  DevState *st = r.st;
+  const uint32_t it = static_cast<uint32_t>(st->iter);
+  const int s = r.cdest[c];
+  const int par = r.cpar[c];
+  const float e_star = st->e_star;
+  const float sigma = r.rw_sigma;
+  const int p = r.p;
+  const int h = 2 * ((d + 1) / 2);
+  const int nblk_norm = h >> 2, nblk_all = (h + 3) >> 2;
+  float pa[NPL], pb[NPL];
+  load_prior_lane<NPL>(pr, lane, d, pa, pb);
+  float x[NPL], xp[NPL];
+#pragma unroll
+  for (int t = 0; t < NPL; ++t) {
+    const int i = lane + 32 * t;
+    x[t] = i < d ? r.Xs[static_cast<long long>(par) * r.dp + i] : 0.f;
+  }
+  float e = r.Es[par];
+  bool dummy;
+  float lp = prior_logp<NPL>(x, pr, pa, pb, lane, d, dummy);
+  unsigned long long n_probe = 0, n_eval = 0, n_rej = 0;
+  for (int j = 0; j < p; ++j) {
+    for (int b = lane; b < nblk_all; b += 32) {
+      uint4 u4 = philox_block(r, it, s, kPhaseRw, j, b);
+      float u0 = u01(u4.x), u1 = u01(u4.y), u2 = u01(u4.z), u3 = u01(u4.w);
+      float r0 = sqrtf(-2.f * logf(u0)), r1 = sqrtf(-2.f * logf(u2));
+      float s0, c0, s1, c1;
+      sincospif(2.f * u1, &s0, &c0);
+      sincospif(2.f * u3, &s1, &c1);
+      const int i0 = 4 * b;
+      if (i0 < d) sZ[i0] = r0 * c0;
+      if (i0 + 1 < d) sZ[i0 + 1] = r0 * s0;
+      if (b < nblk_norm) {
+        if (i0 + 2 < d) sZ[i0 + 2] = r1 * c1;
+        if (i0 + 3 < d) sZ[i0 + 3] = r1 * s1;
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < NPL; ++t) {
+      const int i = lane + 32 * t;
+      float acc = 0.f;
+      if (i < d) {
+        const float *row = sL + i * ldl;
+        for (int m = 0; m <= i; ++m) acc = fmaf(row[m], sZ[m], acc);
+      }
+      xp[t] = fmaf(sigma, acc, x[t]);
+    }
+    __syncwarp();
+    const uint4 hb = philox_block(r, it, s, kPhaseRw, j, h >> 2);
+    const float u = u01(word(hb, h & 3));
+    ++n_probe;
+    bool inside;
+    const float lpp = prior_logp<NPL>(xp, pr, pa, pb, lane, d, inside);
+    int evaluated = 0, accepted = 0;
+    if (inside && logf(u) < lpp - lp) {
+      const float ep = warp_energy<NPL, KIND>(xp, en, es, sY, lane);
+      evaluated = 1;
+      ++n_eval;
+      if (isnan(ep)) {
+        if (lane == 0) raise_error(st, NSS_ERR_NAN);
+      } else if (ep < e_star) {
+        accepted = 1;
+#pragma unroll
+        for (int t = 0; t < NPL; ++t) x[t] = xp[t];
+        e = ep;
+        lp = lpp;
+      }
+    }
+    n_rej += accepted ? 0 : 1;
+    if (lane == 0)
+      r.counts[static_cast<long long>(c) * p + j] =
+          (static_cast<uint32_t>(evaluated) << 16) | (static_cast<uint32_t>(accepted) << 24);
+  }
+#pragma unroll
+  for (int t = 0; t < NPL; ++t) {
+    const int i = lane + 32 * t;
+    if (i < d) r.X[static_cast<long long>(s) * r.dp + i] = x[t];
+  }
+  if (lane == 0) {
+    r.E[s] = e;
+    if (par != s) r.birth[s] = e_star;
+    atomicAdd(&st->probes, n_probe);
+    atomicAdd(&st->evals, n_eval);
+    atomicAdd(&st->nulls, n_rej);
+  }
+}
+
 // Prior draws with rejection until E is finite (R-20); one warp per gid.
 template <int NPL, int KIND>
 __global__ void __launch_bounds__(256) k_init(RunDev r, PriorDev pr, EnergyDev en) {
@@ -262,6 +378,25 @@ void launch_hrss_t(const RunDev &r, const PriorDev &pr, const EnergyDev &en, con
 }
 
 template <int NPL, int KIND>
+void launch_rw_t(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc) {
+  const int ldl = odd_stride(r.d);
+  const int nc = r.c1 - r.c0;
+  if (nc <= 0) return;
+  int wpb = nc / 296;
+  wpb = wpb < 1 ? 1 : (wpb > 8 ? 8 : wpb);
+  const size_t smem = (static_cast<size_t>(r.d) * ldl + energy_param_floats(KIND, r.d, en.n_comp) +
+                       static_cast<size_t>(wpb) * 2 * NPL * 32) * sizeof(float);
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && attr < smem) {
+    cudaFuncSetAttribute(k_rw<NPL, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    attr = smem;
+  }
+  NSS_PIN_CARVEOUT((k_rw<NPL, KIND>));
+  k_rw<NPL, KIND><<<(nc + wpb - 1) / wpb, wpb * 32, smem, lc.stream>>>(r, pr, en);
+  ++*lc.launch_counter;
+}
+
+template <int NPL, int KIND>
 void launch_init_t(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc) {
   const int wpb = 8;
   const size_t smem = (energy_param_floats(KIND, r.d, en.n_comp) + static_cast<size_t>(wpb) * NPL * 32) * sizeof(float);
@@ -323,6 +458,10 @@ int hrss_engine(const RunDev &r, const EnergyDev &en) {
 }
 
 void launch_hrss(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc) {
+  if (r.mutation == NSS_MUT_RW) {  // F1 baseline mutation
+    NSS_DISPATCH(launch_rw_t, r, pr, en, lc);
+    return;
+  }
   if (hrss_engine(r, en) == 1) {
     launch_hrss_lane(r, pr, en, lc);
     return;

@@ -148,6 +148,7 @@ bool validate(const nss_prior *p, const nss_energy *e, const nss_config *cfg) {
     return false;
   if (cfg->n_volume_sims < 2 || !(cfg->width > 0.0) || cfg->max_dead < cfg->n_live) return false;
   if (cfg->update_all != 0 && cfg->update_all != 1) return false;
+  if (cfg->mutation != NSS_MUT_HRSS && cfg->mutation != NSS_MUT_RW) return false;
   if (cfg->width_rule != NSS_W_OPTIMAL && cfg->width_rule != NSS_W_FIXED) return false;
   if (cfg->dir_norm != NSS_DIR_MAHALANOBIS && cfg->dir_norm != NSS_DIR_EUCLIDEAN) return false;
   if (cfg->quadrature != NSS_Q_TRAPEZOID && cfg->quadrature != NSS_Q_RECTANGLE) return false;
@@ -317,6 +318,7 @@ nss_status exchange(nss_ctx *c) {
 // 0 warp, 1 lane, 2 batch
 int resolve_engine(const nss_ctx *c) {
   const int want = c->r.engine;
+  if (c->r.mutation == NSS_MUT_RW) return 0;  // F1: warp-per-chain random walk (launch_hrss)
   if (c->en.kind == NSS_E_GP_ARD) return 2;  // no per-warp GP energy
   const bool expensive = c->en.kind == NSS_E_LOGREG && c->lr_ok;
   if (want == NSS_ENGINE_BATCH) return 2;
@@ -615,7 +617,8 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
   en.c = static_cast<float>(energy->c);
   en.sigma_y = static_cast<float>(energy->sigma_y);
   en.jitter = static_cast<float>(energy->jitter);
-  if (en.kind != NSS_E_GP_ARD && !energy_supported(en)) {
+  if ((en.kind == NSS_E_GP_ARD && cfg->mutation == NSS_MUT_RW) ||
+      (en.kind != NSS_E_GP_ARD && !energy_supported(en))) {
     nss_destroy(c);
     return NSS_ERR_UNSUPPORTED;
   }
@@ -736,6 +739,8 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
   r.max_dead = cfg->max_dead;
   const long long nch = cfg->update_all ? n : k;
   r.nch = static_cast<int>(nch);
+  r.mutation = cfg->mutation;
+  r.rw_sigma = static_cast<float>(cfg->width * 2.38 / std::sqrt(static_cast<double>(d)));
   r.c0 = 0;
   r.c1 = static_cast<int>(nch);
   r.seed_lo = static_cast<uint32_t>(cfg->seed);

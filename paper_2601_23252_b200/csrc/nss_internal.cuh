@@ -10,7 +10,8 @@ namespace nss {
 
 constexpr int kMaxDim = NSS_MAX_DIM;
 constexpr int kMaxComp = 16;
-constexpr uint32_t kPhaseInit = 1, kPhaseResample = 2, kPhaseHrss = 3, kPhaseVolume = 4, kPhasePosterior = 5;
+constexpr uint32_t kPhaseInit = 1, kPhaseResample = 2, kPhaseHrss = 3, kPhaseVolume = 4, kPhasePosterior = 5,
+                   kPhaseRw = 6;
 
 // ----------------------------------------------------------------------------
 // Device-resident run state (one small struct, read by every kernel).
@@ -77,6 +78,8 @@ struct RunDev {
   // the pre-mutation live set when survivors move too)
   int nch;
   int *cdest, *cpar;
+  int mutation;               // NSS_MUT_HRSS or NSS_MUT_RW (F1)
+  float rw_sigma;             // RW proposal scale c 2.38 / sqrt(d)
   const float *Xs, *Es;
   long long max_dead;
   uint32_t seed_lo, seed_hi;

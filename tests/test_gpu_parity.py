@@ -339,3 +339,26 @@ def test_update_all_single_iteration_parity(name):
     assert tg["dest_gid"].size == kw["n_live"]
     dg, dr = gpu.dead(), ref.dead()
     assert np.array_equal(dg["gid"], dr["gid"])
+
+
+RW_CASES = {
+    "mog_box": (lambda: W.mog(4, n_comp=2, seed=4, mean_box=3.0, min_sep=3.0), dict(n_live=150, k=15, steps=20)),
+    "corr_gauss_prior": (lambda: W.corr_gauss(12, seed=2), dict(n_live=200, k=20, steps=12)),
+    "funnel": (lambda: W.funnel(16), dict(n_live=200, k=20, steps=16)),
+    "logreg": (lambda: W.logreg(5, n_data=300, seed=3), dict(n_live=120, k=12, steps=10)),
+    "update_all": (lambda: W.gauss(3), dict(n_live=100, k=10, steps=6, update_all=1)),
+}
+
+
+@pytest.mark.parametrize("name", sorted(RW_CASES))
+def test_rw_single_iteration_parity(name):
+    """F1 constrained random walk: same bar as HRSS."""
+    make, kw = RW_CASES[name]
+    prob = make()
+    cfg = W.config(seed=13, mutation=W.MUT_RW, **kw)
+    gpu, ref = inject_pair(prob, cfg, warm_iters=1)
+    st = compare_iteration(gpu, ref, prob)
+    c = st["counts_g"]
+    assert np.all(c[..., 0] == 0) and np.all(c[..., 1] == 0)
+    assert 0 < c[..., 3].mean() < 1  # some proposals accepted, some rejected
+    assert gpu.info()["expansions"] == 0
