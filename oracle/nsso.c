@@ -21,7 +21,7 @@
 /* kappa_infinity as printed in the paper, P:2125 ("kappa_infty ~ 1.3035"). */
 #define KAPPA_INF_PAPER 1.3035
 
-enum { PH_INIT = 1, PH_RESAMPLE = 2, PH_HRSS = 3, PH_VOLUME = 4, PH_POSTERIOR = 5, PH_RW = 6 };
+enum { PH_INIT = 1, PH_RESAMPLE = 2, PH_HRSS = 3, PH_VOLUME = 4, PH_POSTERIOR = 5, PH_RW = 6, PH_SMC = 7 };
 
 /* ------------------------------------------------------------------------ */
 /* Counter-based RNG: Philox4x32-10 (Salmon et al. 2011). */
@@ -115,6 +115,10 @@ struct nsso_ctx {
   int32_t *subset;
   int64_t n_subset; /* -1 = all */
   int nan_seen;
+  /* F3 tempered SMC-SS: particles are X/E, beta, accumulated log Z */
+  int smc;
+  double smc_rho, beta, smc_logz;
+  int32_t *smc_par; /* resampled parent of every particle, last stage */
 };
 
 static void *xcalloc(size_t n, size_t sz) { return calloc(n ? n : 1, sz); }
@@ -347,6 +351,8 @@ typedef struct {
   double e_last;     /* energy at the last in() point that passed the prior */
   double min_margin; /* smallest relative decision margin seen */
   int64_t probes, evals;
+  int tempered;      /* F3: slice of Pi exp(-beta E), no hard threshold */
+  double beta;
 } slice_ctx;
 
 static double fabs_max1(double a) { a = fabs(a); return a > 1.0 ? a : 1.0; }
@@ -366,6 +372,18 @@ static int in_slice(slice_ctx *s, double t) {
     }
   }
   double lp = log_prior(c, s->xp);
+  if (s->tempered) {
+    /* F3: x + t v in the support and log Pi - beta E >= log y */
+    if (!(lp > -INFINITY)) return 0;
+    double e = energy(c, s->xp);
+    s->evals++;
+    if (isnan(e)) { c->nan_seen = 1; return 0; }
+    double f = lp - s->beta * e;
+    double m = (f - s->log_y) / fabs_max1(s->log_y);
+    if (fabs(m) < s->min_margin) s->min_margin = fabs(m);
+    s->e_last = e;
+    return f >= s->log_y;
+  }
   if (c->prior_kind == NSSO_PRIOR_GAUSS_DIAG) {
     double m = (lp - s->log_y) / fabs_max1(s->log_y);
     if (fabs(m) < s->min_margin) s->min_margin = fabs(m);
@@ -393,9 +411,11 @@ static int slice_step(nsso_ctx *c, const double *x0, double e0, const double *v,
   s.c = c; s.x = x0; s.v = v; s.e_star = e_star;
   s.xp = (double *)xcalloc((size_t)d, sizeof(double));
   s.min_margin = INFINITY; s.probes = 0; s.evals = 0; s.e_last = NAN;
-  /* slice height: log y = log Pi(x) + ln u_h  (DESIGN R-9) */
+  s.tempered = c->smc; s.beta = c->beta;
+  /* slice height: log y = log Pi(x) + ln u_h  (DESIGN R-9); tempered
+   * (F3): log y = log Pi(x) - beta E(x) + ln u_h */
   double u_h = nsso_draw_uniform(seed, iter, gid, PH_HRSS, step, h);
-  s.log_y = log_prior(c, x0) + log(u_h);
+  s.log_y = log_prior(c, x0) - (s.tempered ? s.beta * e0 : 0.0) + log(u_h);
   /* randomised initial bracket of width w around t = 0:
    * [-U, w - U], U = w u_b */
   double u_b = nsso_draw_uniform(seed, iter, gid, PH_HRSS, step, h + 1);
@@ -706,6 +726,7 @@ int nsso_init_ex(const nsso_prior *p, const nsso_energy *e, const nsso_config *c
 
 void nsso_destroy(nsso_ctx *c) {
   if (!c) return;
+  free(c->smc_par);
   free(c->lo); free(c->hi); free(c->pmean); free(c->psd);
   free(c->e_w); free(c->e_mu); free(c->e_sigma); free(c->e_prec); free(c->e_x); free(c->e_y);
   free(c->X); free(c->E); free(c->birth); free(c->L);
@@ -1081,6 +1102,121 @@ int nsso_resample(nsso_ctx *c, double beta, int64_t m, uint64_t seed, int64_t *i
   free(lw); free(cum);
   return NSSO_OK;
 }
+
+/* ------------------------------------------------------------------------ */
+/* F3: adaptive tempered SMC with the HRSS kernel (SMC-SS,        */
+/* P:710-713)                                                     */
+/* ------------------------------------------------------------------------ */
+/* ESS of the normalised incremental weights exp(-db E_i),
+ * computed with the weights shifted by min E (exact ratio). */
+static double smc_ess(const double *E, int64_t m, double db, double emin) {
+  double s = 0.0, s2 = 0.0;
+  for (int64_t i = 0; i < m; ++i) {
+    double w = exp(-db * (E[i] - emin));
+    s += w;
+    s2 += w * w;
+  }
+  return s * s / s2;
+}
+
+/* Next temperature: bisection on db in (0, 1 - beta_t] for
+ * ESS = rho m, to 1e-10 in db; the whole remaining step when ESS stays above
+ * rho m. */
+int nsso_smc_next_beta(const double *E, int64_t m, double beta_t, double rho, double *beta_next) {
+  if (!E || m < 1 || !beta_next || !(rho > 0.0 && rho < 1.0) || !(beta_t < 1.0)) return NSSO_ERR_INVALID_ARG;
+  double emin = INFINITY;
+  for (int64_t i = 0; i < m; ++i) if (E[i] < emin) emin = E[i];
+  double hi = 1.0 - beta_t;
+  if (smc_ess(E, m, hi, emin) >= rho * (double)m) { *beta_next = 1.0; return NSSO_OK; }
+  double lo = 0.0;
+  while (hi - lo > 1e-10) {
+    double mid = 0.5 * (lo + hi);
+    if (smc_ess(E, m, mid, emin) >= rho * (double)m) lo = mid; else hi = mid;
+  }
+  *beta_next = beta_t + lo;
+  return NSSO_OK;
+}
+
+int nsso_smc_init(const nsso_prior *p, const nsso_energy *e, const nsso_config *cfg, double rho, nsso_ctx **out) {
+  if (!(rho > 0.0 && rho < 1.0)) return NSSO_ERR_INVALID_ARG;
+  int st = nsso_init(p, e, cfg, out);
+  if (st) return st;
+  (*out)->smc = 1;
+  (*out)->smc_rho = rho;
+  (*out)->beta = 0.0;
+  (*out)->smc_logz = 0.0;
+  (*out)->smc_par = (int32_t *)xcalloc((size_t)cfg->n_live, sizeof(int32_t));
+  return NSSO_OK;
+}
+
+/* One SMC stage t = iter + 1: next temperature, log Z += log mean w
+ * (P:663-668), multinomial resampling by the normalised weights (u_j =
+ * uniform 0 of stream (t, j, SMC = 7, 0)), metric of the resampled particles,
+ * p tempered HRSS steps per particle (stream (t, j, HRSS, step)). */
+int nsso_smc_stage(nsso_ctx *c) {
+  if (!c || !c->smc) return NSSO_ERR_INVALID_ARG;
+  if (c->beta >= 1.0) return NSSO_ERR_STATE;
+  int d = c->d;
+  int64_t m = c->n;
+  int p = c->cfg.steps;
+  uint32_t t = (uint32_t)(c->iter + 1);
+  double bn;
+  int st = nsso_smc_next_beta(c->E, m, c->beta, c->smc_rho, &bn);
+  if (st) return st;
+  double db = bn - c->beta;
+  double emin = INFINITY;
+  for (int64_t i = 0; i < m; ++i) if (c->E[i] < emin) emin = c->E[i];
+  double *cum = (double *)xcalloc((size_t)m, sizeof(double));
+  double s = 0.0;
+  for (int64_t i = 0; i < m; ++i) s += exp(-db * (c->E[i] - emin));
+  c->smc_logz += -db * emin + log(s) - log((double)m);
+  double run = 0.0;
+  for (int64_t i = 0; i < m; ++i) { run += exp(-db * (c->E[i] - emin)) / s; cum[i] = run; }
+  c->beta = bn;
+  double *X0 = dup_d(c->X, (size_t)(m * d)), *E0 = dup_d(c->E, (size_t)m);
+  for (int64_t j = 0; j < m; ++j) {
+    double u = nsso_draw_uniform(c->cfg.seed, t, (uint32_t)j, PH_SMC, 0, 0);
+    int64_t lo = 0, hi = m - 1;
+    while (lo < hi) { int64_t mid = (lo + hi) / 2; if (u < cum[mid]) hi = mid; else lo = mid + 1; }
+    memcpy(&c->X[j * d], &X0[lo * d], sizeof(double) * (size_t)d);
+    c->E[j] = E0[lo];
+    c->smc_par[j] = (int32_t)lo;
+  }
+  free(X0); free(E0); free(cum);
+  compute_metric(c);
+  double *x = (double *)xcalloc((size_t)d, sizeof(double));
+  double *xn = (double *)xcalloc((size_t)d, sizeof(double));
+  double *z = (double *)xcalloc((size_t)d + 1, sizeof(double));
+  double *v = (double *)xcalloc((size_t)d, sizeof(double));
+  for (int64_t j = 0; j < m; ++j) {
+    memcpy(x, &c->X[j * d], sizeof(double) * (size_t)d);
+    double e = c->E[j];
+    for (int q = 0; q < p; ++q) {
+      int32_t cnt[4];
+      double mm, en;
+      direction(c, t, (uint32_t)j, (uint32_t)q, z, v);
+      slice_step(c, x, e, v, c->w, INFINITY, t, (uint32_t)j, (uint32_t)q, xn, &en, cnt, &mm);
+      memcpy(x, xn, sizeof(double) * (size_t)d);
+      e = en;
+    }
+    memcpy(&c->X[j * d], x, sizeof(double) * (size_t)d);
+    c->E[j] = e;
+  }
+  free(x); free(xn); free(z); free(v);
+  c->iter++;
+  if (c->nan_seen) return NSSO_ERR_NAN;
+  return NSSO_OK;
+}
+
+int nsso_smc_state(nsso_ctx *c, double *beta, double *log_z, int64_t *stage, int32_t *parents) {
+  if (!c || !c->smc) return NSSO_ERR_INVALID_ARG;
+  if (parents) memcpy(parents, c->smc_par, sizeof(int32_t) * (size_t)c->n);
+  if (beta) *beta = c->beta;
+  if (log_z) *log_z = c->smc_logz;
+  if (stage) *stage = c->iter;
+  return NSSO_OK;
+}
+
 
 static void fill_info(nsso_ctx *c, nsso_step_info *info) {
   memset(info, 0, sizeof(*info));

@@ -113,6 +113,20 @@ int nsso_init(const nsso_prior *prior, const nsso_energy *energy,
 int nsso_init_ex(const nsso_prior *prior, const nsso_energy *energy,
                  const nsso_config *cfg, int draw_live, nsso_ctx **out);
 int nsso_step(nsso_ctx *ctx, nsso_step_info *info);
+
+/* ---- F3: adaptive tempered SMC with the HRSS kernel (SMC-SS) ----
+ * A context whose n_live particles start as prior draws (as nsso_init) and
+ * move through pi_beta ~ Pi exp(-beta E): each stage picks the next beta by
+ * bisection on ESS = rho m (nsso_smc_next_beta), adds log mean w to log Z,
+ * resamples multinomially (uniform 0 of stream (stage, j, SMC = 7, 0)),
+ * recomputes the metric from the resampled particles and applies `steps`
+ * tempered HRSS steps per particle (slice of Pi exp(-beta E), no threshold).
+ * k is unused (give 1). nsso_smc_stage returns STATE once beta = 1. */
+int nsso_smc_init(const nsso_prior *prior, const nsso_energy *energy, const nsso_config *cfg, double rho,
+                  nsso_ctx **out);
+int nsso_smc_stage(nsso_ctx *ctx);
+int nsso_smc_state(nsso_ctx *ctx, double *beta, double *log_z, int64_t *stage, int32_t *parents /* n */);
+int nsso_smc_next_beta(const double *E, int64_t m, double beta_t, double rho, double *beta_next);
 int nsso_run(nsso_ctx *ctx, int64_t max_iters, nsso_step_info *info);
 int nsso_finalise(nsso_ctx *ctx);
 int nsso_evidence(nsso_ctx *ctx, double *log_z, double *log_z_err);

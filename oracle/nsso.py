@@ -84,6 +84,10 @@ def lib():
         L.nsso_evidence.argtypes = [vp, P(C.c_double), P(C.c_double)]
         L.nsso_evidence_reps.argtypes = [vp, P(C.c_double)]
         L.nsso_samples.argtypes = [vp, P(C.c_double), P(C.c_double), C.c_int64, P(C.c_int64)]
+        L.nsso_smc_init.argtypes = [P(Prior), P(Energy), P(Config), C.c_double, P(vp)]
+        L.nsso_smc_stage.argtypes = [vp]
+        L.nsso_smc_state.argtypes = [vp, P(C.c_double), P(C.c_double), P(C.c_int64), P(C.c_int32)]
+        L.nsso_smc_next_beta.argtypes = [P(C.c_double), C.c_int64, C.c_double, C.c_double, P(C.c_double)]
         L.nsso_rw_step.argtypes = [vp, P(C.c_double), C.c_double, C.c_double, C.c_uint32, C.c_uint32, C.c_uint32,
                                     P(C.c_double), P(C.c_double), P(C.c_int32)]
         L.nsso_posterior.argtypes = [vp, C.c_double, P(C.c_double), P(C.c_double), P(C.c_double),
@@ -150,6 +154,13 @@ def _f64(a) -> Optional[np.ndarray]:
 
 
 # ---- unit hooks --------------------------------------------------------------
+def smc_next_beta(E, beta_t: float, rho: float) -> float:
+    e = _f64(E)
+    out = C.c_double()
+    _check(lib().nsso_smc_next_beta(_dp(e), e.size, float(beta_t), float(rho), C.byref(out)), "nsso_smc_next_beta")
+    return out.value
+
+
 def philox(ctr: Sequence[int], key: Sequence[int]):
     c = (C.c_uint32 * 4)(*ctr)
     k = (C.c_uint32 * 2)(*key)
@@ -175,7 +186,8 @@ def draw_normals(seed, it, gid, phase, sub, d) -> np.ndarray:
 class Oracle:
     """One oracle NSS run (nsso_ctx)."""
 
-    def __init__(self, problem, cfg: Dict, draw_live: bool = True):
+    def __init__(self, problem, cfg: Dict, draw_live: bool = True, smc_rho: Optional[float] = None):
+        """smc_rho: build an F3 tempered SMC-SS context (nsso_smc_init) instead of NS."""
         self.problem = problem
         self.cfg = dict(cfg)
         d = problem.d
@@ -196,7 +208,12 @@ class Oracle:
                     c=problem.c, sigma_y=problem.sigma_y, jitter=problem.jitter)
         cf = Config(**self.cfg)
         h = C.c_void_p()
-        _check(lib().nsso_init_ex(C.byref(pr), C.byref(en), C.byref(cf), int(draw_live), C.byref(h)), "nsso_init")
+        if smc_rho is not None:
+            _check(lib().nsso_smc_init(C.byref(pr), C.byref(en), C.byref(cf), float(smc_rho), C.byref(h)),
+                   "nsso_smc_init")
+        else:
+            _check(lib().nsso_init_ex(C.byref(pr), C.byref(en), C.byref(cf), int(draw_live), C.byref(h)),
+                   "nsso_init")
         self._h = h
         self.d = d
         self.n = self.cfg["n_live"]
@@ -349,6 +366,25 @@ class Oracle:
     def log_prior(self, x) -> float:
         x = _f64(x)
         return lib().nsso_log_prior_at(self._h, _dp(x))
+
+    # ---- F3 tempered SMC-SS ----
+    def smc_stage(self):
+        _check(lib().nsso_smc_stage(self._h), "nsso_smc_stage")
+
+    def smc_state(self):
+        """(beta, log Z, stage, resampled parents of the last stage)."""
+        b, lz, t = C.c_double(), C.c_double(), C.c_int64()
+        par = np.zeros(self.n, np.int32)
+        _check(lib().nsso_smc_state(self._h, C.byref(b), C.byref(lz), C.byref(t),
+                                    par.ctypes.data_as(C.POINTER(C.c_int32))), "nsso_smc_state")
+        return b.value, lz.value, t.value, par
+
+    def smc_run(self, max_stages: int = 10_000):
+        for _ in range(max_stages):
+            if self.smc_state()[0] >= 1.0:
+                break
+            self.smc_stage()
+        return self.smc_state()
 
     def rw_step(self, x0, e0: float, e_star: float, it: int, gid: int, step: int):
         """F1: one constrained random-walk proposal (nsso_rw_step)."""
