@@ -189,6 +189,27 @@ const char *nss_last_error(const nss_ctx *ctx);
 /* ---- parity hooks (exported for the tests; not on the user path) ---- */
 /* Inject a live set (n*d fp32 positions, n fp32 energies); the next nss_step
  * is iteration `next_iteration`.  Recomputes the metric from x. */
+/* F3 adaptive tempered SMC with the HRSS kernel (SMC-SS, P:635-681,
+ * P:710-713), the paper's closest control.  nss_smc_init draws n_live
+ * particles from the prior (as nss_init; k is unused, give 1) and returns a
+ * context whose particles move through pi_beta ~ Pi exp(-beta E): each
+ * nss_smc_stage picks beta_{t+1} by bisection on ESS = rho m (to 1e-10,
+ * S:357-366), adds log mean exp(-(beta_{t+1} - beta_t) E_i) to log Z,
+ * resamples multinomially (uniform 0 of Philox stream (stage, j, SMC = 7, 0)),
+ * recomputes the metric from the resampled particles and applies `steps`
+ * tempered HRSS steps per particle (slice of Pi exp(-beta E), no threshold;
+ * warp engine).  Particles are read with nss_get_live; nss_smc_state gives
+ * beta, log Z, the stage count and the last resampling parents (n, nullable).
+ * Multi-GPU (dist): the particles' HRSS chains are split as for NS.
+ * Errors: INVALID_ARG (rho not in (0,1), update_all or RW mutation),
+ * UNSUPPORTED (GP energy), STATE (not an SMC context). */
+nss_status nss_smc_init(const nss_prior *prior, const nss_energy *energy, const nss_config *cfg, double rho,
+                        const nss_dist *dist, nss_ctx **out);
+nss_status nss_smc_stage(nss_ctx *ctx);
+nss_status nss_smc_state(nss_ctx *ctx, double *beta, double *log_z, int64_t *stage, int32_t *parents);
+/* Stages until beta = 1 (at most max_stages); log_z nullable. */
+nss_status nss_smc_run(nss_ctx *ctx, int64_t max_stages, double *log_z);
+
 /* F2 posterior products at inverse temperature beta >= 0 (the
  * same dead points reweighted, w_i^(r)(beta) = exp(-beta E_i) dX_i^(r);
  * log Z(beta) mean and std (ddof 1) over the R volume replicas,

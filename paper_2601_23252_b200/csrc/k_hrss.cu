@@ -52,6 +52,8 @@ __global__ void __launch_bounds__(256) k_hrss(RunDev r, PriorDev pr, EnergyDev e
   const float e_star = st->e_star;
   const float w = st->width;
   const int p = r.p;
+  const bool tempered = r.tempered != 0;                   // F3: slice of Pi exp(-beta E)
+  const float beta = tempered ? static_cast<float>(st->smc_beta) : 0.f;
   const bool euclid = r.dir_norm == NSS_DIR_EUCLIDEAN;
   const int h = 2 * ((d + 1) / 2);           // first non-normal draw index
   const int nblk_norm = h >> 2;              // Philox blocks fully made of normals
@@ -113,7 +115,7 @@ __global__ void __launch_bounds__(256) k_hrss(RunDev r, PriorDev pr, EnergyDev e
     const uint4 hb = philox_block(r, it, s, kPhaseHrss, j, h >> 2);
     const float u_h = u01(word(hb, h & 3));
     const float u_b = u01(word(hb, (h + 1) & 3));
-    const float log_y = lp + logf(u_h);
+    const float log_y = (tempered ? fmaf(-beta, e, lp) : lp) + logf(u_h);
     float lft = -w * u_b;
     float rgt = lft + w;
 
@@ -125,7 +127,7 @@ __global__ void __launch_bounds__(256) k_hrss(RunDev r, PriorDev pr, EnergyDev e
       for (int t = 0; t < NPL; ++t) xp[t] = fmaf(tt, v[t], x[t]);
       bool inside;
       float lpp = prior_logp<NPL>(xp, pr, pa, pb, lane, d, inside);
-      if (!inside || !(lpp >= log_y)) return false;
+      if (!inside || (!tempered && !(lpp >= log_y))) return false;
       float ep = warp_energy<NPL, KIND>(xp, en, es, sY, lane);
       ++n_eval;
       if (isnan(ep)) {
@@ -134,7 +136,7 @@ __global__ void __launch_bounds__(256) k_hrss(RunDev r, PriorDev pr, EnergyDev e
       }
       pr_last.e = ep;
       pr_last.lp = lpp;
-      return ep < e_star;
+      return tempered ? (fmaf(-beta, ep, lpp) >= log_y) : (ep < e_star);
     };
 
     // ---- linear stepping-out, capped per side (R-10) ----

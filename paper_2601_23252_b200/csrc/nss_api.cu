@@ -92,6 +92,12 @@ struct nss_ctx {
   void *comm = nullptr;
   int rank = 0, world = 1, kc = 0;
   float *xbuf = nullptr, *xall = nullptr;
+  // F3 tempered SMC-SS (k_smc.cu): particles are the live set
+  bool smc = false;
+  double smc_rho = 0.9;
+  double *smc_cum = nullptr;
+  int *smc_par = nullptr;
+  float *smc_xs = nullptr, *smc_es = nullptr;
 };
 
 static const int kRoundsPerChunk = 32;
@@ -318,6 +324,7 @@ nss_status exchange(nss_ctx *c) {
 // 0 warp, 1 lane, 2 batch
 int resolve_engine(const nss_ctx *c) {
   const int want = c->r.engine;
+  if (c->smc) return 0;  // F3: tempered HRSS on the warp engine
   if (c->r.mutation == NSS_MUT_RW) return 0;  // F1: warp-per-chain random walk (launch_hrss)
   if (c->en.kind == NSS_E_GP_ARD) return 2;  // no per-warp GP energy
   const bool expensive = c->en.kind == NSS_E_LOGREG && c->lr_ok;
@@ -1339,6 +1346,96 @@ NSS_API nss_status nss_set_chain_range(nss_ctx *c, int32_t c0, int32_t c1) {
   c->r.c0 = c0;
   c->r.c1 = c1;
   return NSS_OK;
+}
+
+// ---- F3: adaptive tempered SMC with the HRSS kernel (SMC-SS) ----
+NSS_API nss_status nss_smc_init(const nss_prior *prior, const nss_energy *energy, const nss_config *cfg, double rho,
+                                const nss_dist *dist, nss_ctx **out) {
+  if (!out || !cfg || !(rho > 0.0 && rho < 1.0)) return NSS_ERR_INVALID_ARG;
+  if (energy && energy->kind == NSS_E_GP_ARD) return NSS_ERR_UNSUPPORTED;
+  if (cfg->update_all || cfg->mutation != NSS_MUT_HRSS) return NSS_ERR_INVALID_ARG;
+  nss_status s = nss_init(prior, energy, cfg, dist, out);
+  if (s) return s;
+  nss_ctx *c = *out;
+  const int n = c->r.n;
+  int *ident = nullptr;
+  auto bail = [&](nss_status st) {
+    nss_destroy(c);
+    *out = nullptr;
+    return st;
+  };
+  if ((s = dalloc(c, &c->smc_cum, n))) return bail(s);
+  if ((s = dalloc(c, &c->smc_par, n))) return bail(s);
+  if ((s = dalloc(c, &c->smc_xs, static_cast<size_t>(n) * c->dp))) return bail(s);
+  if ((s = dalloc(c, &c->smc_es, n))) return bail(s);
+  if ((s = dalloc(c, &ident, n))) return bail(s);
+  uint32_t *counts = nullptr;  // per-particle HRSS counts (nss_init sized them for k chains)
+  if ((s = dalloc(c, &counts, static_cast<size_t>(n) * (cfg->steps > 0 ? cfg->steps : 1)))) return bail(s);
+  c->r.counts = counts;
+  std::vector<int> id(n);
+  for (int i = 0; i < n; ++i) id[i] = i;
+  if (cudaMemcpy(ident, id.data(), n * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess) return bail(NSS_ERR_CUDA);
+  c->smc = true;
+  c->smc_rho = rho;
+  RunDev &r = c->r;
+  r.tempered = 1;
+  r.engine = NSS_ENGINE_WARP;
+  r.nch = n;
+  r.cdest = ident;
+  r.cpar = ident;
+  r.Xs = r.X;
+  r.Es = r.E;
+  r.c0 = 0;
+  r.c1 = n;
+  if (c->comm) {
+    c->kc = (n + c->world - 1) / c->world;
+    r.c0 = std::min(n, c->rank * c->kc);
+    r.c1 = std::min(n, r.c0 + c->kc);
+    const size_t row = static_cast<size_t>(c->dp) + 1;
+    if ((s = dalloc(c, &c->xbuf, static_cast<size_t>(c->kc) * row))) return bail(s);
+    if ((s = dalloc(c, &c->xall, static_cast<size_t>(c->world) * c->kc * row))) return bail(s);
+  }
+  return NSS_OK;
+}
+
+NSS_API nss_status nss_smc_stage(nss_ctx *c) {
+  nss_status s = check_usable(c);
+  if (s) return s;
+  if (!c->smc) return fail(c, NSS_ERR_STATE, "not an SMC context");
+  LaunchCtx lc = lctx(c);
+  launch_smc_stage(c->r, c->smc_rho, c->smc_cum, c->smc_par, c->smc_xs, c->smc_es, lc);
+  launch_metric(c->r, c->cfg.metric_reg, c->cfg.width_rule, c->cfg.width, 0, c->partials, c->ticket, c->nblk, lc);
+  launch_hrss(c->r, c->pr, c->en, lc);
+  if ((s = exchange(c))) return s;
+  CK(cudaGetLastError());
+  return NSS_OK;
+}
+
+NSS_API nss_status nss_smc_state(nss_ctx *c, double *beta, double *log_z, int64_t *stage, int32_t *parents) {
+  nss_status s = check_usable(c);
+  if (s) return s;
+  if (!c->smc) return fail(c, NSS_ERR_STATE, "not an SMC context");
+  c->term_stale = false;  // no NS termination probe in SMC mode
+  if ((s = pull_state(c))) return s;
+  if ((s = device_error(c))) return s;
+  if (beta) *beta = c->h_st->smc_beta;
+  if (log_z) *log_z = c->h_st->smc_logz;
+  if (stage) *stage = c->h_st->iter;
+  if (parents) CK(cudaMemcpy(parents, c->smc_par, c->r.n * sizeof(int), cudaMemcpyDeviceToHost));
+  return NSS_OK;
+}
+
+NSS_API nss_status nss_smc_run(nss_ctx *c, int64_t max_stages, double *log_z) {
+  nss_status s = check_usable(c);
+  if (s) return s;
+  if (!c->smc) return fail(c, NSS_ERR_STATE, "not an SMC context");
+  double beta = 0.0;
+  for (int64_t t = 0; t < max_stages; ++t) {
+    if ((s = nss_smc_state(c, &beta, nullptr, nullptr, nullptr))) return s;
+    if (beta >= 1.0) break;
+    if ((s = nss_smc_stage(c))) return s;
+  }
+  return nss_smc_state(c, nullptr, log_z, nullptr, nullptr);
 }
 
 NSS_API nss_status nss_launch_count(nss_ctx *c, int64_t *launches) {

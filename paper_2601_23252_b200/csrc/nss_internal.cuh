@@ -11,7 +11,7 @@ namespace nss {
 constexpr int kMaxDim = NSS_MAX_DIM;
 constexpr int kMaxComp = 16;
 constexpr uint32_t kPhaseInit = 1, kPhaseResample = 2, kPhaseHrss = 3, kPhaseVolume = 4, kPhasePosterior = 5,
-                   kPhaseRw = 6;
+                   kPhaseRw = 6, kPhaseSmc = 7;
 
 // ----------------------------------------------------------------------------
 // Device-resident run state (one small struct, read by every kernel).
@@ -32,6 +32,7 @@ struct DevState {
   unsigned long long probes, evals, expansions, shrinks, nulls;
   unsigned long long init_evals, init_attempts;
   unsigned long long stamp[16];  // %globaltimer stamps (ns) for latency profiling
+  double smc_beta, smc_logz;     // F3 tempered SMC: current temperature, accumulated log Z
 };
 
 // Energy parameters laid out for the kernels (device pointers, fp32).
@@ -79,6 +80,7 @@ struct RunDev {
   int nch;
   int *cdest, *cpar;
   int mutation;               // NSS_MUT_HRSS or NSS_MUT_RW (F1)
+  int tempered;               // F3: HRSS on Pi exp(-beta E) (beta = st->smc_beta), no threshold
   float rw_sigma;             // RW proposal scale c 2.38 / sqrt(d)
   const float *Xs, *Es;
   long long max_dead;
@@ -215,6 +217,8 @@ bool lane_engine_ok(const RunDev &r, const EnergyDev &en);
 void launch_hrss_lane(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc);
 // k_metric.cu: A5 metric (+ A9 termination when iterating)
 void launch_term_probe(const RunDev &r, const LaunchCtx &lc);
+void launch_smc_stage(const RunDev &r, double rho, double *cum, int *parents, float *Xsnap, float *Esnap,
+                      const LaunchCtx &lc);
 void launch_chains_all(const RunDev &r, int *cdest, int *cpar, float *Xs, float *Es, const LaunchCtx &lc);
 void launch_metric(const RunDev &r, double metric_reg, int width_rule, double width_param,
                    int end_of_iteration, double *partials, unsigned *ticket, int n_blocks, const LaunchCtx &lc);

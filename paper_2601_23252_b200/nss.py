@@ -74,7 +74,7 @@ EXPORTS = ["nss_get_unique_id", "nss_init", "nss_step", "nss_steps", "nss_run", 
            "nss_dead", "nss_volume_reps", "nss_set_kernel_timing", "nss_kernel_time",
            "nss_launch_count", "nss_set_hrss_engine", "nss_get_hrss_engine",
            "nss_phase_times", "nss_set_overlap", "nss_set_graph",
-           "nss_debug_stamps", "nss_lr_energy_batch", "nss_gp_energy_batch", "nss_set_chain_range", "nss_posterior", "nss_resample"]
+           "nss_debug_stamps", "nss_lr_energy_batch", "nss_gp_energy_batch", "nss_set_chain_range", "nss_posterior", "nss_resample", "nss_smc_init", "nss_smc_stage", "nss_smc_state", "nss_smc_run"]
 
 _lib = None
 
@@ -122,6 +122,10 @@ def lib():
     L.nss_lr_energy_batch.argtypes = [P(C.c_double), P(C.c_double), C.c_int64, C.c_int32, P(C.c_double),
                                       C.c_int64, P(C.c_double)]
     L.nss_set_chain_range.argtypes = [vp, C.c_int32, C.c_int32]
+    L.nss_smc_init.argtypes = [P(nss_prior), P(nss_energy), P(nss_config), C.c_double, P(nss_dist), P(vp)]
+    L.nss_smc_stage.argtypes = [vp]
+    L.nss_smc_state.argtypes = [vp, P(C.c_double), P(C.c_double), P(C.c_int64), P(C.c_int32)]
+    L.nss_smc_run.argtypes = [vp, C.c_int64, P(C.c_double)]
     L.nss_posterior.argtypes = [vp, C.c_double, P(C.c_double), P(C.c_double), P(C.c_double), P(C.c_double),
                                 C.c_int64]
     L.nss_resample.argtypes = [vp, C.c_double, C.c_int64, C.c_uint64, P(C.c_int64), P(C.c_double)]
@@ -180,9 +184,11 @@ class Sampler:
     """One NSS run on one GPU (nss_ctx).  `problem` is a workloads.Problem and
     `cfg` a workloads.config() dict."""
 
-    def __init__(self, problem, cfg: Dict, stream: Optional[int] = None, dist=None):
+    def __init__(self, problem, cfg: Dict, stream: Optional[int] = None, dist=None,
+                 smc_rho: Optional[float] = None):
         """dist: None (one GPU) or (rank, world, nccl_uid bytes) -- see
-        paper_2601_23252_b200.dist.sharded_sampler."""
+        paper_2601_23252_b200.dist.sharded_sampler.  smc_rho: build an F3
+        tempered SMC-SS context (nss_smc_init) instead of NS."""
         self.problem = problem
         self.cfg = dict(cfg)
         self._keep = []
@@ -216,8 +222,12 @@ class Sampler:
             dd = nss_dist(rank=self.rank, world=self.world,
                           nccl_uid=C.cast(uid, C.POINTER(C.c_uint8)) if uid is not None else None,
                           cuda_stream=C.c_void_p(stream) if stream is not None else None)
-        st = lib().nss_init(C.byref(pr), C.byref(en), C.byref(cf),
-                            C.byref(dd) if dd is not None else None, C.byref(self._h))
+        if smc_rho is not None:
+            st = lib().nss_smc_init(C.byref(pr), C.byref(en), C.byref(cf), float(smc_rho),
+                                    C.byref(dd) if dd is not None else None, C.byref(self._h))
+        else:
+            st = lib().nss_init(C.byref(pr), C.byref(en), C.byref(cf),
+                                C.byref(dd) if dd is not None else None, C.byref(self._h))
         if st != 0:
             raise NssError(st, "nss_init")
         self.d, self.n, self.k = d, self.cfg["n_live"], self.cfg["k"]
@@ -227,6 +237,22 @@ class Sampler:
         if st != 0:
             msg = lib().nss_last_error(self._h) if self._h else b""
             raise NssError(st, where, (msg or b"").decode())
+
+    # ---- F3 tempered SMC-SS ----
+    def smc_stage(self):
+        self._check(lib().nss_smc_stage(self._h), "nss_smc_stage")
+
+    def smc_state(self):
+        """(beta, log Z, stage, resampled parents of the last stage)."""
+        b, lz, t = C.c_double(), C.c_double(), C.c_int64()
+        par = np.zeros(self.n, np.int32)
+        self._check(lib().nss_smc_state(self._h, C.byref(b), C.byref(lz), C.byref(t), _ip(par)), "nss_smc_state")
+        return b.value, lz.value, t.value, par
+
+    def smc_run(self, max_stages: int = 10_000):
+        lz = C.c_double()
+        self._check(lib().nss_smc_run(self._h, int(max_stages), C.byref(lz)), "nss_smc_run")
+        return self.smc_state()
 
     def posterior(self, beta: float = 1.0, weights: bool = False):
         """F2: (log Z(beta) mean, std over replicas, Kish ESS[, normalised log weights])."""

@@ -1,0 +1,80 @@
+"""F3 tempered SMC-SS on the B200 against the fp64 oracle: teacher-forced
+stages (identical particles injected on both sides) must agree on the next
+temperature, the log-Z increment and the resampling parents exactly (up to
+fp64 rounding), and on the mutated particles within the parity tolerance;
+full runs reach the analytic evidence."""
+import math
+
+import numpy as np
+import pytest
+
+from paper_2601_23252_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+CASES = {
+    "gauss2": (lambda: W.gauss(2), dict(n_live=300, k=1, steps=6)),
+    "mog4": (lambda: W.mog(4, n_comp=2, seed=4, mean_box=3.0, min_sep=3.0), dict(n_live=400, k=1, steps=4)),
+    "corr12": (lambda: W.corr_gauss(12, seed=2), dict(n_live=256, k=1, steps=6)),
+}
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_smc_stage_parity(name):
+    from oracle import nsso
+    from paper_2601_23252_b200 import nss
+    make, kw = CASES[name]
+    prob = make()
+    cfg = W.config(seed=5, **kw)
+    ref = nsso.Oracle(prob, cfg, smc_rho=0.9)
+    gpu = nss.Sampler(prob, cfg, smc_rho=0.9)
+    scale = np.asarray(prob.hi) - np.asarray(prob.lo) if prob.prior_kind == W.PRIOR_BOX else np.asarray(prob.sd)
+    for t in range(1, 4):
+        x, _ = ref.get_live()
+        x32 = x.astype(np.float32)
+        e32 = np.array([ref.energy(q) for q in x32.astype(np.float64)]).astype(np.float32)
+        ref.set_live(x32.astype(np.float64), e32.astype(np.float64), t)
+        gpu.set_live(x32, e32, t)
+        ref.smc_stage()
+        gpu.smc_stage()
+        br, lr, tr, pr = ref.smc_state()
+        bg, lg, tg, pg = gpu.smc_state()
+        assert tg == tr == t
+        assert abs(bg - br) < 1e-9 and abs(lg - lr) < 1e-8, (t, bg, br, lg, lr)
+        assert np.array_equal(pg, pr)
+        xg, eg = gpu.get_live()
+        xr, er = ref.get_live()
+        ok = np.all(np.abs(xg - xr) <= 1e-5 * (np.abs(xr) + scale), axis=1) & \
+            (np.abs(eg - er) <= 1e-5 * np.maximum(1.0, np.abs(er)))
+        assert ok.mean() >= 0.99, (t, ok.mean())
+        if br >= 1.0:
+            break
+
+
+def test_smc_full_run_analytic_c1():
+    from paper_2601_23252_b200 import nss
+    truth = 2 * math.log(math.erf(5 / math.sqrt(2))) - 2 * math.log(10)
+    lz = []
+    for seed in range(1, 7):
+        g = nss.Sampler(W.gauss(2), W.config(n_live=400, k=1, steps=10, seed=seed), smc_rho=0.9)
+        b, l, t, _ = g.smc_run()
+        assert b == 1.0 and 2 <= t < 40
+        lz.append(l)
+        g.close()
+    lz = np.array(lz)
+    assert abs(lz.mean() - truth) < 3 * lz.std(ddof=1) / math.sqrt(lz.size) + 0.02, (lz, truth)
+
+
+def test_smc_rejects_gp_and_bad_rho():
+    from paper_2601_23252_b200 import nss
+    with pytest.raises(nss.NssError) as ei:
+        nss.Sampler(W.gauss(2), W.config(n_live=50, k=1, steps=2), smc_rho=1.5)
+    assert ei.value.code == 1
