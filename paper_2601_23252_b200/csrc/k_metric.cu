@@ -18,8 +18,15 @@ namespace nss {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kLoSharedMax = 64;  // factor kept in shared memory up to this d
 constexpr double kKappaInf = 1.3035;
 constexpr double kPi = 3.14159265358979323846;
+
+// shared-memory slot for the per-group entry sums, after this CTA's rows
+__device__ __forceinline__ double *raw_groups(double *sm, int nent, int d, int npair, int rows, int dp) {
+  float *raw = reinterpret_cast<float *>(sm + nent + d + (2 * npair + 7) / 8);
+  return reinterpret_cast<double *>(raw + ((static_cast<long long>(rows) * dp + 1) & ~1LL));
+}
 
 __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials, unsigned *ticket, int nblk,
                                                      double reg, int width_rule, double width_param,
@@ -64,35 +71,50 @@ __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials,
   }
   __syncthreads();
   if (tid == 0 && blockIdx.x == 0) st->stamp[9] = global_ns();
-  for (int e = tid; e < nent; e += blockDim.x) {
-    // four independent accumulators (fixed assignment: row mod 4) break the
+  // G row groups per entry when the entries leave threads idle (small d):
+  // thread t takes entry t % nent over the rows r = grp, grp + G, ... of the
+  // chunk; the G group sums are added in group order (deterministic)
+  const int G = nent < static_cast<int>(blockDim.x) ? static_cast<int>(blockDim.x) / nent : 1;
+  double *Sg = raw_groups(sm, nent, d, npair, rows, dp);
+  for (int t = tid; t < nent * G; t += blockDim.x) {
+    const int e = t % nent, grp = t / nent;
+    // four independent accumulators (fixed assignment: row mod 4G) break the
     // DFMA dependency chain
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    const int step = 4 * G;
     if (e < npair) {
       const int i = pi[e], j = pj[e];
       const double si = shift[i], sj = shift[j];
-      int rr = 0;
-      for (; rr + 3 < rows; rr += 4) {
+      int rr = grp;
+      for (; rr + 3 * G < rows; rr += step) {
         a0 = fma(static_cast<double>(raw[rr * dp + i]) - si, static_cast<double>(raw[rr * dp + j]) - sj, a0);
-        a1 = fma(static_cast<double>(raw[(rr + 1) * dp + i]) - si, static_cast<double>(raw[(rr + 1) * dp + j]) - sj, a1);
-        a2 = fma(static_cast<double>(raw[(rr + 2) * dp + i]) - si, static_cast<double>(raw[(rr + 2) * dp + j]) - sj, a2);
-        a3 = fma(static_cast<double>(raw[(rr + 3) * dp + i]) - si, static_cast<double>(raw[(rr + 3) * dp + j]) - sj, a3);
+        a1 = fma(static_cast<double>(raw[(rr + G) * dp + i]) - si, static_cast<double>(raw[(rr + G) * dp + j]) - sj, a1);
+        a2 = fma(static_cast<double>(raw[(rr + 2 * G) * dp + i]) - si,
+                 static_cast<double>(raw[(rr + 2 * G) * dp + j]) - sj, a2);
+        a3 = fma(static_cast<double>(raw[(rr + 3 * G) * dp + i]) - si,
+                 static_cast<double>(raw[(rr + 3 * G) * dp + j]) - sj, a3);
       }
-      for (; rr < rows; ++rr)
+      for (; rr < rows; rr += G)
         a0 = fma(static_cast<double>(raw[rr * dp + i]) - si, static_cast<double>(raw[rr * dp + j]) - sj, a0);
     } else {
       const int i = e - npair;
       const double si = shift[i];
-      int rr = 0;
-      for (; rr + 3 < rows; rr += 4) {
+      int rr = grp;
+      for (; rr + 3 * G < rows; rr += step) {
         a0 += static_cast<double>(raw[rr * dp + i]) - si;
-        a1 += static_cast<double>(raw[(rr + 1) * dp + i]) - si;
-        a2 += static_cast<double>(raw[(rr + 2) * dp + i]) - si;
-        a3 += static_cast<double>(raw[(rr + 3) * dp + i]) - si;
+        a1 += static_cast<double>(raw[(rr + G) * dp + i]) - si;
+        a2 += static_cast<double>(raw[(rr + 2 * G) * dp + i]) - si;
+        a3 += static_cast<double>(raw[(rr + 3 * G) * dp + i]) - si;
       }
-      for (; rr < rows; ++rr) a0 += static_cast<double>(raw[rr * dp + i]) - si;
+      for (; rr < rows; rr += G) a0 += static_cast<double>(raw[rr * dp + i]) - si;
     }
-    S[e] = (a0 + a1) + (a2 + a3);
+    Sg[grp * nent + e] = (a0 + a1) + (a2 + a3);
+  }
+  __syncthreads();
+  for (int e = tid; e < nent; e += blockDim.x) {
+    double acc = 0.0;
+    for (int g = 0; g < G; ++g) acc += Sg[g * nent + e];
+    S[e] = acc;
   }
   __syncthreads();
   double *out = partials + static_cast<long long>(blockIdx.x) * (nent + 1);
@@ -116,11 +138,14 @@ __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials,
   // ---------------- phase 2 (last CTA): reduce, regularise, factorise ----------------
   const int ld = d | 1;       // odd stride: column walks are bank-conflict free
   double *A = sm;            // d*ld (reuses phase-1 shared memory)
-  double *Lo = r.L64;        // d*d  output factor, written straight to global
   double *S1 = A + d * ld;   // d
+  // d*d output factor: shared memory up to d = 64 (copied to L64, L, LT at the
+  // end), else written straight to global
+  const bool lo_shared = d <= kLoSharedMax;
+  double *Lo = lo_shared ? S1 + d : r.L64;
   // lower-triangle pairs in column-major order: column j's trailing block
   // {(i, l): j < l <= i} is a contiguous suffix starting at coff(j + 1)
-  unsigned char *ti = reinterpret_cast<unsigned char *>(S1 + d);
+  unsigned char *ti = reinterpret_cast<unsigned char *>(S1 + d + (lo_shared ? d * d : 0));
   unsigned char *tl = ti + npair;
   __shared__ double sh_md;
   __shared__ double sh_red[kThreads / 32];
@@ -216,7 +241,10 @@ __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials,
   for (int e = tid; e < d * r.dp; e += blockDim.x) {
     const int i = e / r.dp, j = e - i * r.dp;
     r.L[e] = j < d ? static_cast<float>(Lo[i * d + j]) : 0.0f;
-    if (j < d) r.LT[j * r.dp + i] = static_cast<float>(Lo[i * d + j]);  // column-major copy
+    if (j < d) {
+      r.LT[j * r.dp + i] = static_cast<float>(Lo[i * d + j]);  // column-major copy
+      r.L64[i * d + j] = Lo[i * d + j];
+    }
   }
   if (tid == 0) st->stamp[12] = global_ns();
   // slice width (R-7)
@@ -279,9 +307,11 @@ size_t metric_smem(int n, int d, int nblk) {
   const int npair = d * (d + 1) / 2, nent = npair + d;
   const int dp = (d + 3) & ~3;
   const int rows = (n + nblk - 1) / nblk;
+  const int G = nent < kThreads ? kThreads / nent : 1;  // row groups (raw_groups)
   const size_t p1 = static_cast<size_t>(nent + d) * 8 + ((2 * static_cast<size_t>(npair) + 7) / 8) * 8 +
-                    static_cast<size_t>(rows) * dp * 4 + 64;
-  const size_t p2 = (static_cast<size_t>(d) * (d | 1) + d) * 8 + 2 * static_cast<size_t>(npair) + 16;
+                    (static_cast<size_t>(rows) * dp + 1) / 2 * 8 + static_cast<size_t>(G) * nent * 8 + 64;
+  const size_t p2 = (static_cast<size_t>(d) * (d | 1) + d + (d <= kLoSharedMax ? static_cast<size_t>(d) * d : 0)) * 8 +
+                    2 * static_cast<size_t>(npair) + 16;
   return p1 > p2 ? p1 : p2;
 }
 
