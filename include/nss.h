@@ -265,6 +265,8 @@ nss_status nss_set_chain_range(nss_ctx *ctx, int32_t c0, int32_t c1);
  * E_out: P values. */
 nss_status nss_lr_energy_batch(const double *X, const double *y, int64_t N, int32_t d, const double *theta,
                                int64_t P, double *E_out);
+/* (Measurement: with NSS_LR_REPS=R in the environment the call also times R
+ * repeats of the energy pass with CUDA events and prints the mean to stderr.) */
 
 /* Kernel check: GP ARD-RBF negative log marginal likelihoods (P:935-962
  * shape; DESIGN R-22) for P hyperparameter points phi (P*(d_in+2) row-major,

@@ -25,6 +25,8 @@ struct BatchDev {
   float *partial[2];          // [slices][p_stride] energy partial sums per row
   int *slices;                // [2] slices written by the energy pass of each parity
   __nv_bfloat16 *A[2];        // logistic regression: [3][p_stride][128] bf16 splits, else null
+  float *lin[2];              // logistic regression: per-row linear part theta~ . g, else null
+  const float *g;             // logistic regression: g = X^T (1/2 - y) (128 floats), else null
 };
 
 // k_batch.cu

@@ -53,6 +53,7 @@ __device__ __forceinline__ float probe_energy(const BatchDev &b, int parity, int
   const int ns = b.slices[parity];
   double acc = 0.0;
   for (int q = lane; q < ns; q += 32) acc += b.partial[parity][static_cast<long long>(q) * b.p_stride + row];
+  if (b.lin[parity] && lane == 0) acc += static_cast<double>(b.lin[parity][row]);  // logistic regression: theta . g
   return static_cast<float>(warp_sum_d(acc));
 }
 
@@ -66,8 +67,11 @@ __device__ __forceinline__ void emit_probe(const BatchDev &b, int parity, int ro
     if (i < d) dst[i] = xp[t];
   }
   if (b.A[parity]) {
-    // bf16x3 split for the tensor-core logistic-regression energy (K padded to 128)
+    // bf16x3 split for the tensor-core logistic-regression energy (K padded to
+    // 128), and the row's linear term theta~ . g (theta~ = hi + mid, the terms
+    // the tensor cores contract)
     __nv_bfloat16 *A = b.A[parity];
+    float lin = 0.f;
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       const int kk = lane + 32 * t;
@@ -79,7 +83,10 @@ __device__ __forceinline__ void emit_probe(const BatchDev &b, int parity, int ro
       A[static_cast<long long>(row) * 128 + kk] = hi;
       A[(static_cast<long long>(b.p_stride) + row) * 128 + kk] = mid;
       A[(2ll * b.p_stride + row) * 128 + kk] = lo;
+      lin = fmaf(__bfloat162float(hi) + __bfloat162float(mid), __ldg(b.g + kk), lin);
     }
+    lin = warp_sum(lin);
+    if (lane == 0) b.lin[parity][row] = lin;
   }
 }
 
@@ -116,7 +123,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_batch_begin(RunDev r, P
 }
 
 template <int NPL>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32) k_batch_advance(RunDev r, PriorDev pr, BatchDev b,
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 3) k_batch_advance(RunDev r, PriorDev pr, BatchDev b,
                                                                        int parity) {
   extern __shared__ float sm[];
   const int d = r.d, lane = threadIdx.x & 31, wib = threadIdx.x >> 5;

@@ -19,10 +19,12 @@
 // unit belongs to another probe tile; data tiles stream through a 4-stage TMA
 // ring; the MMA warp accumulates each tile into one of four TMEM buffers while
 // four epilogue warps drain the previous one.  Each epilogue thread owns one
-// probe row: it accumulates max(a,0) - y a and the product of (1 + e^-|a|)
-// (one ex2 per element, one lg2 per 64), with no cross-lane reduction.  Unit
+// probe row: it accumulates |a| and the product of (1 + e^-|a|) (the linear part theta . g is added per row by the consumer)
+// (one ex2 per element, one lg2 per 32), with no cross-lane reduction.  Unit
 // sums go to partial[slice][probe] and are summed in slice order by the
 // consumer, so energies are deterministic for a given P.
+#include <cstdlib>
+
 #include "nss_internal.cuh"
 #include "tc_ptx.cuh"
 
@@ -68,6 +70,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     k_lr_energy(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const float *y,
                 float *partial, int *slices_out, const int *n_probe_ptr, int *reset_counter, int p_stride,
                 int n_data, int n_tiles) {
+  (void)y;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sA = smem;
@@ -186,57 +189,43 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&bars->tempty[acc]);  // buffer fully read: release it
-        // softplus(a) - y a = max(a,0) - y a + log(1 + e^-|a|): two independent
-        // chains each of the linear part and of the product of (1 + e^-|a|)
-        float lin0 = 0.f, lin1 = 0.f, p0 = 1.f, p1 = 1.f;
+        // softplus(a) - y a = |a|/2 + a/2 - y a + log(1 + e^-|a|); the linear
+        // part sum_r (1/2 - y_r) a_r = theta . g is added per probe row by the
+        // consumer (lr_engine.cu), so per element: sum |a| and the product of
+        // (1 + e^-|a|) (one ex2; one lg2 per 32 factors), two chains each
+        float s0 = 0.f, s1 = 0.f, p0 = 1.f, p1 = 1.f;
         const int valid = n_data - col0;  // >= 64 except in the ragged last tile
-        const float4 *y4 = reinterpret_cast<const float4 *>(y + col0);
         if (valid >= 64) {
-          // full tile (all but the last): no masks
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const float4 yy = __ldg(y4 + q);
-            const float yv[4] = {yy.x, yy.y, yy.z, yy.w};
-#pragma unroll
-            for (int w = 0; w < 4; ++w) {
-              const int cc = 4 * q + w;
-              const float a = v[cc >> 5][cc & 31];
-              const float e = tc::ex2_approx(-fabsf(a) * 1.4426950408889634f);
-              const float l = fmaf(-yv[w], a, fmaxf(a, 0.f));
-              if (w & 1) {
-                p1 = fmaf(p1, e, p1);
-                lin1 += l;
-              } else {
-                p0 = fmaf(p0, e, p0);
-                lin0 += l;
-              }
+          for (int cc = 0; cc < 64; ++cc) {
+            const float a = v[cc >> 5][cc & 31];
+            const float e = tc::ex2_approx(-fabsf(a) * 1.4426950408889634f);
+            if (cc & 1) {
+              p1 = fmaf(p1, e, p1);
+              s1 += fabsf(a);
+            } else {
+              p0 = fmaf(p0, e, p0);
+              s0 += fabsf(a);
             }
           }
         } else {
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const float4 yy = __ldg(y4 + q);
-            const float yv[4] = {yy.x, yy.y, yy.z, yy.w};
-#pragma unroll
-            for (int w = 0; w < 4; ++w) {
-              const int cc = 4 * q + w;
-              if (cc < valid) {  // padded data rows contribute nothing
-                const float a = v[cc >> 5][cc & 31];
-                const float e = tc::ex2_approx(-fabsf(a) * 1.4426950408889634f);
-                const float l = fmaf(-yv[w], a, fmaxf(a, 0.f));
-                if (w & 1) {
-                  p1 = fmaf(p1, e, p1);
-                  lin1 += l;
-                } else {
-                  p0 = fmaf(p0, e, p0);
-                  lin0 += l;
-                }
+          for (int cc = 0; cc < 64; ++cc) {
+            if (cc < valid) {  // padded data rows contribute nothing
+              const float a = v[cc >> 5][cc & 31];
+              const float e = tc::ex2_approx(-fabsf(a) * 1.4426950408889634f);
+              if (cc & 1) {
+                p1 = fmaf(p1, e, p1);
+                s1 += fabsf(a);
+              } else {
+                p0 = fmaf(p0, e, p0);
+                s0 += fabsf(a);
               }
             }
           }
         }
         // each product has <= 32 factors in (1, 2]: no overflow
-        e_sum += static_cast<double>(fmaf(0.6931471805599453f, __log2f(p0) + __log2f(p1), lin0 + lin1));
+        e_sum += static_cast<double>(fmaf(0.6931471805599453f, __log2f(p0) + __log2f(p1), 0.5f * (s0 + s1)));
       }
       const int row = m * BM + row_in_tile;
       // the two column halves write adjacent slices: slice index 2 s + half

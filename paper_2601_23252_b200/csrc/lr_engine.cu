@@ -35,12 +35,22 @@ __global__ void k_split3(const float *P, int ldp, const int *n_probe_ptr, int d,
   }
 }
 
-__global__ void k_lr_reduce(const float *partial, int p_stride, const int *slices, const int *n_probe_ptr, float *E) {
+// E = kernel slices + theta~ . g with theta~ = hi + mid, the two bf16 terms
+// the tensor cores contract (the same split as k_split3 / emit_probe)
+__global__ void k_lr_reduce(const float *partial, int p_stride, const int *slices, const int *n_probe_ptr, float *E,
+                            const float *P, int ldp, int d, const float *g) {
   const int n_probe = *n_probe_ptr, n_splits = *slices;
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n_probe; p += gridDim.x * blockDim.x) {
     double s = 0.0;
     for (int q = 0; q < n_splits; ++q) s += partial[static_cast<long long>(q) * p_stride + p];
-    E[p] = static_cast<float>(s);
+    float lin = 0.f;
+    for (int k = 0; k < d; ++k) {
+      const float v = P[static_cast<long long>(p) * ldp + k];
+      const float hi = __bfloat162float(__float2bfloat16_rn(v));
+      const float mid = __bfloat162float(__float2bfloat16_rn(v - hi));
+      lin = fmaf(hi + mid, g[k], lin);
+    }
+    E[p] = static_cast<float>(s + lin);
   }
 }
 
@@ -91,18 +101,26 @@ cudaError_t lr_setup(LrEngine &L, const double *X, const double *y, long long N,
   L.n_splits = lr_max_slices(L.n_tiles);
   std::vector<__nv_bfloat16> xb(static_cast<size_t>(L.n_pad) * 128, __float2bfloat16_rn(0.f));
   std::vector<float> yf(static_cast<size_t>(L.n_pad), 0.f);
+  std::vector<double> g64(128, 0.0);
   for (long long r = 0; r < N; ++r) {
-    for (int k = 0; k < d; ++k) xb[r * 128 + k] = __float2bfloat16_rn(static_cast<float>(X[r * d + k]));
+    for (int k = 0; k < d; ++k) {
+      xb[r * 128 + k] = __float2bfloat16_rn(static_cast<float>(X[r * d + k]));
+      g64[k] += (0.5 - y[r]) * X[r * d + k];
+    }
     yf[r] = static_cast<float>(y[r]);
   }
+  std::vector<float> gf(128);
+  for (int k = 0; k < 128; ++k) gf[k] = static_cast<float>(g64[k]);
   cudaError_t e;
   if ((e = cudaMalloc(&L.Xb, xb.size() * sizeof(__nv_bfloat16)))) return e;
   if ((e = cudaMalloc(&L.y, yf.size() * sizeof(float)))) return e;
+  if ((e = cudaMalloc(&L.g, 128 * sizeof(float)))) return e;
+  if ((e = cudaMemcpy(L.g, gf.data(), 128 * sizeof(float), cudaMemcpyHostToDevice))) return e;
   for (int q = 0; q < 2; ++q) {
     if ((e = cudaMalloc(&L.A[q], 3ull * L.p_stride * 128 * sizeof(__nv_bfloat16)))) return e;
     if ((e = cudaMemset(L.A[q], 0, 3ull * L.p_stride * 128 * sizeof(__nv_bfloat16)))) return e;
-    if ((e = cudaMalloc(&L.partial[q], static_cast<size_t>(L.n_splits) * L.p_stride * sizeof(float)))) return e;
-    if ((e = cudaMemset(L.partial[q], 0, static_cast<size_t>(L.n_splits) * L.p_stride * sizeof(float)))) return e;
+    if ((e = cudaMalloc(&L.partial[q], static_cast<size_t>(L.n_splits + 1) * L.p_stride * sizeof(float)))) return e;
+    if ((e = cudaMemset(L.partial[q], 0, static_cast<size_t>(L.n_splits + 1) * L.p_stride * sizeof(float)))) return e;
   }
   if ((e = cudaMalloc(&L.slices, 2 * sizeof(int)))) return e;
   if ((e = cudaMemset(L.slices, 0, 2 * sizeof(int)))) return e;
@@ -117,6 +135,7 @@ cudaError_t lr_setup(LrEngine &L, const double *X, const double *y, long long N,
 void lr_free(LrEngine &L) {
   cudaFree(L.Xb);
   cudaFree(L.y);
+  cudaFree(L.g);
   cudaFree(L.slices);
   for (int q = 0; q < 2; ++q) {
     cudaFree(L.A[q]);
@@ -130,7 +149,8 @@ void lr_energies(const LrEngine &L, const float *P, int ldp, const int *n_probe,
   k_split3<<<296, 256, 0, lc.stream>>>(P, ldp, n_probe, L.d, L.A[0], L.p_stride);
   launch_lr_energy(L.tmA[0], L.tmB, L.y, L.partial[0], L.slices, n_probe, nullptr, L.p_stride,
                    static_cast<int>(L.N), lc);
-  k_lr_reduce<<<(L.max_probe + 255) / 256, 256, 0, lc.stream>>>(L.partial[0], L.p_stride, L.slices, n_probe, E);
+  k_lr_reduce<<<(L.max_probe + 255) / 256, 256, 0, lc.stream>>>(L.partial[0], L.p_stride, L.slices, n_probe, E, P, ldp,
+                                                                  L.d, L.g);
   *lc.launch_counter += 2;
 }
 

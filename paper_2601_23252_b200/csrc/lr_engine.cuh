@@ -12,8 +12,12 @@ struct LrEngine {
   int d = 0, n_tiles = 0, p_stride = 0, max_probe = 0, n_splits = 1;
   __nv_bfloat16 *Xb = nullptr;  // [n_pad][128] bf16 data rows (K padded with zeros)
   float *y = nullptr;           // [n_pad] labels (0 past N)
+  // linear part of the energy: sum_r (1/2 - y_r) a_r = theta . g, g = X^T (1/2 - y)
+  // (fp64 on the host, 128 floats, zero past d); per-row values live in the
+  // extra slot n_splits of partial[parity]
+  float *g = nullptr;
   __nv_bfloat16 *A[2] = {nullptr, nullptr};   // per round parity: [3][p_stride][128] splits hi / mid / lo
-  float *partial[2] = {nullptr, nullptr};     // per round parity: [n_splits][p_stride]
+  float *partial[2] = {nullptr, nullptr};     // per round parity: [n_splits + 1][p_stride]
   int *slices = nullptr;                      // [2] data slices used by the last pass of each parity
   CUtensorMap tmA[2]{}, tmB{};
 };

@@ -370,7 +370,9 @@ nss_status ensure_batch(nss_ctx *c) {
     for (int q = 0; q < 2; ++q) {
       b.partial[q] = c->lr.partial[q];
       b.A[q] = c->lr.A[q];
+      b.lin[q] = c->lr.partial[q] + static_cast<size_t>(c->lr.n_splits) * c->lr.p_stride;
     }
+    b.g = c->lr.g;
   } else {
     b.n_splits = 1;
     b.p_stride = b.max_rows;
@@ -384,7 +386,9 @@ nss_status ensure_batch(nss_ctx *c) {
       nss_status s;
       if ((s = dalloc(c, &b.partial[q], static_cast<size_t>(b.max_rows)))) return s;
       b.A[q] = nullptr;
+      b.lin[q] = nullptr;
     }
+    b.g = nullptr;
   }
   c->batch_backend = backend;
   return NSS_OK;
@@ -1275,6 +1279,19 @@ NSS_API nss_status nss_lr_energy_batch(const double *X, const double *y, int64_t
   if (!e) {
     lr_energies(L, dP, d, dn, dE, LaunchCtx{st, &launches});
     e = cudaGetLastError();
+    if (const char *rp = getenv("NSS_LR_REPS")) {  // measurement hook: time R repeats of the energy pass
+      const int reps = atoi(rp);
+      cudaEvent_t ea, eb;
+      cudaEventCreate(&ea);
+      cudaEventCreate(&eb);
+      cudaEventRecord(ea, st);
+      for (int q = 0; q < reps; ++q) lr_energies(L, dP, d, dn, dE, LaunchCtx{st, &launches});
+      cudaEventRecord(eb, st);
+      cudaEventSynchronize(eb);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ea, eb);
+      fprintf(stderr, "lr_energies x%d: %.3f us each\n", reps, 1000.f * ms / reps);
+    }
   }
   std::vector<float> Ef(P);
   if (!e) e = cudaStreamSynchronize(st);
