@@ -13,8 +13,9 @@ struct ESm {          // shared-memory image of the energy parameters
   const float *mu;    // GAUSS/CORR: d; MOG: K*d
   const float *isig;  // GAUSS: d; MOG: K*d
   const float *logc;  // MOG: K
-  const float *prec;  // CORR: d rows of stride ldp
+  const float *prec;  // CORR: d rows of stride ldp (the precision P, or its factor U when tri)
   int ldp;
+  bool tri;           // CORR: rows hold U with P = U^T U (upper triangular): q = |U r|^2
 };
 
 __host__ __device__ inline int odd_stride(int d) { return d | 1; }
@@ -33,6 +34,7 @@ __device__ inline void stage_energy(const EnergyDev &en, float *sp, ESm &es) {
   const int d = en.d, tid = threadIdx.x, nt = blockDim.x;
   es.ldp = odd_stride(d);
   es.mu = es.isig = es.logc = es.prec = nullptr;
+  es.tri = false;
   if (en.kind == NSS_E_GAUSS) {
     for (int i = tid; i < d; i += nt) { sp[i] = en.mu[i]; sp[d + i] = en.isig[i]; }
     es.mu = sp; es.isig = sp + d;
@@ -44,11 +46,12 @@ __device__ inline void stage_energy(const EnergyDev &en, float *sp, ESm &es) {
   } else if (en.kind == NSS_E_CORR_GAUSS) {
     for (int i = tid; i < d; i += nt) sp[i] = en.mu[i];
     float *P = sp + d;
+    const float *src = en.ufac ? en.ufac : en.prec;  // the triangular factor halves the work
     for (int e = tid; e < d * d; e += nt) {
       int i = e / d, j = e - i * d;
-      P[i * es.ldp + j] = en.prec[e];
+      P[i * es.ldp + j] = src[e];
     }
-    es.mu = sp; es.prec = P;
+    es.mu = sp; es.prec = P; es.tri = en.ufac != nullptr;
   }
 }
 
@@ -153,15 +156,49 @@ __device__ __forceinline__ float warp_energy(const float (&x)[NPL], const Energy
     }
     __syncwarp();
     float q = 0.f;
+    if (es.tri) {
+      // (U r)_i = sum_{m >= i} U_im r_m, q = sum_i (U r)_i^2.  Column
+      // segment s = [32 s, 32 s + 32) only meets rows t <= s (U is zero below
+      // the diagonal), so the loop is uniform across lanes and the rows of a
+      // lane accumulate as independent chains (two per row in segment 0).
+      float acc[NPL], acc0b = 0.f;
+#pragma unroll
+      for (int t = 0; t < NPL; ++t) acc[t] = 0.f;
+      const float *rows[NPL];
+#pragma unroll
+      for (int t = 0; t < NPL; ++t) rows[t] = es.prec + (lane + 32 * t < d ? lane + 32 * t : 0) * es.ldp;
+#pragma unroll
+      for (int sg = 0; sg < NPL; ++sg) {
+        const int m0 = 32 * sg, m1 = min(d, m0 + 32);
+        int m = m0;
+        if (sg == 0) {
+          for (; m + 1 < m1; m += 2) {
+            acc[0] = fmaf(rows[0][m], wbuf[m], acc[0]);
+            acc0b = fmaf(rows[0][m + 1], wbuf[m + 1], acc0b);
+          }
+        }
+        for (; m < m1; ++m) {
+          const float w = wbuf[m];
+#pragma unroll
+          for (int t = 0; t < NPL; ++t)
+            if (t <= sg) acc[t] = fmaf(rows[t][m], w, acc[t]);
+        }
+      }
+      acc[0] += acc0b;
+#pragma unroll
+      for (int t = 0; t < NPL; ++t)
+        if (lane + 32 * t < d) q = fmaf(acc[t], acc[t], q);
+    } else {
 #pragma unroll
     for (int t = 0; t < NPL; ++t) {
       const int i = lane + 32 * t;
       if (i < d) {
         const float *row = es.prec + i * es.ldp;
         float py = 0.f;
-        for (int m = 0; m < d; ++m) py = fmaf(row[m], wbuf[m], py);
+        for (int m = 0; m < d; ++m) py = fmaf(row[m], wbuf[m], py);  // (P r)_i; q = sum_i r_i (P r)_i
         q = fmaf(wbuf[i], py, q);
       }
+    }
     }
     q = warp_sum(q);
     __syncwarp();

@@ -664,6 +664,28 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
     en.mu = tmp;
     if ((s = upload_f32(c, &tmp, energy->prec, static_cast<size_t>(d) * d))) return bail(s);
     en.prec = tmp;
+    // P = L L^T in fp64 (host); U = L^T lets the warp energy form |U r|^2
+    // with half the multiply-adds of r^T P r (same value up to rounding)
+    std::vector<double> Lc(static_cast<size_t>(d) * d, 0.0);
+    bool pd = true;
+    for (int j = 0; j < d && pd; ++j) {
+      double s2 = energy->prec[j * d + j];
+      for (int q = 0; q < j; ++q) s2 -= Lc[j * d + q] * Lc[j * d + q];
+      if (!(s2 > 0.0)) { pd = false; break; }
+      Lc[j * d + j] = std::sqrt(s2);
+      for (int i = j + 1; i < d; ++i) {
+        double t = energy->prec[i * d + j];
+        for (int q = 0; q < j; ++q) t -= Lc[i * d + q] * Lc[j * d + q];
+        Lc[i * d + j] = t / Lc[j * d + j];
+      }
+    }
+    if (pd) {
+      std::vector<double> U(static_cast<size_t>(d) * d, 0.0);
+      for (int i = 0; i < d; ++i)
+        for (int m = i; m < d; ++m) U[i * d + m] = Lc[m * d + i];
+      if ((s = upload_f32(c, &tmp, U.data(), U.size()))) return bail(s);
+      en.ufac = tmp;
+    }
   } else if (en.kind == NSS_E_LOGREG) {
     const size_t nx = static_cast<size_t>(energy->n_data) * d;
     c->lr_ok = d <= 112 && lr_data_bf16_exact(energy->data_x, static_cast<long long>(nx));

@@ -49,6 +49,7 @@ struct EnergyDev {
   const float *isig;    // GAUSS: d; MOG: K*d  (1/sigma)
   const float *logc;    // MOG: K  (log w_j - sum log sigma_j - d/2 log 2pi)
   const float *prec;    // CORR: d*d
+  const float *ufac;    // CORR: U (d*d row-major, upper) with P = U^T U, or null
   const float *data_x;  // LOGREG: N*d; GP: N*d_in
   const float *data_y;  // LOGREG / GP: N
   // one-probe-per-lane engine tables, padded to 32 coordinates with neutral
