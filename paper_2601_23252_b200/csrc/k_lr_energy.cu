@@ -18,7 +18,7 @@
 // swizzle atoms, 64 KB) in shared memory and reloads it only when its next
 // unit belongs to another probe tile; data tiles stream through a 4-stage TMA
 // ring; the MMA warp accumulates each tile into one of four TMEM buffers while
-// four epilogue warps drain the previous one.  Each epilogue thread owns one
+// sixteen epilogue warps drain the previous one.  Each epilogue thread owns one
 // probe row: it accumulates |a| and the product of (1 + e^-|a|) (the linear part theta . g is added per row by the consumer)
 // (one ex2 per element, one lg2 per 32), with no cross-lane reduction.  Unit
 // sums go to partial[slice][probe] and are summed in slice order by the
@@ -41,7 +41,9 @@ constexpr int kAcc = 4;          // TMEM accumulator buffers (4 x 128 columns)
 constexpr int kAtom = BM * 128;  // bytes of one [128 rows x 128 B] swizzle-128B region
 constexpr int kSmemA = kSplits * 2 * kAtom;      // splits x 2 k-blocks
 constexpr int kSmemB = kStages * 2 * kAtom;      // stages x 2 k-blocks
-constexpr int kEpiWarps = 8;                     // two per TMEM lane quarter (column halves)
+constexpr int kEpiWarps = 16;                    // four per TMEM lane quarter (column quarters)
+constexpr int kColParts = kEpiWarps / 4;         // column parts of a tile (one per epilogue warp of a quarter)
+constexpr int kPartCols = BN / kColParts;        // columns per part (32: one tcgen05.ld)
 constexpr int kThreads = 64 + 32 * kEpiWarps;    // warp 0 TMA, warp 1 MMA, warps 2.. epilogue
 constexpr int kUnitsPerSM = 8;
 
@@ -82,7 +84,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const Sched sch(n_probe, n_tiles, G);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     if (reset_counter) *reset_counter = 0;  // the next round's row counter
-    *slices_out = 2 * sch.S;                // per unit: one slice per column half
+    *slices_out = kColParts * sch.S;        // per unit: one slice per column part
   }
   int u0, u1;
   sch.range(blockIdx.x, G, u0, u1);
@@ -168,9 +170,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= 2) {
-    // ---------------- epilogue: one probe row per thread, half the columns ----------------
+    // ---------------- epilogue: one probe row per thread, a quarter of the columns ----------------
     const int quarter = warp & 3;             // TMEM lanes this warp may access
-    const int chalf = (warp - 2) >> 2;        // column half of the tile: 0 or 1
+    const int chalf = (warp - 2) >> 2;        // column part of the tile: 0 .. kColParts-1
     const int row_in_tile = quarter * 32 + lane;
     int it = 0;
     for (int u = u0; u < u1; ++u) {
@@ -181,11 +183,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int acc = it % kAcc;
         tc::mbar_wait(&bars->tfull[acc], (it / kAcc) & 1);
         tc::tc_fence_after();
-        const int cbase = chalf * (BN / 2);
+        const int cbase = chalf * kPartCols;
         const int col0 = t * BN + cbase;
-        float v[2][32];
+        float v[1][32];
         tc::tmem_ld32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + cbase, v[0]);
-        tc::tmem_ld32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + cbase + 32, v[1]);
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&bars->tempty[acc]);  // buffer fully read: release it
@@ -194,11 +195,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         // consumer (lr_engine.cu), so per element: sum |a| and the product of
         // (1 + e^-|a|) (one ex2; one lg2 per 32 factors), two chains each
         float s0 = 0.f, s1 = 0.f, p0 = 1.f, p1 = 1.f;
-        const int valid = n_data - col0;  // >= 64 except in the ragged last tile
-        if (valid >= 64) {
+        const int valid = n_data - col0;  // >= kPartCols except in the ragged last tile
+        if (valid >= kPartCols) {
 #pragma unroll
-          for (int cc = 0; cc < 64; ++cc) {
-            const float a = v[cc >> 5][cc & 31];
+          for (int cc = 0; cc < kPartCols; ++cc) {
+            const float a = v[0][cc];
             const float e = tc::ex2_approx(-fabsf(a) * 1.4426950408889634f);
             if (cc & 1) {
               p1 = fmaf(p1, e, p1);
@@ -210,9 +211,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         } else {
 #pragma unroll
-          for (int cc = 0; cc < 64; ++cc) {
+          for (int cc = 0; cc < kPartCols; ++cc) {
             if (cc < valid) {  // padded data rows contribute nothing
-              const float a = v[cc >> 5][cc & 31];
+              const float a = v[0][cc];
               const float e = tc::ex2_approx(-fabsf(a) * 1.4426950408889634f);
               if (cc & 1) {
                 p1 = fmaf(p1, e, p1);
@@ -224,12 +225,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        // each product has <= 32 factors in (1, 2]: no overflow
+        // each product has <= 16 factors in (1, 2]: no overflow
         e_sum += static_cast<double>(fmaf(0.6931471805599453f, __log2f(p0) + __log2f(p1), 0.5f * (s0 + s1)));
       }
       const int row = m * BM + row_in_tile;
-      // the two column halves write adjacent slices: slice index 2 s + half
-      if (row < n_probe) partial[static_cast<long long>(2 * s + chalf) * p_stride + row] = static_cast<float>(e_sum);
+      // the column parts write adjacent slices: slice index kColParts s + part
+      if (row < n_probe)
+        partial[static_cast<long long>(kColParts * s + chalf) * p_stride + row] = static_cast<float>(e_sum);
     }
   }
   tc::tc_fence_before();
@@ -242,7 +244,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 size_t lr_energy_smem() { return kSmemA + kSmemB + sizeof(Bars) + 1024; }
 int lr_energy_splits() { return kSplits; }
 
-int lr_max_slices(int n_tiles) { return 2 * n_tiles; }
+int lr_max_slices(int n_tiles) { return kColParts * n_tiles; }
 
 void launch_lr_energy(const CUtensorMap &tmA, const CUtensorMap &tmB, const float *y, float *partial, int *slices_out,
                       const int *n_probe, int *reset_counter, int p_stride, int n_data, const LaunchCtx &lc) {
