@@ -85,3 +85,33 @@ def test_two_chain_blocks_reproduce_full_iteration(name):
             assert np.array_equal(x, xf) and np.array_equal(e, ef), f"iteration {it}"
     evals = sum(s.info()["energy_evals"] for s in ranks)
     assert evals == full.info()["energy_evals"]
+
+
+def test_sharded_sampler_through_torch_distributed_world1():
+    """The torch.distributed plumbing of dist.py on the GPU box: an NCCL process
+    group of one rank, rank 0's NCCL id broadcast, a sharded sampler whose run
+    equals the plain one."""
+    import socket
+
+    import torch
+    import torch.distributed as td
+    from paper_2601_23252_b200 import nss
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    td.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                          device_id=torch.device("cuda", 0))
+    try:
+        prob, cfg = W.gauss(3), W.config(n_live=300, k=30, steps=4, seed=8)
+        a = D.sharded_sampler(prob, cfg)
+        b = nss.Sampler(prob, cfg)
+        for s in (a, b):
+            s.steps(5)
+        xa, ea = a.get_live()
+        xb, eb = b.get_live()
+        assert np.array_equal(xa, xb) and np.array_equal(ea, eb)
+        tot = D.job_totals(a.info())
+        assert tot["energy_evals"] == b.info()["energy_evals"]
+    finally:
+        td.destroy_process_group()
