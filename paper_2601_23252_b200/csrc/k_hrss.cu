@@ -74,6 +74,15 @@ __global__ void __launch_bounds__(256) k_hrss(RunDev r, PriorDev pr, EnergyDev e
   unsigned long long n_probe = 0, n_eval = 0, n_exp = 0, n_shr = 0, n_null = 0;
 
   for (int j = 0; j < p; ++j) {
+    if (r.Vpre) {
+      // ---- direction precomputed for this (chain, step) by k_dirs ----
+      const float *vr = r.Vpre + (static_cast<long long>(c - r.c0) * p + j) * r.dp;
+#pragma unroll
+      for (int t = 0; t < NPL; ++t) {
+        const int i = lane + 32 * t;
+        v[t] = i < d ? __ldg(vr + i) : 0.f;
+      }
+    } else {
     // ---- direction v = L z / |z| (Mahalanobis, R-6) or L z / |L z| ----
     for (int b = lane; b < nblk_all; b += 32) {
       uint4 u4 = philox_block(r, it, s, kPhaseHrss, j, b);
@@ -110,6 +119,7 @@ __global__ void __launch_bounds__(256) k_hrss(RunDev r, PriorDev pr, EnergyDev e
 #pragma unroll
     for (int t = 0; t < NPL; ++t) v[t] *= inv;
     __syncwarp();
+    }
 
     // ---- slice height and initial bracket (R-9) ----
     const uint4 hb = philox_block(r, it, s, kPhaseHrss, j, h >> 2);
@@ -193,6 +203,89 @@ __global__ void __launch_bounds__(256) k_hrss(RunDev r, PriorDev pr, EnergyDev e
     atomicAdd(&st->shrinks, n_shr);
     atomicAdd(&st->nulls, n_null);
   }
+}
+
+// Directions of every (chain, step) of the iteration at once (large d): the
+// same draws and arithmetic as the in-chain direction of k_hrss, one warp per
+// (chain, step) over the whole GPU instead of serially inside each chain:
+// V[(c - c0) p + j] = L z / |z| (Mahalanobis) or L z / |L z|.
+template <int NPL>
+__global__ void __launch_bounds__(256) k_dirs(RunDev r, float *V) {
+  extern __shared__ float sm[];
+  __shared__ int sh_flag;
+  const int d = r.d, lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  const int ldl = odd_stride(d);
+  float *sL = sm;
+  float *sZ = sL + d * ldl + wib * (NPL * 32);
+  if (threadIdx.x == 0) sh_flag = (r.st->terminated || r.st->error || r.st->finalised) ? 1 : 0;
+  for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
+    int i = e / d, j = e - i * d;
+    sL[i * ldl + j] = r.L[i * r.dp + j];
+  }
+  __syncthreads();
+  if (sh_flag) return;
+  const long long q = static_cast<long long>(blockIdx.x) * wpb + wib;  // (c - c0) * p + j
+  const int p = r.p;
+  if (q >= static_cast<long long>(r.c1 - r.c0) * p) return;
+  const int c = r.c0 + static_cast<int>(q / p), j = static_cast<int>(q % p);
+  const uint32_t it = static_cast<uint32_t>(r.st->iter);
+  const int s = r.cdest[c];
+  const bool euclid = r.dir_norm == NSS_DIR_EUCLIDEAN;
+  const int h = 2 * ((d + 1) / 2);
+  const int nblk_norm = h >> 2, nblk_all = (h + 3) >> 2;
+  for (int b = lane; b < nblk_all; b += 32) {
+    uint4 u4 = philox_block(r, it, s, kPhaseHrss, j, b);
+    float u0 = u01(u4.x), u1 = u01(u4.y), u2 = u01(u4.z), u3 = u01(u4.w);
+    float r0 = sqrtf(-2.f * logf(u0)), r1 = sqrtf(-2.f * logf(u2));
+    float s0, c0, s1, c1;
+    sincospif(2.f * u1, &s0, &c0);
+    sincospif(2.f * u3, &s1, &c1);
+    const int i0 = 4 * b;
+    if (i0 < d) sZ[i0] = r0 * c0;
+    if (i0 + 1 < d) sZ[i0 + 1] = r0 * s0;
+    if (b < nblk_norm) {
+      if (i0 + 2 < d) sZ[i0 + 2] = r1 * c1;
+      if (i0 + 3 < d) sZ[i0 + 3] = r1 * s1;
+    }
+  }
+  __syncwarp();
+  float v[NPL], zz = 0.f, vv = 0.f;
+#pragma unroll
+  for (int t = 0; t < NPL; ++t) {
+    const int i = lane + 32 * t;
+    float acc = 0.f;
+    if (i < d) {
+      const float zi = sZ[i];
+      zz = fmaf(zi, zi, zz);
+      const float *row = sL + i * ldl;
+      for (int m = 0; m <= i; ++m) acc = fmaf(row[m], sZ[m], acc);
+    }
+    v[t] = acc;
+    vv = fmaf(acc, acc, vv);
+  }
+  const float inv = 1.f / sqrtf(warp_sum(euclid ? vv : zz));
+  float *out = V + q * r.dp;
+#pragma unroll
+  for (int t = 0; t < NPL; ++t) {
+    const int i = lane + 32 * t;
+    if (i < d) out[i] = v[t] * inv;
+  }
+}
+
+template <int NPL>
+void launch_dirs_t(const RunDev &r, float *V, const LaunchCtx &lc) {
+  const long long work = static_cast<long long>(r.c1 - r.c0) * r.p;
+  if (work <= 0) return;
+  const int wpb = 8;
+  const size_t smem = (static_cast<size_t>(r.d) * odd_stride(r.d) + static_cast<size_t>(wpb) * NPL * 32) * sizeof(float);
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && attr < smem) {
+    cudaFuncSetAttribute(k_dirs<NPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    attr = smem;
+  }
+  NSS_PIN_CARVEOUT(k_dirs<NPL>);
+  k_dirs<NPL><<<static_cast<int>((work + wpb - 1) / wpb), wpb * 32, smem, lc.stream>>>(r, V);
+  ++*lc.launch_counter;
 }
 
 // F1 constrained Gaussian random walk: one warp per
@@ -467,6 +560,14 @@ void launch_hrss(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const
   if (hrss_engine(r, en) == 1) {
     launch_hrss_lane(r, pr, en, lc);
     return;
+  }
+  if (r.Vpre) {  // large d: all directions of the iteration first (k_dirs)
+    switch ((r.d + 31) / 32) {
+      case 1: launch_dirs_t<1>(r, r.Vpre, lc); break;
+      case 2: launch_dirs_t<2>(r, r.Vpre, lc); break;
+      case 3: launch_dirs_t<3>(r, r.Vpre, lc); break;
+      default: launch_dirs_t<4>(r, r.Vpre, lc); break;
+    }
   }
   NSS_DISPATCH(launch_hrss_t, r, pr, en, lc);
 }

@@ -92,6 +92,8 @@ struct nss_ctx {
   void *comm = nullptr;
   int rank = 0, world = 1, kc = 0;
   float *xbuf = nullptr, *xall = nullptr;
+  float *vpre = nullptr;  // k_dirs output (warp engine, d > 32)
+  size_t vpre_floats = 0;
   // F3 tempered SMC-SS (k_smc.cu): particles are the live set
   bool smc = false;
   double smc_rho = 0.9;
@@ -503,7 +505,29 @@ nss_status enqueue_iteration_batch(nss_ctx *c) {
 
 // One outer iteration: replayed from a captured graph, or launched eagerly in
 // timing mode (events bracket each kernel) or when graphs are disabled.
+// Warp engine at large d: room for every (chain, step) direction of an
+// iteration, precomputed by k_dirs (allocated once, before any graph capture).
+nss_status ensure_vpre(nss_ctx *c) {
+  RunDev &r = c->r;
+  const bool want = r.d > 32 && r.mutation == NSS_MUT_HRSS && resolve_engine(c) == 0 &&
+                    hrss_engine(r, c->en) == 0;
+  const size_t need = static_cast<size_t>(r.c1 - r.c0) * (r.p > 0 ? r.p : 1) * c->dp;
+  if (!want || need == 0 || need * sizeof(float) > (1ull << 30)) {
+    r.Vpre = nullptr;
+    return NSS_OK;
+  }
+  if (!c->vpre || c->vpre_floats < need) {
+    nss_status s;
+    if ((s = dalloc(c, &c->vpre, need))) return s;
+    c->vpre_floats = need;
+  }
+  r.Vpre = c->vpre;
+  return NSS_OK;
+}
+
 nss_status enqueue_iteration(nss_ctx *c) {
+  nss_status vs = ensure_vpre(c);
+  if (vs) return vs;
   const bool wm = c->metric_pending;
   c->term_stale = true;
   c->metric_pending = true;
@@ -1441,6 +1465,7 @@ NSS_API nss_status nss_smc_stage(nss_ctx *c) {
   nss_status s = check_usable(c);
   if (s) return s;
   if (!c->smc) return fail(c, NSS_ERR_STATE, "not an SMC context");
+  if ((s = ensure_vpre(c))) return s;
   LaunchCtx lc = lctx(c);
   launch_smc_stage(c->r, c->smc_rho, c->smc_cum, c->smc_par, c->smc_xs, c->smc_es, lc);
   launch_metric(c->r, c->cfg.metric_reg, c->cfg.width_rule, c->cfg.width, 0, c->partials, c->ticket, c->nblk, lc);

@@ -82,6 +82,8 @@ struct RunDev {
   int *cdest, *cpar;
   int mutation;               // NSS_MUT_HRSS or NSS_MUT_RW (F1)
   int tempered;               // F3: HRSS on Pi exp(-beta E) (beta = st->smc_beta), no threshold
+  float *Vpre;                // warp engine, large d: directions of every (chain, step) of the
+                              // iteration, computed up front by k_dirs ((c1-c0) p rows of dp), or null
   float rw_sigma;             // RW proposal scale c 2.38 / sqrt(d)
   const float *Xs, *Es;
   long long max_dead;
