@@ -58,6 +58,7 @@ struct nss_ctx {
   double *summary = nullptr;  // device: [mean, std, closed lz_0..R]
   DevState *h_st = nullptr;   // pinned mirror of the device state
   int *h_one = nullptr;       // pinned constant 1 (finalised flag)
+  double *h_lz0 = nullptr;    // pinned mirror of replica 0's log Z (step info)
   bool poisoned = false;
   std::string err;
   long long launches = 0;
@@ -203,6 +204,7 @@ nss_status pull_state(nss_ctx *c) {
     c->term_stale = false;
   }
   CK(cudaMemcpyAsync(c->h_st, c->r.st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
+  if (c->r.lz) CK(cudaMemcpyAsync(c->h_lz0, c->r.lz, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   return NSS_OK;
 }
@@ -220,9 +222,7 @@ void fill_info(nss_ctx *c, nss_step_info *info) {
   info->log_z_live = s.log_z_live;
   info->terminated = s.terminated;
   info->finalised = s.finalised;
-  double lz0 = -INFINITY;
-  cudaMemcpy(&lz0, c->r.lz, sizeof(double), cudaMemcpyDeviceToHost);
-  info->log_z_det = lz0;
+  info->log_z_det = *c->h_lz0;  // copied with the state by pull_state
 }
 
 nss_status collect_timing(nss_ctx *c) {
@@ -634,6 +634,8 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
   }
   if (cudaMallocHost(&c->h_st, sizeof(DevState)) != cudaSuccess) return bail(NSS_ERR_CUDA);
   if (cudaMallocHost(&c->h_one, sizeof(int)) != cudaSuccess) return bail(NSS_ERR_CUDA);
+  if (cudaMallocHost(&c->h_lz0, sizeof(double)) != cudaSuccess) return bail(NSS_ERR_CUDA);
+  *c->h_lz0 = -INFINITY;
   if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess) return bail(NSS_ERR_CUDA);
   if (cudaEventCreateWithFlags(&c->ev_sel, cudaEventDisableTiming) != cudaSuccess) return bail(NSS_ERR_CUDA);
   if (cudaEventCreateWithFlags(&c->ev_evid, cudaEventDisableTiming) != cudaSuccess) return bail(NSS_ERR_CUDA);
@@ -1097,6 +1099,7 @@ NSS_API nss_status nss_destroy(nss_ctx *c) {
   }
   if (c->h_st) cudaFreeHost(c->h_st);
   if (c->h_one) cudaFreeHost(c->h_one);
+  if (c->h_lz0) cudaFreeHost(c->h_lz0);
   if (c->side) { cudaStreamSynchronize(c->side); cudaStreamDestroy(c->side); }
   if (c->ev_sel) cudaEventDestroy(c->ev_sel);
   if (c->ev_evid) cudaEventDestroy(c->ev_evid);
