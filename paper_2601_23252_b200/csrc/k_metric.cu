@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials,
   // thread t takes entry t % nent over the rows r = grp, grp + G, ... of the
   // chunk; the G group sums are added in group order (deterministic)
   const int G = nent < static_cast<int>(blockDim.x) ? static_cast<int>(blockDim.x) / nent : 1;
-  double *Sg = raw_groups(sm, nent, d, npair, rows, dp);
+  double *Sg = G > 1 ? raw_groups(sm, nent, d, npair, rows, dp) : S;  // one group: sum straight into S
   for (int t = tid; t < nent * G; t += blockDim.x) {
     const int e = t % nent, grp = t / nent;
     // four independent accumulators (fixed assignment: row mod 4G) break the
@@ -111,11 +111,12 @@ __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials,
     Sg[grp * nent + e] = (a0 + a1) + (a2 + a3);
   }
   __syncthreads();
-  for (int e = tid; e < nent; e += blockDim.x) {
-    double acc = 0.0;
-    for (int g = 0; g < G; ++g) acc += Sg[g * nent + e];
-    S[e] = acc;
-  }
+  if (G > 1)
+    for (int e = tid; e < nent; e += blockDim.x) {
+      double acc = 0.0;
+      for (int g = 0; g < G; ++g) acc += Sg[g * nent + e];
+      S[e] = acc;
+    }
   __syncthreads();
   double *out = partials + static_cast<long long>(blockIdx.x) * (nent + 1);
   for (int e = tid; e < nent; e += blockDim.x) out[e] = S[e];
@@ -309,7 +310,7 @@ size_t metric_smem(int n, int d, int nblk) {
   const int rows = (n + nblk - 1) / nblk;
   const int G = nent < kThreads ? kThreads / nent : 1;  // row groups (raw_groups)
   const size_t p1 = static_cast<size_t>(nent + d) * 8 + ((2 * static_cast<size_t>(npair) + 7) / 8) * 8 +
-                    (static_cast<size_t>(rows) * dp + 1) / 2 * 8 + static_cast<size_t>(G) * nent * 8 + 64;
+                    (static_cast<size_t>(rows) * dp + 1) / 2 * 8 + (G > 1 ? static_cast<size_t>(G) * nent * 8 : 0) + 64;
   const size_t p2 = (static_cast<size_t>(d) * (d | 1) + d + (d <= kLoSharedMax ? static_cast<size_t>(d) * d : 0)) * 8 +
                     2 * static_cast<size_t>(npair) + 16;
   return p1 > p2 ? p1 : p2;

@@ -10,7 +10,7 @@ import pytest
 from scipy import special, stats
 
 from paper_2601_23252_b200 import workloads as W
-from tests.parity_util import compare_iteration, inject_pair
+from tests.parity_util import compare_iteration, inject_pair, prior_scale
 
 pytestmark = pytest.mark.gpu
 
@@ -50,6 +50,7 @@ CASES = {
     "stepout_cap": (lambda: W.gauss(2, half_width=50.0, sigma=20.0),
                     dict(n_live=100, k=10, steps=4, width_rule=W.W_FIXED, width=0.05, max_stepout=3), 0),
     "shrink_cap": (lambda: W.gauss(4), dict(n_live=100, k=10, steps=4, max_shrink=2), 2),
+    "d128_max": (lambda: W.gauss(128, half_width=4.0), dict(n_live=300, k=30, steps=2), 0),
     # large-n thresholding paths of k_select: 32-bit ordinals on chip + chunked
     # bitonic dead-order sort; keys in global memory
     "select_ord32": (lambda: W.gauss(3), dict(n_live=20_000, k=9_000, steps=2), 0),
@@ -362,3 +363,52 @@ def test_rw_single_iteration_parity(name):
     assert np.all(c[..., 0] == 0) and np.all(c[..., 1] == 0)
     assert 0 < c[..., 3].mean() < 1  # some proposals accepted, some rejected
     assert gpu.info()["expansions"] == 0
+
+
+def _full_size_subset(name, chains, seed=3):
+    """A BASELINE configuration at full size through the engine bench.py times;
+    the oracle replays a subset of the chains of the same iteration.  Live
+    points: seeded prior draws (numpy), energies from the oracle (not the GPU)."""
+    from oracle import nsso
+    from paper_2601_23252_b200 import nss
+    prob, cfg = W.workload(name, seed=seed)
+    rng = np.random.default_rng(101)
+    n, d = cfg["n_live"], prob.d
+    if prob.prior_kind == W.PRIOR_BOX:
+        x0 = (prob.lo + (prob.hi - prob.lo) * rng.random((n, d))).astype(np.float32)
+    else:
+        x0 = (prob.mean + prob.sd * rng.standard_normal((n, d))).astype(np.float32)
+    ref = nsso.Oracle(prob, cfg, draw_live=False)
+    e0 = np.array([ref.energy(q) for q in x0.astype(np.float64)]).astype(np.float32)
+    ref.set_live(x0.astype(np.float64), e0.astype(np.float64), 1)
+    gpu = nss.Sampler(prob, cfg)
+    gpu.set_live(x0, e0, 1)
+    ref.set_chain_subset(chains)
+    gpu.step()
+    ref.step()
+    tg, tr = gpu.trace(), ref.trace()
+    for key in ("dead_gid", "dest_gid", "parent_gid"):
+        assert np.array_equal(tg[key], tr[key]), key
+    xg, eg = gpu.get_live()
+    xr, er = ref.get_live()
+    scale = prior_scale(prob)
+    good = 0
+    for c in chains:
+        diff = np.nonzero(np.any(tg["counts"][c] != tr["counts"][c], axis=1))[0]
+        if diff.size:
+            assert np.min(tr["min_margin"][c, : diff[0] + 1]) < 1e-5, (c, diff[0])
+            continue
+        good += 1
+        s = tg["dest_gid"][c]
+        assert np.all(np.abs(xg[s] - xr[s]) <= 1e-5 * (np.abs(xr[s]) + scale))
+        assert abs(eg[s] - er[s]) <= 1e-5 * max(1.0, abs(er[s]))
+    assert good >= len(chains) - 1
+    return gpu
+
+
+@pytest.mark.parametrize("name", ["C3a", "C3b"])
+def test_c3_full_size_iteration_subset(name):
+    """C3a / C3b at full size (n=1e4, k=1e3, p=100, d=100): warp engine with
+    precomputed directions, chains 0, 1, 499, 998, 999 replayed by the oracle."""
+    gpu = _full_size_subset(name, [0, 1, 499, 998, 999])
+    assert gpu.engine() == "warp"
