@@ -51,6 +51,7 @@ CASES = {
                     dict(n_live=100, k=10, steps=4, width_rule=W.W_FIXED, width=0.05, max_stepout=3), 0),
     "shrink_cap": (lambda: W.gauss(4), dict(n_live=100, k=10, steps=4, max_shrink=2), 2),
     "d128_max": (lambda: W.gauss(128, half_width=4.0), dict(n_live=300, k=30, steps=2), 0),
+    "select_large": (lambda: W.gauss(2), dict(n_live=100_000, k=50_000, steps=1, max_dead=400_000), 0),
     # large-n thresholding paths of k_select: 32-bit ordinals on chip + chunked
     # bitonic dead-order sort; keys in global memory
     "select_ord32": (lambda: W.gauss(3), dict(n_live=20_000, k=9_000, steps=2), 0),
