@@ -197,6 +197,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3) k_batch_advance(RunDev
         break;
       }
       const int j = s.step;
+      if (r.Vpre) {  // precomputed for this (chain, step) by k_dirs (bit-identical)
+        const float *vr = r.Vpre + (static_cast<long long>(c - r.c0) * p + j) * r.dp;
+#pragma unroll
+        for (int t = 0; t < NPL; ++t) {
+          const int i = lane + 32 * t;
+          v[t] = i < d ? __ldg(vr + i) : 0.f;
+        }
+      } else {
       // direction v = L z / |z| (R-6), stream (it, dest, HRSS, j)
       for (int bk = lane; bk < nblk_all; bk += 32) {
         const uint4 u4 = philox_block(r, it, dest, kPhaseHrss, j, bk);
@@ -241,6 +249,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3) k_batch_advance(RunDev
 #pragma unroll
       for (int t = 0; t < NPL; ++t) v[t] *= inv;
       __syncwarp();
+      }
       const uint4 hb = philox_block(r, it, dest, kPhaseHrss, j, h >> 2);
       s.log_y = s.lp + logf(u01(word(hb, h & 3)));
       s.l0 = -w * u01(word(hb, (h + 1) & 3));

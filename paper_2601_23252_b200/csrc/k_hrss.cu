@@ -529,6 +529,16 @@ void launch_init_t(const RunDev &r, const PriorDev &pr, const EnergyDev &en, con
 
 }  // namespace
 
+void launch_dirs(const RunDev &r, const LaunchCtx &lc) {
+  if (!r.Vpre) return;
+  switch ((r.d + 31) / 32) {
+    case 1: launch_dirs_t<1>(r, r.Vpre, lc); break;
+    case 2: launch_dirs_t<2>(r, r.Vpre, lc); break;
+    case 3: launch_dirs_t<3>(r, r.Vpre, lc); break;
+    default: launch_dirs_t<4>(r, r.Vpre, lc); break;
+  }
+}
+
 bool energy_supported(const EnergyDev &en) {
   switch (en.kind) {
     case NSS_E_FLAT: case NSS_E_GAUSS: case NSS_E_MOG: case NSS_E_CORR_GAUSS: case NSS_E_FUNNEL:
@@ -561,14 +571,7 @@ void launch_hrss(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const
     launch_hrss_lane(r, pr, en, lc);
     return;
   }
-  if (r.Vpre) {  // large d: all directions of the iteration first (k_dirs)
-    switch ((r.d + 31) / 32) {
-      case 1: launch_dirs_t<1>(r, r.Vpre, lc); break;
-      case 2: launch_dirs_t<2>(r, r.Vpre, lc); break;
-      case 3: launch_dirs_t<3>(r, r.Vpre, lc); break;
-      default: launch_dirs_t<4>(r, r.Vpre, lc); break;
-    }
-  }
+  launch_dirs(r, lc);  // large d: all directions of the iteration first (k_dirs)
   NSS_DISPATCH(launch_hrss_t, r, pr, en, lc);
 }
 

@@ -451,6 +451,7 @@ nss_status enqueue_iteration_batch(nss_ctx *c) {
   if ((s = timed_launch(c, 2, c->side, [&] { launch_evidence(c->r, 0, ls); }))) return s;
   CK(cudaEventRecord(c->ev_evid, c->side));
   auto rounds = [&]() -> nss_status {
+    launch_dirs(c->r, lc);  // large d: every direction of the iteration up front
     batch_begin(c->r, c->pr, c->bd, lc);
     const long long max_rounds =
         static_cast<long long>(c->r.p) * (c->r.max_stepout + 2 + c->r.max_shrink) + kRoundsPerChunk;
@@ -509,8 +510,9 @@ nss_status enqueue_iteration_batch(nss_ctx *c) {
 // iteration, precomputed by k_dirs (allocated once, before any graph capture).
 nss_status ensure_vpre(nss_ctx *c) {
   RunDev &r = c->r;
-  const bool want = r.d > 32 && r.mutation == NSS_MUT_HRSS && resolve_engine(c) == 0 &&
-                    hrss_engine(r, c->en) == 0;
+  const int eng = resolve_engine(c);
+  const bool want = r.d > 32 && r.mutation == NSS_MUT_HRSS &&
+                    ((eng == 0 && hrss_engine(r, c->en) == 0) || eng == 2);
   const size_t need = static_cast<size_t>(r.c1 - r.c0) * (r.p > 0 ? r.p : 1) * c->dp;
   if (!want || need == 0 || need * sizeof(float) > (1ull << 30)) {
     r.Vpre = nullptr;

@@ -220,6 +220,7 @@ bool lane_engine_ok(const RunDev &r, const EnergyDev &en);
 void launch_hrss_lane(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc);
 // k_metric.cu: A5 metric (+ A9 termination when iterating)
 void launch_term_probe(const RunDev &r, const LaunchCtx &lc);
+void launch_dirs(const RunDev &r, const LaunchCtx &lc);  // k_dirs when r.Vpre (k_hrss.cu)
 void launch_smc_stage(const RunDev &r, double rho, double *cum, int *parents, float *Xsnap, float *Esnap,
                       const LaunchCtx &lc);
 void launch_chains_all(const RunDev &r, int *cdest, int *cpar, float *Xs, float *Es, const LaunchCtx &lc);
