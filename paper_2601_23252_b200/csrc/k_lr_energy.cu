@@ -69,10 +69,9 @@ struct Sched {
 };
 
 __global__ void __launch_bounds__(kThreads, 1)
-    k_lr_energy(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const float *y,
+    k_lr_energy(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 float *partial, int *slices_out, const int *n_probe_ptr, int *reset_counter, int p_stride,
                 int n_data, int n_tiles) {
-  (void)y;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sA = smem;
@@ -246,7 +245,7 @@ int lr_energy_splits() { return kSplits; }
 
 int lr_max_slices(int n_tiles) { return kColParts * n_tiles; }
 
-void launch_lr_energy(const CUtensorMap &tmA, const CUtensorMap &tmB, const float *y, float *partial, int *slices_out,
+void launch_lr_energy(const CUtensorMap &tmA, const CUtensorMap &tmB, float *partial, int *slices_out,
                       const int *n_probe, int *reset_counter, int p_stride, int n_data, const LaunchCtx &lc) {
   static bool attr = false;
   if (!attr) {
@@ -261,7 +260,7 @@ void launch_lr_energy(const CUtensorMap &tmA, const CUtensorMap &tmB, const floa
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int n_tiles = (n_data + BN - 1) / BN;
-  k_lr_energy<<<sms, kThreads, lr_energy_smem(), lc.stream>>>(tmA, tmB, y, partial, slices_out, n_probe, reset_counter,
+  k_lr_energy<<<sms, kThreads, lr_energy_smem(), lc.stream>>>(tmA, tmB, partial, slices_out, n_probe, reset_counter,
                                                              p_stride, n_data, n_tiles);
   ++*lc.launch_counter;
 }

@@ -13,7 +13,7 @@ namespace nss {
 
 size_t lr_energy_smem();
 int lr_max_slices(int n_tiles);
-void launch_lr_energy(const CUtensorMap &tmA, const CUtensorMap &tmB, const float *y, float *partial, int *slices_out,
+void launch_lr_energy(const CUtensorMap &tmA, const CUtensorMap &tmB, float *partial, int *slices_out,
                       const int *n_probe, int *reset_counter, int p_stride, int n_data, const LaunchCtx &lc);
 
 namespace {
@@ -100,20 +100,17 @@ cudaError_t lr_setup(LrEngine &L, const double *X, const double *y, long long N,
   // data slices per probe tile are chosen per round by the kernel (<= n_tiles)
   L.n_splits = lr_max_slices(L.n_tiles);
   std::vector<__nv_bfloat16> xb(static_cast<size_t>(L.n_pad) * 128, __float2bfloat16_rn(0.f));
-  std::vector<float> yf(static_cast<size_t>(L.n_pad), 0.f);
   std::vector<double> g64(128, 0.0);
   for (long long r = 0; r < N; ++r) {
     for (int k = 0; k < d; ++k) {
       xb[r * 128 + k] = __float2bfloat16_rn(static_cast<float>(X[r * d + k]));
       g64[k] += (0.5 - y[r]) * X[r * d + k];
     }
-    yf[r] = static_cast<float>(y[r]);
   }
   std::vector<float> gf(128);
   for (int k = 0; k < 128; ++k) gf[k] = static_cast<float>(g64[k]);
   cudaError_t e;
   if ((e = cudaMalloc(&L.Xb, xb.size() * sizeof(__nv_bfloat16)))) return e;
-  if ((e = cudaMalloc(&L.y, yf.size() * sizeof(float)))) return e;
   if ((e = cudaMalloc(&L.g, 128 * sizeof(float)))) return e;
   if ((e = cudaMemcpy(L.g, gf.data(), 128 * sizeof(float), cudaMemcpyHostToDevice))) return e;
   for (int q = 0; q < 2; ++q) {
@@ -125,7 +122,6 @@ cudaError_t lr_setup(LrEngine &L, const double *X, const double *y, long long N,
   if ((e = cudaMalloc(&L.slices, 2 * sizeof(int)))) return e;
   if ((e = cudaMemset(L.slices, 0, 2 * sizeof(int)))) return e;
   if ((e = cudaMemcpy(L.Xb, xb.data(), xb.size() * sizeof(__nv_bfloat16), cudaMemcpyHostToDevice))) return e;
-  if ((e = cudaMemcpy(L.y, yf.data(), yf.size() * sizeof(float), cudaMemcpyHostToDevice))) return e;
   if (!make_map(&L.tmB, L.Xb, L.n_pad)) return cudaErrorInvalidValue;
   for (int q = 0; q < 2; ++q)
     if (!make_map(&L.tmA[q], L.A[q], 3ll * L.p_stride)) return cudaErrorInvalidValue;
@@ -134,7 +130,6 @@ cudaError_t lr_setup(LrEngine &L, const double *X, const double *y, long long N,
 
 void lr_free(LrEngine &L) {
   cudaFree(L.Xb);
-  cudaFree(L.y);
   cudaFree(L.g);
   cudaFree(L.slices);
   for (int q = 0; q < 2; ++q) {
@@ -147,7 +142,7 @@ void lr_free(LrEngine &L) {
 // E[p] for the first *n_probe rows of P (row stride ldp, fp32).
 void lr_energies(const LrEngine &L, const float *P, int ldp, const int *n_probe, float *E, const LaunchCtx &lc) {
   k_split3<<<296, 256, 0, lc.stream>>>(P, ldp, n_probe, L.d, L.A[0], L.p_stride);
-  launch_lr_energy(L.tmA[0], L.tmB, L.y, L.partial[0], L.slices, n_probe, nullptr, L.p_stride,
+  launch_lr_energy(L.tmA[0], L.tmB, L.partial[0], L.slices, n_probe, nullptr, L.p_stride,
                    static_cast<int>(L.N), lc);
   k_lr_reduce<<<(L.max_probe + 255) / 256, 256, 0, lc.stream>>>(L.partial[0], L.p_stride, L.slices, n_probe, E, P, ldp,
                                                                   L.d, L.g);
@@ -155,7 +150,7 @@ void lr_energies(const LrEngine &L, const float *P, int ldp, const int *n_probe,
 }
 
 void lr_energy_pass(const LrEngine &L, int parity, const int *n_probe, int *reset_counter, const LaunchCtx &lc) {
-  launch_lr_energy(L.tmA[parity], L.tmB, L.y, L.partial[parity], L.slices + parity, n_probe, reset_counter,
+  launch_lr_energy(L.tmA[parity], L.tmB, L.partial[parity], L.slices + parity, n_probe, reset_counter,
                    L.p_stride, static_cast<int>(L.N), lc);
 }
 

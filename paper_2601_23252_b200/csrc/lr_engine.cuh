@@ -11,7 +11,6 @@ struct LrEngine {
   long long N = 0, n_pad = 0;
   int d = 0, n_tiles = 0, p_stride = 0, max_probe = 0, n_splits = 1;
   __nv_bfloat16 *Xb = nullptr;  // [n_pad][128] bf16 data rows (K padded with zeros)
-  float *y = nullptr;           // [n_pad] labels (0 past N)
   // linear part of the energy: sum_r (1/2 - y_r) a_r = theta . g, g = X^T (1/2 - y)
   // (fp64 on the host, 128 floats, zero past d); per-row values live in the
   // extra slot n_splits of partial[parity]
