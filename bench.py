@@ -393,6 +393,30 @@ def main():
     value = tot_evals / (t_max / 1e3)
     job_iters = iters if shard else iters * world
 
+    # ---- context only (not the metric): the same iterations back to back,
+    #      no flush and no per-step events, one event pair around the batch
+    bb = None
+    if not shard and world == 1:
+        s2 = new_run(seed=20_000)
+        for _ in range(3):
+            s2.step(sync=False)
+        s2.sync()
+        nb = min(args.steps, lim - 3)
+        ib0 = s2.info()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(nb):
+            s2.step(sync=False)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ib1 = s2.info()
+        ms_bb = a.elapsed_time(b)
+        bb = {"us_per_iteration": 1e3 * ms_bb / max(ib1["iteration"] - ib0["iteration"], 1),
+              "evals_per_s": (ib1["energy_evals"] - ib0["energy_evals"]) / (ms_bb / 1e3),
+              "what": f"{nb} iterations back to back, L2 warm, no per-step events (context, not the metric)"}
+        s2.close()
+
     # ---- end-to-end through the public API: init from host buffers, K steps
     #      each reading back its step info, evidence at the end ----
     s.close()
@@ -437,6 +461,7 @@ def main():
             "iterations_per_s": job_iters / (t_max / 1e3),
             "probes_per_s": tot_probes / (t_max / 1e3),
             "gpu_launches": launches,
+            "back_to_back": bb,
             "phase_ms_per_step": {nm: v[0] / max(args.steps, 1) for nm, v in ph_ms.items()},
             "roofline": roof,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": problem_bytes(prob) / e2e_steps,
