@@ -241,6 +241,51 @@ __device__ __forceinline__ float warp_energy(const float (&x)[NPL], const Energy
   }
 }
 
+// Correlated-Gaussian energy split over the WPC = 2 warps of a chain (large
+// d, factored form): both warps hold the same point; warp `sub` takes the
+// row blocks {0, 3} (sub 0) or {1, 2} (sub 1) of U -- balanced work, since
+// row block t only meets column segments >= t -- and the two partial sums
+// meet in shared memory behind a named barrier of the chain's 64 threads.
+// red: 4 floats per chain (two parities x two warps); `par` alternates per
+// call so one barrier per call suffices.  Identical result in both warps.
+template <int NPL>
+__device__ __forceinline__ float corr_energy_split(const float (&x)[NPL], const EnergyDev &en, const ESm &es,
+                                                   float *wbuf, float *red, int lane, int sub, int bar_id,
+                                                   int &par) {
+  const int d = en.d;
+#pragma unroll
+  for (int t = 0; t < NPL; ++t) {
+    const int i = lane + 32 * t;
+    if (i < d) wbuf[i] = x[t] - es.mu[i];  // both warps write the same values
+  }
+  __syncwarp();
+  float q = 0.f;
+#pragma unroll
+  for (int t = 0; t < NPL; ++t) {
+    const bool mine = (sub == 0) ? (t == 0 || t == 3) : (t == 1 || t == 2);
+    const int i = lane + 32 * t;
+    if (mine && i < d) {
+      const float *row = es.prec + i * es.ldp;
+      float a0 = 0.f, a1 = 0.f;
+      int m = 32 * t;
+      for (; m + 1 < d; m += 2) {
+        a0 = fmaf(row[m], wbuf[m], a0);
+        a1 = fmaf(row[m + 1], wbuf[m + 1], a1);
+      }
+      if (m < d) a0 = fmaf(row[m], wbuf[m], a0);
+      const float a = a0 + a1;
+      q = fmaf(a, a, q);
+    }
+  }
+  q = warp_sum(q);
+  if (lane == 0) red[par * 2 + sub] = q;
+  asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+  const float tot = red[par * 2] + red[par * 2 + 1];
+  par ^= 1;
+  __syncwarp();
+  return 0.5f * tot + en.c;
+}
+
 // log Pi(x) and support test (box: all lanes inside; Gaussian: always inside).
 template <int NPL>
 __device__ __forceinline__ float prior_logp(const float (&x)[NPL], const PriorDev &pr, const float (&pa)[NPL],

@@ -22,28 +22,39 @@ struct Probe {
   float lp;
 };
 
-template <int NPL, int KIND>
+// WPC warps per chain: 2 for the correlated Gaussian at large d (the energy
+// rows split over the two warps, corr_energy_split), else 1.  Every warp of a
+// chain runs the same control flow on the same values; warp 0 writes.
+template <int NPL, int KIND, int WPC>
 __global__ void __launch_bounds__(256) k_hrss(RunDev r, PriorDev pr, EnergyDev en) {
   extern __shared__ float sm[];
   __shared__ int sh_flag;
-  const int d = r.d, lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  __shared__ float sh_red[8 * 4];
+  const int d = r.d, lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = (blockDim.x >> 5) / WPC;
+  const int sub = wib % WPC, cib = wib / WPC;  // warp within the chain, chain within the block
   const int ldl = odd_stride(d);
+  const bool stage_l = r.Vpre == nullptr;  // L only for in-chain directions
   float *sL = sm;
-  float *sP = sL + d * ldl;
+  float *sP = sL + (stage_l ? d * ldl : 0);
   const int npar = energy_param_floats(KIND, d, en.n_comp);
   float *sZ = sP + npar + wib * (2 * NPL * 32);
   float *sY = sZ + NPL * 32;
   if (threadIdx.x == 0) sh_flag = (r.st->terminated || r.st->error || r.st->finalised) ? 1 : 0;
-  for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
-    int i = e / d, j = e - i * d;
-    sL[i * ldl + j] = r.L[i * r.dp + j];
-  }
+  if (stage_l)
+    for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
+      int i = e / d, j = e - i * d;
+      sL[i * ldl + j] = r.L[i * r.dp + j];
+    }
   ESm es;
   stage_energy(en, sP, es);
   __syncthreads();
   if (sh_flag) return;
-  const int c = r.c0 + blockIdx.x * wpb + wib;
-  if (c >= r.c1) return;
+  const int c = r.c0 + blockIdx.x * wpb + cib;
+  if (c >= r.c1) return;  // uniform over the chain's warps
+  float *wred = sh_red + cib * 4;
+  int epar = 0;
+  (void)wred;
+  (void)epar;
 
   DevState *st = r.st;
   const uint32_t it = static_cast<uint32_t>(st->iter)  /* set by the select kernel */;
@@ -138,7 +149,13 @@ __global__ void __launch_bounds__(256) k_hrss(RunDev r, PriorDev pr, EnergyDev e
       bool inside;
       float lpp = prior_logp<NPL>(xp, pr, pa, pb, lane, d, inside);
       if (!inside || (!tempered && !(lpp >= log_y))) return false;
-      float ep = warp_energy<NPL, KIND>(xp, en, es, sY, lane);
+      float ep;
+      if constexpr (WPC == 2 && KIND == NSS_E_CORR_GAUSS) {
+        ep = es.tri ? corr_energy_split<NPL>(xp, en, es, sY - sub * (2 * NPL * 32), wred, lane, sub, 1 + cib, epar)
+                    : warp_energy<NPL, KIND>(xp, en, es, sY, lane);
+      } else {
+        ep = warp_energy<NPL, KIND>(xp, en, es, sY, lane);
+      }
       ++n_eval;
       if (isnan(ep)) {
         if (lane == 0) raise_error(st, NSS_ERR_NAN);
@@ -182,13 +199,14 @@ __global__ void __launch_bounds__(256) k_hrss(RunDev r, PriorDev pr, EnergyDev e
     n_exp += nl + nr;
     n_shr += ns;
     n_null += acc ? 0 : 1;
-    if (lane == 0)
+    if (lane == 0 && sub == 0)
       r.counts[static_cast<long long>(c) * p + j] =
           static_cast<uint32_t>(nl) | (static_cast<uint32_t>(nr) << 8) | (static_cast<uint32_t>(ns) << 16) |
           (static_cast<uint32_t>(acc) << 24);
   }
 
   // ---- replace ----
+  if (sub != 0) return;
 #pragma unroll
   for (int t = 0; t < NPL; ++t) {
     const int i = lane + 32 * t;
@@ -452,24 +470,37 @@ __global__ void __launch_bounds__(256) k_init(RunDev r, PriorDev pr, EnergyDev e
   }
 }
 
-template <int NPL, int KIND>
-void launch_hrss_t(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc) {
+template <int NPL, int KIND, int WPC>
+void launch_hrss_w(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc) {
   const int ldl = odd_stride(r.d);
   const int nc = r.c1 - r.c0;
   if (nc <= 0) return;
-  int wpb = nc / 296;
-  wpb = wpb < 1 ? 1 : (wpb > 8 ? 8 : wpb);
-  const size_t smem = (static_cast<size_t>(r.d) * ldl + energy_param_floats(KIND, r.d, en.n_comp) +
-                       static_cast<size_t>(wpb) * 2 * NPL * 32) * sizeof(float);
+  int wpb = nc / 296;  // chains per block
+  wpb = wpb < 1 ? 1 : (wpb > 8 / WPC ? 8 / WPC : wpb);
+  const size_t sl = r.Vpre ? 0 : static_cast<size_t>(r.d) * ldl;
+  const size_t smem = (sl + energy_param_floats(KIND, r.d, en.n_comp) +
+                       static_cast<size_t>(wpb) * WPC * 2 * NPL * 32) * sizeof(float);
   static size_t attr = 0;
   if (smem > 48 * 1024 && attr < smem) {
-    cudaFuncSetAttribute(k_hrss<NPL, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(k_hrss<NPL, KIND, WPC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
     attr = smem;
   }
   const int blocks = (nc + wpb - 1) / wpb;
-  NSS_PIN_CARVEOUT((k_hrss<NPL, KIND>));
-  k_hrss<NPL, KIND><<<blocks, wpb * 32, smem, lc.stream>>>(r, pr, en);
+  NSS_PIN_CARVEOUT((k_hrss<NPL, KIND, WPC>));
+  k_hrss<NPL, KIND, WPC><<<blocks, wpb * WPC * 32, smem, lc.stream>>>(r, pr, en);
   ++*lc.launch_counter;
+}
+
+template <int NPL, int KIND>
+void launch_hrss_t(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc) {
+  if constexpr (KIND == NSS_E_CORR_GAUSS && NPL >= 2) {
+    if (en.ufac) {  // factored energy: rows split over two warps per chain
+      launch_hrss_w<NPL, KIND, 2>(r, pr, en, lc);
+      return;
+    }
+  }
+  launch_hrss_w<NPL, KIND, 1>(r, pr, en, lc);
 }
 
 template <int NPL, int KIND>
