@@ -45,6 +45,7 @@ METRIC = "constrained energy evals/sec"
 UNIT = "evals/s"
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 TRAFFIC_PATH = os.path.join(ROOT, "profiles", "traffic.json")
+FP64_PATH = os.path.join(ROOT, "profiles", "r01_measured_fp64_tf32.json")  # scripts/fp64_peak.py (cuBLAS DGEMM)
 N_SM = 148
 FP32_LANES, FP64_LANES = 128, 64  # per SM per clock (FMA units)
 RUN_LIMIT = {"C1": 40, "C2": 200, "C3a": 60, "C3b": 60, "C4": 20, "C5": 4}
@@ -506,9 +507,13 @@ def roofline(prob, engine, ph_ms, alg_flops, peaks, traffic, mhz, step_ms, evals
         src = "bf16_tflops_sustained of measured (MEASURED_PEAKS.json)" if "bf16_tflops_sustained" in peaks \
             else "1.4 PFLOP/s sustained of fallback"
     else:
-        peak = N_SM * FP64_LANES * 2 * mhz * 1e6 / 1e12
-        bound, kname = "alu", "k_gp_energy"
-        src = f"148 SM x 64 FP64 lanes x 2 x {mhz:.0f} MHz (derived)"
+        fp64 = read_json(FP64_PATH).get("fp64_tflops")
+        bound, kname = "tensor", "k_gp_energy"  # DMMA (fp64 tensor) trailing updates and TRSM
+        if fp64:
+            peak, src = fp64, "fp64 cuBLAS DGEMM of measured (profiles/r01_measured_fp64_tf32.json)"
+        else:
+            peak = N_SM * FP64_LANES * 2 * mhz * 1e6 / 1e12
+            src = f"148 SM x 64 FP64 lanes x 2 x {mhz:.0f} MHz (derived)"
     achieved = evals * flops_per_row / (en_ms / 1e3) / 1e12 if en_ms > 0 else 0.0
     return {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "traffic": traffic.get(kname), "kernel": kname, "kernel_ms_avg": en_ms / max(en_n, 1),
