@@ -358,7 +358,13 @@ __global__ void __launch_bounds__(kThreads) k_select_smem(RunDev r, bool rows) {
   int *surv = reinterpret_cast<int *>(sorted + k);  // n - k
   int *dest = surv + (n - k);                        // k
   if (tid == 0) st->stamp[0] = global_ns();
-  // independent global loads first, flags checked afterwards
+  // independent global loads first, flags checked afterwards; thread 0 also
+  // fetches the evidence state the termination test needs (cold after a flush)
+  double lx0 = 0.0, lz0 = 0.0;
+  if (tid == 0) {
+    lx0 = r.lx_cur[0];
+    lz0 = r.lz[0];
+  }
   unsigned long long mn = ~0ull, mx = 0ull;
   for (int g = tid; g < n; g += blockDim.x) {
     const unsigned long long key = key_of(r.E[g], g);
@@ -373,7 +379,7 @@ __global__ void __launch_bounds__(kThreads) k_select_smem(RunDev r, bool rows) {
   if (tid == 0) st->stamp[1] = global_ns();
   block_minmax(mn, mx, red);
   // A9 before the iteration (R-19), then the capacity rule (R-26)
-  if (tid == 0) sh_kk = term_check(r, st, energy_of_key(mn)) ? 1 : (nd + k + n > r.max_dead ? 2 : 0);
+  if (tid == 0) sh_kk = term_check_v(r, st, energy_of_key(mn), lx0, lz0) ? 1 : (nd + k + n > r.max_dead ? 2 : 0);
   __syncthreads();
   if (sh_kk) {
     if (sh_kk == 2 && tid == 0) raise_error(st, NSS_ERR_CAPACITY);

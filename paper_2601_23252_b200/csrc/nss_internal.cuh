@@ -169,9 +169,8 @@ __device__ __forceinline__ void raise_error(DevState *st, int code) { atomicCAS(
 // log X (replica 0) is below e^{term} of log Z_0 + Z_live.  Evaluated before
 // each iteration by the select kernel (one thread) and by k_term_probe when
 // the host asks; records E_min and log Z_live; returns the decision.
-__device__ inline bool term_check(const RunDev &r, DevState *st, float emin) {
-  const double lz_live = -static_cast<double>(emin) + r.lx_cur[0];
-  const double lz0 = r.lz[0];
+__device__ inline bool term_check_v(const RunDev &r, DevState *st, float emin, double lx0, double lz0) {
+  const double lz_live = -static_cast<double>(emin) + lx0;
   const double mm = fmax(lz0, lz_live);
   const double tot = (mm == -INFINITY) ? -INFINITY : mm + log(exp(lz0 - mm) + exp(lz_live - mm));
   const bool stop = st->n_dead > 0 && (lz_live - tot) < static_cast<double>(r.term_log_ratio);
@@ -179,6 +178,9 @@ __device__ inline bool term_check(const RunDev &r, DevState *st, float emin) {
   st->log_z_live = lz_live;
   if (stop) st->terminated = 1;
   return stop;
+}
+__device__ inline bool term_check(const RunDev &r, DevState *st, float emin) {
+  return term_check_v(r, st, emin, r.lx_cur[0], r.lz[0]);
 }
 
 // ----------------------------------------------------------------------------
