@@ -43,6 +43,8 @@ struct nss_ctx {
   PriorDev pr{};
   EnergyDev en{};
   std::vector<void *> allocs;
+  char *arena = nullptr;  // current small-allocation arena (dalloc)
+  size_t arena_used = 0;
   double *partials = nullptr;
   unsigned *ticket = nullptr;   // last-block-done counter of k_metric
   cudaStream_t side = nullptr;  // evidence runs here, concurrently with HRSS
@@ -56,6 +58,7 @@ struct nss_ctx {
   bool term_stale = false;
   int nblk = 1;
   double *summary = nullptr;  // device: [mean, std, closed lz_0..R]
+  void *h_block = nullptr;    // one pinned allocation for all host mirrors below
   DevState *h_st = nullptr;   // pinned mirror of the device state
   int *h_one = nullptr;       // pinned constant 1 (finalised flag)
   double *h_lz0 = nullptr;    // pinned mirror of replica 0's log Z (step info)
@@ -87,7 +90,7 @@ struct nss_ctx {
   std::vector<double> lr_x, lr_y;
   cudaGraphExec_t round_graph = nullptr;
   long long round_graph_launches = 0;
-  int *h_nprobe = nullptr;  // pinned
+  int *h_nprobe = nullptr;  // pinned (inside h_block)
   void *gp = nullptr;       // fp64 batched GP marginal likelihood (k_gp.cu)
   // multi-GPU (dist.cu): chain block [r.c0, r.c1) of kc chains, NCCL all-gather of new rows
   void *comm = nullptr;
@@ -123,15 +126,37 @@ nss_status exchange(nss_ctx *c);
     }                                                                              \
   } while (0)
 
+// Zeroed device memory owned by the context.  Small requests are carved from
+// 16 MB arenas (one cudaMalloc + memset each: nss_init makes dozens of
+// allocations), large ones get their own; 256-byte alignment throughout.
 template <class T>
 nss_status dalloc(nss_ctx *c, T **p, size_t count) {
+  const size_t bytes = (count * sizeof(T) + 16 + 255) & ~size_t(255);
+  constexpr size_t kArena = size_t(16) << 20;
+  if (bytes <= kArena / 8) {
+    if (!c->arena || c->arena_used + bytes > kArena) {
+      void *q = nullptr;
+      cudaError_t e = cudaMalloc(&q, kArena);
+      if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        return fail(c, NSS_ERR_OOM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+      }
+      cudaMemset(q, 0, kArena);
+      c->allocs.push_back(q);
+      c->arena = static_cast<char *>(q);
+      c->arena_used = 0;
+    }
+    *p = reinterpret_cast<T *>(c->arena + c->arena_used);
+    c->arena_used += bytes;
+    return NSS_OK;
+  }
   void *q = nullptr;
-  cudaError_t e = cudaMalloc(&q, count * sizeof(T) + 16);
+  cudaError_t e = cudaMalloc(&q, bytes);
   if (e != cudaSuccess) {
     (void)cudaGetLastError();
     return fail(c, NSS_ERR_OOM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
   }
-  cudaMemset(q, 0, count * sizeof(T) + 16);
+  cudaMemset(q, 0, bytes);
   c->allocs.push_back(q);
   *p = static_cast<T *>(q);
   return NSS_OK;
@@ -358,7 +383,7 @@ nss_status ensure_batch(nss_ctx *c) {
     for (int q = 0; q < 2; ++q)
       if ((s = dalloc(c, &b.P[q], static_cast<size_t>(b.max_rows) * c->dp))) return s;
     if ((s = dalloc(c, &b.n_probe, 2))) return s;
-    if (cudaMallocHost(&c->h_nprobe, sizeof(int)) != cudaSuccess) return fail(c, NSS_ERR_CUDA, "cudaMallocHost");
+    // c->h_nprobe lives in the pinned block allocated by nss_init
     c->batch_alloc = true;
   }
   if (backend == 2) {
@@ -634,9 +659,15 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) return bail(NSS_ERR_CUDA);
     c->own_stream = true;
   }
-  if (cudaMallocHost(&c->h_st, sizeof(DevState)) != cudaSuccess) return bail(NSS_ERR_CUDA);
-  if (cudaMallocHost(&c->h_one, sizeof(int)) != cudaSuccess) return bail(NSS_ERR_CUDA);
-  if (cudaMallocHost(&c->h_lz0, sizeof(double)) != cudaSuccess) return bail(NSS_ERR_CUDA);
+  // one page-locked block for the host mirrors (page locking is slow: one call)
+  if (cudaMallocHost(&c->h_block, 4096) != cudaSuccess) return bail(NSS_ERR_CUDA);
+  {
+    char *hb = static_cast<char *>(c->h_block);
+    c->h_st = reinterpret_cast<DevState *>(hb);
+    c->h_lz0 = reinterpret_cast<double *>(hb + ((sizeof(DevState) + 63) & ~size_t(63)));
+    c->h_one = reinterpret_cast<int *>(reinterpret_cast<char *>(c->h_lz0) + 64);
+    c->h_nprobe = c->h_one + 16;
+  }
   *c->h_lz0 = -INFINITY;
   if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess) return bail(NSS_ERR_CUDA);
   if (cudaEventCreateWithFlags(&c->ev_sel, cudaEventDisableTiming) != cudaSuccess) return bail(NSS_ERR_CUDA);
@@ -1092,16 +1123,14 @@ NSS_API nss_status nss_destroy(nss_ctx *c) {
   if (c->lr.Xb) lr_free(c->lr);
   if (c->gp) gp_free(c->gp);
   if (c->comm) nccl_comm_free(c->comm);
-  if (c->h_nprobe) cudaFreeHost(c->h_nprobe);
+
   for (void *p : c->allocs) cudaFree(p);
   for (auto e : c->ev_free) cudaEventDestroy(e);
   for (auto &t : c->ev_pending) {
     cudaEventDestroy(t.a);
     cudaEventDestroy(t.b);
   }
-  if (c->h_st) cudaFreeHost(c->h_st);
-  if (c->h_one) cudaFreeHost(c->h_one);
-  if (c->h_lz0) cudaFreeHost(c->h_lz0);
+  if (c->h_block) cudaFreeHost(c->h_block);
   if (c->side) { cudaStreamSynchronize(c->side); cudaStreamDestroy(c->side); }
   if (c->ev_sel) cudaEventDestroy(c->ev_sel);
   if (c->ev_evid) cudaEventDestroy(c->ev_evid);
