@@ -288,9 +288,12 @@ __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials,
 // A9 / R-19 on demand (the host asks for the run's state between
 // iterations): minimum live energy, then the same test the next select
 // kernel would make.
-__global__ void __launch_bounds__(kThreads) k_term_probe(RunDev r) {
+// With `mirror` (host-mapped pinned memory) it then writes the device state
+// and replica 0's log Z there, so reading the state costs the host one
+// kernel and one synchronisation, no copies.
+__global__ void __launch_bounds__(kThreads) k_term_probe(RunDev r, int probe, DevState *mirror, double *lz0_mirror) {
   DevState *st = r.st;
-  if (st->error || st->finalised || st->terminated) return;
+  if (probe && !(st->error || st->finalised || st->terminated)) {
   __shared__ float red[kThreads / 32];
   float emin = INFINITY;
   for (int g = threadIdx.x; g < r.n; g += blockDim.x) emin = fminf(emin, r.E[g]);
@@ -301,6 +304,15 @@ __global__ void __launch_bounds__(kThreads) k_term_probe(RunDev r) {
     for (int w = 1; w < kThreads / 32; ++w) emin = fminf(emin, red[w]);
     emin = fminf(emin, red[0]);
     term_check(r, st, emin);
+  }
+  }
+  if (mirror) {
+    __syncthreads();
+    const unsigned *src = reinterpret_cast<const unsigned *>(st);
+    unsigned *dst = reinterpret_cast<unsigned *>(mirror);
+    for (int i = threadIdx.x; i < static_cast<int>(sizeof(DevState) / 4); i += blockDim.x) dst[i] = src[i];
+    if (threadIdx.x == 0) *lz0_mirror = r.lz[0];
+    __threadfence_system();
   }
 }
 
@@ -328,8 +340,8 @@ int metric_blocks(int n, int d) {
   return b < 1 ? 1 : b;
 }
 
-void launch_term_probe(const RunDev &r, const LaunchCtx &lc) {
-  k_term_probe<<<1, kThreads, 0, lc.stream>>>(r);
+void launch_term_probe(const RunDev &r, const LaunchCtx &lc, int probe, DevState *mirror, double *lz0_mirror) {
+  k_term_probe<<<1, kThreads, 0, lc.stream>>>(r, probe, mirror, lz0_mirror);
   ++*lc.launch_counter;
 }
 

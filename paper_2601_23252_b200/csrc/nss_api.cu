@@ -58,7 +58,9 @@ struct nss_ctx {
   bool term_stale = false;
   int nblk = 1;
   double *summary = nullptr;  // device: [mean, std, closed lz_0..R]
-  void *h_block = nullptr;    // one pinned allocation for all host mirrors below
+  void *h_block = nullptr;    // one pinned (host-mapped) allocation for all host mirrors below
+  DevState *d_h_st = nullptr;  // device aliases of h_st / h_lz0 (mapped)
+  double *d_h_lz0 = nullptr;
   DevState *h_st = nullptr;   // pinned mirror of the device state
   int *h_one = nullptr;       // pinned constant 1 (finalised flag)
   double *h_lz0 = nullptr;    // pinned mirror of replica 0's log Z (step info)
@@ -222,14 +224,23 @@ nss_status device_error(nss_ctx *c) {
   return NSS_OK;
 }
 
+// The device state into the host mirror: one kernel (A9 at the end of the
+// last enqueued iteration when stale, R-19) that also writes the state into
+// host-mapped pinned memory, then a synchronisation.
 nss_status pull_state(nss_ctx *c) {
-  if (c->term_stale) {  // A9 at the end of the last enqueued iteration (R-19)
-    LaunchCtx lc{c->stream, &c->launches};
-    launch_term_probe(c->r, lc);
+  LaunchCtx lc{c->stream, &c->launches};
+  if (c->d_h_st && c->r.lz) {
+    launch_term_probe(c->r, lc, c->term_stale ? 1 : 0, c->d_h_st, c->d_h_lz0);
     c->term_stale = false;
+    CK(cudaGetLastError());
+  } else {
+    if (c->term_stale) {
+      launch_term_probe(c->r, lc);
+      c->term_stale = false;
+    }
+    CK(cudaMemcpyAsync(c->h_st, c->r.st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
+    if (c->r.lz) CK(cudaMemcpyAsync(c->h_lz0, c->r.lz, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   }
-  CK(cudaMemcpyAsync(c->h_st, c->r.st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
-  if (c->r.lz) CK(cudaMemcpyAsync(c->h_lz0, c->r.lz, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   return NSS_OK;
 }
@@ -660,13 +671,19 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
     c->own_stream = true;
   }
   // one page-locked block for the host mirrors (page locking is slow: one call)
-  if (cudaMallocHost(&c->h_block, 4096) != cudaSuccess) return bail(NSS_ERR_CUDA);
+  if (cudaHostAlloc(&c->h_block, 4096, cudaHostAllocMapped) != cudaSuccess) return bail(NSS_ERR_CUDA);
   {
     char *hb = static_cast<char *>(c->h_block);
     c->h_st = reinterpret_cast<DevState *>(hb);
     c->h_lz0 = reinterpret_cast<double *>(hb + ((sizeof(DevState) + 63) & ~size_t(63)));
     c->h_one = reinterpret_cast<int *>(reinterpret_cast<char *>(c->h_lz0) + 64);
     c->h_nprobe = c->h_one + 16;
+    void *dp = nullptr;
+    if (cudaHostGetDevicePointer(&dp, c->h_block, 0) == cudaSuccess) {
+      c->d_h_st = static_cast<DevState *>(dp);
+      c->d_h_lz0 = reinterpret_cast<double *>(static_cast<char *>(dp) + (reinterpret_cast<char *>(c->h_lz0) -
+                                                                         static_cast<char *>(c->h_block)));
+    }
   }
   *c->h_lz0 = -INFINITY;
   if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess) return bail(NSS_ERR_CUDA);

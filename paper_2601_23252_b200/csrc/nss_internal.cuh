@@ -221,7 +221,8 @@ int hrss_engine(const RunDev &r, const EnergyDev &en);  // 0 warp-cooperative, 1
 bool lane_engine_ok(const RunDev &r, const EnergyDev &en);
 void launch_hrss_lane(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc);
 // k_metric.cu: A5 metric (+ A9 termination when iterating)
-void launch_term_probe(const RunDev &r, const LaunchCtx &lc);
+void launch_term_probe(const RunDev &r, const LaunchCtx &lc, int probe = 1, DevState *mirror = nullptr,
+                       double *lz0_mirror = nullptr);
 void launch_dirs(const RunDev &r, const LaunchCtx &lc);  // k_dirs when r.Vpre (k_hrss.cu)
 void launch_smc_stage(const RunDev &r, double rho, double *cum, int *parents, float *Xsnap, float *Esnap,
                       const LaunchCtx &lc);
