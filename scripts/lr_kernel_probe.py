@@ -9,6 +9,8 @@ import numpy as np  # noqa: E402
 from paper_2601_23252_b200 import nss, workloads as W  # noqa: E402
 
 P = int(sys.argv[1]) if len(sys.argv) > 1 else 8000
+if len(sys.argv) > 2:  # a variant library (scripts/build_lr_variants.sh)
+    nss.LIB_PATH = os.path.abspath(sys.argv[2])
 prob = W.logreg(100, 10_000)
 theta = np.random.default_rng(1).standard_normal((P, 100)) * 0.3
 os.environ.setdefault("NSS_LR_REPS", "50")
