@@ -25,8 +25,11 @@ namespace nss {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int PB = 64;       // panel width = trailing-update tile edge
-constexpr int LDR = PB + 4;  // row-major panel tile stride: 68 = 4 mod 16 -> conflict-free DMMA fragments
+constexpr int PB = 64;        // block edge: column blocks of L and the output tiles
+constexpr int LDR = PB + 4;   // stride of the 64 x 64 shared tiles: 68 = 4 mod 16 -> conflict-free DMMA fragments
+constexpr int KC = 32;        // k-chunk width of the stored L tiles
+constexpr int LDC = KC + 4;   // stride of a stored / staged chunk tile (36 = 4 mod 16)
+constexpr int CT = PB * LDC;  // doubles per chunk tile (18 KB)
 constexpr double kLn2Pi = 1.8378770664093454836;
 
 struct GpDev {
@@ -34,8 +37,9 @@ struct GpDev {
   const double *X;  // N x D inputs
   const double *y;  // N targets
   double jitter;
-  double *scratch;  // per CTA slot: (N+1) x N
+  double *scratch;  // per CTA slot: nrb x nkc chunk tiles of L
   double *e64;      // optional fp64 copy of the energies (nss_gp_energy_batch)
+  int nrb, nkc;     // row blocks of [L; alpha^T] (N + 1 rows), 32-wide chunks per row block
 };
 
 __device__ __forceinline__ double block_sum(double v, double *red) {
@@ -49,19 +53,14 @@ __device__ __forceinline__ double block_sum(double v, double *red) {
   return s;
 }
 
-// rows [r0, r0+rows) x panel columns [k0, k0+kb) of A -> row-major tile T[r][c]
-// with asynchronous 16-B copies (zero-filled past the edges); the caller
-// commits and waits (cp.async.commit_group / wait_group).
-__device__ __forceinline__ void load_panel_tile(double *T, const double *A, int lda, int r0, int rows, int k0,
-                                                int kb) {
-  constexpr int G = PB / 2;  // 16-B granules per tile row
-  for (int e = threadIdx.x; e < PB * G; e += kThreads) {
-    const int r = e / G, c = 2 * (e - r * G);
-    const int valid = (r < rows) ? max(0, min(2, kb - c)) : 0;
-    const double *src = valid ? A + static_cast<long long>(r0 + r) * lda + k0 + c : A;
-    const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(T + r * LDR + c));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid * 8)
-                 : "memory");
+// the first `rows` rows of a stored chunk tile (contiguous, already in the
+// padded shared layout) -> shared memory with 16-B asynchronous copies; the
+// caller commits and waits
+__device__ __forceinline__ void load_chunk(double *dst, const double *src, int rows) {
+  const int ng = rows * (LDC / 2);
+  for (int e = threadIdx.x; e < ng; e += kThreads) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst + 2 * e));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + 2 * e) : "memory");
   }
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
@@ -76,42 +75,72 @@ __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-// acc(32 x 16 per warp) += Ta(rows) . Tb(rows)^T over k < kb: 4 x 2 DMMA
-// 8x8 tiles, operand rows at m_base / n_base of the row-major tiles
+// acc(32 x 16 per warp) += Ta(rows) . Tb(rows)^T over k < KB (KB = 0: kb at
+// run time): 4 x 2 DMMA 8x8 tiles, operand rows at m_base / n_base of
+// row-major tiles of stride LD; only the first mcnt 8-row groups of the warp
+// (warp-uniform) are computed
+template <int LD, int KB>
 __device__ __forceinline__ void mma_rows(const double *Ta, const double *Tb, int kb, int m_base, int n_base, int gq,
-                                         int tq, double (&acc)[4][2][2]) {
-  const double *pa = Ta + (m_base + gq) * LDR + tq;
-  const double *pb = Tb + (n_base + gq) * LDR + tq;
+                                         int tq, int mcnt, double (&acc)[4][2][2]) {
+  const double *pa = Ta + (m_base + gq) * LD + tq;
+  const double *pb = Tb + (n_base + gq) * LD + tq;
+  const int kend = KB ? KB : kb;
+  if (mcnt >= 4) {
 #pragma unroll 4
-  for (int c = 0; c < kb; c += 4) {
-    double av[4], bv[2];
+    for (int c = 0; c < kend; c += 4) {
+      double av[4], bv[2];
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi) av[mi] = pa[8 * mi * LDR + c];
+      for (int mi = 0; mi < 4; ++mi) av[mi] = pa[8 * mi * LD + c];
 #pragma unroll
-    for (int ni = 0; ni < 2; ++ni) bv[ni] = pb[8 * ni * LDR + c];
+      for (int ni = 0; ni < 2; ++ni) bv[ni] = pb[8 * ni * LD + c];
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
+      for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-      for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], av[mi], bv[ni]);
+        for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], av[mi], bv[ni]);
+    }
+  } else if (mcnt > 0) {
+    for (int c = 0; c < kend; c += 4) {
+      double bv[2];
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni) bv[ni] = pb[8 * ni * LD + c];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+        if (mi < mcnt) {
+          const double a = pa[8 * mi * LD + c];
+#pragma unroll
+          for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a, bv[ni]);
+        }
+    }
   }
 }
 
+// Left-looking blocked Cholesky of the (N+1) x N lower trapezoid [K; y^T]
+// (its last row becomes alpha^T = (L^-1 y)^T).  For each 64-wide column
+// block j and each row block i >= j, the 64 x 64 tile
+//   T = [K; y^T](i, j) - L(i, :j) L(j, :j)^T
+// is accumulated in registers on the DMMA tensor cores from the stored L
+// chunk tiles (double-buffered cp.async stream, each output tile read and
+// written exactly once), K(i, j) is generated on the fly from X (never
+// stored), then the diagonal tile is factorised in shared memory (one barrier
+// per column) with its inverse W = L_jj^-1, and each tile below it becomes
+// L(i, j) = T W^T (DMMA), stored as two 64 x 32 chunk tiles.
 __global__ void __launch_bounds__(kThreads, 2) k_gp_energy(GpDev g, BatchDev b, int parity, int dp) {
   extern __shared__ double sm[];
   const int N = g.N, D = g.D, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int lda = (N + 1) & ~1;  // even row stride: 16-B aligned panel granules for cp.async
   if (blockIdx.x == 0 && tid == 0) b.n_probe[parity ^ 1] = 0;  // the next round's row counter
   const int n = b.n_probe[parity];
   if (static_cast<int>(blockIdx.x) >= n) return;
-  double *Ti = sm;                // PB x LDR: panel rows of the current row block (then its X rows)
-  double *Tj = Ti + PB * LDR;     // PB x LDR: X rows of an earlier row block; the diagonal block first
-  double *W = Tj + PB * LDR;      // PB x LDR: L_kk^-1 (lower), zero above the diagonal and past kb
-  double *diag = W + PB * LDR;    // PB: L_cc
-  double *red = diag + PB;        // 8
+  double *Ci = sm;            // 2 x CT: chunks of row block i (stage buffers); T aliases them
+  double *Cj = Ci + 2 * CT;   // 2 x CT: chunks of row block j
+  double *W = Cj + 2 * CT;    // PB x LDR: L_jj^-1 (lower), zero above the diagonal and past kb
+  double *diag = W + PB * LDR;  // PB: L_cc
+  double *red = diag + PB;      // 8
+  double *T = Ci;               // PB x LDR (4352 <= 2 CT doubles)
   __shared__ double sh_par[NSS_MAX_DIM + 2];
   __shared__ int sh_fail;
-  double *A = g.scratch + static_cast<long long>(blockIdx.x) * (N + 1) * lda;
-  double *Lkk = Tj;
+  const long long slot = static_cast<long long>(g.nrb) * g.nkc * CT;
+  double *Ls = g.scratch + static_cast<long long>(blockIdx.x) * slot;
+  const int nkc = g.nkc, nrb = g.nrb, ncb = (N + PB - 1) / PB;
   const int ty = tid >> 4, tx = tid & 15;  // diagonal-block owner map
   // DMMA warp tiles: warp (wr, wc) owns rows 32 wr .. +32, columns 16 wc .. +16
   const int m_base = (wid >> 2) * 32, n_base = (wid & 3) * 16, gq = lane >> 2, tq = lane & 3;
@@ -124,206 +153,193 @@ __global__ void __launch_bounds__(kThreads, 2) k_gp_energy(GpDev g, BatchDev b, 
     if (tid == 0) sh_fail = 0;
     __syncthreads();
     const double sf2 = sh_par[D], diag_add = sh_par[D + 1] + g.jitter;
-    // ---- build [K; y^T] (lower trapezoid) ----
-    for (int i = wid; i <= N; i += kThreads / 32) {
-      double *row = A + static_cast<long long>(i) * lda;
-      if (i == N) {
-        for (int j = lane; j < N; j += 32) row[j] = g.y[j];
-        continue;
-      }
-      for (int j = lane; j <= i; j += 32) {
-        double s = 0.0;
-        for (int q = 0; q < D; ++q) {
-          const double t = (__ldg(g.X + i * D + q) - __ldg(g.X + j * D + q)) * sh_par[q];
-          s = fma(t, t, s);
-        }
-        row[j] = sf2 * exp(-0.5 * s) + (i == j ? diag_add : 0.0);
-      }
-    }
-    __syncthreads();
     double logdet_part = 0.0;  // lane-held sums of log pivots (warp 0)
-    for (int k0 = 0; k0 < N; k0 += PB) {
-      const int kb = min(PB, N - k0);
-      // 1. diagonal block -> shared memory; all threads, one barrier per
-      //    column: column j updates the block with its unscaled values
-      //    (A_rl -= A_rj A_lj / A_jj) while column j-1 is scaled by 1/L_{j-1,j-1};
-      //    thread (ty, tx) owns rows ty + 16 u and columns tx + 16 v
-      for (int e = tid; e < PB * PB; e += kThreads) {
-        const int r = e / PB, c = e - r * PB;
-        Lkk[r * LDR + c] = (r < kb && c <= r) ? A[static_cast<long long>(k0 + r) * lda + k0 + c] : 0.0;
-      }
-      __syncthreads();
-      bool bad = false;  // uniform: every thread reads the same pivot
-      for (int j = 0; j < kb; ++j) {
-        const double ajj = Lkk[j * LDR + j];
-        if (!(ajj > 0.0)) {
-          bad = true;
-          if (tid == 0) sh_fail = 1;
-          break;
-        }
-        const double iajj = 1.0 / ajj;
-        if (j > 0) {
-          const double ipm = 1.0 / diag[j - 1];
-          for (int r = j + tid; r < kb; r += kThreads) Lkk[r * LDR + j - 1] *= ipm;
-        }
-        if (tid == 0) diag[j] = sqrt(ajj);
-        double cj[4];
+    double alpha2 = 0.0;       // thread-held sums of alpha_c^2
+    for (int j = 0; j < ncb && !sh_fail; ++j) {
+      const int j0 = j * PB, kb = min(PB, N - j0), nch = 2 * j;
+      const int kr = (kb + 3) & ~3;  // DMMA k range of the W product (W and T zero past kb)
+      for (int i = j; i < nrb; ++i) {
+        const int i0 = i * PB, rows = min(PB, N + 1 - i0);
+        const bool dt = i == j;
+        const int mcnt = min(4, max(0, (rows - m_base + 7) >> 3));
+        double acc[4][2][2];
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const int l = tx + 16 * v;
-          cj[v] = (l > j && l < kb) ? Lkk[l * LDR + j] * iajj : 0.0;
-        }
+        for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int r = ty + 16 * u;
-          if (r > j && r < kb) {
-            const double arj = Lkk[r * LDR + j];
+          for (int ni = 0; ni < 2; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+        // ---- acc = L(i, :j) L(j, :j)^T over 32-wide chunks ----
+        if (nch > 0) {
+          const double *Li = Ls + static_cast<long long>(i) * nkc * CT;
+          const double *Lj = Ls + static_cast<long long>(j) * nkc * CT;
+          load_chunk(Ci, Li, rows);
+          if (!dt) load_chunk(Cj, Lj, PB);
+          cp_async_commit();
+          for (int c = 0; c < nch; ++c) {
+            const int s = c & 1;
+            if (c + 1 < nch) {
+              load_chunk(Ci + (s ^ 1) * CT, Li + (c + 1) * CT, rows);
+              if (!dt) load_chunk(Cj + (s ^ 1) * CT, Lj + (c + 1) * CT, PB);
+              cp_async_commit();
+              cp_async_wait<1>();
+            } else {
+              cp_async_wait<0>();
+            }
+            __syncthreads();
+            mma_rows<LDC, KC>(Ci + s * CT, (dt ? Ci : Cj) + s * CT, KC, m_base, n_base, gq, tq, mcnt, acc);
+            __syncthreads();  // the stage is refilled (or T written) next
+          }
+        }
+        // ---- T = [K; y^T](i, j) - acc: lower part of the diagonal tile, zero
+        //      outside the trapezoid and past kb ----
+        {
+          int gr[4], gc[4];
+          double s[4][4];
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi) gr[mi] = i0 + m_base + 8 * mi + gq;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) gc[q] = j0 + n_base + 8 * (q >> 1) + 2 * tq + (q & 1);
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) s[mi][q] = 0.0;
+          for (int dd = 0; dd < D; ++dd) {
+            const double il = sh_par[dd];
+            double xr[4], xc[4];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) xr[mi] = gr[mi] < N ? __ldg(g.X + gr[mi] * D + dd) * il : 0.0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) xc[q] = gc[q] < N ? __ldg(g.X + gc[q] * D + dd) * il : 0.0;
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const double t = xr[mi] - xc[q];
+                s[mi][q] = fma(t, t, s[mi][q]);
+              }
+          }
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int r = gr[mi] - i0, c = gc[q] - j0;
+              const bool ok = gr[mi] <= N && c < kb && (!dt || c <= r || gr[mi] >= j0 + kb);
+              double v = 0.0;
+              if (ok) {
+                const double kv = gr[mi] == N ? __ldg(g.y + gc[q])
+                                              : sf2 * exp(-0.5 * s[mi][q]) + (gr[mi] == gc[q] ? diag_add : 0.0);
+                v = kv - acc[mi][q >> 1][q & 1];
+              }
+              T[r * LDR + c] = v;
+            }
+        }
+        __syncthreads();
+        if (dt) {
+          // ---- factorise the diagonal tile in place; all threads, one
+          //      barrier per column: column jj updates the block with its
+          //      unscaled values (A_rl -= A_rj A_lj / A_jj) while column jj-1
+          //      is scaled by 1/L_{jj-1,jj-1}; thread (ty, tx) owns rows
+          //      ty + 16 u and columns tx + 16 v ----
+          bool bad = false;  // uniform: every thread reads the same pivot
+          for (int jj = 0; jj < kb; ++jj) {
+            const double ajj = T[jj * LDR + jj];
+            if (!(ajj > 0.0)) {
+              bad = true;
+              if (tid == 0) sh_fail = 1;
+              break;
+            }
+            const double iajj = 1.0 / ajj;
+            if (jj > 0) {
+              const double ipm = 1.0 / diag[jj - 1];
+              for (int r = jj + tid; r < kb; r += kThreads) T[r * LDR + jj - 1] *= ipm;
+            }
+            if (tid == 0) diag[jj] = sqrt(ajj);
+            double cj[4];
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
               const int l = tx + 16 * v;
-              if (l > j && l <= r) Lkk[r * LDR + l] = fma(-arj, cj[v], Lkk[r * LDR + l]);
+              cj[v] = (l > jj && l < kb) ? T[l * LDR + jj] * iajj : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int r = ty + 16 * u;
+              if (r > jj && r < kb) {
+                const double arj = T[r * LDR + jj];
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                  const int l = tx + 16 * v;
+                  if (l > jj && l <= r) T[r * LDR + l] = fma(-arj, cj[v], T[r * LDR + l]);
+                }
+              }
+            }
+            __syncthreads();
+          }
+          if (!bad) {
+            for (int c = tid; c < kb; c += kThreads) T[c * LDR + c] = diag[c];
+            if (tid < 32) {
+              double lg = 0.0;
+              for (int c = lane; c < kb; c += 32) lg += log(diag[c]);
+              logdet_part += lg;
             }
           }
+          __syncthreads();
+          if (sh_fail) break;
+          // ---- W = L_jj^-1 by forward substitution, column c by the 4 lanes
+          //      4c'..4c'+3 of a warp (partial sums over l split 4 ways):
+          //      W_cc = 1 / L_cc, W_ic = -(sum_{c <= l < i} L_il W_lc) / L_ii ----
+          {
+            const int c = tid >> 2, part = tid & 3;  // 64 columns x 4 parts, warp-uniform loop bounds
+            for (int e = tid; e < PB * PB; e += kThreads) W[(e / PB) * LDR + (e % PB)] = 0.0;
+            __syncthreads();
+            if (c < kb && part == 0) W[c * LDR + c] = 1.0 / diag[c];
+            __syncwarp();
+            for (int ii = 1; ii < kb; ++ii) {
+              const bool act = c < ii;  // (c < kb follows)
+              double sacc = 0.0;
+              if (act)
+                for (int l = c + part; l < ii; l += 4) sacc = fma(T[ii * LDR + l], W[l * LDR + c], sacc);
+              sacc += __shfl_xor_sync(0xffffffffu, sacc, 1);
+              sacc += __shfl_xor_sync(0xffffffffu, sacc, 2);
+              if (act && part == 0) W[ii * LDR + c] = -sacc / diag[ii];
+              __syncwarp();
+            }
+          }
+          __syncthreads();
+          if (rows <= kb) continue;  // no row below the diagonal in this block (y row is in a later block)
         }
-        __syncthreads();
-      }
-      if (!bad) {
-        for (int c = tid; c < kb; c += kThreads) Lkk[c * LDR + c] = diag[c];
-        if (tid < 32) {
-          double lg = 0.0;
-          for (int c = lane; c < kb; c += 32) lg += log(diag[c]);
-          logdet_part += lg;
-        }
-      }
-      __syncthreads();
-      if (sh_fail) break;
-      // 2. W = L_kk^-1 by forward substitution, column c by the 4 lanes
-      //    4c'..4c'+3 of a warp (partial sums over l split 4 ways):
-      //    W_cc = 1 / L_cc, W_ic = -(sum_{c <= l < i} L_il W_lc) / L_ii
-      {
-        const int c = tid >> 2, part = tid & 3;  // 64 columns x 4 parts, warp-uniform loop bounds
-        for (int e = tid; e < PB * PB; e += kThreads) W[(e / PB) * LDR + (e % PB)] = 0.0;
-        __syncthreads();
-        if (c < kb && part == 0) W[c * LDR + c] = 1.0 / diag[c];
-        __syncwarp();
-        for (int i = 1; i < kb; ++i) {
-          const bool act = c < i;  // (c < kb follows)
-          double s = 0.0;
-          if (act)
-            for (int l = c + part; l < i; l += 4) s = fma(Lkk[i * LDR + l], W[l * LDR + c], s);
-          s += __shfl_xor_sync(0xffffffffu, s, 1);
-          s += __shfl_xor_sync(0xffffffffu, s, 2);
-          if (act && part == 0) W[i * LDR + c] = -s / diag[i];
-          __syncwarp();
-        }
-      }
-      __syncthreads();
-      // 3. row blocks of [r0, N] (the y row included): X = A_panel W^T on the
-      //    fp64 tensor cores, written back to A and kept in Ti, then the
-      //    trailing update A[i][j] -= sum_c X[i][c] X[j][c] for the tiles
-      //    (bi, bj <= bi), columns r0..min(i, N-1)
-      const int r0 = k0 + kb;
-      const int nrb = (N + 1 - r0 + PB - 1) / PB, ncb = (N - r0 + PB - 1) / PB;
-      const int kr = (kb + 3) & ~3;  // DMMA k range (W and Ti zero past kb)
-      for (int bi = 0; bi < nrb; ++bi) {
-        const int i0 = r0 + bi * PB;
-        const int rows = min(PB, N + 1 - i0);
-        load_panel_tile(Ti, A, lda, i0, rows, k0, kb);
-        cp_async_commit();
-        cp_async_wait<0>();
-        __syncthreads();
+        // ---- L(i, j) = T W^T (rows of the diagonal tile above kb are not
+        //      needed; the y row yields alpha) ----
         {
-          double acc[4][2][2];
 #pragma unroll
           for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
             for (int ni = 0; ni < 2; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-          mma_rows(Ti, W, kr, m_base, n_base, gq, tq, acc);
-          __syncthreads();  // every warp is done reading Ti
+          mma_rows<LDR, 0>(T, W, kr, m_base, n_base, gq, tq, mcnt, acc);
 #pragma unroll
-          for (int mi = 0; mi < 4; ++mi)
+          for (int mi = 0; mi < 4; ++mi) {
+            const int r = m_base + 8 * mi + gq;
+            if (i0 + r == N) {
 #pragma unroll
-            for (int ni = 0; ni < 2; ++ni)
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                const int r = m_base + 8 * mi + gq, cc = n_base + 8 * ni + 2 * tq + h;
-                Ti[r * LDR + cc] = acc[mi][ni][h];  // zero past rows / kb
-                if (r < rows && cc < kb) A[static_cast<long long>(i0 + r) * lda + k0 + cc] = acc[mi][ni][h];
-              }
-          __syncthreads();
-        }
-        const int nbj = min(bi + 1, ncb);
-        for (int bj = 0; bj < nbj; ++bj) {
-          const int j0 = r0 + bj * PB;
-          const int cols = min(PB, N - j0);
-          if (bj != bi) {
-            load_panel_tile(Tj, A, lda, j0, cols, k0, kb);
-            cp_async_commit();
+              for (int ni = 0; ni < 2; ++ni) alpha2 += acc[mi][ni][0] * acc[mi][ni][0] + acc[mi][ni][1] * acc[mi][ni][1];
+            }
           }
-          // prefetch the 16 outputs (their latency hides behind the tile loads
-          // and the product); interior tiles (full, strictly below the
-          // diagonal) need no masks and use 16-B accesses
-          const bool interior = bj < bi && rows == PB && cols == PB;
-          double *Ot = A + static_cast<long long>(i0 + m_base + gq) * lda + j0 + n_base + 2 * tq;
-          double cur[4][2][2], acc[4][2][2];
-          if (interior) {
+          if (!dt) {
+            double *Lo = Ls + (static_cast<long long>(i) * nkc + 2 * j) * CT;
 #pragma unroll
-            for (int mi = 0; mi < 4; ++mi)
+            for (int ni = 0; ni < 2; ++ni) {
+              const int cc = n_base + 8 * ni + 2 * tq;
+              double *o = Lo + (cc >> 5) * CT + (cc & 31);
 #pragma unroll
-              for (int ni = 0; ni < 2; ++ni) {
-                const double2 v = *reinterpret_cast<const double2 *>(Ot + 8 * mi * lda + 8 * ni);
-                cur[mi][ni][0] = v.x;
-                cur[mi][ni][1] = v.y;
-              }
-          } else {
-#pragma unroll
-            for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-              for (int ni = 0; ni < 2; ++ni)
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                  const int r = m_base + 8 * mi + gq, cc = n_base + 8 * ni + 2 * tq + h;
-                  cur[mi][ni][h] = (r < rows && cc < cols && j0 + cc <= i0 + r) ? Ot[8 * mi * lda + 8 * ni + h] : 0.0;
-                }
+              for (int mi = 0; mi < 4; ++mi)
+                *reinterpret_cast<double2 *>(o + (m_base + 8 * mi + gq) * LDC) =
+                    make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+            }
           }
-#pragma unroll
-          for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-            for (int ni = 0; ni < 2; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-          if (bj != bi) cp_async_wait<0>();
-          __syncthreads();
-          mma_rows(Ti, bj == bi ? Ti : Tj, kr, m_base, n_base, gq, tq, acc);
-          if (interior) {
-#pragma unroll
-            for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-              for (int ni = 0; ni < 2; ++ni)
-                *reinterpret_cast<double2 *>(Ot + 8 * mi * lda + 8 * ni) =
-                    make_double2(cur[mi][ni][0] - acc[mi][ni][0], cur[mi][ni][1] - acc[mi][ni][1]);
-          } else {
-#pragma unroll
-            for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-              for (int ni = 0; ni < 2; ++ni)
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                  const int r = m_base + 8 * mi + gq, cc = n_base + 8 * ni + 2 * tq + h;
-                  if (r < rows && cc < cols && j0 + cc <= i0 + r)
-                    Ot[8 * mi * lda + 8 * ni + h] = cur[mi][ni][h] - acc[mi][ni][h];
-                }
-          }
-          __syncthreads();  // Tj is refilled by the next tile
+          __syncthreads();  // T (= the chunk stages) is overwritten by the next tile
         }
       }
     }
     // ---- E = 1/2 |alpha|^2 + sum log L_ii + N/2 log 2 pi ----
-    double q = 0.0;
-    if (!sh_fail)
-      for (int j = tid; j < N; j += kThreads) {
-        const double al = A[static_cast<long long>(N) * lda + j];
-        q = fma(al, al, q);
-      }
-    const double qs = block_sum(q, red);
+    const double qs = block_sum(alpha2, red);
     const double ld = block_sum(wid == 0 ? logdet_part : 0.0, red);
     if (tid == 0) {
       const double e = sh_fail ? INFINITY : 0.5 * qs + ld + 0.5 * N * kLn2Pi;
@@ -352,9 +368,12 @@ bool gp_setup(void **handle, const double *X, const double *y, int N, int D, dou
   E->g.N = N;
   E->g.D = D;
   E->g.jitter = jitter;
+  const int nrb = (N + 1 + PB - 1) / PB, nkc = 2 * ((N + PB - 1) / PB);
+  E->g.nrb = nrb;
+  E->g.nkc = nkc;
   double *dX = nullptr, *dy = nullptr, *sc = nullptr;
   if (cudaMalloc(&dX, sizeof(double) * N * D) || cudaMalloc(&dy, sizeof(double) * N) ||
-      cudaMalloc(&sc, sizeof(double) * static_cast<size_t>(sms) * (N + 1) * ((N + 1) & ~1))) {
+      cudaMalloc(&sc, sizeof(double) * static_cast<size_t>(sms) * nrb * nkc * CT)) {
     cudaFree(dX);
     cudaFree(dy);
     cudaFree(sc);
@@ -366,7 +385,7 @@ bool gp_setup(void **handle, const double *X, const double *y, int N, int D, dou
   E->g.X = dX;
   E->g.y = dy;
   E->g.scratch = sc;
-  E->smem = (3 * static_cast<size_t>(PB) * LDR + PB + 16) * sizeof(double);
+  E->smem = (4 * static_cast<size_t>(CT) + PB * LDR + PB + 16) * sizeof(double);
   cudaFuncSetAttribute(k_gp_energy, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(E->smem));
   *handle = E;
   return E->smem <= 200 * 1024;
