@@ -508,7 +508,9 @@ def roofline(prob, engine, ph_ms, alg_flops, peaks, traffic, mhz, step_ms, evals
             else "1.4 PFLOP/s sustained of fallback"
     else:
         fp64 = read_json(FP64_PATH).get("fp64_tflops")
-        bound, kname = "tensor", "k_gp_energy"  # DMMA (fp64 tensor) trailing updates and TRSM
+        # DMMA (fp64 tensor) Cholesky updates and TRSM; the fused chain kernel
+        # (default) runs the HRSS state machine and the GP energies in one launch
+        bound, kname = "tensor", "k_gp_energy" if os.environ.get("NSS_GP_ROUNDS") else "k_gp_chains"
         if fp64:
             peak, src = fp64, "fp64 cuBLAS DGEMM of measured (profiles/r01_measured_fp64_tf32.json)"
         else:

@@ -45,5 +45,8 @@ bool gp_setup(void **handle, const double *X, const double *y, int N, int D, dou
 void gp_free(void *handle);
 void gp_set_out64(void *handle, double *e64);  // also write fp64 energies (kernel checks)
 void gp_energy_pass(void *handle, const BatchDev &b, int parity, const LaunchCtx &lc);
+// the fused engine: every chain of [r.c0, r.c1) run to completion by one CTA
+// (HRSS state machine + GP energies of its probes), no per-round barrier
+bool gp_chains_pass(void *handle, const RunDev &r, const PriorDev &pr, const BatchDev &b, const LaunchCtx &lc);
 
 }  // namespace nss

@@ -1,0 +1,330 @@
+// The per-chain HRSS state machine of the batched engines (P:733-749,
+// identical decisions and draws to k_hrss.cu), shared by the round-synchronous
+// advance kernel (k_batch.cu) and the fused GP chain kernel (k_gp.cu).
+//
+// One warp per chain runs the sequential HRSS state machine and stops whenever
+// it needs an energy: it appends the probe point x + t v to the probe buffer
+// of this round (atomic row ticket; the row index never changes the value
+// computed), remembers which row it owns, and returns.  Probes that leave the
+// prior support or fall below the slice height are resolved in place without
+// an energy.  Both stepping-out endpoints of a side are independent of the
+// other side, so a chain issues the next left and the next right endpoint in
+// the same round (two probes) without evaluating anything the sequential
+// algorithm would not.
+#pragma once
+#include "batch.cuh"
+#include "energy.cuh"
+
+namespace nss {
+namespace {
+
+struct ChainRegs {
+  int phase, step, nl, nr, ns, ldone, rdone, row0, row1;
+  float l0, r0, lft, rgt, log_y, e, lp, t0, t1, lp0, lp1;
+  unsigned c_probe, c_eval, c_exp, c_shr, c_null;
+};
+
+__device__ __forceinline__ void load_chain(const BatchDev &b, int c, ChainRegs &s) {
+  s.phase = b.phase[c]; s.step = b.step[c]; s.nl = b.nl[c]; s.nr = b.nr[c]; s.ns = b.ns[c];
+  s.ldone = b.ldone[c]; s.rdone = b.rdone[c]; s.row0 = b.row0[c]; s.row1 = b.row1[c];
+  s.l0 = b.l0[c]; s.r0 = b.r0[c]; s.lft = b.lft[c]; s.rgt = b.rgt[c]; s.log_y = b.log_y[c];
+  s.e = b.e[c]; s.lp = b.lp[c]; s.t0 = b.t0[c]; s.t1 = b.t1[c]; s.lp0 = b.lp0[c]; s.lp1 = b.lp1[c];
+  s.c_probe = b.cnt[c]; s.c_eval = b.cnt[b.k + c]; s.c_exp = b.cnt[2 * b.k + c];
+  s.c_shr = b.cnt[3 * b.k + c]; s.c_null = b.cnt[4 * b.k + c];
+}
+
+__device__ __forceinline__ void store_chain(const BatchDev &b, int c, const ChainRegs &s) {
+  b.phase[c] = s.phase; b.step[c] = s.step; b.nl[c] = s.nl; b.nr[c] = s.nr; b.ns[c] = s.ns;
+  b.ldone[c] = s.ldone; b.rdone[c] = s.rdone; b.row0[c] = s.row0; b.row1[c] = s.row1;
+  b.l0[c] = s.l0; b.r0[c] = s.r0; b.lft[c] = s.lft; b.rgt[c] = s.rgt; b.log_y[c] = s.log_y;
+  b.e[c] = s.e; b.lp[c] = s.lp; b.t0[c] = s.t0; b.t1[c] = s.t1; b.lp0[c] = s.lp0; b.lp1[c] = s.lp1;
+  b.cnt[c] = s.c_probe; b.cnt[b.k + c] = s.c_eval; b.cnt[2 * b.k + c] = s.c_exp;
+  b.cnt[3 * b.k + c] = s.c_shr; b.cnt[4 * b.k + c] = s.c_null;
+}
+
+// energy of probe row `row` of the given parity: the slices are loaded by the
+// lanes in parallel and summed by a fixed shuffle tree (deterministic); every
+// lane returns the total
+__device__ __forceinline__ float probe_energy(const BatchDev &b, int parity, int row, int lane) {
+  const int ns = b.slices[parity];
+  double acc = 0.0;
+  for (int q = lane; q < ns; q += 32) acc += b.partial[parity][static_cast<long long>(q) * b.p_stride + row];
+  if (b.lin[parity] && lane == 0) acc += static_cast<double>(b.lin[parity][row]);  // logistic regression: theta . g
+  return static_cast<float>(warp_sum_d(acc));
+}
+
+template <int NPL>
+__device__ __forceinline__ void emit_probe(const BatchDev &b, int parity, int row, const float (&xp)[NPL], int d,
+                                           int lane) {
+  float *dst = b.P[parity] + static_cast<long long>(row) * b.dp;
+#pragma unroll
+  for (int t = 0; t < NPL; ++t) {
+    const int i = lane + 32 * t;
+    if (i < d) dst[i] = xp[t];
+  }
+  if (b.A[parity]) {
+    // bf16x3 split for the tensor-core logistic-regression energy (K padded to
+    // 128), and the row's linear term theta~ . g (theta~ = hi + mid, the terms
+    // the tensor cores contract)
+    __nv_bfloat16 *A = b.A[parity];
+    float lin = 0.f;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int kk = lane + 32 * t;
+      const float v = (t < NPL && kk < d) ? xp[t < NPL ? t : 0] : 0.f;
+      const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+      const float r1 = v - __bfloat162float(hi);
+      const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+      const __nv_bfloat16 lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
+      A[static_cast<long long>(row) * 128 + kk] = hi;
+      A[(static_cast<long long>(b.p_stride) + row) * 128 + kk] = mid;
+      A[(2ll * b.p_stride + row) * 128 + kk] = lo;
+      lin = fmaf(__bfloat162float(hi) + __bfloat162float(mid), __ldg(b.g + kk), lin);
+    }
+    lin = warp_sum(lin);
+    if (lane == 0) b.lin[parity][row] = lin;
+  }
+}
+
+// One warp advances chain c: fold in the energies of the probes it issued in
+// the previous round (parity ^ 1), run the sequential HRSS state machine until
+// it needs new energies (probes appended to the rows of `parity`) or finishes
+// its p steps; the state lives in the BatchDev arrays between calls.  sZ:
+// NPL * 32 floats of shared memory owned by the warp.
+template <int NPL>
+__device__ __forceinline__ void advance_chain(const RunDev &r, const PriorDev &pr, const BatchDev &b, int parity,
+                                              int c, float *sZ) {
+  const int d = r.d, lane = threadIdx.x & 31;
+  const DevState *st = r.st;
+  if (st->terminated || st->error || st->finalised) return;  // uniform (written by other kernels)
+  ChainRegs s;
+  load_chain(b, c, s);
+  if (s.phase == kPhDone) return;
+
+  const uint32_t it = static_cast<uint32_t>(st->iter)  /* set by the select kernel */;
+  const int dest = r.cdest[c];
+  const float e_star = st->e_star, w = st->width;
+  const int p = r.p, cap = r.max_stepout, maxs = r.max_shrink;
+  const bool euclid = r.dir_norm == NSS_DIR_EUCLIDEAN;
+  const int h = 2 * ((d + 1) / 2);
+  const int nblk_norm = h >> 2, nblk_all = (h + 3) >> 2;
+  const int prev = parity ^ 1;
+
+  float pa[NPL], pb[NPL], x[NPL], v[NPL], xp[NPL];
+  load_prior_lane<NPL>(pr, lane, d, pa, pb);
+#pragma unroll
+  for (int t = 0; t < NPL; ++t) {
+    const int i = lane + 32 * t;
+    x[t] = i < d ? b.x[static_cast<long long>(c) * b.dp + i] : 0.f;
+    v[t] = i < d ? b.v[static_cast<long long>(c) * b.dp + i] : 0.f;
+  }
+  // results of the probes this chain issued last round
+  float E0 = 0.f, E1 = 0.f;
+  if (s.row0 >= 0) E0 = probe_energy(b, prev, s.row0, lane);
+  if (s.row1 >= 0) E1 = probe_energy(b, prev, s.row1, lane);
+  bool nan_seen = false;
+
+  // in-slice test of x + t v against the prior part (support and height);
+  // returns false when no energy is needed because the point is out
+  auto prior_ok = [&](float tt, float &lpp) -> bool {
+#pragma unroll
+    for (int q = 0; q < NPL; ++q) xp[q] = fmaf(tt, v[q], x[q]);
+    bool inside;
+    lpp = prior_logp<NPL>(xp, pr, pa, pb, lane, d, inside);
+    return inside && (lpp >= s.log_y);
+  };
+  auto issue = [&](float tt) -> int {
+    int row = 0;
+    if (lane == 0) row = atomicAdd(&b.n_probe[parity], 1);
+    row = __shfl_sync(kFull, row, 0);
+#pragma unroll
+    for (int q = 0; q < NPL; ++q) xp[q] = fmaf(tt, v[q], x[q]);
+    emit_probe<NPL>(b, parity, row, xp, d, lane);
+    return row;
+  };
+  auto end_step = [&](int accepted) {
+    s.c_exp += s.nl + s.nr;
+    s.c_shr += s.ns;
+    s.c_null += accepted ? 0 : 1;
+    if (lane == 0)
+      r.counts[static_cast<long long>(c) * p + s.step] =
+          static_cast<uint32_t>(s.nl) | (static_cast<uint32_t>(s.nr) << 8) | (static_cast<uint32_t>(s.ns) << 16) |
+          (static_cast<uint32_t>(accepted) << 24);
+    s.step += 1;
+    s.phase = kPhDir;
+  };
+
+  bool wait = false;
+  while (!wait && s.phase != kPhDone) {
+    if (s.phase == kPhDir) {
+      if (s.step >= p) {
+        s.phase = kPhDone;
+        break;
+      }
+      const int j = s.step;
+      if (r.Vpre) {  // precomputed for this (chain, step) by k_dirs (bit-identical)
+        const float *vr = r.Vpre + (static_cast<long long>(c - r.c0) * p + j) * r.dp;
+#pragma unroll
+        for (int t = 0; t < NPL; ++t) {
+          const int i = lane + 32 * t;
+          v[t] = i < d ? __ldg(vr + i) : 0.f;
+        }
+      } else {
+      // direction v = L z / |z| (R-6), stream (it, dest, HRSS, j)
+      for (int bk = lane; bk < nblk_all; bk += 32) {
+        const uint4 u4 = philox_block(r, it, dest, kPhaseHrss, j, bk);
+        const float r0 = sqrtf(-2.f * logf(u01(u4.x))), r1 = sqrtf(-2.f * logf(u01(u4.z)));
+        float s0, c0, s1, c1;
+        sincospif(2.f * u01(u4.y), &s0, &c0);
+        sincospif(2.f * u01(u4.w), &s1, &c1);
+        const int i0 = 4 * bk;
+        if (i0 < d) sZ[i0] = r0 * c0;
+        if (i0 + 1 < d) sZ[i0 + 1] = r0 * s0;
+        if (bk < nblk_norm) {
+          if (i0 + 2 < d) sZ[i0 + 2] = r1 * c1;
+          if (i0 + 3 < d) sZ[i0 + 3] = r1 * s1;
+        }
+      }
+      __syncwarp();
+      // v = L z, column by column: column m of L is contiguous in LT, so each
+      // step is one coalesced load per lane-row block
+      float zz = 0.f, vv = 0.f;
+#pragma unroll
+      for (int t = 0; t < NPL; ++t) v[t] = 0.f;
+#pragma unroll 8
+      for (int m = 0; m < d; ++m) {  // unrolled: 8 columns of loads in flight
+        const float zm = sZ[m];
+        const float *col = r.LT + static_cast<long long>(m) * r.dp;
+#pragma unroll
+        for (int t = 0; t < NPL; ++t) {
+          const int i = lane + 32 * t;
+          if (i < d) v[t] = fmaf(__ldg(col + i), zm, v[t]);  // L[i][m] = 0 for m > i
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < NPL; ++t) {
+        const int i = lane + 32 * t;
+        if (i < d) {
+          const float zi = sZ[i];
+          zz = fmaf(zi, zi, zz);
+        }
+        vv = fmaf(v[t], v[t], vv);
+      }
+      const float inv = 1.f / sqrtf(warp_sum(euclid ? vv : zz));
+#pragma unroll
+      for (int t = 0; t < NPL; ++t) v[t] *= inv;
+      __syncwarp();
+      }
+      const uint4 hb = philox_block(r, it, dest, kPhaseHrss, j, h >> 2);
+      s.log_y = s.lp + logf(u01(word(hb, h & 3)));
+      s.l0 = -w * u01(word(hb, (h + 1) & 3));
+      s.r0 = s.l0 + w;
+      s.nl = s.nr = s.ns = 0;
+      s.ldone = s.rdone = 0;
+      s.row0 = s.row1 = -1;
+      s.phase = kPhStepOut;
+      continue;
+    }
+    if (s.phase == kPhStepOut) {
+      // fold in last round's endpoint results (R-10)
+      if (s.row0 >= 0) {
+        s.c_eval += 1;
+        nan_seen = nan_seen || isnan(E0);
+        if (E0 < e_star) s.nl += 1; else s.ldone = 1;
+        s.row0 = -1;
+      }
+      if (s.row1 >= 0) {
+        s.c_eval += 1;
+        nan_seen = nan_seen || isnan(E1);
+        if (E1 < e_star) s.nr += 1; else s.rdone = 1;
+        s.row1 = -1;
+      }
+      // next endpoints: resolve prior-rejected ones in place, issue the rest
+      while (!s.ldone) {
+        if (s.nl >= cap) { s.ldone = 1; break; }
+        const float tt = fmaf(-static_cast<float>(s.nl), w, s.l0);
+        s.c_probe += 1;
+        float lpp;
+        if (!prior_ok(tt, lpp)) { s.ldone = 1; break; }
+        s.row0 = issue(tt);
+        s.t0 = tt;
+        s.lp0 = lpp;
+        break;
+      }
+      while (!s.rdone) {
+        if (s.nr >= cap) { s.rdone = 1; break; }
+        const float tt = fmaf(static_cast<float>(s.nr), w, s.r0);
+        s.c_probe += 1;
+        float lpp;
+        if (!prior_ok(tt, lpp)) { s.rdone = 1; break; }
+        s.row1 = issue(tt);
+        s.t1 = tt;
+        s.lp1 = lpp;
+        break;
+      }
+      if (s.row0 >= 0 || s.row1 >= 0) {
+        wait = true;
+        break;
+      }
+      s.lft = fmaf(-static_cast<float>(s.nl), w, s.l0);
+      s.rgt = fmaf(static_cast<float>(s.nr), w, s.r0);
+      s.ns = 0;
+      s.phase = kPhShrink;
+      continue;
+    }
+    // ---- shrinkage (R-12/R-13) ----
+    if (s.row0 >= 0) {
+      s.c_eval += 1;
+      nan_seen = nan_seen || isnan(E0);
+      s.row0 = -1;
+      if (E0 < e_star) {
+#pragma unroll
+        for (int q = 0; q < NPL; ++q) x[q] = fmaf(s.t0, v[q], x[q]);
+        s.e = E0;
+        s.lp = s.lp0;
+        end_step(1);
+        continue;
+      }
+      if (s.t0 < 0.f) s.lft = s.t0; else s.rgt = s.t0;
+    }
+    bool issued = false;
+    while (s.ns < maxs) {
+      const int q = h + 2 + s.ns;
+      const uint4 ub = philox_block(r, it, dest, kPhaseHrss, s.step, static_cast<uint32_t>(q >> 2));
+      const float tt = fmaf(u01(word(ub, q & 3)), s.rgt - s.lft, s.lft);
+      s.ns += 1;
+      s.c_probe += 1;
+      float lpp;
+      if (!prior_ok(tt, lpp)) {
+        if (tt < 0.f) s.lft = tt; else s.rgt = tt;
+        continue;
+      }
+      s.row0 = issue(tt);
+      s.t0 = tt;
+      s.lp0 = lpp;
+      issued = true;
+      break;
+    }
+    if (issued) {
+      wait = true;
+      break;
+    }
+    end_step(0);  // shrink cap reached: null move
+  }
+
+#pragma unroll
+  for (int t = 0; t < NPL; ++t) {
+    const int i = lane + 32 * t;
+    if (i < d) {
+      b.x[static_cast<long long>(c) * b.dp + i] = x[t];
+      b.v[static_cast<long long>(c) * b.dp + i] = v[t];
+    }
+  }
+  if (lane == 0) {
+    store_chain(b, c, s);
+    if (nan_seen) raise_error(r.st, NSS_ERR_NAN);
+  }
+}
+
+}  // namespace
+}  // namespace nss

@@ -87,6 +87,7 @@ struct nss_ctx {
   BatchDev bd{};
   bool batch_alloc = false;
   int batch_backend = 0;  // 1 generic warp-per-probe energy, 2 tensor-core logistic regression, 3 GP
+  bool gp_rounds = getenv("NSS_GP_ROUNDS") != nullptr;  // GP: round-synchronous engine instead of the fused chains
   LrEngine lr{};
   bool lr_ok = false;     // logistic-regression data are bf16-exact and d <= 112
   std::vector<double> lr_x, lr_y;
@@ -489,6 +490,14 @@ nss_status enqueue_iteration_batch(nss_ctx *c) {
   auto rounds = [&]() -> nss_status {
     launch_dirs(c->r, lc);  // large d: every direction of the iteration up front
     batch_begin(c->r, c->pr, c->bd, lc);
+    if (c->batch_backend == 3 && !c->gp_rounds) {  // fused chains: one launch, no host polling
+      bool ok = true;
+      const nss_status st = timed_launch(c, 4, c->stream, [&] { ok = gp_chains_pass(c->gp, c->r, c->pr, c->bd, lc); });
+      if (st) return st;
+      if (!ok) return fail(c, NSS_ERR_OOM, "GP chain buffers");
+      batch_finish(c->r, c->bd, lc);
+      return NSS_OK;
+    }
     const long long max_rounds =
         static_cast<long long>(c->r.p) * (c->r.max_stepout + 2 + c->r.max_shrink) + kRoundsPerChunk;
     for (long long done = 0; done < max_rounds; done += kRoundsPerChunk) {

@@ -75,8 +75,19 @@ GP_CASES = {
 }
 
 
+def _gp_mode(monkeypatch, mode):
+    """GP chains run fused (one CTA per chain, default) or round-synchronous
+    (NSS_GP_ROUNDS, read by nss_init)."""
+    if mode == "rounds":
+        monkeypatch.setenv("NSS_GP_ROUNDS", "1")
+    else:
+        monkeypatch.delenv("NSS_GP_ROUNDS", raising=False)
+
+
+@pytest.mark.parametrize("mode", ["fused", "rounds"])
 @pytest.mark.parametrize("name", sorted(GP_CASES))
-def test_gp_single_iteration_parity(name):
+def test_gp_single_iteration_parity(name, mode, monkeypatch):
+    _gp_mode(monkeypatch, mode)
     make, kw, warm = GP_CASES[name]
     prob = make()
     cfg = W.config(seed=11, **kw)
@@ -139,3 +150,29 @@ def test_c5_full_size_iteration_subset():
         assert np.allclose(xg[s], xr[s], rtol=1e-5, atol=1e-5)
         assert abs(eg[s] - er[s]) <= 1e-5 * abs(er[s])
     assert good >= 2
+
+
+def test_gp_fused_equals_rounds(monkeypatch):
+    """The fused chain kernel and the round-synchronous engine run the same
+    state machine on the same energies: two iterations from one injected
+    state give bit-identical traces, live sets and dead stores."""
+    from paper_2601_23252_b200 import nss
+    prob = W.gp_ard(6, 64, seed=5)
+    cfg = W.config(seed=11, n_live=128, k=64, steps=8)
+    rng = np.random.default_rng(7)
+    x0 = rng.standard_normal((cfg["n_live"], prob.d)).astype(np.float32)
+    e0 = _np_energy(prob, x0.astype(np.float64)).astype(np.float32)
+    out = {}
+    for mode in ("fused", "rounds"):
+        _gp_mode(monkeypatch, mode)
+        g = nss.Sampler(prob, cfg)
+        g.set_live(x0, e0, 1)
+        g.step()
+        g.step()
+        out[mode] = (g.trace(), g.get_live(), g.dead())
+        g.close()
+    (tf, (xf, ef), df), (tr, (xr, er), dr) = out["fused"], out["rounds"]
+    for key in ("dead_gid", "dest_gid", "parent_gid", "counts"):
+        assert np.array_equal(tf[key], tr[key]), key
+    assert np.array_equal(xf, xr) and np.array_equal(ef, er)
+    assert np.array_equal(df["gid"], dr["gid"]) and np.array_equal(df["e"], dr["e"])
