@@ -152,13 +152,16 @@ def test_c5_full_size_iteration_subset():
     assert good >= 2
 
 
-def test_gp_fused_equals_rounds(monkeypatch):
+@pytest.mark.parametrize("d_in,n_data,n_live,k,steps", [(6, 64, 128, 64, 8), (2, 40, 1024, 600, 3)])
+def test_gp_fused_equals_rounds(monkeypatch, d_in, n_data, n_live, k, steps):
     """The fused chain kernel and the round-synchronous engine run the same
     state machine on the same energies: two iterations from one injected
-    state give bit-identical traces, live sets and dead stores."""
+    state give bit-identical traces, live sets and dead stores.  The second
+    case has more chains (600) than the fused kernel has CTAs (296), so CTAs
+    take several chains from the queue."""
     from paper_2601_23252_b200 import nss
-    prob = W.gp_ard(6, 64, seed=5)
-    cfg = W.config(seed=11, n_live=128, k=64, steps=8)
+    prob = W.gp_ard(d_in, n_data, seed=5)
+    cfg = W.config(seed=11, n_live=n_live, k=k, steps=steps)
     rng = np.random.default_rng(7)
     x0 = rng.standard_normal((cfg["n_live"], prob.d)).astype(np.float32)
     e0 = _np_energy(prob, x0.astype(np.float64)).astype(np.float32)
