@@ -1,3 +1,4 @@
+#include <chrono>
 // C ABI (include/nss.h) and host orchestration of one NSS run on one GPU.
 //
 // The host only validates, allocates, uploads the problem once, enqueues the
@@ -8,6 +9,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -132,20 +134,69 @@ nss_status exchange(nss_ctx *c);
 // Zeroed device memory owned by the context.  Small requests are carved from
 // 16 MB arenas (one cudaMalloc + memset each: nss_init makes dozens of
 // allocations), large ones get their own; 256-byte alignment throughout.
-template <class T>
+// Device memory comes from the device's stream-ordered pool (cudaMallocAsync
+// on the context's stream), which keeps freed blocks for the next context
+// (release threshold), so nss_init / nss_destroy cycles cost microseconds
+// instead of cudaMalloc + synchronous memset per buffer.
+void ensure_pool() {
+  static std::mutex mu;
+  static bool done[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+  std::lock_guard<std::mutex> g(mu);
+  if (done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = uint64_t(8) << 30;  // freed blocks kept for reuse, up to 8 GB
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done[dev] = true;
+}
+
+// The mapped page-locked 4 KB host mirror of a context: page locking costs
+// milliseconds, so destroyed contexts return their block to a process-wide
+// free list.
+std::mutex g_pinned_mu;
+std::vector<void *> g_pinned_free;
+void *pinned_block() {
+  {
+    std::lock_guard<std::mutex> g(g_pinned_mu);
+    if (!g_pinned_free.empty()) {
+      void *p = g_pinned_free.back();
+      g_pinned_free.pop_back();
+      memset(p, 0, 4096);
+      return p;
+    }
+  }
+  void *p = nullptr;
+  if (cudaHostAlloc(&p, 4096, cudaHostAllocMapped) != cudaSuccess) return nullptr;
+  memset(p, 0, 4096);
+  return p;
+}
+void pinned_release(void *p) {
+  std::lock_guard<std::mutex> g(g_pinned_mu);
+  g_pinned_free.push_back(p);
+}
+
+template <typename T>
 nss_status dalloc(nss_ctx *c, T **p, size_t count) {
   const size_t bytes = (count * sizeof(T) + 16 + 255) & ~size_t(255);
   constexpr size_t kArena = size_t(16) << 20;
+  auto get = [&](size_t nb, void **q) -> nss_status {
+    cudaError_t e = cudaMallocAsync(q, nb, c->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(*q, 0, nb, c->stream);
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      return fail(c, NSS_ERR_OOM, std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
+    }
+    c->allocs.push_back(*q);
+    return NSS_OK;
+  };
   if (bytes <= kArena / 8) {
     if (!c->arena || c->arena_used + bytes > kArena) {
       void *q = nullptr;
-      cudaError_t e = cudaMalloc(&q, kArena);
-      if (e != cudaSuccess) {
-        (void)cudaGetLastError();
-        return fail(c, NSS_ERR_OOM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
-      }
-      cudaMemset(q, 0, kArena);
-      c->allocs.push_back(q);
+      nss_status s = get(kArena, &q);
+      if (s) return s;
       c->arena = static_cast<char *>(q);
       c->arena_used = 0;
     }
@@ -154,13 +205,8 @@ nss_status dalloc(nss_ctx *c, T **p, size_t count) {
     return NSS_OK;
   }
   void *q = nullptr;
-  cudaError_t e = cudaMalloc(&q, bytes);
-  if (e != cudaSuccess) {
-    (void)cudaGetLastError();
-    return fail(c, NSS_ERR_OOM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
-  }
-  cudaMemset(q, 0, bytes);
-  c->allocs.push_back(q);
+  nss_status s = get(bytes, &q);
+  if (s) return s;
   *p = static_cast<T *>(q);
   return NSS_OK;
 }
@@ -171,7 +217,8 @@ nss_status upload_f32(nss_ctx *c, float **dst, const double *src, size_t count) 
   if (!count || !src) return NSS_OK;
   std::vector<float> tmp(count);
   for (size_t i = 0; i < count; ++i) tmp[i] = static_cast<float>(src[i]);
-  CK(cudaMemcpy(*dst, tmp.data(), count * sizeof(float), cudaMemcpyHostToDevice));
+  // stream-ordered after the allocation; a pageable source is staged before the call returns
+  CK(cudaMemcpyAsync(*dst, tmp.data(), count * sizeof(float), cudaMemcpyHostToDevice, c->stream));
   return NSS_OK;
 }
 
@@ -419,7 +466,7 @@ nss_status ensure_batch(nss_ctx *c) {
       nss_status s;
       if ((s = dalloc(c, &b.slices, 2))) return s;
       const int ones[2] = {1, 1};
-      CK(cudaMemcpy(b.slices, ones, sizeof(ones), cudaMemcpyHostToDevice));
+      CK(cudaMemcpyAsync(b.slices, ones, sizeof(ones), cudaMemcpyHostToDevice, c->stream));
     }
     for (int q = 0; q < 2; ++q) {
       nss_status s;
@@ -663,6 +710,16 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
                (dist->world > 1 && !dist->nccl_uid)))
     return NSS_ERR_INVALID_ARG;
   nss_ctx *c = new nss_ctx();
+  // measurement hook (NSS_INIT_PROF): host wall time of the phases of nss_init
+  const bool iprof = getenv("NSS_INIT_PROF") != nullptr;
+  auto it0 = std::chrono::steady_clock::now();
+  auto ip = [&](const char *what) {
+    if (!iprof) return;
+    cudaDeviceSynchronize();
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "nss_init %-12s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(t - it0).count());
+    it0 = t;
+  };
   c->cfg = *cfg;
   const int d = prior->d;
   c->d = d;
@@ -680,7 +737,8 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
     c->own_stream = true;
   }
   // one page-locked block for the host mirrors (page locking is slow: one call)
-  if (cudaHostAlloc(&c->h_block, 4096, cudaHostAllocMapped) != cudaSuccess) return bail(NSS_ERR_CUDA);
+  ensure_pool();
+  if (!(c->h_block = pinned_block())) return bail(NSS_ERR_CUDA);
   {
     char *hb = static_cast<char *>(c->h_block);
     c->h_st = reinterpret_cast<DevState *>(hb);
@@ -695,6 +753,7 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
     }
   }
   *c->h_lz0 = -INFINITY;
+  ip("pinned");
   if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess) return bail(NSS_ERR_CUDA);
   if (cudaEventCreateWithFlags(&c->ev_sel, cudaEventDisableTiming) != cudaSuccess) return bail(NSS_ERR_CUDA);
   if (cudaEventCreateWithFlags(&c->ev_evid, cudaEventDisableTiming) != cudaSuccess) return bail(NSS_ERR_CUDA);
@@ -865,6 +924,7 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
   r.seed_hi = static_cast<uint32_t>(cfg->seed >> 32);
   r.term_log_ratio = static_cast<float>(cfg->term_log_ratio);
   const size_t cap = static_cast<size_t>(cfg->max_dead);
+  ip("setup");
   if ((s = dalloc(c, &r.X, static_cast<size_t>(n) * c->dp))) return bail(s);
   if ((s = dalloc(c, &r.E, n))) return bail(s);
   if ((s = dalloc(c, &r.birth, n))) return bail(s);
@@ -912,9 +972,10 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
   if ((s = dalloc(c, &c->ticket, 1))) return bail(s);
   {
     std::vector<double> ninf(R + 1, -INFINITY);
-    if (cudaMemcpy(r.lz, ninf.data(), (R + 1) * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
+    if (cudaMemcpyAsync(r.lz, ninf.data(), (R + 1) * sizeof(double), cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
       return bail(NSS_ERR_CUDA);
   }
+  ip("alloc");
   // ---- multi-GPU: this rank's chain block and the NCCL communicator ----
   if (dist && dist->nccl_uid) {
     c->rank = dist->rank;
@@ -938,10 +999,12 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
   } else {
     launch_init(r, pr, en, lc);
   }
+  ip("comm");
   launch_metric(r, cfg->metric_reg, cfg->width_rule, cfg->width, 0, c->partials, c->ticket, c->nblk, lc);
   if (cudaGetLastError() != cudaSuccess) return bail(NSS_ERR_CUDA);
   if ((s = pull_state(c))) return bail(s);
   if ((s = device_error(c))) return bail(s);
+  ip("kernels");
   *out = c;
   return NSS_OK;
 }
@@ -1144,25 +1207,29 @@ NSS_API nss_status nss_sync(nss_ctx *c) {
 
 NSS_API nss_status nss_destroy(nss_ctx *c) {
   if (!c) return NSS_ERR_INVALID_ARG;
+  if (c->side) cudaStreamSynchronize(c->side);
+  if (c->side2) cudaStreamSynchronize(c->side2);
   if (c->stream) cudaStreamSynchronize(c->stream);
   drop_graph(c);
   if (c->lr.Xb) lr_free(c->lr);
   if (c->gp) gp_free(c->gp);
   if (c->comm) nccl_comm_free(c->comm);
 
-  for (void *p : c->allocs) cudaFree(p);
+  // every stream is idle: the blocks go back to the pool in stream order
+  for (void *p : c->allocs) cudaFreeAsync(p, c->stream);
+  if (c->stream) cudaStreamSynchronize(c->stream);
   for (auto e : c->ev_free) cudaEventDestroy(e);
   for (auto &t : c->ev_pending) {
     cudaEventDestroy(t.a);
     cudaEventDestroy(t.b);
   }
-  if (c->h_block) cudaFreeHost(c->h_block);
-  if (c->side) { cudaStreamSynchronize(c->side); cudaStreamDestroy(c->side); }
+  if (c->h_block) pinned_release(c->h_block);
+  if (c->side) cudaStreamDestroy(c->side);
   if (c->ev_sel) cudaEventDestroy(c->ev_sel);
   if (c->ev_evid) cudaEventDestroy(c->ev_evid);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_met) cudaEventDestroy(c->ev_met);
-  if (c->side2) { cudaStreamSynchronize(c->side2); cudaStreamDestroy(c->side2); }
+  if (c->side2) cudaStreamDestroy(c->side2);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return NSS_OK;
@@ -1497,7 +1564,8 @@ NSS_API nss_status nss_smc_init(const nss_prior *prior, const nss_energy *energy
   c->r.counts = counts;
   std::vector<int> id(n);
   for (int i = 0; i < n; ++i) id[i] = i;
-  if (cudaMemcpy(ident, id.data(), n * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess) return bail(NSS_ERR_CUDA);
+  if (cudaMemcpyAsync(ident, id.data(), n * sizeof(int), cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+    return bail(NSS_ERR_CUDA);
   c->smc = true;
   c->smc_rho = rho;
   RunDev &r = c->r;
