@@ -165,6 +165,13 @@ __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials,
     const bool is_min = e == nent;
     double acc = is_min ? INFINITY : 0.0;
     int b = 0;
+    for (; b + 15 < nblk; b += 16) {  // 16 independent loads in flight per thread (same summation order)
+      double v[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] = partials[static_cast<long long>(b + q) * (nent + 1) + e];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) acc = is_min ? fmin(acc, v[q]) : acc + v[q];
+    }
     for (; b + 7 < nblk; b += 8) {
       double v[8];
 #pragma unroll
@@ -223,9 +230,27 @@ __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials,
       const double ipiv = rsqrt(ajj), inv = 1.0 / ajj;
       for (int i = j + tid; i < d; i += nthr) Lo[i * d + j] = (i == j) ? ajj * ipiv : A[i * ld + j] * ipiv;
       const int off = (j + 1) * d - (j + 1) * j / 2;
-      for (int q = off + tid; q < npair; q += nthr) {
-        const int i = ti[q], l = tl[q];
-        A[i * ld + l] -= A[i * ld + j] * A[l * ld + j] * inv;
+      // four entries per batch: every load before any store (the entries are
+      // distinct and column j is not written), so the dependent smem round
+      // trips of the four overlap
+      for (int q0 = off + tid; q0 < npair; q0 += 4 * nthr) {
+        int ii[4], ll[4];
+        double aij[4], alj[4], ail[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int q = q0 + u * nthr;
+          ii[u] = q < npair ? ti[q] : 0;
+          ll[u] = q < npair ? tl[q] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          aij[u] = A[ii[u] * ld + j];
+          alj[u] = A[ll[u] * ld + j];
+          ail[u] = A[ii[u] * ld + ll[u]];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (q0 + u * nthr < npair) A[ii[u] * ld + ll[u]] = ail[u] - aij[u] * alj[u] * inv;
       }
       if (one_warp) __syncwarp(); else __syncthreads();
     }
