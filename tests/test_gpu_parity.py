@@ -231,6 +231,34 @@ def test_determinism_gpu():
     assert np.array_equal(a.evidence_reps(), b.evidence_reps())
 
 
+def test_determinism_recycled_memory():
+    """Device buffers come from a stream-ordered pool that keeps freed blocks
+    (nss_init in well under a millisecond): a run on memory recycled from a
+    context that left NaNs everywhere equals the same run made first."""
+    from paper_2601_23252_b200 import nss
+    prob = W.mog(10)
+    cfg = W.config(n_live=2000, k=200, steps=10, seed=9)
+    a = nss.Sampler(prob, cfg)
+    a.steps(20)
+    da, ra = a.dead(), a.evidence_reps()
+    a.close()
+    dirty = nss.Sampler(prob, dict(cfg, seed=123))
+    nan_x = np.full((cfg["n_live"], prob.d), np.nan, dtype=np.float32)
+    dirty.set_live(nan_x, np.full(cfg["n_live"], np.nan, dtype=np.float32), 1)
+    try:
+        dirty.step()
+    except nss.NssError:
+        pass  # NaN energies raise NSS_ERR_NAN; the buffers are dirty either way
+    dirty.close()
+    b = nss.Sampler(prob, cfg)
+    b.steps(20)
+    db, rb = b.dead(), b.evidence_reps()
+    b.close()
+    for key in da:
+        assert np.array_equal(da[key], db[key]), key
+    assert np.array_equal(ra, rb)
+
+
 def test_termination_flat_matches_oracle():
     from oracle import nsso
     from paper_2601_23252_b200 import nss
