@@ -428,7 +428,7 @@ nss_status ensure_batch(nss_ctx *c) {
   if (!c->batch_alloc) {
     b.k = k;
     b.dp = c->dp;
-    b.max_rows = backend == 3 ? std::max(2 * k, c->r.n) : 2 * k;  // GP also draws the n initial points
+    b.max_rows = backend >= 2 ? std::max(2 * k, c->r.n) : 2 * k;  // GP / LR also draw the n initial points
     nss_status s;
     int **ints[] = {&b.phase, &b.step, &b.nl, &b.nr, &b.ns, &b.ldone, &b.rdone, &b.row0, &b.row1};
     for (int **q : ints)
@@ -659,7 +659,7 @@ nss_status enqueue_iteration(nss_ctx *c) {
   return NSS_OK;
 }
 
-// R-20 for energies with only a batched implementation: every attempt draws
+// R-20 for energies with a batched implementation (GP, tensor-core LR): every attempt draws
 // the still-pending live points into the probe buffer, one energy pass
 // evaluates them, and the accept pass keeps the finite ones.
 nss_status init_batched(nss_ctx *c) {
@@ -676,7 +676,10 @@ nss_status init_batched(nss_ctx *c) {
     CK(cudaMemsetAsync(c->bd.n_probe, 0, 2 * sizeof(int), c->stream));
     CK(cudaMemsetAsync(npend, 0, sizeof(int), c->stream));
     batch_init_draw(c->r, c->pr, c->bd, pending, map, a, lc);
-    gp_energy_pass(c->gp, c->bd, 0, lc);
+    if (c->batch_backend == 3)
+      gp_energy_pass(c->gp, c->bd, 0, lc);
+    else  // tensor-core logistic regression: energies written in place over slice 0 of the partials
+      lr_energies(c->lr, c->bd.P[0], c->dp, c->bd.n_probe, c->bd.partial[0], lc);
     batch_init_accept(c->r, c->bd, map, pending, npend, lc);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(c->h_nprobe, npend, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
@@ -994,7 +997,9 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
   }
   // ---- init: prior draws (R-20), then the first metric ----
   LaunchCtx lc = lctx(c);
-  if (en.kind == NSS_E_GP_ARD) {
+  // energies with a batched tensor-core / Cholesky implementation initialise
+  // through it (the n prior draws are one batch), the rest per warp
+  if (en.kind == NSS_E_GP_ARD || (en.kind == NSS_E_LOGREG && c->lr_ok)) {
     if ((s = init_batched(c))) return bail(s);
   } else {
     launch_init(r, pr, en, lc);
