@@ -19,6 +19,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kLoSharedMax = 64;  // factor kept in shared memory up to this d
+constexpr int kSplitMinD = 33;    // from this d on the metric is three launches (grid-wide reduction)
 constexpr double kKappaInf = 1.3035;
 constexpr double kPi = 3.14159265358979323846;
 
@@ -28,9 +29,14 @@ __device__ __forceinline__ double *raw_groups(double *sm, int nent, int d, int n
   return reinterpret_cast<double *>(raw + ((static_cast<long long>(rows) * dp + 1) & ~1LL));
 }
 
+// mode 0: one launch (phase 1 in every CTA, phase 2 in the last one by
+// ticket); mode 1: phase 1 only (partials written, no ticket); mode 2: phase 2
+// only, in one CTA, from `partials` already reduced to one row (nblk = 1) by
+// k_metric_reduce.  Large d uses 1 -> reduce -> 2 (a grid-wide reduction
+// instead of one CTA reading every partial); the sums are the same.
 __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials, unsigned *ticket, int nblk,
                                                      double reg, int width_rule, double width_param,
-                                                     int end_of_iter) {
+                                                     int end_of_iter, int mode) {
   DevState *st = r.st;
   if (st->error) return;
   if (end_of_iter && st->finalised) return;
@@ -47,6 +53,7 @@ __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials,
   __shared__ float red_min[kThreads / 32];
   __shared__ int sh_last;
 
+  if (mode != 2) {
   if (tid == 0 && blockIdx.x == 0) st->stamp[8] = global_ns();
   // ---------------- phase 1: partial shifted sums of this CTA's rows ----------------
   const int chunk = (n + nblk - 1) / nblk;
@@ -128,12 +135,16 @@ __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials,
     float mn = red_min[0];
     for (int w = 1; w < kThreads / 32; ++w) mn = fminf(mn, red_min[w]);
     out[nent] = static_cast<double>(mn);
-    __threadfence();
-    sh_last = atomicAdd(ticket, 1u) == static_cast<unsigned>(nblk - 1);
+    if (mode == 0) {
+      __threadfence();
+      sh_last = atomicAdd(ticket, 1u) == static_cast<unsigned>(nblk - 1);
+    }
   }
+  if (mode == 1) return;
   __syncthreads();
   if (!sh_last) return;
   __threadfence();
+  }
   if (tid == 0) st->stamp[10] = global_ns();
 
   // ---------------- phase 2 (last CTA): reduce, regularise, factorise ----------------
@@ -310,6 +321,33 @@ __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials,
   }
 }
 
+// The large-d reduction of k_metric's partials: thread e sums entry e over
+// the blocks in block order (the order and operations of the one-CTA
+// reduction in phase 2, so the sums are identical); entry nent holds the
+// minimum energy.
+__global__ void __launch_bounds__(128) k_metric_reduce(RunDev r, const double *partials, int nblk, int nent1,
+                                                       double *sums, int end_of_iter) {
+  const DevState *st = r.st;
+  if (st->error || (end_of_iter && st->finalised)) return;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nent1) return;
+  const bool is_min = e == nent1 - 1;
+  double acc = is_min ? INFINITY : 0.0;
+  int b = 0;
+  for (; b + 15 < nblk; b += 16) {
+    double v[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = partials[static_cast<long long>(b + q) * nent1 + e];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) acc = is_min ? fmin(acc, v[q]) : acc + v[q];
+  }
+  for (; b < nblk; ++b) {
+    const double v = partials[static_cast<long long>(b) * nent1 + e];
+    acc = is_min ? fmin(acc, v) : acc + v;
+  }
+  sums[e] = acc;
+}
+
 // A9 / R-19 on demand (the host asks for the run's state between
 // iterations): minimum live energy, then the same test the next select
 // kernel would make.
@@ -378,9 +416,24 @@ void launch_metric(const RunDev &r, double metric_reg, int width_rule, double wi
     attr = true;
   }
   NSS_PIN_CARVEOUT(k_metric);
-  k_metric<<<n_blocks, kThreads, metric_smem(r.n, r.d, n_blocks), lc.stream>>>(r, partials, ticket, n_blocks, metric_reg,
-                                                                 width_rule, width_param, end_of_iteration);
-  ++*lc.launch_counter;
+  const size_t smem = metric_smem(r.n, r.d, n_blocks);
+  if (r.d < kSplitMinD || n_blocks == 1) {
+    k_metric<<<n_blocks, kThreads, smem, lc.stream>>>(r, partials, ticket, n_blocks, metric_reg, width_rule,
+                                                      width_param, end_of_iteration, 0);
+    ++*lc.launch_counter;
+    return;
+  }
+  // large d: partials by every CTA, a grid-wide reduction into the row after
+  // the partials (nss_init sizes the buffer for n_blocks + 1 rows), then the
+  // factorisation from that one row
+  const int nent1 = r.d * (r.d + 1) / 2 + r.d + 1;
+  double *sums = partials + static_cast<long long>(n_blocks) * nent1;
+  k_metric<<<n_blocks, kThreads, smem, lc.stream>>>(r, partials, ticket, n_blocks, metric_reg, width_rule,
+                                                    width_param, end_of_iteration, 1);
+  k_metric_reduce<<<(nent1 + 127) / 128, 128, 0, lc.stream>>>(r, partials, n_blocks, nent1, sums, end_of_iteration);
+  k_metric<<<1, kThreads, smem, lc.stream>>>(r, sums, ticket, 1, metric_reg, width_rule, width_param,
+                                             end_of_iteration, 2);
+  *lc.launch_counter += 3;
 }
 
 }  // namespace nss

@@ -971,7 +971,7 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
   if ((s = dalloc(c, &c->summary, R + 3))) return bail(s);
   c->nblk = metric_blocks(r.n, d);
   const int nent = d * (d + 1) / 2 + d + 1;
-  if ((s = dalloc(c, &c->partials, static_cast<size_t>(c->nblk) * nent))) return bail(s);
+  if ((s = dalloc(c, &c->partials, static_cast<size_t>(c->nblk + 1) * nent))) return bail(s);  // + the reduced row
   if ((s = dalloc(c, &c->ticket, 1))) return bail(s);
   {
     std::vector<double> ninf(R + 1, -INFINITY);
