@@ -25,8 +25,8 @@ constexpr double kPi = 3.14159265358979323846;
 
 // shared-memory slot for the per-group entry sums, after this CTA's rows
 __device__ __forceinline__ double *raw_groups(double *sm, int nent, int d, int npair, int rows, int dp) {
-  float *raw = reinterpret_cast<float *>(sm + nent + d + (2 * npair + 7) / 8);
-  return reinterpret_cast<double *>(raw + ((static_cast<long long>(rows) * dp + 1) & ~1LL));
+  double *yd = sm + nent + d + (2 * npair + 7) / 8;
+  return yd + static_cast<long long>(rows) * dp;
 }
 
 // mode 0: one launch (phase 1 in every CTA, phase 2 in the last one by
@@ -48,8 +48,9 @@ __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials,
   double *shift = S + nent;               // d
   unsigned char *pi = reinterpret_cast<unsigned char *>(shift + d);
   unsigned char *pj = pi + npair;
-  // this CTA's rows as stored (fp32, row stride dp), after the pair tables
-  float *raw = reinterpret_cast<float *>(sm + nent + d + (2 * npair + 7) / 8);
+  // this CTA's rows shifted by row 0, y = x - x_0 in fp64 (row stride dp),
+  // after the pair tables: converted once here, not once per entry
+  double *yd = sm + nent + d + (2 * npair + 7) / 8;
   __shared__ float red_min[kThreads / 32];
   __shared__ int sh_last;
 
@@ -63,7 +64,10 @@ __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials,
   // one batch of loads: the chunk is contiguous in X
   {
     const float *src = r.X + static_cast<long long>(g0) * dp;
-    for (int q = tid; q < rows * dp; q += blockDim.x) raw[q] = src[q];
+    for (int q = tid; q < rows * dp; q += blockDim.x) {
+      const int c = q % dp;
+      yd[q] = c < d ? static_cast<double>(src[q]) - static_cast<double>(r.X[c]) : 0.0;
+    }
   }
   float emin = INFINITY;
   for (int g = g0 + tid; g < g1; g += blockDim.x) emin = fminf(emin, r.E[g]);
@@ -91,29 +95,27 @@ __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials,
     const int step = 4 * G;
     if (e < npair) {
       const int i = pi[e], j = pj[e];
-      const double si = shift[i], sj = shift[j];
       int rr = grp;
       for (; rr + 3 * G < rows; rr += step) {
-        a0 = fma(static_cast<double>(raw[rr * dp + i]) - si, static_cast<double>(raw[rr * dp + j]) - sj, a0);
-        a1 = fma(static_cast<double>(raw[(rr + G) * dp + i]) - si, static_cast<double>(raw[(rr + G) * dp + j]) - sj, a1);
-        a2 = fma(static_cast<double>(raw[(rr + 2 * G) * dp + i]) - si,
-                 static_cast<double>(raw[(rr + 2 * G) * dp + j]) - sj, a2);
-        a3 = fma(static_cast<double>(raw[(rr + 3 * G) * dp + i]) - si,
-                 static_cast<double>(raw[(rr + 3 * G) * dp + j]) - sj, a3);
+        a0 = fma(yd[rr * dp + i], yd[rr * dp + j], a0);
+        a1 = fma(yd[(rr + G) * dp + i], yd[(rr + G) * dp + j], a1);
+        a2 = fma(yd[(rr + 2 * G) * dp + i],
+                 yd[(rr + 2 * G) * dp + j], a2);
+        a3 = fma(yd[(rr + 3 * G) * dp + i],
+                 yd[(rr + 3 * G) * dp + j], a3);
       }
       for (; rr < rows; rr += G)
-        a0 = fma(static_cast<double>(raw[rr * dp + i]) - si, static_cast<double>(raw[rr * dp + j]) - sj, a0);
+        a0 = fma(yd[rr * dp + i], yd[rr * dp + j], a0);
     } else {
       const int i = e - npair;
-      const double si = shift[i];
       int rr = grp;
       for (; rr + 3 * G < rows; rr += step) {
-        a0 += static_cast<double>(raw[rr * dp + i]) - si;
-        a1 += static_cast<double>(raw[(rr + G) * dp + i]) - si;
-        a2 += static_cast<double>(raw[(rr + 2 * G) * dp + i]) - si;
-        a3 += static_cast<double>(raw[(rr + 3 * G) * dp + i]) - si;
+        a0 += yd[rr * dp + i];
+        a1 += yd[(rr + G) * dp + i];
+        a2 += yd[(rr + 2 * G) * dp + i];
+        a3 += yd[(rr + 3 * G) * dp + i];
       }
-      for (; rr < rows; rr += G) a0 += static_cast<double>(raw[rr * dp + i]) - si;
+      for (; rr < rows; rr += G) a0 += yd[rr * dp + i];
     }
     Sg[grp * nent + e] = (a0 + a1) + (a2 + a3);
   }
@@ -385,7 +387,7 @@ size_t metric_smem(int n, int d, int nblk) {
   const int rows = (n + nblk - 1) / nblk;
   const int G = nent < kThreads ? kThreads / nent : 1;  // row groups (raw_groups)
   const size_t p1 = static_cast<size_t>(nent + d) * 8 + ((2 * static_cast<size_t>(npair) + 7) / 8) * 8 +
-                    (static_cast<size_t>(rows) * dp + 1) / 2 * 8 + (G > 1 ? static_cast<size_t>(G) * nent * 8 : 0) + 64;
+                    static_cast<size_t>(rows) * dp * 8 + (G > 1 ? static_cast<size_t>(G) * nent * 8 : 0) + 64;
   const size_t p2 = (static_cast<size_t>(d) * (d | 1) + d + (d <= kLoSharedMax ? static_cast<size_t>(d) * d : 0)) * 8 +
                     2 * static_cast<size_t>(npair) + 16;
   return p1 > p2 ? p1 : p2;
@@ -397,7 +399,12 @@ int metric_blocks(int n, int d) {
   const int npair = d * (d + 1) / 2;
   const int dp = (d + 3) & ~3;
   int rows_per_block = npair > 1000 ? 160 : 128;
-  const int rows_max = 96 * 1024 / (dp * 4);  // the CTA's rows stay in shared memory
+  // the CTA's rows stay in shared memory as fp64, beside the entry sums and
+  // pair tables, within the 200 KB the kernel is given
+  const int nent = npair + d, G = nent < kThreads ? kThreads / nent : 1;
+  const long long fixed = 64 + static_cast<long long>(nent + d) * 8 + ((2LL * npair + 7) / 8) * 8 +
+                          (G > 1 ? static_cast<long long>(G) * nent * 8 : 0);
+  const int rows_max = static_cast<int>((200LL * 1024 - fixed) / (dp * 8));
   if (rows_per_block > rows_max) rows_per_block = rows_max;
   const int b = (n + rows_per_block - 1) / rows_per_block;
   return b < 1 ? 1 : b;
