@@ -18,7 +18,7 @@ namespace nss {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kLoSharedMax = 64;  // factor kept in shared memory up to this d
+constexpr int kLoSharedMax = 100;  // factor kept in shared memory up to this d (A + factor within 200 KB)
 constexpr int kSplitMinD = 33;    // from this d on the metric is three launches (grid-wide reduction)
 constexpr double kKappaInf = 1.3035;
 constexpr double kPi = 3.14159265358979323846;
@@ -228,12 +228,92 @@ __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials,
     S1[i] = A[i * ld + i];  // regularised diagonal, kept for the fallback
   }
   __syncthreads();
+  if (tid == 0) st->stamp[14] = global_ns();
   // right-looking Cholesky, one barrier per column: every thread reads the
   // pivot, writes its share of column j of L and of the trailing update
   // A_il -= A_ij A_lj / A_jj (column j itself is never rewritten)
   const bool one_warp = d <= 32;
   const int nthr = one_warp ? 32 : static_cast<int>(blockDim.x);
-  if (tid < nthr) {
+  if (d >= kSplitMinD) {
+    // large d: blocked right-looking, 8-column panels.  Warp 0 factorises
+    // the panel in registers (lane l: rows j0 + l + 32 k, pivots and panel
+    // rows exchanged by shuffles, one rsqrt per column), then all threads
+    // apply the rank-8 update A_il -= sum_c L_i,j0+c L_l,j0+c to the trailing
+    // lower triangle: two barriers per panel instead of one per column.
+    constexpr int NB = 8;
+    const int ty = tid >> 4, tx = tid & 15;
+    for (int j0 = 0; j0 < d; j0 += NB) {
+      const int nb = min(NB, d - j0);
+      if (tid < 32) {
+        double pv[4][NB];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int c = 0; c < NB; ++c) {
+            const int rr = j0 + tid + 32 * k;
+            pv[k][c] = (rr < d && c < nb && j0 + c <= rr) ? A[rr * ld + j0 + c] : 0.0;
+          }
+        bool bad = false;
+#pragma unroll
+        for (int c = 0; c < NB; ++c) {
+          if (c < nb && !bad) {
+            const double piv = __shfl_sync(0xffffffffu, pv[0][c], c);  // row j0 + c: lane c, k = 0
+            if (!(piv > 0.0) || !isfinite(piv)) {
+              bad = true;  // uniform
+            } else {
+              const double rs = rsqrt(piv);
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const int rr = j0 + tid + 32 * k;
+                if (rr == j0 + c) pv[k][c] = piv * rs;
+                else if (rr > j0 + c) pv[k][c] *= rs;
+              }
+#pragma unroll
+              for (int c2 = c + 1; c2 < NB; ++c2) {
+                const double l2 = __shfl_sync(0xffffffffu, pv[0][c], c2);  // L_{j0+c2, j0+c}
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  const int rr = j0 + tid + 32 * k;
+                  if (c2 < nb && rr >= j0 + c2) pv[k][c2] = fma(-pv[k][c], l2, pv[k][c2]);
+                }
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int c = 0; c < NB; ++c) {
+            const int rr = j0 + tid + 32 * k;
+            if (rr < d && c < nb && j0 + c <= rr) {
+              A[rr * ld + j0 + c] = pv[k][c];
+              Lo[rr * d + j0 + c] = pv[k][c];
+            }
+          }
+        if (bad && tid == 0) sh_fail = 1;
+      }
+      __syncthreads();
+      if (sh_fail) break;  // uniform
+      const int b0 = j0 + nb;
+      for (int u = 0; u < 8; ++u) {
+        const int i = b0 + ty + 16 * u;
+        if (i >= d) break;
+        double li[NB];
+#pragma unroll
+        for (int c = 0; c < NB; ++c) li[c] = c < nb ? A[i * ld + j0 + c] : 0.0;
+        for (int v = 0; v < 8; ++v) {
+          const int l = b0 + tx + 16 * v;
+          if (l > i) break;
+          double sacc = 0.0;
+#pragma unroll
+          for (int c = 0; c < NB; ++c)
+            if (c < nb) sacc = fma(li[c], A[l * ld + j0 + c], sacc);
+          A[i * ld + l] -= sacc;
+        }
+      }
+      __syncthreads();
+    }
+  } else if (tid < nthr) {
     for (int j = 0; j < d; ++j) {
       const double ajj = A[j * ld + j];
       if (!(ajj > 0.0) || !isfinite(ajj)) {
@@ -269,6 +349,7 @@ __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials,
     }
   }
   __syncthreads();
+  if (tid == 0) st->stamp[15] = global_ns();
   if (sh_fail) {  // R-8 fallback: diag(sqrt(Sigma_jj)), 1 where the variance is 0
     for (int e = tid; e < d * d; e += blockDim.x) {
       const int i = e / d, j = e - i * d;

@@ -25,3 +25,4 @@ print(name, "select phases (ns): load", sel[0], "minmax", sel[1], "radix", sel[2
       "outputs", sel[5], " total", st[6] - st[0])
 print(name, "metric phases (ns): load", met[0], "compute+ticket", met[1], "psum", met[2], "chol", met[3], "tail", met[4],
       " total", st[13] - st[8], " select->metric start", st[8] - st[6])
+print(name, "metric chol split (ns): normalise", st[14] - st[11], "factorise", st[15] - st[14], "copies", st[12] - st[15])
