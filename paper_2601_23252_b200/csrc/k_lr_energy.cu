@@ -33,24 +33,34 @@ namespace nss {
 namespace {
 
 constexpr int BM = 128;          // probes per tile (UMMA M)
-constexpr int BN = 128;          // data rows per tile (UMMA N)
 constexpr int KSTEPS = 7;        // K = 112 >= d
 constexpr int kSplits = 2;       // bf16 terms per probe coordinate
-constexpr int kStages = 4;       // TMA ring depth for X tiles
-constexpr int kAcc = 4;          // TMEM accumulator buffers (4 x 128 columns)
-constexpr int kAtom = BM * 128;  // bytes of one [128 rows x 128 B] swizzle-128B region
+constexpr int kAtom = BM * 128;  // bytes of one [128 rows x 128 B] swizzle-128B region (probe tile)
 constexpr int kSmemA = kSplits * 2 * kAtom;      // splits x 2 k-blocks
-constexpr int kSmemB = kStages * 2 * kAtom;      // stages x 2 k-blocks
 constexpr int kEpiWarps = 16;                    // four per TMEM lane quarter (column quarters)
 constexpr int kColParts = kEpiWarps / 4;         // column parts of a tile (one per epilogue warp of a quarter)
-constexpr int kPartCols = BN / kColParts;        // columns per part (32: one tcgen05.ld)
 constexpr int kThreads = 64 + 32 * kEpiWarps;    // warp 0 TMA, warp 1 MMA, warps 2.. epilogue
 constexpr int kUnitsPerSM = 8;
+constexpr int kMaxRing = 4;
+
+// Data-tile width BN (UMMA N): 128 (4-stage TMA ring, 4 TMEM accumulators of
+// 128 columns) or 256 (half the operand bytes per flop; 2 stages, 2
+// accumulators of 256 columns, two tcgen05.ld per epilogue warp and tile).
+template <int BN_>
+struct LrCfg {
+  static constexpr int BN = BN_;
+  static constexpr int kStages = BN_ == 128 ? 4 : 2;          // TMA ring depth for X tiles
+  static constexpr int kAcc = BN_ == 128 ? 4 : 2;             // TMEM accumulators (kAcc x BN = 512 columns)
+  static constexpr int kAtomB = BN_ * 128;                    // one [BN rows x 128 B] swizzle-128B region
+  static constexpr int kSmemB = kStages * 2 * kAtomB;         // stages x 2 k-blocks
+  static constexpr int kPartCols = BN_ / kColParts;           // columns per epilogue part
+  static constexpr int kChunks = kPartCols / 32;              // tcgen05.ld.32x32b.x32 per part
+};
 
 struct __align__(8) Bars {
   uint64_t a_full, a_empty;
-  uint64_t full[kStages], empty[kStages];
-  uint64_t tfull[kAcc], tempty[kAcc];
+  uint64_t full[kMaxRing], empty[kMaxRing];
+  uint64_t tfull[kMaxRing], tempty[kMaxRing];
   uint32_t tmem_base;
 };
 
@@ -68,15 +78,18 @@ struct Sched {
   }
 };
 
+template <int BN_>
 __global__ void __launch_bounds__(kThreads, 1)
     k_lr_energy(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 float *partial, int *slices_out, const int *n_probe_ptr, int *reset_counter, int p_stride,
                 int n_data, int n_tiles) {
+  using C = LrCfg<BN_>;
+  constexpr int BN = C::BN, kStages = C::kStages, kAcc = C::kAcc, kPartCols = C::kPartCols;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sA = smem;
   uint8_t *sB = smem + kSmemA;
-  Bars *bars = reinterpret_cast<Bars *>(smem + kSmemA + kSmemB);
+  Bars *bars = reinterpret_cast<Bars *>(smem + kSmemA + C::kSmemB);
 
   const int G = gridDim.x;
   const int n_probe = *n_probe_ptr;
@@ -129,9 +142,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int t = t0; t < t1; ++t, ++it) {
         const int st = it % kStages;
         if (it >= kStages) tc::mbar_wait(&bars->empty[st], ((it / kStages) - 1) & 1);
-        tc::mbar_arrive_expect_tx(&bars->full[st], 2 * kAtom);
+        tc::mbar_arrive_expect_tx(&bars->full[st], 2 * C::kAtomB);
         for (int kb = 0; kb < 2; ++kb)
-          tc::tma_load_2d(sB + (st * 2 + kb) * kAtom, &tmB, &bars->full[st], kb * 64, t * BN);
+          tc::tma_load_2d(sB + (st * 2 + kb) * C::kAtomB, &tmB, &bars->full[st], kb * 64, t * BN);
       }
     }
   } else if (warp == 1 && lane == 0) {
@@ -160,7 +173,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int ks = 0; ks < KSTEPS; ++ks) {
             const int kb = ks >> 2, koff = (ks & 3) * 32;  // 16 bf16 = 32 B per k-step
             const uint64_t ad = tc::umma_desc_sw128(sA + (q * 2 + kb) * kAtom + koff);
-            const uint64_t bd = tc::umma_desc_sw128(sB + (st * 2 + kb) * kAtom + koff);
+            const uint64_t bd = tc::umma_desc_sw128(sB + (st * 2 + kb) * C::kAtomB + koff);
             tc::umma_f16(d_tmem, ad, bd, idesc, (q | ks) != 0);
           }
         }
@@ -184,21 +197,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::tc_fence_after();
         const int cbase = chalf * kPartCols;
         const int col0 = t * BN + cbase;
-        float v[1][32];
-        tc::tmem_ld32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + cbase, v[0]);
+        float v[C::kChunks][32];
+#pragma unroll
+        for (int ch = 0; ch < C::kChunks; ++ch)
+          tc::tmem_ld32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + cbase + 32 * ch, v[ch]);
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&bars->tempty[acc]);  // buffer fully read: release it
         // softplus(a) - y a = |a|/2 + a/2 - y a + log(1 + e^-|a|); the linear
         // part sum_r (1/2 - y_r) a_r = theta . g is added per probe row by the
         // consumer (lr_engine.cu), so per element: sum |a| and the product of
-        // (1 + e^-|a|) (one ex2; one lg2 per 32 factors), two chains each
+        // (1 + e^-|a|) (one ex2; one lg2 per kPartCols / 2 factors), two chains each
         float s0 = 0.f, s1 = 0.f, p0 = 1.f, p1 = 1.f;
         const int valid = n_data - col0;  // >= kPartCols except in the ragged last tile
         if (valid >= kPartCols) {
 #pragma unroll
           for (int cc = 0; cc < kPartCols; ++cc) {
-            const float a = v[0][cc];
+            const float a = v[cc >> 5][cc & 31];
             const float e = tc::ex2_approx(-fabsf(a) * 1.4426950408889634f);
             if (cc & 1) {
               p1 = fmaf(p1, e, p1);
@@ -212,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int cc = 0; cc < kPartCols; ++cc) {
             if (cc < valid) {  // padded data rows contribute nothing
-              const float a = v[0][cc];
+              const float a = v[cc >> 5][cc & 31];
               const float e = tc::ex2_approx(-fabsf(a) * 1.4426950408889634f);
               if (cc & 1) {
                 p1 = fmaf(p1, e, p1);
@@ -224,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        // each product has <= 16 factors in (1, 2]: no overflow
+        // each product has <= kPartCols / 2 <= 32 factors in (1, 2]: no overflow
         e_sum += static_cast<double>(fmaf(0.6931471805599453f, __log2f(p0) + __log2f(p1), 0.5f * (s0 + s1)));
       }
       const int row = m * BM + row_in_tile;
@@ -238,31 +253,45 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tc::tmem_dealloc<kAcc * BN>(tmem);
 }
 
-}  // namespace
+template <int BN_>
+size_t smem_of() { return kSmemA + LrCfg<BN_>::kSmemB + sizeof(Bars) + 1024; }
 
-size_t lr_energy_smem() { return kSmemA + kSmemB + sizeof(Bars) + 1024; }
-int lr_energy_splits() { return kSplits; }
-
-int lr_max_slices(int n_tiles) { return kColParts * n_tiles; }
-
-void launch_lr_energy(const CUtensorMap &tmA, const CUtensorMap &tmB, float *partial, int *slices_out,
-                      const int *n_probe, int *reset_counter, int p_stride, int n_data, const LaunchCtx &lc) {
+template <int BN_>
+void launch_bn(const CUtensorMap &tmA, const CUtensorMap &tmB, float *partial, int *slices_out, const int *n_probe,
+               int *reset_counter, int p_stride, int n_data, const LaunchCtx &lc) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_lr_energy, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lr_energy_smem()));
+    cudaFuncSetAttribute(k_lr_energy<BN_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem_of<BN_>()));
     attr = true;
   }
-  NSS_PIN_CARVEOUT(k_lr_energy);
+  NSS_PIN_CARVEOUT(k_lr_energy<BN_>);
   static int sms = 0;
   if (!sms) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int n_tiles = (n_data + BN - 1) / BN;
-  k_lr_energy<<<sms, kThreads, lr_energy_smem(), lc.stream>>>(tmA, tmB, partial, slices_out, n_probe, reset_counter,
-                                                             p_stride, n_data, n_tiles);
+  const int n_tiles = (n_data + BN_ - 1) / BN_;
+  k_lr_energy<BN_><<<sms, kThreads, smem_of<BN_>(), lc.stream>>>(tmA, tmB, partial, slices_out, n_probe,
+                                                                 reset_counter, p_stride, n_data, n_tiles);
   ++*lc.launch_counter;
+}
+
+}  // namespace
+
+size_t lr_energy_smem() { return smem_of<128>() > smem_of<256>() ? smem_of<128>() : smem_of<256>(); }
+int lr_energy_splits() { return kSplits; }
+
+// slices per probe row: kColParts per data slice, at most one data slice per 128-row tile
+int lr_max_slices(int n_tiles) { return kColParts * n_tiles; }
+
+void launch_lr_energy(const CUtensorMap &tmA, const CUtensorMap &tmB, float *partial, int *slices_out,
+                      const int *n_probe, int *reset_counter, int p_stride, int n_data, int bn, const LaunchCtx &lc) {
+  if (bn == 256)
+    launch_bn<256>(tmA, tmB, partial, slices_out, n_probe, reset_counter, p_stride, n_data, lc);
+  else
+    launch_bn<128>(tmA, tmB, partial, slices_out, n_probe, reset_counter, p_stride, n_data, lc);
 }
 
 }  // namespace nss

@@ -7,6 +7,8 @@
 #include <cmath>
 #include <vector>
 
+#include <cstdlib>
+
 #include "lr_engine.cuh"
 
 namespace nss {
@@ -14,7 +16,7 @@ namespace nss {
 size_t lr_energy_smem();
 int lr_max_slices(int n_tiles);
 void launch_lr_energy(const CUtensorMap &tmA, const CUtensorMap &tmB, float *partial, int *slices_out,
-                      const int *n_probe, int *reset_counter, int p_stride, int n_data, const LaunchCtx &lc);
+                      const int *n_probe, int *reset_counter, int p_stride, int n_data, int bn, const LaunchCtx &lc);
 
 namespace {
 
@@ -66,13 +68,13 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-// 2-D bf16 tensor [rows][128] (K contiguous), box {64, 128}, 128-byte swizzle
-bool make_map(CUtensorMap *map, void *base, long long rows) {
+// 2-D bf16 tensor [rows][128] (K contiguous), box {64, box_rows}, 128-byte swizzle
+bool make_map(CUtensorMap *map, void *base, long long rows, unsigned box_rows = 128) {
   auto enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[2] = {128, static_cast<cuuint64_t>(rows)};
   cuuint64_t strides[1] = {128 * sizeof(__nv_bfloat16)};
-  cuuint32_t box[2] = {64, 128};
+  cuuint32_t box[2] = {64, box_rows};
   cuuint32_t estr[2] = {1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -122,7 +124,10 @@ cudaError_t lr_setup(LrEngine &L, const double *X, const double *y, long long N,
   if ((e = cudaMalloc(&L.slices, 2 * sizeof(int)))) return e;
   if ((e = cudaMemset(L.slices, 0, 2 * sizeof(int)))) return e;
   if ((e = cudaMemcpy(L.Xb, xb.data(), xb.size() * sizeof(__nv_bfloat16), cudaMemcpyHostToDevice))) return e;
-  if (!make_map(&L.tmB, L.Xb, L.n_pad)) return cudaErrorInvalidValue;
+  // data tiles of BN = 256 rows (half the operand bytes per flop of 128; rows
+  // past n_pad are zero-filled by TMA); NSS_LR_BN=128 selects 128-row tiles
+  L.bn = (getenv("NSS_LR_BN") && atoi(getenv("NSS_LR_BN")) == 128) ? 128 : 256;
+  if (!make_map(&L.tmB, L.Xb, L.n_pad, static_cast<unsigned>(L.bn))) return cudaErrorInvalidValue;
   for (int q = 0; q < 2; ++q)
     if (!make_map(&L.tmA[q], L.A[q], 3ll * L.p_stride)) return cudaErrorInvalidValue;
   return cudaSuccess;
@@ -143,7 +148,7 @@ void lr_free(LrEngine &L) {
 void lr_energies(const LrEngine &L, const float *P, int ldp, const int *n_probe, float *E, const LaunchCtx &lc) {
   k_split3<<<296, 256, 0, lc.stream>>>(P, ldp, n_probe, L.d, L.A[0], L.p_stride);
   launch_lr_energy(L.tmA[0], L.tmB, L.partial[0], L.slices, n_probe, nullptr, L.p_stride,
-                   static_cast<int>(L.N), lc);
+                   static_cast<int>(L.N), L.bn, lc);
   k_lr_reduce<<<(L.max_probe + 255) / 256, 256, 0, lc.stream>>>(L.partial[0], L.p_stride, L.slices, n_probe, E, P, ldp,
                                                                   L.d, L.g);
   *lc.launch_counter += 2;
@@ -151,7 +156,7 @@ void lr_energies(const LrEngine &L, const float *P, int ldp, const int *n_probe,
 
 void lr_energy_pass(const LrEngine &L, int parity, const int *n_probe, int *reset_counter, const LaunchCtx &lc) {
   launch_lr_energy(L.tmA[parity], L.tmB, L.partial[parity], L.slices + parity, n_probe, reset_counter,
-                   L.p_stride, static_cast<int>(L.N), lc);
+                   L.p_stride, static_cast<int>(L.N), L.bn, lc);
 }
 
 }  // namespace nss

@@ -10,6 +10,7 @@ namespace nss {
 struct LrEngine {
   long long N = 0, n_pad = 0;
   int d = 0, n_tiles = 0, p_stride = 0, max_probe = 0, n_splits = 1;
+  int bn = 128;                 // data-tile width of the tensor-core pass (UMMA N): 128 or 256
   __nv_bfloat16 *Xb = nullptr;  // [n_pad][128] bf16 data rows (K padded with zeros)
   // linear part of the energy: sum_r (1/2 - y_r) a_r = theta . g, g = X^T (1/2 - y)
   // (fp64 on the host, 128 floats, zero past d); per-row values live in the
