@@ -85,6 +85,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 int n_data, int n_tiles) {
   using C = LrCfg<BN_>;
   constexpr int BN = C::BN, kStages = C::kStages, kAcc = C::kAcc, kPartCols = C::kPartCols;
+  __shared__ double red4[4][kColParts][32];  // per lane quarter: the column parts' unit sums
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sA = smem;
@@ -96,7 +97,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const Sched sch(n_probe, n_tiles, G);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     if (reset_counter) *reset_counter = 0;  // the next round's row counter
-    *slices_out = kColParts * sch.S;        // per unit: one slice per column part
+    *slices_out = sch.S;                    // per unit: one slice (the column parts combined on chip)
   }
   int u0, u1;
   sch.range(blockIdx.x, G, u0, u1);
@@ -243,9 +244,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         e_sum += static_cast<double>(fmaf(0.6931471805599453f, __log2f(p0) + __log2f(p1), 0.5f * (s0 + s1)));
       }
       const int row = m * BM + row_in_tile;
-      // the column parts write adjacent slices: slice index kColParts s + part
-      if (row < n_probe)
-        partial[static_cast<long long>(kColParts * s + chalf) * p_stride + row] = static_cast<float>(e_sum);
+      // the kColParts warps of a TMEM lane quarter combine their column parts
+      // in shared memory (fixed order, fp64) behind a named barrier of the
+      // quarter's 128 threads: one slice per unit and probe row
+      red4[quarter][chalf][lane] = e_sum;
+      asm volatile("bar.sync %0, %1;" ::"r"(2 + quarter), "r"(32 * kColParts) : "memory");
+      if (chalf == 0 && row < n_probe) {
+        double tot = 0.0;
+#pragma unroll
+        for (int c = 0; c < kColParts; ++c) tot += red4[quarter][c][lane];
+        partial[static_cast<long long>(s) * p_stride + row] = static_cast<float>(tot);
+      }
+      asm volatile("bar.sync %0, %1;" ::"r"(2 + quarter), "r"(32 * kColParts) : "memory");  // red4 is reused
     }
   }
   tc::tc_fence_before();
