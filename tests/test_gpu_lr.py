@@ -38,6 +38,21 @@ def test_lr_energy_batch(d, n_data, P):
         assert abs(o.energy(theta[i]) - e_ref[i]) < 1e-9 * max(1, abs(e_ref[i]))
 
 
+@pytest.mark.parametrize("bn", ["128", "256"])
+@pytest.mark.parametrize("n_data,P", [(10_000, 300), (1000, 129)])
+def test_lr_energy_batch_tile_widths(bn, n_data, P, monkeypatch):
+    """Both data-tile widths of the tcgen05 pass (N = 256 default, 128 via
+    NSS_LR_BN, read when the engine is set up) against the fp64 reference,
+    including a ragged last data tile (1000 = 3 x 256 + 232)."""
+    from paper_2601_23252_b200 import nss
+    monkeypatch.setenv("NSS_LR_BN", bn)
+    prob = W.logreg(100, n_data=n_data, seed=11)
+    theta = np.random.default_rng(P).standard_normal((P, 100)) * 0.7
+    e_gpu = nss.lr_energy_batch(prob.data_x, prob.data_y, theta)
+    e_ref = _ref_energy(prob, theta)
+    assert np.all(np.abs(e_gpu - e_ref) <= 1e-5 * np.maximum(1.0, np.abs(e_ref))), np.max(np.abs(e_gpu - e_ref))
+
+
 def test_lr_energy_rejects_non_bf16_data():
     from paper_2601_23252_b200 import nss
     prob = W.logreg(4, n_data=50, seed=1)
