@@ -462,7 +462,9 @@ __global__ void __launch_bounds__(kThreads) k_term_probe(RunDev r, int probe, De
   }
 }
 
-size_t metric_smem(int n, int d, int nblk) {
+// mode 0: both phases; 1: phase 1 only (the large-d partials: sized for
+// their rows alone, so two CTAs fit per SM); 2: phase 2 only
+size_t metric_smem(int n, int d, int nblk, int mode = 0) {
   const int npair = d * (d + 1) / 2, nent = npair + d;
   const int dp = (d + 3) & ~3;
   const int rows = (n + nblk - 1) / nblk;
@@ -471,7 +473,7 @@ size_t metric_smem(int n, int d, int nblk) {
                     static_cast<size_t>(rows) * dp * 8 + (G > 1 ? static_cast<size_t>(G) * nent * 8 : 0) + 64;
   const size_t p2 = (static_cast<size_t>(d) * (d | 1) + d + (d <= kLoSharedMax ? static_cast<size_t>(d) * d : 0)) * 8 +
                     2 * static_cast<size_t>(npair) + 16;
-  return p1 > p2 ? p1 : p2;
+  return mode == 1 ? p1 : mode == 2 ? p2 : (p1 > p2 ? p1 : p2);
 }
 
 }  // namespace
@@ -479,7 +481,9 @@ size_t metric_smem(int n, int d, int nblk) {
 int metric_blocks(int n, int d) {
   const int npair = d * (d + 1) / 2;
   const int dp = (d + 3) & ~3;
-  int rows_per_block = npair > 1000 ? 160 : 128;
+  // large d: the grid-wide reduction makes more CTAs cheap, so every SM takes
+  // a short chunk of rows; small d: one launch, the last CTA reduces
+  int rows_per_block = d >= kSplitMinD ? 64 : (npair > 1000 ? 160 : 128);
   // the CTA's rows stay in shared memory as fp64, beside the entry sums and
   // pair tables, within the 200 KB the kernel is given
   const int nent = npair + d, G = nent < kThreads ? kThreads / nent : 1;
@@ -516,11 +520,11 @@ void launch_metric(const RunDev &r, double metric_reg, int width_rule, double wi
   // factorisation from that one row
   const int nent1 = r.d * (r.d + 1) / 2 + r.d + 1;
   double *sums = partials + static_cast<long long>(n_blocks) * nent1;
-  k_metric<<<n_blocks, kThreads, smem, lc.stream>>>(r, partials, ticket, n_blocks, metric_reg, width_rule,
-                                                    width_param, end_of_iteration, 1);
+  k_metric<<<n_blocks, kThreads, metric_smem(r.n, r.d, n_blocks, 1), lc.stream>>>(
+      r, partials, ticket, n_blocks, metric_reg, width_rule, width_param, end_of_iteration, 1);
   k_metric_reduce<<<(nent1 + 127) / 128, 128, 0, lc.stream>>>(r, partials, n_blocks, nent1, sums, end_of_iteration);
-  k_metric<<<1, kThreads, smem, lc.stream>>>(r, sums, ticket, 1, metric_reg, width_rule, width_param,
-                                             end_of_iteration, 2);
+  k_metric<<<1, kThreads, metric_smem(r.n, r.d, n_blocks, 2), lc.stream>>>(r, sums, ticket, 1, metric_reg, width_rule,
+                                                                          width_param, end_of_iteration, 2);
   *lc.launch_counter += 3;
 }
 
