@@ -190,6 +190,23 @@ def test_full_run_c2_analytic():
         assert abs(lz - truth) <= max(3 * sig, 0.05), (lz, sig, truth)
 
 
+def test_full_run_c3a_analytic_p3d():
+    """C3a at full size (d = 100, kappa = 100, n = 1e4, k = 1e3) run to
+    termination with p = 3d HRSS steps (the paper's high-d setting):
+    log N(mu_L; 0, Sigma_L + 25 I) within max(3 sigma, 0.05).  (At p = d the
+    chains under-mix and log Z comes out 3-5 sigma high,
+    profiles/r01_accuracy.md.)"""
+    from scipy import stats as st
+    prob, cfg = W.workload("C3a")
+    truth = st.multivariate_normal(np.zeros(prob.d), prob.meta["sigma_l"] + np.diag(prob.sd ** 2)).logpdf(
+        prob.mu - prob.mean)
+    res = _run_logz(prob, dict(n_live=cfg["n_live"], k=cfg["k"], steps=3 * prob.d,
+                               max_dead=cfg["n_live"] + cfg["k"] * 8000), [1])
+    for lz, sig, info in res:
+        assert info["terminated"]
+        assert abs(lz - truth) <= max(3 * sig, 0.05), (lz, sig, truth)
+
+
 def test_full_run_gpu_vs_oracle_c1():
     """Same seed: GPU and oracle full runs agree within the combined spread."""
     from oracle import nsso
