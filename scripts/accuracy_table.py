@@ -37,6 +37,20 @@ def truth_corr(prob):
     return -float(prob.c) + 0.5 * d * math.log(2 * math.pi) - 0.5 * logdetP + lz
 
 
+def truth_funnel(prob):
+    # box [-20, 20]^d (R-23): Z = |box|^-1 int_{-20}^{20} N(y; 0, sy^2) prod_{n<d} P(|x_n| <= 20 ; sd e^{y/2}) dy
+    from scipy import integrate, special
+    d, sy = prob.d, float(prob.sigma_y)
+    half = float(prob.hi[0])
+
+    def integrand(y):
+        m = special.erf(half / (math.exp(y / 2) * math.sqrt(2)))
+        return math.exp(stats.norm(0, sy).logpdf(y) + (d - 1) * math.log(max(m, 1e-300)))
+
+    val, _ = integrate.quad(integrand, -half, half, points=[-10, -5, 0, 5], limit=400)
+    return math.log(val) - d * math.log(2 * half)
+
+
 def runs(name, prob, cfg, seeds):
     rows = []
     for s in seeds:
@@ -57,6 +71,10 @@ def main():
         # a full d = 100 run takes several thousand iterations: a dead store for 8000 (3.2 GB of rows)
         ("C3a corrgauss100", W.workload("C3a")[0], dict(W.workload("C3a")[1], max_dead=10_000 + 1000 * 8000),
          None, range(1, 4)),
+        ("C3b funnel100", W.workload("C3b")[0], dict(W.workload("C3b")[1], max_dead=10_000 + 1000 * 8000),
+         None, range(1, 4)),
+        ("C3b funnel100 p=3d", W.workload("C3b")[0],
+         dict(W.workload("C3b")[1], max_dead=10_000 + 1000 * 8000, steps=300), None, range(1, 4)),
         # p = 3d HRSS steps, the paper's setting for high-dimensional problems
         ("C3a corrgauss100 p=3d", W.workload("C3a")[0],
          dict(W.workload("C3a")[1], max_dead=10_000 + 1000 * 8000, steps=300), None, range(1, 4)),
@@ -69,7 +87,8 @@ def main():
     print("|---|---|---|---|---|---|---|---|---|---|---|")
     for name, prob, cfg, truth, seeds in cases:
         if truth is None:
-            truth = truth_mog(prob) if prob.energy_kind == W.E_MOG else truth_corr(prob)
+            truth = (truth_mog(prob) if prob.energy_kind == W.E_MOG else
+                     truth_funnel(prob) if prob.energy_kind == W.E_FUNNEL else truth_corr(prob))
         for s, lz, sig, it, ev, dt in runs(name, prob, cfg, seeds):
             diff = abs(lz - truth)
             bound = max(3 * sig, 0.05)
