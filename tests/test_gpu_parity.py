@@ -454,7 +454,7 @@ def _full_size_subset(name, chains, seed=3):
 
 @pytest.mark.parametrize("name", ["C3a", "C3b"])
 def test_c3_full_size_iteration_subset(name):
-    """C3a / C3b at full size (n=1e4, k=1e3, p=100, d=100): warp engine with
+    """C3a / C3b at full size (n=1e4, k=1e3, p=300, d=100): warp engine with
     precomputed directions, chains 0, 1, 499, 998, 999 replayed by the oracle."""
     gpu = _full_size_subset(name, [0, 1, 499, 998, 999])
     assert gpu.engine() == "warp"
