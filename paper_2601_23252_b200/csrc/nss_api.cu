@@ -85,6 +85,11 @@ struct nss_ctx {
   bool use_graph = true;
   cudaGraphExec_t graph = nullptr, graph0 = nullptr;  // with / without the deferred metric
   long long graph_launches = 0, graph0_launches = 0;
+  // `graph` + the termination probe writing the state to the mapped host
+  // mirror, for nss_step with info: the host then only synchronises
+  cudaGraphExec_t graph_info = nullptr;
+  long long graph_info_launches = 0;
+  bool probe_in_graph = false;  // the last iteration's graph already ran the probe
   // round-synchronous batch engine (k_batch.cu) and its energy backends
   BatchDev bd{};
   bool batch_alloc = false;
@@ -277,7 +282,10 @@ nss_status device_error(nss_ctx *c) {
 // host-mapped pinned memory, then a synchronisation.
 nss_status pull_state(nss_ctx *c) {
   LaunchCtx lc{c->stream, &c->launches};
-  if (c->d_h_st && c->r.lz) {
+  if (c->probe_in_graph) {  // the iteration's graph ended with the probe
+    c->probe_in_graph = false;
+    c->term_stale = false;
+  } else if (c->d_h_st && c->r.lz) {
     launch_term_probe(c->r, lc, c->term_stale ? 1 : 0, c->d_h_st, c->d_h_lz0);
     c->term_stale = false;
     CK(cudaGetLastError());
@@ -513,6 +521,10 @@ void drop_graph(nss_ctx *c) {
     cudaGraphExecDestroy(c->round_graph);
     c->round_graph = nullptr;
   }
+  if (c->graph_info) {
+    cudaGraphExecDestroy(c->graph_info);
+    c->graph_info = nullptr;
+  }
 }
 
 // One iteration with the batch engine: the HRSS part is a data-dependent
@@ -619,12 +631,13 @@ nss_status ensure_vpre(nss_ctx *c) {
   return NSS_OK;
 }
 
-nss_status enqueue_iteration(nss_ctx *c) {
+nss_status enqueue_iteration(nss_ctx *c, bool with_probe = false) {
   nss_status vs = ensure_vpre(c);
   if (vs) return vs;
   const bool wm = c->metric_pending;
   c->term_stale = true;
   c->metric_pending = true;
+  c->probe_in_graph = false;
   if (resolve_engine(c) == 2) {
     c->metric_pending = wm;  // the batch path launches the deferred metric itself
     const nss_status s = enqueue_iteration_batch(c);
@@ -632,13 +645,15 @@ nss_status enqueue_iteration(nss_ctx *c) {
     return s;
   }
   if (c->timing || !c->use_graph) return enqueue_iteration_eager(c, wm);
-  cudaGraphExec_t &g = wm ? c->graph : c->graph0;
-  long long &gl = wm ? c->graph_launches : c->graph0_launches;
+  const bool probe = with_probe && wm && c->d_h_st && c->r.lz;
+  cudaGraphExec_t &g = probe ? c->graph_info : wm ? c->graph : c->graph0;
+  long long &gl = probe ? c->graph_info_launches : wm ? c->graph_launches : c->graph0_launches;
   if (!g) {
     const long long before = c->launches;
     cudaGraph_t cg = nullptr;
     CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-    const nss_status s = enqueue_iteration_eager(c, wm);
+    nss_status s = enqueue_iteration_eager(c, wm);
+    if (s == NSS_OK && probe) launch_term_probe(c->r, lctx(c), 1, c->d_h_st, c->d_h_lz0);
     const cudaError_t e = cudaStreamEndCapture(c->stream, &cg);
     if (s != NSS_OK) return s;
     if (e != cudaSuccess) {
@@ -656,6 +671,7 @@ nss_status enqueue_iteration(nss_ctx *c) {
   }
   CK(cudaGraphLaunch(g, c->stream));
   c->launches += gl;
+  c->probe_in_graph = probe;
   return NSS_OK;
 }
 
@@ -1018,7 +1034,7 @@ NSS_API nss_status nss_step(nss_ctx *c, nss_step_info *info) {
   nss_status s = check_usable(c);
   if (s) return s;
   if (c->host_finalised) return fail(c, NSS_ERR_STATE, "run already finalised");
-  if ((s = enqueue_iteration(c))) return s;
+  if ((s = enqueue_iteration(c, info != nullptr))) return s;
   if (info) {
     if ((s = pull_state(c))) return s;
     if ((s = device_error(c))) return s;
