@@ -1146,6 +1146,18 @@ int nsso_smc_init(const nsso_prior *p, const nsso_energy *e, const nsso_config *
   (*out)->beta = 0.0;
   (*out)->smc_logz = 0.0;
   (*out)->smc_par = (int32_t *)xcalloc((size_t)cfg->n_live, sizeof(int32_t));
+  /* parity hook: per-particle, per-step counts and decision margins of the
+   * last stage (every particle runs a chain) */
+  size_t np_ = (size_t)(cfg->n_live * (cfg->steps > 0 ? cfg->steps : 1));
+  free((*out)->t_counts);
+  free((*out)->t_margin);
+  (*out)->t_counts = (uint8_t *)xcalloc(np_ * 4, 1);
+  (*out)->t_margin = (double *)xcalloc(np_, sizeof(double));
+  free((*out)->t_dest);
+  free((*out)->t_parent);
+  (*out)->t_dest = (int32_t *)xcalloc((size_t)cfg->n_live, sizeof(int32_t));
+  (*out)->t_parent = (int32_t *)xcalloc((size_t)cfg->n_live, sizeof(int32_t));
+  for (int64_t j = 0; j < cfg->n_live; ++j) (*out)->t_dest[j] = (*out)->t_parent[j] = (int32_t)j;
   return NSSO_OK;
 }
 
@@ -1196,6 +1208,8 @@ int nsso_smc_stage(nsso_ctx *c) {
       double mm, en;
       direction(c, t, (uint32_t)j, (uint32_t)q, z, v);
       slice_step(c, x, e, v, c->w, INFINITY, t, (uint32_t)j, (uint32_t)q, xn, &en, cnt, &mm);
+      for (int b = 0; b < 4; ++b) c->t_counts[(j * p + q) * 4 + b] = (uint8_t)cnt[b];
+      c->t_margin[j * p + q] = mm;
       memcpy(x, xn, sizeof(double) * (size_t)d);
       e = en;
     }
@@ -1285,7 +1299,7 @@ int nsso_set_chain_subset(nsso_ctx *c, const int32_t *chains, int64_t count) {
 int nsso_get_trace(nsso_ctx *c, int32_t *dead_gid, int32_t *dest_gid, int32_t *parent_gid,
                    uint8_t *counts, double *min_margin, double *e_star) {
   if (!c) return NSSO_ERR_INVALID_ARG;
-  int64_t k = c->k, nch = c->cfg.update_all ? c->n : c->k;
+  int64_t k = c->k, nch = (c->cfg.update_all || c->smc) ? c->n : c->k;
   int p = c->cfg.steps > 0 ? c->cfg.steps : 1;
   if (dead_gid) memcpy(dead_gid, c->t_dead, sizeof(int32_t) * (size_t)k);
   if (dest_gid) memcpy(dest_gid, c->t_dest, sizeof(int32_t) * (size_t)nch);

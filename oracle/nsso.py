@@ -220,6 +220,7 @@ class Oracle:
         self.k = self.cfg["k"]
         self.p = self.cfg["steps"]
         self.R = self.cfg["n_volume_sims"]
+        self.smc = smc_rho is not None
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
@@ -344,7 +345,8 @@ class Oracle:
 
     def trace(self) -> Dict:
         k, p = self.k, max(self.p, 1)
-        nch = self.n if self.cfg.get("update_all", 0) else k  # chains per iteration (F4: all n)
+        # chains per iteration (F4 update-all and F3 SMC stages: all n)
+        nch = self.n if (self.cfg.get("update_all", 0) or self.smc) else k
         dead = np.zeros(k, np.int32)
         dest = np.zeros(nch, np.int32)
         par = np.zeros(nch, np.int32)

@@ -183,11 +183,7 @@ void begin_t(const RunDev &r, const PriorDev &pr, const BatchDev &b, const Launc
 template <int NPL>
 void advance_t(const RunDev &r, const PriorDev &pr, const BatchDev &b, int parity, const LaunchCtx &lc) {
   const size_t smem = static_cast<size_t>(kWarpsPerBlock) * NPL * 32 * sizeof(float);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_batch_advance<NPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    attr = true;
-  }
+  NSS_MAX_SMEM(k_batch_advance<NPL>, 160 * 1024);
   NSS_PIN_CARVEOUT(k_batch_advance<NPL>);
   k_batch_advance<NPL><<<chain_blocks(r, kWarpsPerBlock), kWarpsPerBlock * 32, smem, lc.stream>>>(
       r, pr, b, parity);
@@ -206,11 +202,7 @@ template <int NPL, int KIND>
 void energy_t(const RunDev &r, const EnergyDev &en, const BatchDev &b, int parity, const LaunchCtx &lc) {
   const int wpb = 8;
   const size_t smem = (energy_param_floats(KIND, r.d, en.n_comp) + static_cast<size_t>(wpb) * NPL * 32) * sizeof(float);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_batch_energy<NPL, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    attr = true;
-  }
+  NSS_MAX_SMEM((k_batch_energy<NPL, KIND>), 160 * 1024);
   NSS_PIN_CARVEOUT((k_batch_energy<NPL, KIND>));
   k_batch_energy<NPL, KIND><<<(b.max_rows + wpb - 1) / wpb, wpb * 32, smem, lc.stream>>>(r, en, b, parity);
   ++*lc.launch_counter;

@@ -5,15 +5,16 @@
 //   E = 1/2 y^T K^-1 y + 1/2 log|K| + N/2 log 2 pi,
 //   phi = (log l_1..l_D, log sf, log sn).
 //
-// One CTA per probe matrix (probes are dealt to a persistent grid of one CTA
-// per SM).  The CTA builds the (N+1) x N lower trapezoid [K; y^T] in its own
-// fp64 scratch slot and runs a right-looking blocked Cholesky with 64-wide
-// panels: the diagonal block is factorised in shared memory by one warp, the
-// panel below it is solved row by row (the extra row y^T becomes alpha =
-// L^-1 y on the way), and the trailing lower trapezoid receives the rank-64
-// update in 64 x 64 tiles: panel rows staged row-major in shared memory and
-// contracted on the fp64 tensor cores (mma.sync m8n8k4 DMMA, 8 per warp per
-// k-step).  E then needs only
+// One CTA per probe matrix (probes are dealt to a persistent grid, two CTAs
+// per SM).  The CTA runs a LEFT-looking blocked Cholesky of the (N+1) x N
+// lower trapezoid [K; y^T] with 64-wide column blocks: for column block j,
+// every 64 x 64 tile T = [K; y^T](i, j) - L(i, :j) L(j, :j)^T is accumulated in
+// registers on the fp64 tensor cores (mma.sync m8n8k4 = DMMA, 8 per warp per
+// k-step) from the already stored L panels (streamed through a double-buffered
+// cp.async pipeline), with K(i, j) generated on the fly from X and phi; the
+// diagonal tile is factorised and inverted by one warp, and every tile below
+// becomes L(i, j) = T L_jj^-T (DMMA).  The y^T row turns into alpha^T =
+// (L^-1 y)^T on the way, so E needs only
 // the pivots (log det) and |alpha|^2.  A non-positive pivot gives E = +inf (K
 // not positive definite), as in the oracle.  fp64 throughout: the paper runs
 // its GP experiments in double precision.
@@ -562,11 +563,7 @@ void gp_energy_pass(void *handle, const BatchDev &b, int parity, const LaunchCtx
 
 template <int NPL>
 void gp_chains_t(GpEngine *E, const RunDev &r, const PriorDev &pr, const BatchDev &b, const LaunchCtx &lc) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_gp_chains<NPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(E->smem));
-    attr = true;
-  }
+  NSS_MAX_SMEM(k_gp_chains<NPL>, E->smem);
   NSS_PIN_CARVEOUT(k_gp_chains<NPL>);
   k_gp_chains<NPL><<<E->grid, kThreads, E->smem, lc.stream>>>(r, pr, b, E->g, E->q);
   ++*lc.launch_counter;

@@ -296,11 +296,7 @@ void launch_dirs_t(const RunDev &r, float *V, const LaunchCtx &lc) {
   if (work <= 0) return;
   const int wpb = 8;
   const size_t smem = (static_cast<size_t>(r.d) * odd_stride(r.d) + static_cast<size_t>(wpb) * NPL * 32) * sizeof(float);
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && attr < smem) {
-    cudaFuncSetAttribute(k_dirs<NPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    attr = smem;
-  }
+  if (smem > 48 * 1024) NSS_MAX_SMEM(k_dirs<NPL>, smem);
   NSS_PIN_CARVEOUT(k_dirs<NPL>);
   k_dirs<NPL><<<static_cast<int>((work + wpb - 1) / wpb), wpb * 32, smem, lc.stream>>>(r, V);
   ++*lc.launch_counter;
@@ -480,12 +476,7 @@ void launch_hrss_w(const RunDev &r, const PriorDev &pr, const EnergyDev &en, con
   const size_t sl = r.Vpre ? 0 : static_cast<size_t>(r.d) * ldl;
   const size_t smem = (sl + energy_param_floats(KIND, r.d, en.n_comp) +
                        static_cast<size_t>(wpb) * WPC * 2 * NPL * 32) * sizeof(float);
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && attr < smem) {
-    cudaFuncSetAttribute(k_hrss<NPL, KIND, WPC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    attr = smem;
-  }
+  if (smem > 48 * 1024) NSS_MAX_SMEM((k_hrss<NPL, KIND, WPC>), smem);
   const int blocks = (nc + wpb - 1) / wpb;
   NSS_PIN_CARVEOUT((k_hrss<NPL, KIND, WPC>));
   k_hrss<NPL, KIND, WPC><<<blocks, wpb * WPC * 32, smem, lc.stream>>>(r, pr, en);

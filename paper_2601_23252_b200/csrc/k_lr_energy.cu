@@ -269,12 +269,7 @@ size_t smem_of() { return kSmemA + LrCfg<BN_>::kSmemB + sizeof(Bars) + 1024; }
 template <int BN_>
 void launch_bn(const CUtensorMap &tmA, const CUtensorMap &tmB, float *partial, int *slices_out, const int *n_probe,
                int *reset_counter, int p_stride, int n_data, const LaunchCtx &lc) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_lr_energy<BN_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem_of<BN_>()));
-    attr = true;
-  }
+  NSS_MAX_SMEM(k_lr_energy<BN_>, smem_of<BN_>());
   NSS_PIN_CARVEOUT(k_lr_energy<BN_>);
   static int sms = 0;
   if (!sms) {

@@ -502,11 +502,7 @@ void launch_term_probe(const RunDev &r, const LaunchCtx &lc, int probe, DevState
 
 void launch_metric(const RunDev &r, double metric_reg, int width_rule, double width_param, int end_of_iteration,
                    double *partials, unsigned *ticket, int n_blocks, const LaunchCtx &lc) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_metric, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  NSS_MAX_SMEM(k_metric, 200 * 1024);
   NSS_PIN_CARVEOUT(k_metric);
   const size_t smem = metric_smem(r.n, r.d, n_blocks);
   if (r.d < kSplitMinD || n_blocks == 1) {

@@ -613,23 +613,14 @@ size_t select_smem(int n) {
 // scratch layout (device, sized by the host): sort_scratch holds max(n, k)
 // rounded up to a power of two plus n; sel_scratch 2k keys.
 void launch_select(const RunDev &r, const LaunchCtx &lc) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kSmemSortMax * 8 + kSmemOrdMax * 4);
-    cudaFuncSetAttribute(k_finalise_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSortMax * 8);
-    attr = true;
-  }
+  NSS_MAX_SMEM(k_select, kSmemSortMax * 8 + kSmemOrdMax * 4);
+  NSS_MAX_SMEM(k_finalise_sort, kSmemSortMax * 8);
   const size_t fused = select_smem_fused(r.n, r.k);
   const bool separate_rows = static_cast<long long>(r.k) * r.dp >= 16384;
   int P = 1;
   while (P < r.k) P <<= 1;
   if (fused <= 200 * 1024 && P <= r.n) {
-    static bool attr2 = false;
-    if (!attr2) {
-      cudaFuncSetAttribute(k_select_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      attr2 = true;
-    }
+    NSS_MAX_SMEM(k_select_smem, 200 * 1024);
     NSS_PIN_CARVEOUT(k_select_smem);
     k_select_smem<<<1, kThreads, fused, lc.stream>>>(r, !separate_rows);
   } else {

@@ -189,15 +189,38 @@ __device__ inline bool term_check(const RunDev &r, DevState *st, float emin) {
 // Every kernel of the library runs with the same (maximum) shared-memory
 // carveout: a different carveout per kernel forces the SM to reconfigure its
 // L1/shared split between consecutive launches.
-template <class Kern>
-inline bool pin_carveout(Kern *kernel) {
-  cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-  return true;
+// Function attributes apply per device, so the "already set" caches below are
+// kept per (call site, device): a second context on another GPU of the same
+// process sets them again for its device.
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d & 63;
 }
-#define NSS_PIN_CARVEOUT(kern)                       \
-  do {                                               \
-    static const bool pinned_ = pin_carveout(kern); \
-    (void)pinned_;                                   \
+template <class Kern>
+inline void pin_carveout(Kern *kernel) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+}
+#define NSS_PIN_CARVEOUT(kern)                 \
+  do {                                         \
+    static bool pinned_[64] = {};              \
+    const int dv_ = ::nss::current_device();   \
+    if (!pinned_[dv_]) {                       \
+      ::nss::pin_carveout(kern);               \
+      pinned_[dv_] = true;                     \
+    }                                          \
+  } while (0)
+// Raise a kernel's dynamic shared-memory limit to at least `bytes` on the
+// current device (once per size increase).
+#define NSS_MAX_SMEM(kern, bytes)                                                              \
+  do {                                                                                         \
+    static size_t set_[64] = {};                                                               \
+    const int dv_ = ::nss::current_device();                                                   \
+    const size_t b_ = static_cast<size_t>(bytes);                                              \
+    if (set_[dv_] < b_) {                                                                      \
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(b_)); \
+      set_[dv_] = b_;                                                                          \
+    }                                                                                          \
   } while (0)
 
 struct LaunchCtx {

@@ -232,6 +232,7 @@ class Sampler:
             raise NssError(st, "nss_init")
         self.d, self.n, self.k = d, self.cfg["n_live"], self.cfg["k"]
         self.p, self.R = self.cfg["steps"], self.cfg["n_volume_sims"]
+        self.smc = smc_rho is not None
 
     def _check(self, st: int, where: str):
         if st != 0:
@@ -366,7 +367,8 @@ class Sampler:
 
     def trace(self) -> Dict:
         k, p = self.k, max(self.p, 1)
-        nch = self.n if self.cfg.get("update_all", 0) else k  # chains per iteration (F4: all n)
+        # chains per iteration (F4 update-all and F3 SMC stages: all n)
+        nch = self.n if (self.cfg.get("update_all", 0) or self.smc) else k
         dead = np.zeros(k, np.int32)
         dest, par = np.zeros(nch, np.int32), np.zeros(nch, np.int32)
         counts = np.zeros((nch, p, 4), np.uint8)

@@ -10,7 +10,7 @@ import pytest
 from scipy import special, stats
 
 from paper_2601_23252_b200 import workloads as W
-from tests.parity_util import compare_iteration, inject_pair, prior_scale
+from tests.parity_util import check_subset, compare_iteration, inject_pair, prior_scale
 
 pytestmark = pytest.mark.gpu
 
@@ -73,7 +73,7 @@ def test_single_iteration_parity(name, engine):
     Lr, wr = ref.metric()
     assert np.allclose(Lg, Lr, rtol=1e-5, atol=1e-7 * np.abs(Lr).max())
     assert abs(wg - wr) <= 1e-6 * wr
-    st = compare_iteration(gpu, ref, prob)
+    st = compare_iteration(gpu, ref, prob, f"{name} {engine}")
     if name == "shrink_cap":
         assert (st["counts_g"][:, :, 3] == 0).any()  # some null moves happened
     if name == "stepout_cap":
@@ -104,7 +104,7 @@ def test_several_iterations_teacher_forced():
         e32 = np.array([ref.energy(xi.astype(np.float64)) for xi in x32]).astype(np.float32)
         ref.set_live(x32.astype(np.float64), e32.astype(np.float64), it)
         gpu.set_live(x32, e32, it)
-        compare_iteration(gpu, ref, prob)
+        compare_iteration(gpu, ref, prob, f"C2 teacher-forced it {it}")
 
 
 def test_init_parity():
@@ -175,7 +175,7 @@ def test_full_run_c1_analytic():
     res = _run_logz(W.gauss(2), dict(n_live=200, k=20, steps=10), range(1, 9))
     lz = np.array([r[0] for r in res])
     sig = np.array([r[1] for r in res])
-    assert np.all(np.abs(lz - truth) <= np.maximum(4 * sig, 0.05)), (lz, sig)
+    assert np.all(np.abs(lz - truth) <= np.maximum(3 * sig, 0.05)), (lz, sig)
     assert abs(lz.mean() - truth) <= max(3 * sig.mean() / math.sqrt(len(lz)), 0.05)
     assert all(r[2]["terminated"] and r[2]["finalised"] for r in res)
 
@@ -207,19 +207,89 @@ def test_full_run_c3a_analytic_p3d():
         assert abs(lz - truth) <= max(3 * sig, 0.05), (lz, sig, truth)
 
 
-def test_full_run_gpu_vs_oracle_c1():
-    """Same seed: GPU and oracle full runs agree within the combined spread."""
+def _vs_oracle(prob, kw, seeds, oracle_runs=None):
+    """Same configuration and seed on both sides, full runs to termination:
+    |log Z_GPU - log Z_oracle| <= max(3 sigma, 0.05) per run (north_star,
+    SURVEY C-9 T4), sigma = the two runs' replica spreads combined
+    (sqrt(sg^2 + so^2): the two trajectories are independent draws of the same
+    estimator once fp32 and fp64 decisions part).  oracle_runs: stored oracle
+    results (tests/golden, scripts/golden_oracle_fullruns.py) per seed."""
     from oracle import nsso
-    prob = W.gauss(2)
-    kw = dict(n_live=200, k=20, steps=10)
-    diffs = []
-    for s in range(1, 7):
-        o = nsso.Oracle(prob, W.config(seed=s, **kw))
-        o.run()
-        (lg, sg, _), = _run_logz(prob, kw, [s])
-        lr, sr = o.evidence()
-        diffs.append((lg - lr) / math.hypot(sg, sr))
-    assert np.all(np.abs(diffs) < 4), diffs
+    out = []
+    for s in seeds:
+        if oracle_runs is None:
+            o = nsso.Oracle(prob, W.config(seed=s, **kw))
+            o.run()
+            lr, sr = o.evidence()
+            o.close()
+        else:
+            lr, sr = oracle_runs[s]
+        (lg, sg, info), = _run_logz(prob, kw, [s])
+        assert info["terminated"]
+        bound = max(3 * math.hypot(sg, sr), 0.05)
+        out.append((s, lg, sg, lr, sr))
+        assert abs(lg - lr) <= bound, (s, lg, sg, lr, sr)
+    return out
+
+
+def test_full_run_gpu_vs_oracle_c1():
+    _vs_oracle(W.gauss(2), dict(n_live=200, k=20, steps=10), range(1, 7))
+
+
+def test_full_run_gpu_vs_oracle_c2():
+    """C2 (d = 10 MoG, n = 2000, k = 200, p = 10) at full size, 3 seeds."""
+    _vs_oracle(W.mog(10), dict(n_live=2000, k=200, steps=10), range(1, 4))
+
+
+@pytest.mark.parametrize("name", ["C3a", "C3b"])
+def test_full_run_gpu_vs_oracle_c3_reduced(name):
+    """C3 at reduced n (SURVEY C-9 T4: n = 1000, k = 100; d = 100, p = 3d):
+    the oracle's full runs take 0.5-1.5 h of one core, so their results are
+    stored by scripts/golden_oracle_fullruns.py (oracle only) in
+    tests/golden/oracle_fullrun_<cfg>_s<seed>.json."""
+    import glob
+    import json
+    import os
+    runs = {}
+    for path in sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", f"oracle_fullrun_{name}_s*.json"))):
+        g = json.load(open(path))
+        runs[g["seed"]] = (g["log_z"], g["log_z_err"])
+        cfg = g["cfg"]
+    assert runs, "golden oracle runs missing"
+    prob, _ = W.workload(name)
+    kw = {k: cfg[k] for k in ("n_live", "k", "steps", "max_dead")}
+    _vs_oracle(prob, kw, sorted(runs), oracle_runs=runs)
+
+
+def _funnel_log_z(d, a, sigma_y):
+    """P17 (SURVEY C-8): Z = (2a)^-d int_{-a}^{a} N(y; 0, sigma_y^2)
+    erf(a / (sqrt 2 e^{y/2}))^(d-1) dy for the funnel under U[-a, a]^d
+    (x_n ~ N(0, sd e^{y/2}), R-23), by adaptive quadrature."""
+    from scipy import integrate
+
+    def f(y):
+        return stats.norm.pdf(y, 0.0, sigma_y) * special.erf(a / (math.sqrt(2.0) * math.exp(y / 2))) ** (d - 1)
+    z, _ = integrate.quad(f, -a, a, points=[-10, -5, 0, 5], limit=400, epsabs=0, epsrel=1e-12)
+    return math.log(z) - d * math.log(2 * a)
+
+
+def test_funnel_log_z_quadrature_pin():
+    """The funnel truth itself: d = 10, a = 20 gives -36.946."""
+    assert abs(_funnel_log_z(10, 20.0, 3.0) - (-36.946)) < 5e-4
+
+
+def test_full_run_c3b_funnel_analytic():
+    """C3b at full size (funnel d = 100 under U[-20, 20]^100, n = 1e4, k = 1e3,
+    p = 3d) to termination: |log Z - (-368.985)| <= max(3 sigma, 0.05) per run
+    (P17; P:881-926)."""
+    prob, cfg = W.workload("C3b")
+    truth = _funnel_log_z(prob.d, float(prob.hi[0]), prob.sigma_y)
+    assert abs(truth - (-368.985)) < 1e-3
+    res = _run_logz(prob, dict(n_live=cfg["n_live"], k=cfg["k"], steps=cfg["steps"],
+                               max_dead=cfg["n_live"] + cfg["k"] * 8000), [1, 2])
+    for lz, sig, info in res:
+        assert info["terminated"]
+        assert abs(lz - truth) <= max(3 * sig, 0.05), (lz, sig, truth)
 
 
 def test_posterior_weights_c1():
@@ -340,26 +410,11 @@ def test_c4_full_size_iteration_subset():
     gpu.set_live(x0, e32, 1)
     ref = nsso.Oracle(prob, cfg, draw_live=False)
     ref.set_live(x0.astype(np.float64), e32.astype(np.float64), 1)
-    chains = [0, 1, 777, 5000, 9998, 9999]
+    chains = [0, 1, 2, 777, 2500, 5000, 6001, 7777, 9000, 9998, 9999, 4242]
     ref.set_chain_subset(chains)
     gpu.step()
     ref.step()
-    tg, tr = gpu.trace(), ref.trace()
-    for key in ("dead_gid", "dest_gid", "parent_gid"):
-        assert np.array_equal(tg[key], tr[key]), key
-    xg, eg = gpu.get_live()
-    xr, er = ref.get_live()
-    good = 0
-    for c in chains:
-        diff = np.nonzero(np.any(tg["counts"][c] != tr["counts"][c], axis=1))[0]
-        if diff.size:
-            assert np.min(tr["min_margin"][c, : diff[0] + 1]) < 1e-5, (c, diff[0])
-            continue
-        good += 1
-        s = tg["dest_gid"][c]
-        assert np.allclose(xg[s], xr[s], rtol=1e-5, atol=1e-5)
-        assert abs(eg[s] - er[s]) <= 1e-5 * abs(er[s])
-    assert good >= 5
+    check_subset(gpu, ref, prob, chains, "C4 full-size subset")
     info = gpu.info()
     assert info["null_moves"] == 0 and info["energy_evals"] > 1e6
 
@@ -381,7 +436,7 @@ def test_update_all_single_iteration_parity(name):
     gpu, ref = inject_pair(prob, cfg, warm_iters=1, engine=engine)
     if gpu.engine() != engine:
         pytest.skip(f"{engine} engine does not apply")
-    st = compare_iteration(gpu, ref, prob)
+    st = compare_iteration(gpu, ref, prob, f"update-all {name}")
     tg = gpu.trace()
     assert tg["dest_gid"].size == kw["n_live"]
     dg, dr = gpu.dead(), ref.dead()
@@ -404,7 +459,7 @@ def test_rw_single_iteration_parity(name):
     prob = make()
     cfg = W.config(seed=13, mutation=W.MUT_RW, **kw)
     gpu, ref = inject_pair(prob, cfg, warm_iters=1)
-    st = compare_iteration(gpu, ref, prob)
+    st = compare_iteration(gpu, ref, prob, f"rw {name}")
     c = st["counts_g"]
     assert np.all(c[..., 0] == 0) and np.all(c[..., 1] == 0)
     assert 0 < c[..., 3].mean() < 1  # some proposals accepted, some rejected
@@ -432,23 +487,7 @@ def _full_size_subset(name, chains, seed=3):
     ref.set_chain_subset(chains)
     gpu.step()
     ref.step()
-    tg, tr = gpu.trace(), ref.trace()
-    for key in ("dead_gid", "dest_gid", "parent_gid"):
-        assert np.array_equal(tg[key], tr[key]), key
-    xg, eg = gpu.get_live()
-    xr, er = ref.get_live()
-    scale = prior_scale(prob)
-    good = 0
-    for c in chains:
-        diff = np.nonzero(np.any(tg["counts"][c] != tr["counts"][c], axis=1))[0]
-        if diff.size:
-            assert np.min(tr["min_margin"][c, : diff[0] + 1]) < 1e-5, (c, diff[0])
-            continue
-        good += 1
-        s = tg["dest_gid"][c]
-        assert np.all(np.abs(xg[s] - xr[s]) <= 1e-5 * (np.abs(xr[s]) + scale))
-        assert abs(eg[s] - er[s]) <= 1e-5 * max(1.0, abs(er[s]))
-    assert good >= len(chains) - 1
+    check_subset(gpu, ref, prob, chains, f"{name} full-size subset")
     return gpu
 
 
@@ -456,5 +495,5 @@ def _full_size_subset(name, chains, seed=3):
 def test_c3_full_size_iteration_subset(name):
     """C3a / C3b at full size (n=1e4, k=1e3, p=300, d=100): warp engine with
     precomputed directions, chains 0, 1, 499, 998, 999 replayed by the oracle."""
-    gpu = _full_size_subset(name, [0, 1, 499, 998, 999])
+    gpu = _full_size_subset(name, [0, 1, 2, 3, 100, 250, 499, 500, 640, 777, 998, 999])
     assert gpu.engine() == "warp"

@@ -9,6 +9,7 @@ import numpy as np
 import pytest
 
 from paper_2601_23252_b200 import workloads as W
+from tests.parity_util import classify_chains
 
 pytestmark = pytest.mark.gpu
 
@@ -50,11 +51,15 @@ def test_smc_stage_parity(name):
         assert tg == tr == t
         assert abs(bg - br) < 1e-9 and abs(lg - lr) < 1e-8, (t, bg, br, lg, lr)
         assert np.array_equal(pg, pr)
+        # per-particle HRSS counts exact except precision ties tagged by the
+        # oracle's decision margins (SURVEY C-9 guard band, <= 0.1%)
+        cg, cr = gpu.trace()["counts"], ref.trace()
+        same = classify_chains(cg, cr["counts"], cr["min_margin"], f"smc {name} stage {t}")
         xg, eg = gpu.get_live()
         xr, er = ref.get_live()
         ok = np.all(np.abs(xg - xr) <= 1e-5 * (np.abs(xr) + scale), axis=1) & \
             (np.abs(eg - er) <= 1e-5 * np.maximum(1.0, np.abs(er)))
-        assert ok.mean() >= 0.99, (t, ok.mean())
+        assert np.all(ok[same]), (t, np.nonzero(~ok & same)[0][:5])
         if br >= 1.0:
             break
 
