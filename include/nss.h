@@ -110,15 +110,24 @@ typedef struct {
 
 typedef enum { NSS_MUT_HRSS = 0, NSS_MUT_RW = 1 } nss_mutation;
 
-/* Multi-GPU: one process per GPU.  The HRSS chains of an
- * iteration are split in contiguous blocks of ceil(k / world) chains per rank;
- * the live set and dead store are replicated, and thresholding, resampling,
- * metric and evidence run redundantly on every rank from identical state.
- * After its chains finish, each rank's new rows reach every rank through one
- * NCCL all-gather on the context's stream, so a multi-GPU run is bit-identical
- * to a one-GPU run with the same seed.  nss_info counters (probes, evals, ...)
- * are this rank's; sum them over ranks for job totals.  All ranks must call
- * nss_step / nss_steps / nss_run the same number of times.
+/* Multi-GPU: one process per GPU, world in {1, 2, 4, 8}.
+ * The live set is SHARDED: rank q owns the gids of 8/world of the 8 fixed gid
+ * segments [floor(s n / 8), floor((s + 1) n / 8)) (P:264-283's particles are
+ * independent units).  Each iteration, every rank forms its local top-k
+ * candidates (ord(E), gid keys) and the moment sums of its segments, one NCCL
+ * all-gather exchanges them, and every rank then takes the same decisions
+ * (threshold, dead records, parents, metric, evidence, termination) from the
+ * same bytes; each rank runs the HRSS chains whose destination it owns and
+ * reads parent rows another rank owns straight from that rank's memory over
+ * NVLink (CUDA IPC).  A multi-GPU run is bit-identical to a one-GPU run with
+ * the same seed.  NS with update_all = 1 is UNSUPPORTED sharded.
+ * Per-rank data: nss_info counters (probes, evals, ...) are this rank's (sum
+ * over ranks; init_evals is the same on every rank); the dead store's
+ * positions (nss_dead x, nss_samples x) hold the rows of the points this rank
+ * owned and zeros elsewhere (sum over ranks); every other output is
+ * replicated.  Collective calls (every rank, same order): nss_step, nss_steps,
+ * nss_run, nss_finalise, nss_get_live.  F3 SMC contexts instead replicate the
+ * particles and split their chains (one all-gather of the new rows).
  * Pass NULL for a single GPU.  nccl_uid NULL: no communicator (single GPU). */
 typedef struct {
   int32_t rank, world;
@@ -299,6 +308,21 @@ nss_status nss_set_graph(nss_ctx *ctx, int32_t enable);
 nss_status nss_debug_stamps(nss_ctx *ctx, uint64_t *stamps /* 16 */);
 /* Kernels launched by this context since creation (all kinds). */
 nss_status nss_launch_count(nss_ctx *ctx, int64_t *launches);
+
+/* ---- in-process rank emulation (tests) ----
+ * The `world` ranks of ONE sharded run as `world` contexts on the current GPU
+ * in this process: same partition, kernels and decisions as the NCCL path, the
+ * members share one stream and the exchange buffer, and the peer tables point
+ * at the other members' arrays (no kernel ever waits on another).  out: world
+ * contexts (rank q = out[q]), each freed with nss_destroy.  Errors as nss_init;
+ * INVALID_ARG unless world divides 8. */
+nss_status nss_group_init(const nss_prior *prior, const nss_energy *energy, const nss_config *cfg, int32_t world,
+                          nss_ctx **out);
+/* `count` iterations of the group (all members; asynchronous). */
+nss_status nss_group_step(nss_ctx **ctx, int32_t world, int64_t count);
+/* Every member's live-set arrays completed with the other members' rows (then
+ * nss_get_live, nss_finalise and nss_get_metric work on any member). */
+nss_status nss_group_gather_live(nss_ctx **ctx, int32_t world);
 
 #ifdef __cplusplus
 }

@@ -163,7 +163,7 @@ __device__ __forceinline__ void advance_chain(const RunDev &r, const PriorDev &p
       }
       const int j = s.step;
       if (r.Vpre) {  // precomputed for this (chain, step) by k_dirs (bit-identical)
-        const float *vr = r.Vpre + (static_cast<long long>(c - r.c0) * p + j) * r.dp;
+        const float *vr = r.Vpre + (static_cast<long long>(c - chain_range(r).x) * p + j) * r.dp;
 #pragma unroll
         for (int t = 0; t < NPL; ++t) {
           const int i = lane + 32 * t;

@@ -1,12 +1,15 @@
-// Multi-GPU NSS: one process per GPU, HRSS chains split in
-// contiguous blocks of kc = ceil(k / W) chains per rank, live set and dead
-// store replicated.  Thresholding, resampling, metric and evidence are
-// computed redundantly on every rank from identical state (same kernels, same
-// inputs, same Philox draws), so they need no collective; after its chains
-// finish, each rank packs its kc new rows (x, E) and one NCCL all-gather
-// over NVLink hands every rank all k rows, which are written to their
-// destination slots.  A W-GPU run is therefore bit-identical to a 1-GPU run
-// with the same seed (chains are independent given the iteration's state).
+// Multi-GPU transport: one process per GPU.
+//
+// NS runs shard the live set (k_shard.cu): one in-place NCCL all-gather of a
+// fixed-size block per rank per iteration (candidates + moment sums), and the
+// ranks' live-set arrays mapped into each other's address space with CUDA IPC
+// so the chain kernels read parent rows another rank owns directly over
+// NVLink (ipc_exchange).
+//
+// F3 tempered SMC contexts keep the replicated layout: the HRSS chains are
+// split in contiguous blocks of kc = ceil(n / W) per rank and, after its
+// chains finish, each rank's new rows (x, E) reach every rank through one
+// NCCL all-gather (exchange_chains).
 //
 // NCCL is loaded with dlopen (the copy PyTorch already mapped, when present),
 // so libnss has no link-time dependency on it.
@@ -16,6 +19,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "nss_internal.cuh"
 
@@ -111,6 +115,68 @@ bool nccl_comm_init(void **comm, int world, const uint8_t uid[128], int rank, st
 void nccl_comm_free(void *comm) {
   const NcclApi *api = nccl_api();
   if (api && comm) api->comm_destroy(static_cast<ncclComm_t>(comm));
+}
+
+// In-place all-gather of `bytes` per rank: rank q's block at buf + q * bytes.
+bool nccl_allgather_inplace(void *comm, void *buf, size_t bytes, int rank, cudaStream_t stream, std::string *err) {
+  const NcclApi *api = nccl_api();
+  char *b = static_cast<char *>(buf);
+  const ncclResult_t rc = api->all_gather(b + static_cast<size_t>(rank) * bytes, b, bytes, ncclUint8,
+                                          static_cast<ncclComm_t>(comm), stream);
+  if (rc != ncclSuccess) {
+    *err = std::string("ncclAllGather: ") + (api->error_string ? api->error_string(rc) : "error");
+    return false;
+  }
+  return true;
+}
+
+// CUDA IPC handles of this rank's arrays (nptr of them, cudaMalloc'd) to every
+// rank; peers[i * world + q] = rank q's i-th array mapped here (own: local).
+bool ipc_exchange(void *comm, int world, int rank, void *const *mine, int nptr, void **peers,
+                  std::vector<void *> *opened, cudaStream_t stream, std::string *err) {
+  const size_t hb = sizeof(cudaIpcMemHandle_t);
+  const size_t blk = ((hb * nptr) + 255) & ~static_cast<size_t>(255);
+  std::vector<char> host(blk * world, 0);
+  for (int i = 0; i < nptr; ++i) {
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, mine[i]) != cudaSuccess) {
+      *err = "cudaIpcGetMemHandle failed";
+      return false;
+    }
+    memcpy(host.data() + rank * blk + i * hb, &h, hb);
+  }
+  char *dev = nullptr;
+  if (cudaMalloc(&dev, blk * world) != cudaSuccess) {
+    *err = "cudaMalloc (ipc exchange)";
+    return false;
+  }
+  bool ok = cudaMemcpyAsync(dev + rank * blk, host.data() + rank * blk, blk, cudaMemcpyHostToDevice, stream) ==
+                cudaSuccess &&
+            nccl_allgather_inplace(comm, dev, blk, rank, stream, err) &&
+            cudaMemcpyAsync(host.data(), dev, blk * world, cudaMemcpyDeviceToHost, stream) == cudaSuccess &&
+            cudaStreamSynchronize(stream) == cudaSuccess;
+  cudaFree(dev);
+  if (!ok) {
+    if (err->empty()) *err = "ipc handle exchange failed";
+    return false;
+  }
+  for (int i = 0; i < nptr; ++i)
+    for (int q = 0; q < world; ++q) {
+      if (q == rank) {
+        peers[i * world + q] = mine[i];
+        continue;
+      }
+      cudaIpcMemHandle_t h;
+      memcpy(&h, host.data() + q * blk + i * hb, hb);
+      void *p = nullptr;
+      if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        *err = "cudaIpcOpenMemHandle failed (no peer access between the ranks' GPUs?)";
+        return false;
+      }
+      opened->push_back(p);
+      peers[i * world + q] = p;
+    }
+  return true;
 }
 
 // pack this rank's chain rows, all-gather kc rows per rank, scatter all k rows

@@ -24,21 +24,23 @@ constexpr int kWarpsPerBlock = 8;
 template <int NPL>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_batch_begin(RunDev r, PriorDev pr, BatchDev b) {
   const int lane = threadIdx.x & 31;
-  const int c = r.c0 + blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  const int2 cr = chain_range(r);
+  const int c = cr.x + blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     b.n_probe[0] = 0;
     b.n_probe[1] = 0;
   }
-  if (c >= r.c1) return;
+  if (c >= cr.y) return;
   const DevState *st = r.st;
   const bool off = st->terminated || st->error || st->finalised;
   const int d = r.d, par = r.cpar[c];
   float pa[NPL], pb[NPL], x[NPL];
   load_prior_lane<NPL>(pr, lane, d, pa, pb);
+  const float *xs = start_row(r, par);
 #pragma unroll
   for (int t = 0; t < NPL; ++t) {
     const int i = lane + 32 * t;
-    x[t] = i < d ? r.Xs[static_cast<long long>(par) * r.dp + i] : 0.f;
+    x[t] = i < d ? xs[i] : 0.f;
     if (i < r.dp) b.x[static_cast<long long>(c) * b.dp + i] = x[t];
   }
   bool dummy;
@@ -47,7 +49,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_batch_begin(RunDev r, P
     ChainRegs s{};
     s.phase = off ? kPhDone : kPhDir;
     s.row0 = s.row1 = -1;
-    s.e = r.Es[par];
+    s.e = start_e(r, par);
     s.lp = lp;
     store_chain(b, c, s);
   }
@@ -58,8 +60,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3) k_batch_advance(RunDev
                                                                        int parity) {
   extern __shared__ float sm[];
   const int wib = threadIdx.x >> 5;
-  const int c = r.c0 + blockIdx.x * kWarpsPerBlock + wib;
-  if (c >= r.c1) return;
+  const int2 cr = chain_range(r);
+  const int c = cr.x + blockIdx.x * kWarpsPerBlock + wib;
+  if (c >= cr.y) return;
   advance_chain<NPL>(r, pr, b, parity, c, sm + wib * (NPL * 32));
 }
 
@@ -144,13 +147,14 @@ __global__ void k_binit_accept(RunDev r, BatchDev b, const int *map, int *pendin
 }
 
 __global__ void k_batch_finish(RunDev r, BatchDev b) {
-  const int c = r.c0 + blockIdx.x * blockDim.x + threadIdx.x;
+  const int2 cr = chain_range(r);
+  const int c = cr.x + blockIdx.x * blockDim.x + threadIdx.x;
   DevState *st = r.st;
   if (st->terminated || st->error || st->finalised) return;
   __shared__ unsigned long long acc[5];
   if (threadIdx.x < 5) acc[threadIdx.x] = 0;
   __syncthreads();
-  if (c < r.c1) {
+  if (c < cr.y) {
     const int s = r.cdest[c];
     for (int i = 0; i < r.d; ++i) r.X[static_cast<long long>(s) * r.dp + i] = b.x[static_cast<long long>(c) * b.dp + i];
     r.E[s] = b.e[c];

@@ -429,13 +429,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_gp_chains(RunDev r, PriorDev pr
   if (q.prof && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   for (;;) {
     if (tid == 0) {
-      sh_c = r.c0 + atomicAdd(q.queue, 1);
+      sh_c = chain_range(r).x + atomicAdd(q.queue, 1);
       cnt[0] = 0;
       cnt[1] = 0;
     }
     __syncthreads();
     const int c = sh_c;
-    if (c >= r.c1) break;
+    if (c >= chain_range(r).y) break;
     for (int par = 0;; par ^= 1) {
       if (tid < 32) advance_chain<NPL>(r, pr, bl, par, c, sZ);
       __syncthreads();

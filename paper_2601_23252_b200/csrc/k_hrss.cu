@@ -49,8 +49,9 @@ __global__ void __launch_bounds__(256) k_hrss(RunDev r, PriorDev pr, EnergyDev e
   stage_energy(en, sP, es);
   __syncthreads();
   if (sh_flag) return;
-  const int c = r.c0 + blockIdx.x * wpb + cib;
-  if (c >= r.c1) return;  // uniform over the chain's warps
+  const int2 cr = chain_range(r);
+  const int c = cr.x + blockIdx.x * wpb + cib;
+  if (c >= cr.y) return;  // uniform over the chain's warps
   float *wred = sh_red + cib * 4;
   int epar = 0;
   (void)wred;
@@ -73,12 +74,13 @@ __global__ void __launch_bounds__(256) k_hrss(RunDev r, PriorDev pr, EnergyDev e
   float pa[NPL], pb[NPL];
   load_prior_lane<NPL>(pr, lane, d, pa, pb);
   float x[NPL], v[NPL], xp[NPL];
+  const float *xs = start_row(r, par);
 #pragma unroll
   for (int t = 0; t < NPL; ++t) {
     const int i = lane + 32 * t;
-    x[t] = i < d ? r.Xs[static_cast<long long>(par) * r.dp + i] : 0.f;
+    x[t] = i < d ? xs[i] : 0.f;
   }
-  float e = r.Es[par];
+  float e = start_e(r, par);
   bool dummy;
   float lp = prior_logp<NPL>(x, pr, pa, pb, lane, d, dummy);
 
@@ -87,7 +89,7 @@ __global__ void __launch_bounds__(256) k_hrss(RunDev r, PriorDev pr, EnergyDev e
   for (int j = 0; j < p; ++j) {
     if (r.Vpre) {
       // ---- direction precomputed for this (chain, step) by k_dirs ----
-      const float *vr = r.Vpre + (static_cast<long long>(c - r.c0) * p + j) * r.dp;
+      const float *vr = r.Vpre + (static_cast<long long>(c - cr.x) * p + j) * r.dp;
 #pragma unroll
       for (int t = 0; t < NPL; ++t) {
         const int i = lane + 32 * t;
@@ -244,8 +246,9 @@ __global__ void __launch_bounds__(256) k_dirs(RunDev r, float *V) {
   if (sh_flag) return;
   const long long q = static_cast<long long>(blockIdx.x) * wpb + wib;  // (c - c0) * p + j
   const int p = r.p;
-  if (q >= static_cast<long long>(r.c1 - r.c0) * p) return;
-  const int c = r.c0 + static_cast<int>(q / p), j = static_cast<int>(q % p);
+  const int2 cr = chain_range(r);
+  if (q >= static_cast<long long>(cr.y - cr.x) * p) return;
+  const int c = cr.x + static_cast<int>(q / p), j = static_cast<int>(q % p);
   const uint32_t it = static_cast<uint32_t>(r.st->iter);
   const int s = r.cdest[c];
   const bool euclid = r.dir_norm == NSS_DIR_EUCLIDEAN;
@@ -328,8 +331,9 @@ __global__ void __launch_bounds__(256) k_rw(RunDev r, PriorDev pr, EnergyDev en)
   stage_energy(en, sP, es);
   __syncthreads();
   if (sh_flag) return;
-  const int c = r.c0 + blockIdx.x * wpb + wib;
-  if (c >= r.c1) return;
+  const int2 cr = chain_range(r);
+  const int c = cr.x + blockIdx.x * wpb + wib;
+  if (c >= cr.y) return;
   DevState *st = r.st;
   const uint32_t it = static_cast<uint32_t>(st->iter);
   const int s = r.cdest[c];
@@ -342,12 +346,13 @@ __global__ void __launch_bounds__(256) k_rw(RunDev r, PriorDev pr, EnergyDev en)
   float pa[NPL], pb[NPL];
   load_prior_lane<NPL>(pr, lane, d, pa, pb);
   float x[NPL], xp[NPL];
+  const float *xs = start_row(r, par);
 #pragma unroll
   for (int t = 0; t < NPL; ++t) {
     const int i = lane + 32 * t;
-    x[t] = i < d ? r.Xs[static_cast<long long>(par) * r.dp + i] : 0.f;
+    x[t] = i < d ? xs[i] : 0.f;
   }
-  float e = r.Es[par];
+  float e = start_e(r, par);
   bool dummy;
   float lp = prior_logp<NPL>(x, pr, pa, pb, lane, d, dummy);
   unsigned long long n_probe = 0, n_eval = 0, n_rej = 0;

@@ -210,8 +210,9 @@ __global__ void __launch_bounds__(256) k_hrss_lane(RunDev r, PriorDev pr, Energy
     }
   }
   if constexpr (kSmemTables) __syncthreads();
-  const int c = r.c0 + blockIdx.x * wpb + wib;
-  if (c >= r.c1) return;
+  const int2 cr = chain_range(r);
+  const int c = cr.x + blockIdx.x * wpb + wib;
+  if (c >= cr.y) return;
 
   DevState *st = r.st;
   // issue the independent loads first; the flags are checked after
@@ -235,8 +236,9 @@ __global__ void __launch_bounds__(256) k_hrss_lane(RunDev r, PriorDev pr, Energy
   }
   float x[D], v[D];
 #pragma unroll
-  for (int i = 0; i < D; ++i) x[i] = i < d ? r.Xs[static_cast<long long>(par) * r.dp + i] : 0.f;
-  float e = r.Es[par];
+  const float *xs = start_row(r, par);
+  for (int i = 0; i < D; ++i) x[i] = i < d ? xs[i] : 0.f;
+  float e = start_e(r, par);
   if (st->terminated || st->error || st->finalised) return;
   const uint32_t it = static_cast<uint32_t>(st->iter)  /* set by the select kernel */;
   const float e_star = st->e_star;

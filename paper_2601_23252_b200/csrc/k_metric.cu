@@ -5,8 +5,14 @@
 //
 // One launch: B CTAs accumulate shifted fp64 sums over fixed gid chunks and
 // write them to `partials`; the last CTA to finish (atomic ticket) sums the B
-// partials in block order -- so the result does not depend on which CTA is
-// last and the metric is bit-reproducible -- and factorises.  The Cholesky is
+// partials in a fixed two-level order -- the blocks of each of the kSegs gid
+// segments in block order, then the segment sums in segment order -- so the
+// result does not depend on which CTA is last, and a sharded live set (each
+// rank owning whole segments) reaches the same sums bit for
+// bit -- and factorises.  The sums are of y = x - shift, shift = the mean the
+// previous metric found (the prior's centre before the first): a replicated
+// vector, so every rank of a sharded run can form its partials before any
+// exchange.  The Cholesky is
 // row-owner, one barrier per column: thread i owns row i, every thread reads
 // the pivot directly, the column is written to L (never re-read from A), so the
 // trailing update needs no second barrier.  For d <= 32 it runs in one warp
@@ -29,14 +35,49 @@ __device__ __forceinline__ double *raw_groups(double *sm, int nent, int d, int n
   return yd + static_cast<long long>(rows) * dp;
 }
 
+// Entry e summed over the blocks of segment s in block order.
+__device__ __forceinline__ double fold_segment(const double *partials, int s, int bps, int e, int nent1,
+                                               bool is_min) {
+  double acc = is_min ? INFINITY : 0.0;
+  const double *p = partials + static_cast<long long>(s) * bps * nent1 + e;
+  int b = 0;
+  for (; b + 7 < bps; b += 8) {  // 8 independent loads in flight (same summation order)
+    double v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = p[static_cast<long long>(b + q) * nent1];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc = is_min ? fmin(acc, v[q]) : acc + v[q];
+  }
+  for (; b < bps; ++b) {
+    const double v = p[static_cast<long long>(b) * nent1];
+    acc = is_min ? fmin(acc, v) : acc + v;
+  }
+  return acc;
+}
+
+// Entry e of the whole live set: the kSegs segment sums (rows `stride`
+// apart) added in segment order.
+__device__ __forceinline__ double fold_segments(const double *seg, long long stride, int e, bool is_min) {
+  double acc = is_min ? INFINITY : 0.0;
+#pragma unroll
+  for (int s = 0; s < kSegs; ++s) {
+    const double v = seg[s * stride + e];
+    acc = is_min ? fmin(acc, v) : acc + v;
+  }
+  return acc;
+}
+
 // mode 0: one launch (phase 1 in every CTA, phase 2 in the last one by
-// ticket); mode 1: phase 1 only (partials written, no ticket); mode 2: phase 2
-// only, in one CTA, from `partials` already reduced to one row (nblk = 1) by
-// k_metric_reduce.  Large d uses 1 -> reduce -> 2 (a grid-wide reduction
-// instead of one CTA reading every partial); the sums are the same.
-__global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials, unsigned *ticket, int nblk,
+// ticket); mode 1: phase 1 only (partials written, no ticket) for the blocks
+// blk0 .. blk0 + gridDim.x - 1; mode 2: phase 2 only, in one CTA, from
+// `partials` already reduced to one row by k_metric_reduce (or, sharded, by
+// k_metric_segfold).  Large d uses 1 -> reduce -> 2 (a grid-wide reduction
+// instead of one CTA reading every partial); the sums are the same.  Blocks:
+// segment s = b / bps holds blocks s bps .. s bps + bps - 1, each a chunk of
+// ceil(len_s / bps) of the segment's rows.
+__global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials, unsigned *ticket, int bps,
                                                      double reg, int width_rule, double width_param,
-                                                     int end_of_iter, int mode) {
+                                                     int end_of_iter, int mode, int blk0) {
   DevState *st = r.st;
   if (st->error) return;
   if (end_of_iter && st->finalised) return;
@@ -57,22 +98,26 @@ __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials,
   if (mode != 2) {
   if (tid == 0 && blockIdx.x == 0) st->stamp[8] = global_ns();
   // ---------------- phase 1: partial shifted sums of this CTA's rows ----------------
-  const int chunk = (n + nblk - 1) / nblk;
-  const int g0 = min(n, static_cast<int>(blockIdx.x) * chunk), g1 = min(n, g0 + chunk);
+  const int blk = blk0 + static_cast<int>(blockIdx.x);
+  const int seg = blk / bps, q_in = blk - seg * bps;
+  const int s0 = seg_lo(n, seg), s1 = seg_lo(n, seg + 1);
+  const int chunk = (s1 - s0 + bps - 1) / bps;
+  const int g0 = min(s1, s0 + q_in * chunk), g1 = min(s1, g0 + chunk);
   const int rows = g1 - g0;
   const int dp = r.dp;
+  for (int i = tid; i < d; i += blockDim.x) shift[i] = r.mshift[i];
+  __syncthreads();
   // one batch of loads: the chunk is contiguous in X
   {
     const float *src = r.X + static_cast<long long>(g0) * dp;
     for (int q = tid; q < rows * dp; q += blockDim.x) {
       const int c = q % dp;
-      yd[q] = c < d ? static_cast<double>(src[q]) - static_cast<double>(r.X[c]) : 0.0;
+      yd[q] = c < d ? static_cast<double>(src[q]) - shift[c] : 0.0;
     }
   }
   float emin = INFINITY;
   for (int g = g0 + tid; g < g1; g += blockDim.x) emin = fminf(emin, r.E[g]);
   for (int e = tid; e < nent; e += blockDim.x) S[e] = 0.0;
-  for (int i = tid; i < d; i += blockDim.x) shift[i] = static_cast<double>(r.X[i]);  // row 0
   for (int i = tid; i < d; i += blockDim.x) {
     const int b0 = i * (i + 1) / 2;
     for (int j = 0; j <= i; ++j) {
@@ -127,7 +172,7 @@ __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials,
       S[e] = acc;
     }
   __syncthreads();
-  double *out = partials + static_cast<long long>(blockIdx.x) * (nent + 1);
+  double *out = partials + static_cast<long long>(blk) * (nent + 1);
   for (int e = tid; e < nent; e += blockDim.x) out[e] = S[e];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) emin = fminf(emin, __shfl_xor_sync(0xffffffffu, emin, o));
@@ -139,7 +184,7 @@ __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials,
     out[nent] = static_cast<double>(mn);
     if (mode == 0) {
       __threadfence();
-      sh_last = atomicAdd(ticket, 1u) == static_cast<unsigned>(nblk - 1);
+      sh_last = atomicAdd(ticket, 1u) == static_cast<unsigned>(kSegs * bps - 1);
     }
   }
   if (mode == 1) return;
@@ -173,28 +218,17 @@ __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials,
     }
   }
   for (int e = tid; e <= nent; e += blockDim.x) {
-    // fixed block order; loads issued 8 at a time (independent addresses);
-    // entry nent holds the per-block minimum energy
+    // fixed two-level order (blocks within a segment, then segments); entry
+    // nent holds the per-block minimum energy.  mode 2: one reduced row.
     const bool is_min = e == nent;
-    double acc = is_min ? INFINITY : 0.0;
-    int b = 0;
-    for (; b + 15 < nblk; b += 16) {  // 16 independent loads in flight per thread (same summation order)
-      double v[16];
+    double acc;
+    if (mode == 2) {
+      acc = partials[e];
+    } else {
+      double segs[kSegs];
 #pragma unroll
-      for (int q = 0; q < 16; ++q) v[q] = partials[static_cast<long long>(b + q) * (nent + 1) + e];
-#pragma unroll
-      for (int q = 0; q < 16; ++q) acc = is_min ? fmin(acc, v[q]) : acc + v[q];
-    }
-    for (; b + 7 < nblk; b += 8) {
-      double v[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) v[q] = partials[static_cast<long long>(b + q) * (nent + 1) + e];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) acc = is_min ? fmin(acc, v[q]) : acc + v[q];
-    }
-    for (; b < nblk; ++b) {
-      const double v = partials[static_cast<long long>(b) * (nent + 1) + e];
-      acc = is_min ? fmin(acc, v) : acc + v;
+      for (int s = 0; s < kSegs; ++s) segs[s] = fold_segment(partials, s, bps, e, nent + 1, is_min);
+      acc = fold_segments(segs, 1, 0, is_min);
     }
     if (is_min) {
       sh_emin = static_cast<float>(acc);
@@ -210,6 +244,9 @@ __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials,
   __syncthreads();
   if (tid == 0) st->stamp[11] = global_ns();
   const double nn = static_cast<double>(n);
+  // the live set's mean, the shift of the next metric's sums (every CTA of
+  // this metric is past its phase 1)
+  for (int i = tid; i < d; i += blockDim.x) r.mshift[i] += S1[i] / nn;
   for (int e = tid; e < d * d; e += blockDim.x) {
     const int i = e / d, j = e - i * d;
     if (j <= i) A[i * ld + j] = (A[i * ld + j] - S1[i] * S1[j] / nn) / (nn - 1.0);
@@ -404,31 +441,45 @@ __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials,
   }
 }
 
-// The large-d reduction of k_metric's partials: thread e sums entry e over
-// the blocks in block order (the order and operations of the one-CTA
-// reduction in phase 2, so the sums are identical); entry nent holds the
-// minimum energy.
-__global__ void __launch_bounds__(128) k_metric_reduce(RunDev r, const double *partials, int nblk, int nent1,
-                                                       double *sums, int end_of_iter) {
+// The large-d reduction of k_metric's partials: thread e sums entry e in the
+// two-level order of phase 2 (so the sums are identical); entry nent holds the
+// minimum energy.  seg_out == null: the whole live set into `sums`; else
+// (sharded) the sums of segments seg0 .. seg0 + nseg - 1 into rows of seg_out
+// (row stride nent1).
+__global__ void __launch_bounds__(128) k_metric_reduce(RunDev r, const double *partials, int bps, int nent1,
+                                                       double *sums, int end_of_iter, double *seg_out, int seg0,
+                                                       int nseg) {
   const DevState *st = r.st;
   if (st->error || (end_of_iter && st->finalised)) return;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= nent1) return;
   const bool is_min = e == nent1 - 1;
-  double acc = is_min ? INFINITY : 0.0;
-  int b = 0;
-  for (; b + 15 < nblk; b += 16) {
-    double v[16];
-#pragma unroll
-    for (int q = 0; q < 16; ++q) v[q] = partials[static_cast<long long>(b + q) * nent1 + e];
-#pragma unroll
-    for (int q = 0; q < 16; ++q) acc = is_min ? fmin(acc, v[q]) : acc + v[q];
+  if (seg_out) {
+    for (int s = 0; s < nseg; ++s)
+      seg_out[static_cast<long long>(s) * nent1 + e] = fold_segment(partials, seg0 + s, bps, e, nent1, is_min);
+    return;
   }
-  for (; b < nblk; ++b) {
-    const double v = partials[static_cast<long long>(b) * nent1 + e];
-    acc = is_min ? fmin(acc, v) : acc + v;
-  }
-  sums[e] = acc;
+  double segs[kSegs];
+#pragma unroll
+  for (int s = 0; s < kSegs; ++s) segs[s] = fold_segment(partials, s, bps, e, nent1, is_min);
+  sums[e] = fold_segments(segs, 1, 0, is_min);
+}
+
+// Sharded live set: the kSegs segment rows gathered from every rank (rank q's
+// rows at seg_rows + q * rank_stride, its first segment q * kSegs / world)
+// folded in segment order -- the same sums as k_metric_reduce on one GPU.
+__global__ void __launch_bounds__(128) k_metric_segfold(RunDev r, const double *seg_rows, long long rank_stride,
+                                                        int nent1, double *sums) {
+  if (r.st->error) return;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nent1) return;
+  const bool is_min = e == nent1 - 1;
+  const int per = kSegs / r.world;
+  double segs[kSegs];
+#pragma unroll
+  for (int s = 0; s < kSegs; ++s)
+    segs[s] = seg_rows[(s / per) * rank_stride + static_cast<long long>(s % per) * nent1 + e];
+  sums[e] = fold_segments(segs, 1, 0, is_min);
 }
 
 // A9 / R-19 on demand (the host asks for the run's state between
@@ -464,10 +515,10 @@ __global__ void __launch_bounds__(kThreads) k_term_probe(RunDev r, int probe, De
 
 // mode 0: both phases; 1: phase 1 only (the large-d partials: sized for
 // their rows alone, so two CTAs fit per SM); 2: phase 2 only
-size_t metric_smem(int n, int d, int nblk, int mode = 0) {
+size_t metric_smem(int n, int d, int bps, int mode = 0) {
   const int npair = d * (d + 1) / 2, nent = npair + d;
   const int dp = (d + 3) & ~3;
-  const int rows = (n + nblk - 1) / nblk;
+  const int rows = (seg_lo(n, 1) + 1 + bps - 1) / bps;  // a segment has at most floor(n / kSegs) + 1 rows
   const int G = nent < kThreads ? kThreads / nent : 1;  // row groups (raw_groups)
   const size_t p1 = static_cast<size_t>(nent + d) * 8 + ((2 * static_cast<size_t>(npair) + 7) / 8) * 8 +
                     static_cast<size_t>(rows) * dp * 8 + (G > 1 ? static_cast<size_t>(G) * nent * 8 : 0) + 64;
@@ -478,6 +529,8 @@ size_t metric_smem(int n, int d, int nblk, int mode = 0) {
 
 }  // namespace
 
+// Blocks per segment (the metric's partials: kSegs * this many rows of
+// nent + 1 doubles).
 int metric_blocks(int n, int d) {
   const int npair = d * (d + 1) / 2;
   const int dp = (d + 3) & ~3;
@@ -489,9 +542,10 @@ int metric_blocks(int n, int d) {
   const int nent = npair + d, G = nent < kThreads ? kThreads / nent : 1;
   const long long fixed = 64 + static_cast<long long>(nent + d) * 8 + ((2LL * npair + 7) / 8) * 8 +
                           (G > 1 ? static_cast<long long>(G) * nent * 8 : 0);
-  const int rows_max = static_cast<int>((200LL * 1024 - fixed) / (dp * 8));
+  const int rows_max = static_cast<int>((200LL * 1024 - fixed) / (dp * 8)) - 1;
   if (rows_per_block > rows_max) rows_per_block = rows_max;
-  const int b = (n + rows_per_block - 1) / rows_per_block;
+  const int seg = seg_lo(n, 1) + 1;  // longest segment
+  const int b = (seg + rows_per_block - 1) / rows_per_block;
   return b < 1 ? 1 : b;
 }
 
@@ -501,27 +555,55 @@ void launch_term_probe(const RunDev &r, const LaunchCtx &lc, int probe, DevState
 }
 
 void launch_metric(const RunDev &r, double metric_reg, int width_rule, double width_param, int end_of_iteration,
-                   double *partials, unsigned *ticket, int n_blocks, const LaunchCtx &lc) {
+                   double *partials, unsigned *ticket, int bps, const LaunchCtx &lc) {
   NSS_MAX_SMEM(k_metric, 200 * 1024);
   NSS_PIN_CARVEOUT(k_metric);
-  const size_t smem = metric_smem(r.n, r.d, n_blocks);
-  if (r.d < kSplitMinD || n_blocks == 1) {
-    k_metric<<<n_blocks, kThreads, smem, lc.stream>>>(r, partials, ticket, n_blocks, metric_reg, width_rule,
-                                                      width_param, end_of_iteration, 0);
+  const int nblk = kSegs * bps;
+  if (r.d < kSplitMinD) {
+    k_metric<<<nblk, kThreads, metric_smem(r.n, r.d, bps), lc.stream>>>(r, partials, ticket, bps, metric_reg,
+                                                                        width_rule, width_param, end_of_iteration, 0, 0);
     ++*lc.launch_counter;
     return;
   }
   // large d: partials by every CTA, a grid-wide reduction into the row after
-  // the partials (nss_init sizes the buffer for n_blocks + 1 rows), then the
+  // the partials (nss_init sizes the buffer for nblk + 1 rows), then the
   // factorisation from that one row
   const int nent1 = r.d * (r.d + 1) / 2 + r.d + 1;
-  double *sums = partials + static_cast<long long>(n_blocks) * nent1;
-  k_metric<<<n_blocks, kThreads, metric_smem(r.n, r.d, n_blocks, 1), lc.stream>>>(
-      r, partials, ticket, n_blocks, metric_reg, width_rule, width_param, end_of_iteration, 1);
-  k_metric_reduce<<<(nent1 + 127) / 128, 128, 0, lc.stream>>>(r, partials, n_blocks, nent1, sums, end_of_iteration);
-  k_metric<<<1, kThreads, metric_smem(r.n, r.d, n_blocks, 2), lc.stream>>>(r, sums, ticket, 1, metric_reg, width_rule,
-                                                                          width_param, end_of_iteration, 2);
+  double *sums = partials + static_cast<long long>(nblk) * nent1;
+  k_metric<<<nblk, kThreads, metric_smem(r.n, r.d, bps, 1), lc.stream>>>(
+      r, partials, ticket, bps, metric_reg, width_rule, width_param, end_of_iteration, 1, 0);
+  k_metric_reduce<<<(nent1 + 127) / 128, 128, 0, lc.stream>>>(r, partials, bps, nent1, sums, end_of_iteration,
+                                                               nullptr, 0, 0);
+  k_metric<<<1, kThreads, metric_smem(r.n, r.d, bps, 2), lc.stream>>>(r, sums, ticket, bps, metric_reg, width_rule,
+                                                                      width_param, end_of_iteration, 2, 0);
   *lc.launch_counter += 3;
+}
+
+// Sharded live set, before the exchange: this rank's segments' partials
+// (blocks of segments [seg0, seg0 + nseg)) reduced to one row per segment in
+// seg_out (nseg rows of nent + 1 doubles).
+void launch_metric_shard_partials(const RunDev &r, double *partials, int bps, int seg0, int nseg, double *seg_out,
+                                  const LaunchCtx &lc) {
+  NSS_MAX_SMEM(k_metric, 200 * 1024);
+  NSS_PIN_CARVEOUT(k_metric);
+  const int nent1 = r.d * (r.d + 1) / 2 + r.d + 1;
+  k_metric<<<nseg * bps, kThreads, metric_smem(r.n, r.d, bps, 1), lc.stream>>>(r, partials, nullptr, bps, 0.0, 0,
+                                                                              0.0, 1, 1, seg0 * bps);
+  k_metric_reduce<<<(nent1 + 127) / 128, 128, 0, lc.stream>>>(r, partials, bps, nent1, nullptr, 1, seg_out, seg0,
+                                                               nseg);
+  *lc.launch_counter += 2;
+}
+
+// After the exchange: every segment's row folded in segment order, then the
+// factorisation and width (replicated on every rank).
+void launch_metric_shard_final(const RunDev &r, double metric_reg, int width_rule, double width_param,
+                               const double *seg_rows, long long rank_stride, double *sums, unsigned *ticket,
+                               const LaunchCtx &lc) {
+  const int nent1 = r.d * (r.d + 1) / 2 + r.d + 1;
+  k_metric_segfold<<<(nent1 + 127) / 128, 128, 0, lc.stream>>>(r, seg_rows, rank_stride, nent1, sums);
+  k_metric<<<1, kThreads, metric_smem(r.n, r.d, 1, 2), lc.stream>>>(r, sums, ticket, 1, metric_reg, width_rule,
+                                                                    width_param, 1, 2, 0);
+  *lc.launch_counter += 2;
 }
 
 }  // namespace nss

@@ -32,7 +32,36 @@ void launch_samples(const RunDev &r, long long N, double *logw, double *scratch,
                     double beta, double *zacc);
 void launch_resample(const RunDev &r, long long N, const double *logw, double *cum, long long m, uint64_t seed,
                      long long *idx, double *x, const LaunchCtx &lc);
+// sharded live set (k_shard.cu, k_metric.cu, dist.cu)
+bool nccl_allgather_inplace(void *comm, void *buf, size_t bytes, int rank, cudaStream_t stream, std::string *err);
+bool ipc_exchange(void *comm, int world, int rank, void *const *mine, int nptr, void **peers,
+                  std::vector<void *> *opened, cudaStream_t stream, std::string *err);
+size_t shard_block_bytes(int k, int own_max, int world, int d);
+size_t shard_metric_offset(int k, int own_max);
+void launch_shard_cand(const RunDev &r, char *block, int kc_cap, const LaunchCtx &lc);
+void launch_shard_merge(const RunDev &r, const char *gather, size_t block_bytes, int m_max, int *crange,
+                        const LaunchCtx &lc);
+void launch_shard_dead_rows(const RunDev &r, const LaunchCtx &lc);
+void launch_shard_pack_live(const RunDev &r, float *block, const LaunchCtx &lc);
+void launch_shard_unpack_live(const RunDev &r, const float *buf, long long rows_cap, const LaunchCtx &lc);
+void launch_shard_mask_rows(const RunDev &r, const LaunchCtx &lc);
+void launch_metric_shard_partials(const RunDev &r, double *partials, int bps, int seg0, int nseg, double *seg_out,
+                                  const LaunchCtx &lc);
+void launch_metric_shard_final(const RunDev &r, double metric_reg, int width_rule, double width_param,
+                               const double *seg_rows, long long rank_stride, double *sums, unsigned *ticket,
+                               const LaunchCtx &lc);
 }  // namespace nss
+
+// Ranks of one sharded run emulated in one process on one GPU (nss_group_*):
+// the members share one stream and one gather buffer, so an "all-gather" is
+// every member writing its block in place, and a member's peer table points
+// at the other members' arrays.  Freed with the last member.
+struct nss_group {
+  int world = 0, alive = 0;
+  char *gather = nullptr;
+  float *live = nullptr;
+  cudaStream_t stream = nullptr;
+};
 
 static const int kPhases = 5;
 
@@ -58,7 +87,7 @@ struct nss_ctx {
   // demand (k_term_probe) when the host reads the state.
   bool metric_pending = false;
   bool term_stale = false;
-  int nblk = 1;
+  int bps = 1;  // metric blocks per gid segment (k_metric.cu)
   double *summary = nullptr;  // device: [mean, std, closed lz_0..R]
   void *h_block = nullptr;    // one pinned (host-mapped) allocation for all host mirrors below
   DevState *d_h_st = nullptr;  // device aliases of h_st / h_lz0 (mapped)
@@ -108,6 +137,19 @@ struct nss_ctx {
   float *xbuf = nullptr, *xall = nullptr;
   float *vpre = nullptr;  // k_dirs output (warp engine, d > 32)
   size_t vpre_floats = 0;
+  // sharded live set (k_shard.cu): this rank owns segments
+  // [seg0, seg0 + nseg) = gids [r.rank_lo[rank], r.rank_lo[rank + 1])
+  bool sharded = false;
+  nss_group *group = nullptr;  // in-process emulation of the ranks (nss_group_*), else NCCL
+  int seg0 = 0, nseg = 0, own_max = 0, kc_cap = 0;
+  size_t blk_bytes = 0, met_off = 0;
+  char *gather = nullptr;       // world * blk_bytes
+  float *live_buf = nullptr;    // world * own_max * (dp + 2): live-set gather
+  double *shard_sums = nullptr;
+  int *crange = nullptr;
+  bool stage_wm = false;        // with-metric flag between the group stages of an iteration
+  bool live_gathered = true;    // every rank's rows present locally (init, after a gather)
+  std::vector<void *> ipc_open, raw_allocs;
   // F3 tempered SMC-SS (k_smc.cu): particles are the live set
   bool smc = false;
   double smc_rho = 0.9;
@@ -286,7 +328,9 @@ nss_status pull_state(nss_ctx *c) {
     c->probe_in_graph = false;
     c->term_stale = false;
   } else if (c->d_h_st && c->r.lz) {
-    launch_term_probe(c->r, lc, c->term_stale ? 1 : 0, c->d_h_st, c->d_h_lz0);
+    // sharded: the termination test runs in the next merge (global minimum);
+    // this rank's E holds only its own rows
+    launch_term_probe(c->r, lc, (c->term_stale && !c->sharded) ? 1 : 0, c->d_h_st, c->d_h_lz0);
     c->term_stale = false;
     CK(cudaGetLastError());
   } else {
@@ -360,16 +404,75 @@ nss_status launch_metric_on(nss_ctx *c, cudaStream_t stream, int end_of_iter) {
   LaunchCtx l{stream, &c->launches};
   return timed_launch(c, 3, stream, [&] {
     launch_metric(c->r, c->cfg.metric_reg, c->cfg.width_rule, c->cfg.width, end_of_iter, c->partials, c->ticket,
-                  c->nblk, l);
+                  c->bps, l);
   });
+}
+
+// Stages of a sharded iteration: kPre (rank-local
+// candidates and moment sums into this rank's block), the all-gather, kPost
+// (replicated metric + merge, then this rank's chains).  A one-process context
+// runs kAll; the in-process group drives kPre on every member, then kPost.
+enum Stage { kAll = 0, kPre = 1, kPost = 2 };
+
+nss_status shard_pre(nss_ctx *c, bool with_metric) {
+  LaunchCtx lc = lctx(c);
+  char *mine = c->gather + static_cast<size_t>(c->r.rank) * c->blk_bytes;
+  if (with_metric)
+    launch_metric_shard_partials(c->r, c->partials, c->bps, c->seg0, c->nseg,
+                                 reinterpret_cast<double *>(mine + c->met_off), lc);
+  launch_shard_cand(c->r, mine, c->kc_cap, lc);
+  CK(cudaGetLastError());
+  return NSS_OK;
+}
+
+nss_status shard_exchange(nss_ctx *c) {
+  if (c->group) return NSS_OK;  // members wrote their blocks into the shared buffer
+  std::string err;
+  if (!nccl_allgather_inplace(c->comm, c->gather, c->blk_bytes, c->r.rank, c->stream, &err)) {
+    c->poisoned = true;
+    return fail(c, NSS_ERR_COMM, err);
+  }
+  return NSS_OK;
+}
+
+// Replicated part of a sharded iteration's select phase: metric (fork) and
+// merge, then this rank's dead rows; returns with the metric joined.
+nss_status shard_post_select(nss_ctx *c, bool with_metric) {
+  LaunchCtx lc = lctx(c);
+  nss_status s;
+  if (with_metric) {
+    CK(cudaEventRecord(c->ev_fork, c->stream));
+    CK(cudaStreamWaitEvent(c->side2, c->ev_fork, 0));
+    LaunchCtx l2{c->side2, &c->launches};
+    if ((s = timed_launch(c, 3, c->side2, [&] {
+           launch_metric_shard_final(c->r, c->cfg.metric_reg, c->cfg.width_rule, c->cfg.width,
+                                     reinterpret_cast<const double *>(c->gather + c->met_off),
+                                     static_cast<long long>(c->blk_bytes / 8), c->shard_sums, c->ticket, l2);
+         })))
+      return s;
+    CK(cudaEventRecord(c->ev_met, c->side2));
+  }
+  if ((s = timed_launch(c, 1, c->stream, [&] {
+         launch_shard_merge(c->r, c->gather, c->blk_bytes, c->r.world * c->kc_cap, c->crange, lc);
+         launch_shard_dead_rows(c->r, lc);
+       })))
+    return s;
+  if (with_metric) CK(cudaStreamWaitEvent(c->stream, c->ev_met, 0));
+  return NSS_OK;
 }
 
 // One iteration: [deferred A5 of the previous iteration || A2-A4 select] ->
 // [A8 evidence on the side stream || A6 HRSS] (-> multi-GPU exchange).
-nss_status enqueue_iteration_eager(nss_ctx *c, bool with_metric) {
+nss_status enqueue_iteration_eager(nss_ctx *c, bool with_metric, Stage stage = kAll) {
   LaunchCtx lc = lctx(c);
   nss_status s;
-  if (with_metric) {
+  if (c->sharded) {
+    if (stage != kPost && (s = shard_pre(c, with_metric))) return s;
+    if (stage == kPre) return NSS_OK;
+    if (stage == kAll && (s = shard_exchange(c))) return s;
+    if ((s = shard_post_select(c, with_metric))) return s;
+    with_metric = false;  // joined above
+  } else if (with_metric) {
     if (c->serial_evidence) {
       if ((s = launch_metric_on(c, c->stream, 1))) return s;
     } else {
@@ -379,11 +482,12 @@ nss_status enqueue_iteration_eager(nss_ctx *c, bool with_metric) {
       CK(cudaEventRecord(c->ev_met, c->side2));
     }
   }
-  if ((s = timed_launch(c, 1, c->stream, [&] {
-         launch_select(c->r, lc);
-         if (c->cfg.update_all) launch_chains_all(c->r, c->r.cdest, c->r.cpar, const_cast<float *>(c->r.Xs),
-                                                  const_cast<float *>(c->r.Es), lc);
-       })))
+  if (!c->sharded && (s = timed_launch(c, 1, c->stream, [&] {
+                        launch_select(c->r, lc);
+                        if (c->cfg.update_all)
+                          launch_chains_all(c->r, c->r.cdest, c->r.cpar, const_cast<float *>(c->r.Xs),
+                                            const_cast<float *>(c->r.Es), lc);
+                      })))
     return s;
   if (c->serial_evidence) {
     if ((s = timed_launch(c, 2, c->stream, [&] { launch_evidence(c->r, 0, lc); }))) return s;
@@ -406,7 +510,7 @@ nss_status enqueue_iteration_eager(nss_ctx *c, bool with_metric) {
 
 // Multi-GPU: every rank's new chain rows to every rank.
 nss_status exchange(nss_ctx *c) {
-  if (!c->comm) return NSS_OK;
+  if (!c->comm || c->sharded) return NSS_OK;
   std::string err;
   if (!exchange_chains(c->r, c->comm, c->xbuf, c->xall, c->kc, lctx(c), &err)) {
     c->poisoned = true;
@@ -530,17 +634,24 @@ void drop_graph(nss_ctx *c) {
 // One iteration with the batch engine: the HRSS part is a data-dependent
 // number of rounds, replayed in chunks from a captured graph; the host polls
 // the last round's probe count after each chunk (zero: every chain is done).
-nss_status enqueue_iteration_batch(nss_ctx *c) {
+nss_status enqueue_iteration_batch(nss_ctx *c, Stage stage = kAll) {
   nss_status s;
   if ((s = ensure_batch(c))) return s;
   LaunchCtx lc = lctx(c);
-  if (c->metric_pending && (s = launch_metric_on(c, c->stream, 1))) return s;
-  if ((s = timed_launch(c, 1, c->stream, [&] {
-         launch_select(c->r, lc);
-         if (c->cfg.update_all) launch_chains_all(c->r, c->r.cdest, c->r.cpar, const_cast<float *>(c->r.Xs),
-                                                  const_cast<float *>(c->r.Es), lc);
-       })))
-    return s;
+  if (c->sharded) {
+    if (stage != kPost && (s = shard_pre(c, c->metric_pending))) return s;
+    if (stage == kPre) return NSS_OK;
+    if (stage == kAll && (s = shard_exchange(c))) return s;
+    if ((s = shard_post_select(c, c->metric_pending))) return s;
+  } else {
+    if (c->metric_pending && (s = launch_metric_on(c, c->stream, 1))) return s;
+    if ((s = timed_launch(c, 1, c->stream, [&] {
+           launch_select(c->r, lc);
+           if (c->cfg.update_all) launch_chains_all(c->r, c->r.cdest, c->r.cpar, const_cast<float *>(c->r.Xs),
+                                                    const_cast<float *>(c->r.Es), lc);
+         })))
+      return s;
+  }
   CK(cudaEventRecord(c->ev_sel, c->stream));
   CK(cudaStreamWaitEvent(c->side, c->ev_sel, 0));
   LaunchCtx ls{c->side, &c->launches};
@@ -631,20 +742,27 @@ nss_status ensure_vpre(nss_ctx *c) {
   return NSS_OK;
 }
 
-nss_status enqueue_iteration(nss_ctx *c, bool with_probe = false) {
+nss_status enqueue_iteration(nss_ctx *c, bool with_probe = false, Stage stage = kAll) {
   nss_status vs = ensure_vpre(c);
   if (vs) return vs;
-  const bool wm = c->metric_pending;
-  c->term_stale = true;
-  c->metric_pending = true;
+  // group stages: kPre records the with-metric flag, kPost reuses it
+  const bool wm = stage == kPost ? c->stage_wm : c->metric_pending;
+  c->stage_wm = wm;
+  if (stage == kPre) {
+    c->metric_pending = wm;
+  } else {
+    c->term_stale = true;
+    c->metric_pending = true;
+    c->live_gathered = !c->sharded;
+  }
   c->probe_in_graph = false;
   if (resolve_engine(c) == 2) {
     c->metric_pending = wm;  // the batch path launches the deferred metric itself
-    const nss_status s = enqueue_iteration_batch(c);
-    c->metric_pending = true;
+    const nss_status s = enqueue_iteration_batch(c, stage);
+    c->metric_pending = stage == kPre ? wm : true;
     return s;
   }
-  if (c->timing || !c->use_graph) return enqueue_iteration_eager(c, wm);
+  if (c->timing || !c->use_graph || stage != kAll) return enqueue_iteration_eager(c, wm, stage);
   const bool probe = with_probe && wm && c->d_h_st && c->r.lz;
   cudaGraphExec_t &g = probe ? c->graph_info : wm ? c->graph : c->graph0;
   long long &gl = probe ? c->graph_info_launches : wm ? c->graph_launches : c->graph0_launches;
@@ -720,15 +838,25 @@ NSS_API nss_status nss_get_unique_id(uint8_t out[128]) {
   return nccl_unique_id(out) ? NSS_OK : NSS_ERR_UNSUPPORTED;
 }
 
-NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, const nss_config *cfg,
-                            const nss_dist *dist, nss_ctx **out) {
+// nss_init and its variants: smc_mode keeps the replicated multi-GPU layout
+// (F3); `group` != null builds rank `dist->rank` of an in-process group.
+static nss_status init_impl(const nss_prior *prior, const nss_energy *energy, const nss_config *cfg,
+                            const nss_dist *dist, bool smc_mode, nss_group *group, nss_ctx **out) {
   if (!out) return NSS_ERR_INVALID_ARG;
   *out = nullptr;
   if (!validate(prior, energy, cfg)) return NSS_ERR_INVALID_ARG;
   if (dist && (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world ||
-               (dist->world > 1 && !dist->nccl_uid)))
+               (dist->world > 1 && !dist->nccl_uid && !group)))
     return NSS_ERR_INVALID_ARG;
+  // sharded live set: NS over several ranks (or an in-process group)
+  const bool sharded = !smc_mode && dist && (dist->world > 1 || dist->nccl_uid || group);
+  if (sharded) {
+    if (kSegs % dist->world != 0) return NSS_ERR_INVALID_ARG;  // world in {1, 2, 4, 8}
+    if (cfg->update_all) return NSS_ERR_UNSUPPORTED;
+  }
   nss_ctx *c = new nss_ctx();
+  c->sharded = sharded;
+  c->group = group;
   // measurement hook (NSS_INIT_PROF): host wall time of the phases of nss_init
   const bool iprof = getenv("NSS_INIT_PROF") != nullptr;
   auto it0 = std::chrono::steady_clock::now();
@@ -944,8 +1072,19 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
   r.term_log_ratio = static_cast<float>(cfg->term_log_ratio);
   const size_t cap = static_cast<size_t>(cfg->max_dead);
   ip("setup");
-  if ((s = dalloc(c, &r.X, static_cast<size_t>(n) * c->dp))) return bail(s);
-  if ((s = dalloc(c, &r.E, n))) return bail(s);
+  if (sharded && !group) {
+    // other ranks map X and E with CUDA IPC: plain cudaMalloc allocations
+    for (int q = 0; q < 2; ++q) {
+      const size_t bytes = (q == 0 ? static_cast<size_t>(n) * c->dp : static_cast<size_t>(n)) * sizeof(float);
+      void *p = nullptr;
+      if (cudaMalloc(&p, bytes) != cudaSuccess || cudaMemset(p, 0, bytes) != cudaSuccess) return bail(NSS_ERR_OOM);
+      c->raw_allocs.push_back(p);
+      (q == 0 ? r.X : r.E) = static_cast<float *>(p);
+    }
+  } else {
+    if ((s = dalloc(c, &r.X, static_cast<size_t>(n) * c->dp))) return bail(s);
+    if ((s = dalloc(c, &r.E, n))) return bail(s);
+  }
   if ((s = dalloc(c, &r.birth, n))) return bail(s);
   if ((s = dalloc(c, &r.L, static_cast<size_t>(d) * c->dp))) return bail(s);
   if ((s = dalloc(c, &r.LT, static_cast<size_t>(d) * c->dp))) return bail(s);
@@ -985,9 +1124,18 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
   if ((s = dalloc(c, &r.lz, R + 1))) return bail(s);
   if ((s = dalloc(c, &r.st, 1))) return bail(s);
   if ((s = dalloc(c, &c->summary, R + 3))) return bail(s);
-  c->nblk = metric_blocks(r.n, d);
+  c->bps = metric_blocks(r.n, d);
   const int nent = d * (d + 1) / 2 + d + 1;
-  if ((s = dalloc(c, &c->partials, static_cast<size_t>(c->nblk + 1) * nent))) return bail(s);  // + the reduced row
+  if ((s = dalloc(c, &c->partials, static_cast<size_t>(kSegs * c->bps + 1) * nent))) return bail(s);  // + the reduced row
+  {
+    // the metric's first shift: the prior's centre (k_metric.cu)
+    std::vector<double> ctr(d);
+    for (int i = 0; i < d; ++i)
+      ctr[i] = prior->kind == NSS_PRIOR_BOX ? 0.5 * (prior->lo[i] + prior->hi[i]) : prior->mean[i];
+    if ((s = dalloc(c, &r.mshift, d))) return bail(s);
+    if (cudaMemcpyAsync(r.mshift, ctr.data(), d * sizeof(double), cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+      return bail(NSS_ERR_CUDA);
+  }
   if ((s = dalloc(c, &c->ticket, 1))) return bail(s);
   {
     std::vector<double> ninf(R + 1, -INFINITY);
@@ -995,8 +1143,58 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
       return bail(NSS_ERR_CUDA);
   }
   ip("alloc");
-  // ---- multi-GPU: this rank's chain block and the NCCL communicator ----
-  if (dist && dist->nccl_uid) {
+  // ---- multi-GPU ----
+  r.world = 1;
+  r.rank = 0;
+  r.rank_lo[0] = 0;
+  r.rank_lo[1] = r.n;
+  if (sharded) {
+    // the sharded live set: this rank's segments and gids,
+    // the exchange block, the communicator and the peer tables
+    const int W = dist->world, q = dist->rank;
+    c->rank = q;
+    c->world = W;
+    r.world = W;
+    r.rank = q;
+    for (int j = 0; j <= W; ++j) r.rank_lo[j] = seg_lo(r.n, j * (kSegs / W));
+    c->seg0 = q * (kSegs / W);
+    c->nseg = kSegs / W;
+    c->own_max = 0;
+    for (int j = 0; j < W; ++j) c->own_max = std::max(c->own_max, r.rank_lo[j + 1] - r.rank_lo[j]);
+    c->kc_cap = static_cast<int>(std::min<long long>(k, c->own_max));
+    c->blk_bytes = shard_block_bytes(static_cast<int>(k), c->own_max, W, d);
+    c->met_off = shard_metric_offset(static_cast<int>(k), c->own_max);
+    r.c0 = 0;  // grid bound only: the chains run are those of crange
+    r.c1 = static_cast<int>(std::min<long long>(k, r.rank_lo[q + 1] - r.rank_lo[q]));
+    if ((s = dalloc(c, &c->crange, 2))) return bail(s);
+    r.crange = c->crange;
+    if ((s = dalloc(c, &c->shard_sums, static_cast<size_t>(nent)))) return bail(s);
+    float **tbl = nullptr;
+    if ((s = dalloc(c, &tbl, 2 * static_cast<size_t>(W)))) return bail(s);
+    r.peerX = tbl;
+    r.peerE = tbl + W;
+    if (group) {
+      c->gather = group->gather;
+      c->live_buf = group->live;  // the peer tables are filled by nss_group_init
+    } else {
+      if ((s = dalloc(c, &c->gather, c->blk_bytes * W))) return bail(s);
+      if ((s = dalloc(c, &c->live_buf, static_cast<size_t>(W) * c->own_max * (c->dp + 2)))) return bail(s);
+      std::string err;
+      if (!nccl_comm_init(&c->comm, W, dist->nccl_uid, q, &err)) {
+        c->err = err;
+        return bail(NSS_ERR_COMM);
+      }
+      void *mine[2] = {r.X, r.E};
+      std::vector<void *> peers(2 * W);
+      if (!ipc_exchange(c->comm, W, q, mine, 2, peers.data(), &c->ipc_open, c->stream, &err)) {
+        c->err = err;
+        return bail(NSS_ERR_COMM);
+      }
+      if (cudaMemcpyAsync(tbl, peers.data(), 2 * W * sizeof(void *), cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+        return bail(NSS_ERR_CUDA);
+      if (cudaStreamSynchronize(c->stream) != cudaSuccess) return bail(NSS_ERR_CUDA);
+    }
+  } else if (dist && dist->nccl_uid) {  // F3 SMC: replicated state, chains split
     c->rank = dist->rank;
     c->world = dist->world;
     c->kc = static_cast<int>((nch + c->world - 1) / c->world);
@@ -1021,13 +1219,26 @@ NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, co
     launch_init(r, pr, en, lc);
   }
   ip("comm");
-  launch_metric(r, cfg->metric_reg, cfg->width_rule, cfg->width, 0, c->partials, c->ticket, c->nblk, lc);
+  if (sharded) {
+    // every rank drew all n initial points (same draws); the first metric is
+    // formed from the ranks' segments in the first iteration
+    c->metric_pending = true;
+    c->live_gathered = true;
+    c->use_graph = group == nullptr;
+  } else {
+    launch_metric(r, cfg->metric_reg, cfg->width_rule, cfg->width, 0, c->partials, c->ticket, c->bps, lc);
+  }
   if (cudaGetLastError() != cudaSuccess) return bail(NSS_ERR_CUDA);
   if ((s = pull_state(c))) return bail(s);
   if ((s = device_error(c))) return bail(s);
   ip("kernels");
   *out = c;
   return NSS_OK;
+}
+
+NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, const nss_config *cfg,
+                            const nss_dist *dist, nss_ctx **out) {
+  return init_impl(prior, energy, cfg, dist, false, nullptr, out);
 }
 
 NSS_API nss_status nss_step(nss_ctx *c, nss_step_info *info) {
@@ -1052,12 +1263,33 @@ NSS_API nss_status nss_steps(nss_ctx *c, int64_t count) {
   return NSS_OK;
 }
 
+// Sharded live set: every rank's rows (x, E, birth) into every rank's arrays
+// (one NCCL all-gather; collective).
+nss_status shard_gather_live(nss_ctx *c) {
+  if (c->live_gathered) return NSS_OK;
+  if (c->group) return fail(c, NSS_ERR_STATE, "in-process group member: call nss_group_gather_live");
+  LaunchCtx lc = lctx(c);
+  const size_t row = static_cast<size_t>(c->dp) + 2, cap = static_cast<size_t>(c->own_max);
+  launch_shard_pack_live(c->r, c->live_buf + static_cast<size_t>(c->r.rank) * cap * row, lc);
+  std::string err;
+  if (!nccl_allgather_inplace(c->comm, c->live_buf, cap * row * sizeof(float), c->r.rank, c->stream, &err)) {
+    c->poisoned = true;
+    return fail(c, NSS_ERR_COMM, err);
+  }
+  launch_shard_unpack_live(c->r, c->live_buf, static_cast<long long>(cap), lc);
+  CK(cudaGetLastError());
+  c->live_gathered = true;
+  return NSS_OK;
+}
+
 NSS_API nss_status nss_finalise(nss_ctx *c) {
   nss_status s = check_usable(c);
   if (s) return s;
   if (c->host_finalised) return NSS_OK;
+  if (c->sharded && (s = shard_gather_live(c))) return s;
   LaunchCtx lc = lctx(c);
   launch_finalise_sort(c->r, lc);
+  if (c->sharded) launch_shard_mask_rows(c->r, lc);  // dead rows stay with their owner
   launch_evidence(c->r, 1, lc);
   CK(cudaMemcpyAsync(&c->r.st->finalised, c->h_one, sizeof(int), cudaMemcpyHostToDevice, c->stream));
   CK(cudaGetLastError());
@@ -1234,7 +1466,9 @@ NSS_API nss_status nss_destroy(nss_ctx *c) {
   drop_graph(c);
   if (c->lr.Xb) lr_free(c->lr);
   if (c->gp) gp_free(c->gp);
+  for (void *p : c->ipc_open) cudaIpcCloseMemHandle(p);
   if (c->comm) nccl_comm_free(c->comm);
+  for (void *p : c->raw_allocs) cudaFree(p);
 
   // every stream is idle: the blocks go back to the pool in stream order
   for (void *p : c->allocs) cudaFreeAsync(p, c->stream);
@@ -1252,6 +1486,15 @@ NSS_API nss_status nss_destroy(nss_ctx *c) {
   if (c->ev_met) cudaEventDestroy(c->ev_met);
   if (c->side2) cudaStreamDestroy(c->side2);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  if (nss_group *g = c->group) {
+    if (--g->alive == 0) {
+      cudaStreamSynchronize(g->stream);
+      cudaFree(g->gather);
+      cudaFree(g->live);
+      cudaStreamDestroy(g->stream);
+      delete g;
+    }
+  }
   delete c;
   return NSS_OK;
 }
@@ -1274,9 +1517,10 @@ NSS_API nss_status nss_set_live(nss_ctx *c, const float *x, const float *e, int6
   c->h_st->iter = static_cast<int>(next_iteration - 1);
   c->h_st->terminated = 0;
   CK(cudaMemcpyAsync(c->r.st, c->h_st, sizeof(DevState), cudaMemcpyHostToDevice, c->stream));
-  launch_metric(c->r, c->cfg.metric_reg, c->cfg.width_rule, c->cfg.width, 0, c->partials, c->ticket, c->nblk, lctx(c));
+  launch_metric(c->r, c->cfg.metric_reg, c->cfg.width_rule, c->cfg.width, 0, c->partials, c->ticket, c->bps, lctx(c));
   c->metric_pending = false;
   c->term_stale = false;
+  c->live_gathered = true;
   CK(cudaGetLastError());
   if ((s = pull_state(c))) return s;
   return NSS_OK;
@@ -1285,6 +1529,7 @@ NSS_API nss_status nss_set_live(nss_ctx *c, const float *x, const float *e, int6
 NSS_API nss_status nss_get_live(nss_ctx *c, float *x, float *e) {
   nss_status s = check_usable(c);
   if (s) return s;
+  if (c->sharded && !c->group && (s = shard_gather_live(c))) return s;
   const int n = c->r.n, d = c->d, dp = c->dp;
   CK(cudaStreamSynchronize(c->stream));
   if (x) {
@@ -1301,7 +1546,8 @@ NSS_API nss_status nss_get_metric(nss_ctx *c, double *chol, double *width) {
   nss_status s = check_usable(c);
   if (s) return s;
   if (c->metric_pending) {  // the deferred A5 of the last iteration
-    launch_metric(c->r, c->cfg.metric_reg, c->cfg.width_rule, c->cfg.width, 0, c->partials, c->ticket, c->nblk,
+    if (c->sharded && !c->live_gathered) return fail(c, NSS_ERR_STATE, "sharded: metric formed in the next iteration");
+    launch_metric(c->r, c->cfg.metric_reg, c->cfg.width_rule, c->cfg.width, 0, c->partials, c->ticket, c->bps,
                   lctx(c));
     c->metric_pending = false;
   }
@@ -1565,7 +1811,7 @@ NSS_API nss_status nss_smc_init(const nss_prior *prior, const nss_energy *energy
   if (!out || !cfg || !(rho > 0.0 && rho < 1.0)) return NSS_ERR_INVALID_ARG;
   if (energy && energy->kind == NSS_E_GP_ARD) return NSS_ERR_UNSUPPORTED;
   if (cfg->update_all || cfg->mutation != NSS_MUT_HRSS) return NSS_ERR_INVALID_ARG;
-  nss_status s = nss_init(prior, energy, cfg, dist, out);
+  nss_status s = init_impl(prior, energy, cfg, dist, true, nullptr, out);
   if (s) return s;
   nss_ctx *c = *out;
   const int n = c->r.n;
@@ -1617,7 +1863,7 @@ NSS_API nss_status nss_smc_stage(nss_ctx *c) {
   if ((s = ensure_vpre(c))) return s;
   LaunchCtx lc = lctx(c);
   launch_smc_stage(c->r, c->smc_rho, c->smc_cum, c->smc_par, c->smc_xs, c->smc_es, lc);
-  launch_metric(c->r, c->cfg.metric_reg, c->cfg.width_rule, c->cfg.width, 0, c->partials, c->ticket, c->nblk, lc);
+  launch_metric(c->r, c->cfg.metric_reg, c->cfg.width_rule, c->cfg.width, 0, c->partials, c->ticket, c->bps, lc);
   launch_hrss(c->r, c->pr, c->en, lc);
   if ((s = exchange(c))) return s;
   CK(cudaGetLastError());
@@ -1654,5 +1900,105 @@ NSS_API nss_status nss_smc_run(nss_ctx *c, int64_t max_stages, double *log_z) {
 NSS_API nss_status nss_launch_count(nss_ctx *c, int64_t *launches) {
   if (!c || !launches) return NSS_ERR_INVALID_ARG;
   *launches = c->launches;
+  return NSS_OK;
+}
+
+// ---- in-process group: the ranks of one sharded run on one GPU ----
+NSS_API nss_status nss_group_init(const nss_prior *prior, const nss_energy *energy, const nss_config *cfg,
+                                  int32_t world, nss_ctx **out) {
+  if (!out || world < 1 || kSegs % world != 0 || !cfg || !prior) return NSS_ERR_INVALID_ARG;
+  for (int q = 0; q < world; ++q) out[q] = nullptr;
+  if (!validate(prior, energy, cfg)) return NSS_ERR_INVALID_ARG;
+  nss_group *g = new nss_group();
+  g->world = world;
+  const int n = static_cast<int>(cfg->n_live), d = prior->d, dp = (d + 3) & ~3;
+  int own_max = 0;
+  for (int q = 0; q < world; ++q)
+    own_max = std::max(own_max, seg_lo(n, (q + 1) * (kSegs / world)) - seg_lo(n, q * (kSegs / world)));
+  const size_t blk = shard_block_bytes(static_cast<int>(cfg->k), own_max, world, d);
+  const size_t live = static_cast<size_t>(world) * own_max * (dp + 2) * sizeof(float);
+  if (cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMalloc(&g->gather, blk * world) != cudaSuccess || cudaMemset(g->gather, 0, blk * world) != cudaSuccess ||
+      cudaMalloc(&g->live, live) != cudaSuccess) {
+    cudaFree(g->gather);
+    cudaFree(g->live);
+    if (g->stream) cudaStreamDestroy(g->stream);
+    delete g;
+    return NSS_ERR_OOM;
+  }
+  nss_status s = NSS_OK;
+  for (int q = 0; q < world && s == NSS_OK; ++q) {
+    nss_dist dd{q, world, nullptr, g->stream};
+    s = init_impl(prior, energy, cfg, &dd, false, g, &out[q]);
+    if (s == NSS_OK) ++g->alive;
+  }
+  if (s == NSS_OK) {
+    std::vector<float *> tbl(2 * world);
+    for (int q = 0; q < world; ++q) {
+      tbl[q] = out[q]->r.X;
+      tbl[world + q] = out[q]->r.E;
+    }
+    for (int q = 0; q < world && s == NSS_OK; ++q)
+      if (cudaMemcpy(const_cast<float **>(out[q]->r.peerX), tbl.data(), tbl.size() * sizeof(float *),
+                     cudaMemcpyHostToDevice) != cudaSuccess)
+        s = NSS_ERR_CUDA;
+  }
+  if (s != NSS_OK) {
+    const bool none = g->alive == 0;
+    for (int q = 0; q < world; ++q)
+      if (out[q]) {
+        nss_destroy(out[q]);
+        out[q] = nullptr;
+      }
+    if (none) {
+      cudaFree(g->gather);
+      cudaFree(g->live);
+      cudaStreamDestroy(g->stream);
+      delete g;
+    }
+    return s;
+  }
+  return NSS_OK;
+}
+
+static nss_status group_check(nss_ctx **ctx, int32_t world) {
+  if (!ctx || world < 1) return NSS_ERR_INVALID_ARG;
+  for (int q = 0; q < world; ++q) {
+    nss_status s = check_usable(ctx[q]);
+    if (s) return s;
+    if (!ctx[q]->group || ctx[q]->group != ctx[0]->group || ctx[q]->r.rank != q || ctx[q]->group->world != world)
+      return NSS_ERR_INVALID_ARG;
+    if (ctx[q]->host_finalised) return fail(ctx[q], NSS_ERR_STATE, "run already finalised");
+  }
+  return NSS_OK;
+}
+
+NSS_API nss_status nss_group_step(nss_ctx **ctx, int32_t world, int64_t count) {
+  nss_status s = group_check(ctx, world);
+  if (s) return s;
+  for (int64_t i = 0; i < count; ++i) {
+    for (int q = 0; q < world; ++q)
+      if ((s = enqueue_iteration(ctx[q], false, kPre))) return s;
+    for (int q = 0; q < world; ++q)
+      if ((s = enqueue_iteration(ctx[q], false, kPost))) return s;
+  }
+  return NSS_OK;
+}
+
+NSS_API nss_status nss_group_gather_live(nss_ctx **ctx, int32_t world) {
+  nss_status s = group_check(ctx, world);
+  if (s) return s;
+  for (int q = 0; q < world; ++q) {
+    nss_ctx *c = ctx[q];
+    const size_t row = static_cast<size_t>(c->dp) + 2, cap = static_cast<size_t>(c->own_max);
+    launch_shard_pack_live(c->r, c->live_buf + static_cast<size_t>(q) * cap * row, lctx(c));
+  }
+  for (int q = 0; q < world; ++q) {
+    nss_ctx *c = ctx[q];
+    launch_shard_unpack_live(c->r, c->live_buf, static_cast<long long>(c->own_max), lctx(c));
+    c->live_gathered = true;
+    nss_ctx *cc = c;
+    if (cudaGetLastError() != cudaSuccess) return fail(cc, NSS_ERR_CUDA, "group gather");
+  }
   return NSS_OK;
 }

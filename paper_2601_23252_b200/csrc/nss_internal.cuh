@@ -73,7 +73,20 @@ struct RunDev {
   int dir_norm, quadrature;
   int R;
   int engine;                 // nss_hrss_engine (host-side choice)
-  int c0, c1;                 // HRSS chains [c0, c1) run here (all on one GPU)
+  int c0, c1;                 // HRSS chains [c0, c1) run here (all on one GPU);
+                              // with `crange` the grid bound only (c1 - c0 = the most chains this GPU runs)
+  // sharded live set: rank `rank` of `world` owns the gids
+  // [rank_lo[rank], rank_lo[rank + 1]) -- whole segments of kSegs fixed gid
+  // segments -- and runs the chains whose destination it owns, the ordinal
+  // range crange[0..1) of the ascending destination list (written by the
+  // merge kernel).  Start rows of chains whose parent another rank owns are
+  // read from that rank's live set over NVLink through peerX / peerE.
+  int world, rank;
+  int rank_lo[9];
+  const int *crange;          // device [2], or null (host range c0, c1)
+  float *const *peerX;        // device [world] row bases of every rank's X (own included), or null
+  float *const *peerE;
+  double *mshift;             // d: shift of the metric's moment sums (the previous metric's mean, R-8)
   // HRSS chains of the iteration: nch = k (destinations = deleted slots) or n
   // (F4 update-all: every slot); chain c writes slot cdest[c] starting from
   // row cpar[c] of the start arrays Xs/Es (X/E themselves, or a snapshot of
@@ -105,6 +118,35 @@ struct RunDev {
   double *lx_prev, *lx_cur, *lz;
   DevState *st;
 };
+
+constexpr int kSegs = 8;  // fixed gid segments: the metric's summation tree and the shard unit
+
+// Segment s of the n gids: [seg_lo(n, s), seg_lo(n, s + 1)).
+__host__ __device__ __forceinline__ int seg_lo(int n, int s) {
+  return static_cast<int>((static_cast<long long>(s) * n) / kSegs);
+}
+
+// Chains [x, y) this GPU runs.
+__device__ __forceinline__ int2 chain_range(const RunDev &r) {
+  return r.crange ? make_int2(r.crange[0], r.crange[1]) : make_int2(r.c0, r.c1);
+}
+
+// Rank owning gid g (sharded live set).
+__device__ __forceinline__ int owner_of(const RunDev &r, int g) {
+  int o = 0;
+  while (o + 1 < r.world && g >= r.rank_lo[o + 1]) ++o;
+  return o;
+}
+
+// Start row / energy of a chain whose parent (start point) is gid g: the
+// start arrays Xs/Es, or the owner's live set (possibly a peer GPU's memory).
+__device__ __forceinline__ const float *start_row(const RunDev &r, int g) {
+  const float *base = r.peerX ? r.peerX[owner_of(r, g)] : r.Xs;
+  return base + static_cast<long long>(g) * r.dp;
+}
+__device__ __forceinline__ float start_e(const RunDev &r, int g) {
+  return r.peerE ? r.peerE[owner_of(r, g)][g] : r.Es[g];
+}
 
 // ----------------------------------------------------------------------------
 // Philox4x32-10 and the draw contract

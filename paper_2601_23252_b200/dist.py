@@ -1,15 +1,23 @@
 """Multi-GPU plumbing for NSS: one process per GPU.
 
-The library splits an iteration's k HRSS chains into contiguous blocks of
-ceil(k / world) chains per rank and all-gathers the new rows over NCCL
-(csrc/dist.cu); this module only does what happens once per run on the host:
+NS runs shard the live set: rank q owns the gids of 8/world of the 8 fixed gid
+segments (`shard_ranges`), exchanges its top-k candidates and moment sums with
+one NCCL all-gather per iteration and reads parent rows other ranks own over
+NVLink (csrc/k_shard.cu, csrc/dist.cu).  F3 SMC contexts split the particles'
+chains in blocks of ceil(n / world) (`chain_range`) and all-gather the new
+rows.  This module only does what happens once per run on the host:
 broadcasting rank 0's NCCL unique id over an existing torch.distributed group
-and summing per-rank counters.  `chain_range` mirrors the library's partition
-(nss_api.cu, nss_init) for tests and accounting.
+and summing per-rank counters.
 """
 from __future__ import annotations
 
 from typing import Callable, Dict, Optional, Tuple
+
+
+def shard_ranges(n: int, world: int):
+    """gid range [lo, hi) of every rank of a sharded NS run (include/nss.h)."""
+    from .nss import shard_ranges as _sr
+    return _sr(n, world)
 
 
 def chain_range(k: int, rank: int, world: int) -> Tuple[int, int]:
@@ -45,7 +53,8 @@ def nccl_unique_id() -> bytes:
 
 def sharded_sampler(problem, cfg: Dict, stream: Optional[int] = None, group=None):
     """Sampler for this process's rank of the default (or given) process
-    group: the chain block of this rank, an NCCL communicator over all ranks."""
+    group: this rank's shard of the live set, an NCCL communicator over all
+    ranks (collective: every rank calls it)."""
     import torch.distributed as td
     from . import nss
     rank, world = td.get_rank(group), td.get_world_size(group)

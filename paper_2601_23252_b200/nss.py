@@ -74,7 +74,8 @@ EXPORTS = ["nss_get_unique_id", "nss_init", "nss_step", "nss_steps", "nss_run", 
            "nss_dead", "nss_volume_reps", "nss_set_kernel_timing", "nss_kernel_time",
            "nss_launch_count", "nss_set_hrss_engine", "nss_get_hrss_engine",
            "nss_phase_times", "nss_set_overlap", "nss_set_graph",
-           "nss_debug_stamps", "nss_lr_energy_batch", "nss_gp_energy_batch", "nss_set_chain_range", "nss_posterior", "nss_resample", "nss_smc_init", "nss_smc_stage", "nss_smc_state", "nss_smc_run"]
+           "nss_debug_stamps", "nss_lr_energy_batch", "nss_gp_energy_batch", "nss_set_chain_range", "nss_posterior", "nss_resample", "nss_smc_init", "nss_smc_stage", "nss_smc_state", "nss_smc_run",
+           "nss_group_init", "nss_group_step", "nss_group_gather_live"]
 
 _lib = None
 
@@ -131,6 +132,9 @@ def lib():
     L.nss_resample.argtypes = [vp, C.c_double, C.c_int64, C.c_uint64, P(C.c_int64), P(C.c_double)]
     L.nss_gp_energy_batch.argtypes = [P(C.c_double), P(C.c_double), C.c_int64, C.c_int32, C.c_double,
                                       P(C.c_double), C.c_int64, P(C.c_double)]
+    L.nss_group_init.argtypes = [P(nss_prior), P(nss_energy), P(nss_config), C.c_int32, P(vp)]
+    L.nss_group_step.argtypes = [P(vp), C.c_int32, C.c_int64]
+    L.nss_group_gather_live.argtypes = [P(vp), C.c_int32]
     _lib = L
     return L
 
@@ -233,6 +237,17 @@ class Sampler:
         self.d, self.n, self.k = d, self.cfg["n_live"], self.cfg["k"]
         self.p, self.R = self.cfg["steps"], self.cfg["n_volume_sims"]
         self.smc = smc_rho is not None
+
+    @classmethod
+    def _wrap(cls, problem, cfg: Dict, handle: C.c_void_p, rank: int, world: int, keep):
+        """A Sampler around an existing context (nss_group_init members)."""
+        self = cls.__new__(cls)
+        self.problem, self.cfg, self._keep, self._h = problem, dict(cfg), keep, handle
+        self.rank, self.world = rank, world
+        self.d, self.n, self.k = problem.d, self.cfg["n_live"], self.cfg["k"]
+        self.p, self.R = self.cfg["steps"], self.cfg["n_volume_sims"]
+        self.smc = False
+        return self
 
     def _check(self, st: int, where: str):
         if st != 0:
@@ -426,3 +441,80 @@ class Sampler:
         n = C.c_int64()
         self._check(lib().nss_launch_count(self._h, C.byref(n)), "nss_launch_count")
         return n.value
+
+
+def shard_ranges(n: int, world: int):
+    """gid range [lo, hi) of every rank of a sharded run (include/nss.h):
+    rank q owns segments q*8/world .. (q+1)*8/world - 1 of the 8 fixed gid
+    segments [floor(s n / 8), floor((s + 1) n / 8))."""
+    if world < 1 or 8 % world:
+        raise ValueError("world must divide 8")
+    per = 8 // world
+    return [((q * per * n) // 8, ((q + 1) * per * n) // 8) for q in range(world)]
+
+
+class Group:
+    """The `world` ranks of one sharded run emulated in this process on one GPU
+    (nss_group_init): members[q] is rank q (a Sampler)."""
+
+    def __init__(self, problem, cfg: Dict, world: int):
+        keep = []
+
+        def kp(a):
+            a = _f64(a)
+            if a is not None:
+                keep.append(a)
+            return a
+
+        d = problem.d
+        pr = nss_prior(kind=problem.prior_kind, d=d, lo=_dp(kp(problem.lo)), hi=_dp(kp(problem.hi)),
+                       mean=_dp(kp(problem.mean)), sd=_dp(kp(problem.sd)))
+        en = nss_energy(kind=problem.energy_kind, d=d, n_comp=problem.n_comp, n_data=problem.n_data,
+                        d_in=problem.d_in, w=_dp(kp(problem.w)), mu=_dp(kp(problem.mu)),
+                        sigma=_dp(kp(problem.sigma)), prec=_dp(kp(problem.prec)),
+                        data_x=_dp(kp(problem.data_x)), data_y=_dp(kp(problem.data_y)),
+                        c=problem.c, sigma_y=problem.sigma_y, jitter=problem.jitter)
+        cf = nss_config(**cfg)
+        self.world = int(world)
+        self._arr = (C.c_void_p * self.world)()
+        st = lib().nss_group_init(C.byref(pr), C.byref(en), C.byref(cf), self.world, self._arr)
+        if st != 0:
+            raise NssError(st, "nss_group_init")
+        self.members = [Sampler._wrap(problem, cfg, C.c_void_p(self._arr[q]), q, self.world, keep)
+                        for q in range(self.world)]
+        self.ranges = shard_ranges(cfg["n_live"], self.world)
+
+    def steps(self, count: int):
+        st = lib().nss_group_step(self._arr, self.world, int(count))
+        if st != 0:
+            raise NssError(st, "nss_group_step", (lib().nss_last_error(self._arr[0]) or b"").decode())
+
+    def gather_live(self):
+        st = lib().nss_group_gather_live(self._arr, self.world)
+        if st != 0:
+            raise NssError(st, "nss_group_gather_live")
+
+    def owned_live(self):
+        """The live set assembled from every rank's own rows."""
+        parts = [m.get_live() for m in self.members]
+        x = np.zeros_like(parts[0][0])
+        e = np.zeros_like(parts[0][1])
+        for (a, b), (xq, eq) in zip(self.ranges, parts):
+            x[a:b], e[a:b] = xq[a:b], eq[a:b]
+        return x, e
+
+    def dead(self):
+        """Dead store: replicated records, positions summed over the ranks
+        (each rank holds the rows of the points it owned)."""
+        ds = [m.dead() for m in self.members]
+        out = dict(ds[0])
+        out["x"] = np.sum([q["x"].astype(np.float64) for q in ds], axis=0).astype(np.float32)
+        for q in ds[1:]:
+            for key in ("e", "n_live", "gid", "birth"):
+                if not np.array_equal(q[key], ds[0][key]):
+                    raise AssertionError(f"dead store field {key} differs between ranks")
+        return out
+
+    def close(self):
+        for m in self.members:
+            m.close()

@@ -90,23 +90,74 @@ def test_job_totals_gloo():
         assert out[r]["iteration"] == 5
 
 
+def _merge_candidates(cands, n, k, seed, it):
+    """Host mirror of k_shard_merge (csrc/k_shard.cu): the k largest keys
+    (E, gid) of the gathered candidates, destinations ascending, E*, and the
+    parents -- survivor j = j + (first index i with D[i] - i > j)."""
+    from oracle import nsso
+    allc = sorted((c for part in cands for c in part), key=lambda t: (t[0], t[1]), reverse=True)
+    sel = allc[:k]
+    dead_order = [g for _, g in sel]
+    dest = sorted(dead_order)
+    e_star = sel[-1][0]
+    parents = []
+    for s in dest:
+        u = nsso.draw_u32(seed, it, s, 2, 0, 0)  # RESAMPLE stream, draw 0
+        j = (u * (n - k)) >> 32
+        i = next((i for i, dg in enumerate(dest) if dg - i > j), k)
+        parents.append(j + i)
+    return dead_order, dest, parents, e_star
+
+
 def _oracle_shard_worker(rank, world, name, kw, iters):
+    """The sharded decomposition with the fp64 oracle:
+    rank q owns shard_ranges(n, world)[q]; candidates = its local top-min(k,
+    n_q) keys, all-gathered and merged; it runs the chains whose destination it
+    owns (an ordinal range of D) and the owned new rows are all-gathered.  Must
+    reproduce the one-process oracle bit for bit."""
     import torch.distributed as td
     from oracle import nsso
     prob = _PROBLEMS[name]()
     cfg = W.config(seed=21, **kw)
-    k = cfg["k"]
+    n, k = cfg["n_live"], cfg["k"]
+    a, b = D.shard_ranges(n, world)[rank]
     full = nsso.Oracle(prob, cfg)     # the one-process reference
-    mine = nsso.Oracle(prob, cfg)     # this rank: only its chain block
-    c0, c1 = D.chain_range(k, rank, world)
+    mine = nsso.Oracle(prob, cfg)     # this rank (replicated state, owned chains only)
     for it in range(1, iters + 1):
-        full.step()
-        mine.set_chain_subset(list(range(c0, c1)))
-        mine.step()
-        tr = mine.trace()
         x, e = mine.get_live()
-        dest = tr["dest_gid"]
-        rows = [(int(dest[c]), x[dest[c]].copy(), float(e[dest[c]])) for c in range(c0, c1)]
+        keys = sorted(((float(e[g]), g) for g in range(a, b)), reverse=True)[: min(k, b - a)]
+        cands = [None] * world
+        td.all_gather_object(cands, sorted(keys, key=lambda t: t[1]))
+        dead_order, dest, parents, e_star = _merge_candidates(cands, n, k, cfg["seed"], it)
+        # segment moment sums of the owned rows, folded in segment order (k_metric.cu)
+        shift = x.mean(axis=0)
+        segs = []
+        for s in range(8):
+            lo, hi = (s * n) // 8, ((s + 1) * n) // 8
+            if a <= lo and hi <= b:
+                y = x[lo:hi] - shift
+                segs.append((s, y.sum(axis=0), y.T @ y))
+        allsegs = [None] * world
+        td.all_gather_object(allsegs, segs)
+        segs_all = sorted(sum(allsegs, []), key=lambda t: t[0])
+        assert [t[0] for t in segs_all] == list(range(8))
+        S1 = sum(t[1] for t in segs_all)
+        S2 = sum(t[2] for t in segs_all)
+        cov = (S2 - np.outer(S1, S1) / n) / (n - 1)
+        if not np.allclose(cov, np.cov(x.T), rtol=1e-10, atol=1e-12):
+            return f"iteration {it}: segment moments differ"
+        lo_c = next((i for i, g in enumerate(dest) if g >= a), k)
+        hi_c = next((i for i, g in enumerate(dest) if g >= b), k)
+        mine.set_chain_subset(list(range(lo_c, hi_c)))
+        mine.step()
+        full.step()
+        tr, tf = mine.trace(), full.trace()
+        if list(tf["dead_gid"]) != dead_order or list(tf["dest_gid"]) != dest:
+            return f"iteration {it}: merged candidates differ from the oracle's select"
+        if list(tf["parent_gid"]) != parents or e_star != tf["e_star"]:
+            return f"iteration {it}: parents / E* differ"
+        x, e = mine.get_live()
+        rows = [(int(g), x[g].copy(), float(e[g])) for g in dest[lo_c:hi_c]]
         allrows = [None] * world
         td.all_gather_object(allrows, rows)
         for part in allrows:
@@ -114,15 +165,24 @@ def _oracle_shard_worker(rank, world, name, kw, iters):
                 x[g], e[g] = xg, eg
         mine.set_live(x, e, it + 1)
         xf, ef = full.get_live()
-        tf = full.trace()
-        for key in ("dead_gid", "dest_gid", "parent_gid"):
-            if not np.array_equal(tr[key], tf[key]):
-                return f"iteration {it}: {key} differs"
         if not (np.array_equal(x, xf) and np.array_equal(e, ef)):
             return f"iteration {it}: live set differs"
-        if not np.array_equal(tr["counts"][c0:c1], tf["counts"][c0:c1]):
+        if not np.array_equal(tr["counts"][lo_c:hi_c], tf["counts"][lo_c:hi_c]):
             return f"iteration {it}: counts differ"
     return "ok"
+
+
+def test_shard_ranges_partition():
+    for n in (2, 7, 200, 777, 2000, 20_000):
+        for world in (1, 2, 4, 8):
+            rs = D.shard_ranges(n, world)
+            assert rs[0][0] == 0 and rs[-1][1] == n
+            assert all(rs[q][1] == rs[q + 1][0] for q in range(world - 1))
+            # whole segments: the union of rank q's 8/world segments
+            per = 8 // world
+            assert rs[1 % world][0] == (per * n) // 8 or world == 1
+    with pytest.raises(ValueError):
+        D.shard_ranges(100, 3)
 
 
 _PROBLEMS = {
@@ -136,5 +196,6 @@ _PROBLEMS = {
                                      ("corr", dict(n_live=90, k=30, steps=3)),
                                      ("logreg", dict(n_live=64, k=5, steps=2))])
 def test_sharded_oracle_matches_one_process(name, kw):
-    out = _run(_oracle_shard_worker, 2, name, kw, 3)
-    assert out[0] == "ok" and out[1] == "ok", out
+    for world in (2, 4):
+        out = _run(_oracle_shard_worker, world, name, kw, 3)
+        assert all(out[r] == "ok" for r in range(world)), out

@@ -1,9 +1,18 @@
-"""The multi-GPU path on one B200: (1) a world-1 NCCL
-communicator runs the pack / all-gather / scatter exchange every iteration
-and must leave the run bit-identical to a plain one-GPU run; (2) two contexts
-restricted to the two chain blocks of a world-2 run (no communicator, run one
-after the other, the host doing the exchange) reproduce the full run bit for
-bit on every engine."""
+"""The sharded multi-GPU path (include/nss.h) on B200s.
+
+(1) The `world` ranks of one sharded run emulated in one process on one GPU
+    (nss_group_*: same partition, kernels and decisions as the NCCL path; the
+    members share a stream and the exchange buffer, and read each other's
+    parent rows through their peer tables) reproduce the plain one-GPU run BIT
+    FOR BIT -- live set, dead store, evidence replicas, counters, finalised
+    evidence -- for world = 1, 2, 4, 8 on every engine.
+(2) A world-1 NCCL communicator runs the NCCL path (in-place all-gather,
+    CUDA-IPC peer table, graph capture) every iteration: bit-identical too.
+(3) With two GPUs visible, two processes (NCCL over NVLink) do the same.
+"""
+import os
+import socket
+
 import numpy as np
 import pytest
 
@@ -21,97 +30,154 @@ def _cuda():
 
 
 CASES = {
-    "lane_mog10": (lambda: W.mog(10), dict(n_live=2000, k=200, steps=10), "auto"),
-    "warp_corr": (lambda: W.corr_gauss(40, seed=5), dict(n_live=600, k=61, steps=4), "warp"),
-    "batch_logreg": (lambda: W.logreg(5, n_data=300, seed=3), dict(n_live=300, k=31, steps=3), "batch"),
-    "batch_gp": (lambda: W.gp_ard(2, 40, seed=3), dict(n_live=64, k=17, steps=2), "batch"),
+    "lane_mog10": (lambda: W.mog(10), dict(n_live=2000, k=200, steps=10), 12),
+    "lane_ragged": (lambda: W.mog(6, n_comp=3, seed=17, half_width=8.0, mean_box=4.0, min_sep=4.0),
+                    dict(n_live=777, k=91, steps=5), 10),
+    "warp_corr40": (lambda: W.corr_gauss(40, seed=5), dict(n_live=600, k=61, steps=4), 6),
+    "warp_funnel100": (lambda: W.funnel(100), dict(n_live=1000, k=100, steps=6), 4),
+    "half_k": (lambda: W.gauss(3), dict(n_live=64, k=32, steps=3), 8),
+    "batch_logreg": (lambda: W.logreg(5, n_data=300, seed=3), dict(n_live=300, k=31, steps=3), 5),
+    "batch_gp": (lambda: W.gp_ard(2, 40, seed=3), dict(n_live=64, k=17, steps=2), 3),
 }
 
 
-def _state(s):
-    x, e = s.get_live()
-    return x.copy(), e.copy()
+def _compare(single, x, e, dead, reps, probes, evals):
+    xs, es = single.get_live()
+    assert np.array_equal(xs, x) and np.array_equal(es, e), "live set differs"
+    ds = single.dead()
+    for key in ("e", "n_live", "gid", "birth", "x"):
+        assert np.array_equal(ds[key], dead[key]), f"dead store field {key} differs"
+    assert np.array_equal(single.evidence_reps(), reps), "evidence replicas differ"
+    info = single.info()
+    assert info["probes"] == probes and info["energy_evals"] == evals
 
 
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
 @pytest.mark.parametrize("name", sorted(CASES))
+def test_group_is_bit_identical_to_one_gpu(name, world):
+    from paper_2601_23252_b200 import nss
+    make, kw, iters = CASES[name]
+    prob, cfg = make(), W.config(seed=5, **kw)
+    single = nss.Sampler(prob, cfg)
+    g = nss.Group(prob, cfg, world)
+    assert [m.engine() for m in g.members] == [single.engine()] * world
+    single.steps(iters)
+    g.steps(iters)
+    x, e = g.owned_live()
+    infos = [m.info() for m in g.members]
+    reps = g.members[0].evidence_reps()
+    for m in g.members[1:]:
+        assert np.array_equal(m.evidence_reps(), reps)
+    _compare(single, x, e, g.dead(), reps, sum(i["probes"] for i in infos), sum(i["energy_evals"] for i in infos))
+    assert all(i["iteration"] == iters for i in infos)
+    # the chains were split over the ranks
+    if world > 1 and kw["k"] >= 16:
+        assert sum(i["probes"] > 0 for i in infos) > 1
+    # gather, finalise on every member: the same evidence as one GPU
+    g.gather_live()
+    xg, eg = g.members[world - 1].get_live()
+    assert np.array_equal(xg, x) and np.array_equal(eg, e)
+    single.finalise()
+    for m in g.members:
+        m.finalise()
+    assert np.array_equal(g.dead()["x"], single.dead()["x"])
+    for m in g.members:
+        assert m.evidence() == single.evidence()
+    g.close()
+    single.close()
+
+
+def test_group_runs_to_termination_like_one_gpu():
+    """C1 to its termination rule: same iteration count, same log Z."""
+    from paper_2601_23252_b200 import nss
+    prob, cfg = W.gauss(2), W.config(seed=3, n_live=200, k=20, steps=10)
+    single = nss.Sampler(prob, cfg)
+    info = single.run()
+    g = nss.Group(prob, cfg, 4)
+    for _ in range(400):
+        g.steps(1)
+        if g.members[0].info()["terminated"]:
+            break
+    assert g.members[0].info()["iteration"] == info["iteration"]
+    g.gather_live()
+    for m in g.members:
+        m.finalise()
+        assert m.evidence() == single.evidence()
+
+
+@pytest.mark.parametrize("name", ["lane_mog10", "warp_corr40", "batch_logreg", "batch_gp"])
 def test_world1_nccl_path_is_identity(name):
     from paper_2601_23252_b200 import nss
-    make, kw, engine = CASES[name]
+    make, kw, iters = CASES[name]
     prob, cfg = make(), W.config(seed=5, **kw)
     a = nss.Sampler(prob, cfg)
     b = nss.Sampler(prob, cfg, dist=(0, 1, D.nccl_unique_id()))
-    for s in (a, b):
-        s.set_engine(engine)
-        s.steps(3)
-        s.sync()
-    xa, ea = _state(a)
-    xb, eb = _state(b)
-    assert np.array_equal(xa, xb) and np.array_equal(ea, eb)
-    assert np.array_equal(a.trace()["counts"], b.trace()["counts"])
-    assert a.info()["energy_evals"] == b.info()["energy_evals"]
+    a.steps(iters)
+    b.steps(iters)
+    xb, eb = b.get_live()  # collective gather (trivial at world 1)
+    _compare(a, xb, eb, b.dead(), b.evidence_reps(), b.info()["probes"], b.info()["energy_evals"])
+    b.finalise()
+    a.finalise()
+    assert b.evidence() == a.evidence()
 
 
-@pytest.mark.parametrize("name", sorted(CASES))
-def test_two_chain_blocks_reproduce_full_iteration(name):
-    from paper_2601_23252_b200 import nss
-    make, kw, engine = CASES[name]
-    prob, cfg = make(), W.config(seed=9, **kw)
-    full = nss.Sampler(prob, cfg)
-    ranks = [nss.Sampler(prob, cfg) for _ in range(2)]
-    for r, s in enumerate(ranks):
-        s.set_chain_range(*D.chain_range(cfg["k"], r, 2))
-    for s in [full, *ranks]:
-        s.set_engine(engine)
-    evals = 0
-    for it in range(1, 4):
-        full.step()
-        parts = []
-        for r, s in enumerate(ranks):
-            s.step()
-            x, e = _state(s)
-            dest = s.trace()["dest_gid"]
-            c0, c1 = D.chain_range(cfg["k"], r, 2)
-            parts.append([(int(dest[c]), x[dest[c]], e[dest[c]]) for c in range(c0, c1)])
-        # host all-gather: both ranks apply every rank's rows
-        for s in ranks:
-            x, e = _state(s)
-            for part in parts:
-                for g, xg, eg in part:
-                    x[g], e[g] = xg, eg
-            s.set_live(x, e, it + 1)
-        xf, ef = _state(full)
-        for s in ranks:
-            x, e = _state(s)
-            assert np.array_equal(x, xf) and np.array_equal(e, ef), f"iteration {it}"
-    evals = sum(s.info()["energy_evals"] for s in ranks)
-    assert evals == full.info()["energy_evals"]
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
 
 
-def test_sharded_sampler_through_torch_distributed_world1():
-    """The torch.distributed plumbing of dist.py on the GPU box: an NCCL process
-    group of one rank, rank 0's NCCL id broadcast, a sharded sampler whose run
-    equals the plain one."""
-    import socket
-
+def _two_gpu_worker(rank, world, port, q):
     import torch
     import torch.distributed as td
-    from paper_2601_23252_b200 import nss
-    sock = socket.socket()
-    sock.bind(("127.0.0.1", 0))
-    port = sock.getsockname()[1]
-    sock.close()
-    td.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
-                          device_id=torch.device("cuda", 0))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    td.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
     try:
-        prob, cfg = W.gauss(3), W.config(n_live=300, k=30, steps=4, seed=8)
-        a = D.sharded_sampler(prob, cfg)
-        b = nss.Sampler(prob, cfg)
-        for s in (a, b):
-            s.steps(5)
-        xa, ea = a.get_live()
-        xb, eb = b.get_live()
-        assert np.array_equal(xa, xb) and np.array_equal(ea, eb)
-        tot = D.job_totals(a.info())
-        assert tot["energy_evals"] == b.info()["energy_evals"]
+        from paper_2601_23252_b200 import nss
+        make, kw, iters = CASES["lane_mog10"]
+        prob, cfg = make(), W.config(seed=5, **kw)
+        s = D.sharded_sampler(prob, cfg)
+        s.steps(iters)
+        x, e = s.get_live()
+        dead = s.dead()
+        info = D.job_totals(s.info())
+        q.put((rank, (x, e, dead["x"], s.evidence_reps(), info["probes"])))
+        s.close()
+    except BaseException as ex:
+        q.put((rank, ex))
     finally:
         td.destroy_process_group()
+
+
+def test_two_processes_nccl_bit_identical():
+    """Two ranks on two GPUs (skipped when fewer are visible)."""
+    import torch
+    import torch.multiprocessing as mp
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    from paper_2601_23252_b200 import nss
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_two_gpu_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=600) for _ in range(2))
+    for p in procs:
+        p.join(timeout=120)
+    for r in (0, 1):
+        if isinstance(out[r], BaseException):
+            raise out[r]
+    make, kw, iters = CASES["lane_mog10"]
+    single = nss.Sampler(make(), W.config(seed=5, **kw))
+    single.steps(iters)
+    xs, es = single.get_live()
+    x0, e0, dx0, reps0, probes = out[0]
+    x1, _, dx1, reps1, _ = out[1]
+    assert np.array_equal(x0, xs) and np.array_equal(x1, xs) and np.array_equal(e0, es)
+    assert np.array_equal(dx0 + dx1, single.dead()["x"])
+    assert np.array_equal(reps0, single.evidence_reps()) and np.array_equal(reps1, reps0)
+    assert probes == single.info()["probes"]
