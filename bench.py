@@ -365,7 +365,8 @@ def main():
     from paper_2601_23252_b200 import nss
 
     mode = args.mode if args.mode != "auto" else ("shard" if args.config in SHARDED else "replicas")
-    shard = world > 1 and mode == "shard"
+    # shard at N = 1 only when asked: the NCCL world-1 sharded path (its overhead on one GPU)
+    shard = mode == "shard" and (world > 1 or args.mode == "shard")
     prob, cfg = W.workload(args.config)
     T = REP_ITERS.get(args.config, 50)
     sched = schedule(T, args.steps)
@@ -377,6 +378,8 @@ def main():
     def new_run(seed):
         c = dict(cfg)
         c["seed"] = seed if shard else seed + 1000 * rank
+        if shard and world == 1:  # the world-1 NCCL sharded path
+            return nss.Sampler(prob, c, stream=stream.cuda_stream, dist=(0, 1, D.nccl_unique_id()))
         if shard:
             return D.sharded_sampler(prob, c, stream=stream.cuda_stream)
         return nss.Sampler(prob, c, stream=stream.cuda_stream)

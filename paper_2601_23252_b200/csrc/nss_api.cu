@@ -13,9 +13,18 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "batch.cuh"
 #include "lr_engine.cuh"
 #include "nss_internal.cuh"
+
+// NVTX ranges around the host calls and per-iteration enqueues (SURVEY
+// section 5 tracing); header-only, inert unless a profiler attaches.
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 #define NSS_API extern "C" __attribute__((visibility("default")))
 
@@ -743,6 +752,7 @@ nss_status ensure_vpre(nss_ctx *c) {
 }
 
 nss_status enqueue_iteration(nss_ctx *c, bool with_probe = false, Stage stage = kAll) {
+  NvtxRange nvtx_(stage == kPre ? "iteration (pre)" : stage == kPost ? "iteration (post)" : "iteration");
   nss_status vs = ensure_vpre(c);
   if (vs) return vs;
   // group stages: kPre records the with-metric flag, kPost reuses it
@@ -1238,10 +1248,12 @@ static nss_status init_impl(const nss_prior *prior, const nss_energy *energy, co
 
 NSS_API nss_status nss_init(const nss_prior *prior, const nss_energy *energy, const nss_config *cfg,
                             const nss_dist *dist, nss_ctx **out) {
+  NvtxRange nvtx_("nss_init");
   return init_impl(prior, energy, cfg, dist, false, nullptr, out);
 }
 
 NSS_API nss_status nss_step(nss_ctx *c, nss_step_info *info) {
+  NvtxRange nvtx_("nss_step");
   nss_status s = check_usable(c);
   if (s) return s;
   if (c->host_finalised) return fail(c, NSS_ERR_STATE, "run already finalised");
@@ -1255,6 +1267,7 @@ NSS_API nss_status nss_step(nss_ctx *c, nss_step_info *info) {
 }
 
 NSS_API nss_status nss_steps(nss_ctx *c, int64_t count) {
+  NvtxRange nvtx_("nss_steps");
   nss_status s = check_usable(c);
   if (s) return s;
   if (c->host_finalised) return fail(c, NSS_ERR_STATE, "run already finalised");
@@ -1283,6 +1296,7 @@ nss_status shard_gather_live(nss_ctx *c) {
 }
 
 NSS_API nss_status nss_finalise(nss_ctx *c) {
+  NvtxRange nvtx_("nss_finalise");
   nss_status s = check_usable(c);
   if (s) return s;
   if (c->host_finalised) return NSS_OK;
@@ -1300,6 +1314,7 @@ NSS_API nss_status nss_finalise(nss_ctx *c) {
 }
 
 NSS_API nss_status nss_run(nss_ctx *c, int64_t max_iters, nss_step_info *info) {
+  NvtxRange nvtx_("nss_run");
   nss_status s = check_usable(c);
   if (s) return s;
   if (c->host_finalised) return fail(c, NSS_ERR_STATE, "run already finalised");
@@ -1326,6 +1341,7 @@ NSS_API nss_status nss_run(nss_ctx *c, int64_t max_iters, nss_step_info *info) {
 }
 
 NSS_API nss_status nss_evidence_reps(nss_ctx *c, double *reps) {
+  NvtxRange nvtx_("nss_evidence_reps");
   nss_status s = check_usable(c);
   if (s) return s;
   if ((s = pull_state(c))) return s;
@@ -1349,6 +1365,7 @@ NSS_API nss_status nss_evidence(nss_ctx *c, double *log_z, double *log_z_err) {
 }
 
 NSS_API nss_status nss_samples(nss_ctx *c, double *x, double *log_w, int64_t cap, int64_t *n_out) {
+  NvtxRange nvtx_("nss_samples");
   nss_status s = check_usable(c);
   if (s) return s;
   if (!n_out) return NSS_ERR_INVALID_ARG;
@@ -1434,6 +1451,7 @@ static nss_status posterior_impl(nss_ctx *c, double beta, double *log_z, double 
 
 NSS_API nss_status nss_posterior(nss_ctx *c, double beta, double *log_z, double *log_z_err, double *ess,
                                  double *log_w, int64_t cap) {
+  NvtxRange nvtx_("nss_posterior");
   return posterior_impl(c, beta, log_z, log_z_err, ess, log_w, cap, 0, 0, nullptr, nullptr);
 }
 
@@ -1857,6 +1875,7 @@ NSS_API nss_status nss_smc_init(const nss_prior *prior, const nss_energy *energy
 }
 
 NSS_API nss_status nss_smc_stage(nss_ctx *c) {
+  NvtxRange nvtx_("nss_smc_stage");
   nss_status s = check_usable(c);
   if (s) return s;
   if (!c->smc) return fail(c, NSS_ERR_STATE, "not an SMC context");
@@ -1906,6 +1925,7 @@ NSS_API nss_status nss_launch_count(nss_ctx *c, int64_t *launches) {
 // ---- in-process group: the ranks of one sharded run on one GPU ----
 NSS_API nss_status nss_group_init(const nss_prior *prior, const nss_energy *energy, const nss_config *cfg,
                                   int32_t world, nss_ctx **out) {
+  NvtxRange nvtx_("nss_group_init");
   if (!out || world < 1 || kSegs % world != 0 || !cfg || !prior) return NSS_ERR_INVALID_ARG;
   for (int q = 0; q < world; ++q) out[q] = nullptr;
   if (!validate(prior, energy, cfg)) return NSS_ERR_INVALID_ARG;
@@ -1974,6 +1994,7 @@ static nss_status group_check(nss_ctx **ctx, int32_t world) {
 }
 
 NSS_API nss_status nss_group_step(nss_ctx **ctx, int32_t world, int64_t count) {
+  NvtxRange nvtx_("nss_group_step");
   nss_status s = group_check(ctx, world);
   if (s) return s;
   for (int64_t i = 0; i < count; ++i) {
@@ -1986,6 +2007,7 @@ NSS_API nss_status nss_group_step(nss_ctx **ctx, int32_t world, int64_t count) {
 }
 
 NSS_API nss_status nss_group_gather_live(nss_ctx **ctx, int32_t world) {
+  NvtxRange nvtx_("nss_group_gather_live");
   nss_status s = group_check(ctx, world);
   if (s) return s;
   for (int q = 0; q < world; ++q) {
