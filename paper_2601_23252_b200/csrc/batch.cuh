@@ -4,7 +4,7 @@
 // probe buffer, and one batched energy kernel evaluates all probes at once
 // (tensor cores for logistic regression, batched Cholesky for GP).
 #pragma once
-#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include "nss_internal.cuh"
 
@@ -24,8 +24,9 @@ struct BatchDev {
   int *n_probe;               // [2] rows issued in the round of that parity
   float *partial[2];          // [slices][p_stride] energy partial sums per row
   int *slices;                // [2] slices written by the energy pass of each parity
-  __nv_bfloat16 *A[2];        // logistic regression: [3][p_stride][128] bf16 splits, else null
+  __half *A[2];               // logistic regression: [2][p_stride][128] fp16 splits hi / lo, else null
   float *lin[2];              // logistic regression: per-row linear part theta~ . g, else null
+  double *eacc[2];            // logistic regression: per-row exact fp64 softplus sums (energy pass), else null
   const float *g;             // logistic regression: g = X^T (1/2 - y) (128 floats), else null
 };
 

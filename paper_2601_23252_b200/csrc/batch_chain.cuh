@@ -46,6 +46,8 @@ __device__ __forceinline__ void store_chain(const BatchDev &b, int c, const Chai
 // lanes in parallel and summed by a fixed shuffle tree (deterministic); every
 // lane returns the total
 __device__ __forceinline__ float probe_energy(const BatchDev &b, int parity, int row, int lane) {
+  if (b.eacc[parity])  // logistic regression: exact softplus sum + theta~ . g, one rounding
+    return static_cast<float>(b.eacc[parity][row] + static_cast<double>(b.lin[parity][row]));
   const int ns = b.slices[parity];
   double acc = 0.0;
   for (int q = lane; q < ns; q += 32) acc += b.partial[parity][static_cast<long long>(q) * b.p_stride + row];
@@ -56,33 +58,34 @@ __device__ __forceinline__ float probe_energy(const BatchDev &b, int parity, int
 template <int NPL>
 __device__ __forceinline__ void emit_probe(const BatchDev &b, int parity, int row, const float (&xp)[NPL], int d,
                                            int lane) {
-  float *dst = b.P[parity] + static_cast<long long>(row) * b.dp;
-#pragma unroll
-  for (int t = 0; t < NPL; ++t) {
-    const int i = lane + 32 * t;
-    if (i < d) dst[i] = xp[t];
-  }
   if (b.A[parity]) {
-    // bf16x3 split for the tensor-core logistic-regression energy (K padded to
-    // 128), and the row's linear term theta~ . g (theta~ = hi + mid, the terms
-    // the tensor cores contract)
-    __nv_bfloat16 *A = b.A[parity];
+    // tensor-core logistic regression: only the fp16 hi / lo terms (K padded
+    // to 128) and the row's linear term theta~ . g (theta~ = hi + lo, the
+    // terms the tensor cores contract, R-28); no fp32 row
+    __half *A = b.A[parity];
     float lin = 0.f;
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       const int kk = lane + 32 * t;
       const float v = (t < NPL && kk < d) ? xp[t < NPL ? t : 0] : 0.f;
-      const __nv_bfloat16 hi = __float2bfloat16_rn(v);
-      const float r1 = v - __bfloat162float(hi);
-      const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
-      const __nv_bfloat16 lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
+      const __half hi = __float2half_rn(v);
+      const __half lo = __float2half_rn(v - __half2float(hi));
       A[static_cast<long long>(row) * 128 + kk] = hi;
-      A[(static_cast<long long>(b.p_stride) + row) * 128 + kk] = mid;
-      A[(2ll * b.p_stride + row) * 128 + kk] = lo;
-      lin = fmaf(__bfloat162float(hi) + __bfloat162float(mid), __ldg(b.g + kk), lin);
+      A[(static_cast<long long>(b.p_stride) + row) * 128 + kk] = lo;
+      lin = fmaf(__half2float(hi) + __half2float(lo), __ldg(b.g + kk), lin);
     }
     lin = warp_sum(lin);
-    if (lane == 0) b.lin[parity][row] = lin;
+    if (lane == 0) {
+      b.lin[parity][row] = lin;
+      b.eacc[parity][row] = 0.0;  // the energy pass adds the softplus sums
+    }
+    return;
+  }
+  float *dst = b.P[parity] + static_cast<long long>(row) * b.dp;
+#pragma unroll
+  for (int t = 0; t < NPL; ++t) {
+    const int i = lane + 32 * t;
+    if (i < d) dst[i] = xp[t];
   }
 }
 
@@ -112,12 +115,18 @@ __device__ __forceinline__ void advance_chain(const RunDev &r, const PriorDev &p
 
   float pa[NPL], pb[NPL], x[NPL], v[NPL], xp[NPL];
   load_prior_lane<NPL>(pr, lane, d, pa, pb);
+  // the direction of the current step: from the precomputed directions when
+  // there are any (then never stored back), else the chain's saved copy
+  const float *vsrc = (r.Vpre && s.phase != kPhDir)
+                          ? r.Vpre + (static_cast<long long>(c - chain_range(r).x) * p + s.step) * r.dp
+                          : b.v + static_cast<long long>(c) * b.dp;
 #pragma unroll
   for (int t = 0; t < NPL; ++t) {
     const int i = lane + 32 * t;
     x[t] = i < d ? b.x[static_cast<long long>(c) * b.dp + i] : 0.f;
-    v[t] = i < d ? b.v[static_cast<long long>(c) * b.dp + i] : 0.f;
+    v[t] = i < d ? vsrc[i] : 0.f;
   }
+  bool x_dirty = false;
   // results of the probes this chain issued last round
   float E0 = 0.f, E1 = 0.f;
   if (s.row0 >= 0) E0 = probe_energy(b, prev, s.row0, lane);
@@ -280,6 +289,7 @@ __device__ __forceinline__ void advance_chain(const RunDev &r, const PriorDev &p
       if (E0 < e_star) {
 #pragma unroll
         for (int q = 0; q < NPL; ++q) x[q] = fmaf(s.t0, v[q], x[q]);
+        x_dirty = true;
         s.e = E0;
         s.lp = s.lp0;
         end_step(1);
@@ -312,12 +322,14 @@ __device__ __forceinline__ void advance_chain(const RunDev &r, const PriorDev &p
     end_step(0);  // shrink cap reached: null move
   }
 
+  // write back only what changed: x after an accepted step, v when it is not
+  // re-read from the precomputed directions
 #pragma unroll
   for (int t = 0; t < NPL; ++t) {
     const int i = lane + 32 * t;
     if (i < d) {
-      b.x[static_cast<long long>(c) * b.dp + i] = x[t];
-      b.v[static_cast<long long>(c) * b.dp + i] = v[t];
+      if (x_dirty) b.x[static_cast<long long>(c) * b.dp + i] = x[t];
+      if (!r.Vpre) b.v[static_cast<long long>(c) * b.dp + i] = v[t];
     }
   }
   if (lane == 0) {

@@ -424,6 +424,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_gp_chains(RunDev r, PriorDev pr
   bl.max_rows = 2;
   bl.A[0] = bl.A[1] = nullptr;
   bl.lin[0] = bl.lin[1] = nullptr;
+  bl.eacc[0] = bl.eacc[1] = nullptr;
   volatile int *cnt = bl.n_probe;
   unsigned long long t_start = 0, n_mat = 0, n_ch = 0;
   if (q.prof && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));

@@ -4,25 +4,31 @@
 //   E(theta_p) = sum_{r < N} softplus(a_pr) - y_r a_pr,   a = X theta_p
 //
 // The logits are a dense contraction [P x d] . [d x N], so they run on the
-// tensor cores.  X is stored bf16-exact and each probe is
-// split into bf16 terms theta = hi + mid (16 significant bits; the logit error
-// is ~1e-5 relative per row and ~1e-6 relative on E), whose
-// products accumulate in fp32 in TMEM.  Orientation: M = probes (one TMEM lane
-// = one probe), N = data rows, K = d (padded to 112 = 7 UMMA k-steps of 16).
+// tensor cores in fp16 with fp32 accumulation in TMEM (R-28): each probe is
+// split into fp16 terms theta = hi + lo (22 significant bits, relative error
+// <= 2^-23 like an fp32 round, fp16 range), and X is either fp16-exact (one
+// term: 2 MMAs per k-step, XS = 1) or split the same way, X = Xhi + Xlo
+// (XS = 2: Xhi.hi + Xhi.lo + Xlo.hi, 3 MMAs; the dropped Xlo.lo is below
+// 2^-22).  Orientation: M = probes (one TMEM lane = one probe), N = data
+// rows, K = d (padded to 16 ksteps, <= 128).
 //
-// Persistent, balanced schedule: the grid is one CTA per SM.  The work of a
-// round -- ceil(P/128) probe tiles x T data tiles -- is cut into S slices per
-// probe tile (S chosen so there are ~8 units per SM) and the units are dealt
-// to the CTAs in contiguous ranges, so every SM gets the same number of tile
-// pairs (+-1 unit) whatever P is.  A CTA keeps its probe tile (2 splits x 2
-// swizzle atoms, 64 KB) in shared memory and reloads it only when its next
-// unit belongs to another probe tile; data tiles stream through a 4-stage TMA
-// ring; the MMA warp accumulates each tile into one of four TMEM buffers while
-// sixteen epilogue warps drain the previous one.  Each epilogue thread owns one
-// probe row: it accumulates |a| and the product of (1 + e^-|a|) (the linear part theta . g is added per row by the consumer)
-// (one ex2 per element, one lg2 per 32), with no cross-lane reduction.  Unit
-// sums go to partial[slice][probe] and are summed in slice order by the
-// consumer, so energies are deterministic for a given P.
+// Persistent, balanced schedule: the grid is one CTA per SM and the work of
+// a round -- ceil(P/128) probe tiles x T data tiles = TP tile pairs, in
+// (probe tile, data tile) order -- is cut into G contiguous ranges of
+// floor/ceil(TP/G) pairs, so every SM gets the same number of tile pairs
+// (+-1).  A CTA keeps its probe tile (2 splits x 2 swizzle atoms, 64 KB) in
+// shared memory and reloads it when its range enters the next probe tile
+// (at most a few times); data tiles stream through a TMA ring; the MMA warp
+// accumulates each tile into one of the TMEM buffers while sixteen epilogue
+// warps drain the previous one.  Each epilogue thread owns one probe row and a
+// quarter of the columns: it accumulates |a| and the product of (1 + e^-|a|)
+// (one ex2 per element, one lg2 per 32) into an fp32 value per tile, sums the
+// tiles of its range in fp64 and adds that to the row's fp64 accumulator
+// (which the consumer seeded with the row's linear term theta . g) with one
+// atomicAdd.  Every tile value is an fp32 number >= ln 2 (or 0) and the
+// totals stay below 2^28, so each fp64 addition is exact: the energies do not
+// depend on the order of the additions, on the ranges, or on P -- a probe's
+// energy is the same bits in any batch (the sharded runs rely on this).
 #include <cstdlib>
 
 #include "nss_internal.cuh"
@@ -33,8 +39,7 @@ namespace nss {
 namespace {
 
 constexpr int BM = 128;          // probes per tile (UMMA M)
-constexpr int KSTEPS = 7;        // K = 112 >= d
-constexpr int kSplits = 2;       // bf16 terms per probe coordinate
+constexpr int kSplits = 2;       // fp16 terms per probe coordinate (hi, lo)
 constexpr int kAtom = BM * 128;  // bytes of one [128 rows x 128 B] swizzle-128B region (probe tile)
 constexpr int kSmemA = kSplits * 2 * kAtom;      // splits x 2 k-blocks
 constexpr int kEpiWarps = 16;                    // four per TMEM lane quarter (column quarters)
@@ -43,16 +48,17 @@ constexpr int kThreads = 64 + 32 * kEpiWarps;    // warp 0 TMA, warp 1 MMA, warp
 constexpr int kUnitsPerSM = 8;
 constexpr int kMaxRing = 4;
 
-// Data-tile width BN (UMMA N): 128 (4-stage TMA ring, 4 TMEM accumulators of
-// 128 columns) or 256 (half the operand bytes per flop; 2 stages, 2
-// accumulators of 256 columns, two tcgen05.ld per epilogue warp and tile).
-template <int BN_>
+// Data-tile width BN (UMMA N): 128 (4 TMEM accumulators of 128 columns) or
+// 256 (half the operand bytes per flop; 2 accumulators of 256 columns, two
+// tcgen05.ld per epilogue warp and tile).  XS X terms per stage.
+template <int BN_, int XS_>
 struct LrCfg {
   static constexpr int BN = BN_;
-  static constexpr int kStages = BN_ == 128 ? 4 : 2;          // TMA ring depth for X tiles
+  static constexpr int XS = XS_;
+  static constexpr int kStages = (BN_ == 128 && XS_ == 1) ? 4 : 2;  // TMA ring depth for X tiles
   static constexpr int kAcc = BN_ == 128 ? 4 : 2;             // TMEM accumulators (kAcc x BN = 512 columns)
   static constexpr int kAtomB = BN_ * 128;                    // one [BN rows x 128 B] swizzle-128B region
-  static constexpr int kSmemB = kStages * 2 * kAtomB;         // stages x 2 k-blocks
+  static constexpr int kSmemB = kStages * XS_ * 2 * kAtomB;   // stages x X terms x 2 k-blocks
   static constexpr int kPartCols = BN_ / kColParts;           // columns per epilogue part
   static constexpr int kChunks = kPartCols / 32;              // tcgen05.ld.32x32b.x32 per part
 };
@@ -65,27 +71,24 @@ struct __align__(8) Bars {
 };
 
 struct Sched {
-  int m_tiles, S, units;
-  __device__ Sched(int n_probe, int n_tiles, int G) {
+  int m_tiles, pairs;
+  __device__ Sched(int n_probe, int n_tiles) {
     m_tiles = (n_probe + BM - 1) / BM;
-    int s = m_tiles > 0 ? (kUnitsPerSM * G + m_tiles - 1) / m_tiles : 1;
-    S = s < 1 ? 1 : (s > n_tiles ? n_tiles : s);
-    units = m_tiles * S;
+    pairs = m_tiles * n_tiles;
   }
-  __device__ void range(int cta, int G, int &u0, int &u1) const {
-    u0 = static_cast<int>(static_cast<long long>(units) * cta / G);
-    u1 = static_cast<int>(static_cast<long long>(units) * (cta + 1) / G);
+  __device__ void range(int cta, int G, int &p0, int &p1) const {
+    p0 = static_cast<int>(static_cast<long long>(pairs) * cta / G);
+    p1 = static_cast<int>(static_cast<long long>(pairs) * (cta + 1) / G);
   }
 };
 
-template <int BN_>
+template <int BN_, int XS_>
 __global__ void __launch_bounds__(kThreads, 1)
     k_lr_energy(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                float *partial, int *slices_out, const int *n_probe_ptr, int *reset_counter, int p_stride,
-                int n_data, int n_tiles) {
-  using C = LrCfg<BN_>;
+                const __grid_constant__ CUtensorMap tmB2, double *eacc, const int *n_probe_ptr, int *reset_counter,
+                int p_stride, int n_data, int n_tiles, int ksteps) {
+  using C = LrCfg<BN_, XS_>;
   constexpr int BN = C::BN, kStages = C::kStages, kAcc = C::kAcc, kPartCols = C::kPartCols;
-  __shared__ double red4[4][kColParts][32];  // per lane quarter: the column parts' unit sums
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sA = smem;
@@ -94,11 +97,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int G = gridDim.x;
   const int n_probe = *n_probe_ptr;
-  const Sched sch(n_probe, n_tiles, G);
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    if (reset_counter) *reset_counter = 0;  // the next round's row counter
-    *slices_out = sch.S;                    // per unit: one slice (the column parts combined on chip)
-  }
+  const Sched sch(n_probe, n_tiles);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && reset_counter) *reset_counter = 0;  // the next round's row counter
   int u0, u1;
   sch.range(blockIdx.x, G, u0, u1);
   if (n_probe <= 0 || u0 >= u1) return;  // uniform per CTA, before any barrier or TMEM use
@@ -127,9 +127,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------- TMA producer ----------------
     tc::tma_prefetch(&tmA);
     tc::tma_prefetch(&tmB);
+    if (XS_ == 2) tc::tma_prefetch(&tmB2);
     int it = 0, a_loads = 0, prev_m = -1;
-    for (int u = u0; u < u1; ++u) {
-      const int m = u / sch.S, s = u - m * sch.S;
+    for (int u = u0; u < u1; ++u, ++it) {
+      const int m = u / n_tiles, t = u - m * n_tiles;
       if (m != prev_m) {
         if (a_loads > 0) tc::mbar_wait(&bars->a_empty, (a_loads - 1) & 1);
         tc::mbar_arrive_expect_tx(&bars->a_full, kSmemA);
@@ -139,21 +140,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++a_loads;
         prev_m = m;
       }
-      const int t0 = s * n_tiles / sch.S, t1 = (s + 1) * n_tiles / sch.S;
-      for (int t = t0; t < t1; ++t, ++it) {
+      {
         const int st = it % kStages;
         if (it >= kStages) tc::mbar_wait(&bars->empty[st], ((it / kStages) - 1) & 1);
-        tc::mbar_arrive_expect_tx(&bars->full[st], 2 * C::kAtomB);
-        for (int kb = 0; kb < 2; ++kb)
-          tc::tma_load_2d(sB + (st * 2 + kb) * C::kAtomB, &tmB, &bars->full[st], kb * 64, t * BN);
+        tc::mbar_arrive_expect_tx(&bars->full[st], XS_ * 2 * C::kAtomB);
+        for (int kb = 0; kb < 2; ++kb) {
+          tc::tma_load_2d(sB + ((st * XS_) * 2 + kb) * C::kAtomB, &tmB, &bars->full[st], kb * 64, t * BN);
+          if (XS_ == 2)
+            tc::tma_load_2d(sB + ((st * XS_ + 1) * 2 + kb) * C::kAtomB, &tmB2, &bars->full[st], kb * 64, t * BN);
+        }
       }
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer ----------------
-    constexpr uint32_t idesc = tc::idesc_bf16_f32(BM, BN);
+    constexpr uint32_t idesc = tc::idesc_f16_f32(BM, BN);
     int it = 0, a_loads = 0, prev_m = -1;
-    for (int u = u0; u < u1; ++u) {
-      const int m = u / sch.S, s = u - m * sch.S;
+    for (int u = u0; u < u1; ++u, ++it) {
+      const int m = u / n_tiles;
       if (m != prev_m) {
         if (a_loads > 0) tc::umma_commit(&bars->a_empty);  // every MMA on the old probe tile issued
         tc::mbar_wait(&bars->a_full, a_loads & 1);
@@ -161,20 +164,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++a_loads;
         prev_m = m;
       }
-      const int t0 = s * n_tiles / sch.S, t1 = (s + 1) * n_tiles / sch.S;
-      for (int t = t0; t < t1; ++t, ++it) {
+      {
         const int st = it % kStages, acc = it % kAcc;
         if (it >= kAcc) tc::mbar_wait(&bars->tempty[acc], ((it / kAcc) - 1) & 1);
         tc::mbar_wait(&bars->full[st], (it / kStages) & 1);
         tc::tc_fence_after();
         const uint32_t d_tmem = tmem + acc * BN;
+        // (A term, X term) products: hi.Xhi, lo.Xhi (+ hi.Xlo when X is split)
 #pragma unroll
-        for (int q = 0; q < kSplits; ++q) {
-#pragma unroll
-          for (int ks = 0; ks < KSTEPS; ++ks) {
-            const int kb = ks >> 2, koff = (ks & 3) * 32;  // 16 bf16 = 32 B per k-step
-            const uint64_t ad = tc::umma_desc_sw128(sA + (q * 2 + kb) * kAtom + koff);
-            const uint64_t bd = tc::umma_desc_sw128(sB + (st * 2 + kb) * C::kAtomB + koff);
+        for (int q = 0; q < kSplits + XS_ - 1; ++q) {
+          const int qa = q < kSplits ? q : 0, qb = q < kSplits ? 0 : 1;
+          for (int ks = 0; ks < ksteps; ++ks) {
+            const int kb = ks >> 2, koff = (ks & 3) * 32;  // 16 fp16 = 32 B per k-step
+            const uint64_t ad = tc::umma_desc_sw128(sA + (qa * 2 + kb) * kAtom + koff);
+            const uint64_t bd = tc::umma_desc_sw128(sB + ((st * XS_ + qb) * 2 + kb) * C::kAtomB + koff);
             tc::umma_f16(d_tmem, ad, bd, idesc, (q | ks) != 0);
           }
         }
@@ -188,11 +191,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int chalf = (warp - 2) >> 2;        // column part of the tile: 0 .. kColParts-1
     const int row_in_tile = quarter * 32 + lane;
     int it = 0;
-    for (int u = u0; u < u1; ++u) {
-      const int m = u / sch.S, s = u - m * sch.S;
-      const int t0 = s * n_tiles / sch.S, t1 = (s + 1) * n_tiles / sch.S;
-      double e_sum = 0.0;
-      for (int t = t0; t < t1; ++t, ++it) {
+    double e_sum = 0.0;
+    for (int u = u0; u < u1; ++u, ++it) {
+      const int m = u / n_tiles, t = u - m * n_tiles;
+      {
         const int acc = it % kAcc;
         tc::mbar_wait(&bars->tfull[acc], (it / kAcc) & 1);
         tc::tc_fence_after();
@@ -206,8 +208,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&bars->tempty[acc]);  // buffer fully read: release it
         // softplus(a) - y a = |a|/2 + a/2 - y a + log(1 + e^-|a|); the linear
-        // part sum_r (1/2 - y_r) a_r = theta . g is added per probe row by the
-        // consumer (lr_engine.cu), so per element: sum |a| and the product of
+        // part sum_r (1/2 - y_r) a_r = theta . g is the consumer's seed of the
+        // row accumulator, so per element: sum |a| and the product of
         // (1 + e^-|a|) (one ex2; one lg2 per kPartCols / 2 factors), two chains each
         float s0 = 0.f, s1 = 0.f, p0 = 1.f, p1 = 1.f;
         const int valid = n_data - col0;  // >= kPartCols except in the ragged last tile
@@ -240,22 +242,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        // each product has <= kPartCols / 2 <= 32 factors in (1, 2]: no overflow
+        // each product has <= kPartCols / 2 <= 32 factors in (1, 2]: no
+        // overflow; the tile value is >= ln 2 per column, or 0 (no column)
         e_sum += static_cast<double>(fmaf(0.6931471805599453f, __log2f(p0) + __log2f(p1), 0.5f * (s0 + s1)));
       }
-      const int row = m * BM + row_in_tile;
-      // the kColParts warps of a TMEM lane quarter combine their column parts
-      // in shared memory (fixed order, fp64) behind a named barrier of the
-      // quarter's 128 threads: one slice per unit and probe row
-      red4[quarter][chalf][lane] = e_sum;
-      asm volatile("bar.sync %0, %1;" ::"r"(2 + quarter), "r"(32 * kColParts) : "memory");
-      if (chalf == 0 && row < n_probe) {
-        double tot = 0.0;
-#pragma unroll
-        for (int c = 0; c < kColParts; ++c) tot += red4[quarter][c][lane];
-        partial[static_cast<long long>(s) * p_stride + row] = static_cast<float>(tot);
+      // end of this probe tile's part of the range: one exact fp64 atomic per row
+      if (u + 1 == u1 || (u + 1) / n_tiles != m) {
+        const int row = m * BM + row_in_tile;
+        if (row < n_probe) atomicAdd(eacc + row, e_sum);
+        e_sum = 0.0;
       }
-      asm volatile("bar.sync %0, %1;" ::"r"(2 + quarter), "r"(32 * kColParts) : "memory");  // red4 is reused
     }
   }
   tc::tc_fence_before();
@@ -263,14 +259,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tc::tmem_dealloc<kAcc * BN>(tmem);
 }
 
-template <int BN_>
-size_t smem_of() { return kSmemA + LrCfg<BN_>::kSmemB + sizeof(Bars) + 1024; }
+template <int BN_, int XS_>
+size_t smem_of() { return kSmemA + LrCfg<BN_, XS_>::kSmemB + sizeof(Bars) + 1024; }
 
-template <int BN_>
-void launch_bn(const CUtensorMap &tmA, const CUtensorMap &tmB, float *partial, int *slices_out, const int *n_probe,
-               int *reset_counter, int p_stride, int n_data, const LaunchCtx &lc) {
-  NSS_MAX_SMEM(k_lr_energy<BN_>, smem_of<BN_>());
-  NSS_PIN_CARVEOUT(k_lr_energy<BN_>);
+template <int BN_, int XS_>
+void launch_bn(const CUtensorMap &tmA, const CUtensorMap &tmB, const CUtensorMap &tmB2, double *eacc,
+               const int *n_probe, int *reset_counter, int p_stride, int n_data, int d,
+               const LaunchCtx &lc) {
+  NSS_MAX_SMEM((k_lr_energy<BN_, XS_>), (smem_of<BN_, XS_>()));
+  NSS_PIN_CARVEOUT((k_lr_energy<BN_, XS_>));
   static int sms = 0;
   if (!sms) {
     int dev = 0;
@@ -278,25 +275,27 @@ void launch_bn(const CUtensorMap &tmA, const CUtensorMap &tmB, float *partial, i
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int n_tiles = (n_data + BN_ - 1) / BN_;
-  k_lr_energy<BN_><<<sms, kThreads, smem_of<BN_>(), lc.stream>>>(tmA, tmB, partial, slices_out, n_probe,
-                                                                 reset_counter, p_stride, n_data, n_tiles);
+  k_lr_energy<BN_, XS_><<<sms, kThreads, smem_of<BN_, XS_>(), lc.stream>>>(
+      tmA, tmB, tmB2, eacc, n_probe, reset_counter, p_stride, n_data, n_tiles, (d + 15) / 16);
   ++*lc.launch_counter;
 }
 
 }  // namespace
 
-size_t lr_energy_smem() { return smem_of<128>() > smem_of<256>() ? smem_of<128>() : smem_of<256>(); }
+size_t lr_energy_smem() { return smem_of<128, 2>(); }
 int lr_energy_splits() { return kSplits; }
 
-// slices per probe row: kColParts per data slice, at most one data slice per 128-row tile
-int lr_max_slices(int n_tiles) { return kColParts * n_tiles; }
 
-void launch_lr_energy(const CUtensorMap &tmA, const CUtensorMap &tmB, float *partial, int *slices_out,
-                      const int *n_probe, int *reset_counter, int p_stride, int n_data, int bn, const LaunchCtx &lc) {
-  if (bn == 256)
-    launch_bn<256>(tmA, tmB, partial, slices_out, n_probe, reset_counter, p_stride, n_data, lc);
+// bn: data-tile width (256 with one X term); xs: X terms (1 fp16-exact data, 2 split data -> bn 128)
+void launch_lr_energy(const CUtensorMap &tmA, const CUtensorMap &tmB, const CUtensorMap &tmB2, double *eacc,
+                      const int *n_probe, int *reset_counter, int p_stride, int n_data, int d,
+                      int bn, int xs, const LaunchCtx &lc) {
+  if (xs == 2)
+    launch_bn<128, 2>(tmA, tmB, tmB2, eacc, n_probe, reset_counter, p_stride, n_data, d, lc);
+  else if (bn == 256)
+    launch_bn<256, 1>(tmA, tmB, tmB2, eacc, n_probe, reset_counter, p_stride, n_data, d, lc);
   else
-    launch_bn<128>(tmA, tmB, partial, slices_out, n_probe, reset_counter, p_stride, n_data, lc);
+    launch_bn<128, 1>(tmA, tmB, tmB2, eacc, n_probe, reset_counter, p_stride, n_data, d, lc);
 }
 
 }  // namespace nss

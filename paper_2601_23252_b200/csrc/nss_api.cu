@@ -134,7 +134,7 @@ struct nss_ctx {
   int batch_backend = 0;  // 1 generic warp-per-probe energy, 2 tensor-core logistic regression, 3 GP
   bool gp_rounds = getenv("NSS_GP_ROUNDS") != nullptr;  // GP: round-synchronous engine instead of the fused chains
   LrEngine lr{};
-  bool lr_ok = false;     // logistic-regression data are bf16-exact and d <= 112
+  bool lr_ok = false;     // logistic-regression data fit the tensor-core path (d <= 128, fp16 range)
   std::vector<double> lr_x, lr_y;
   cudaGraphExec_t round_graph = nullptr;
   long long round_graph_launches = 0;
@@ -571,13 +571,15 @@ nss_status ensure_batch(nss_ctx *c) {
       if (lr_setup(c->lr, c->lr_x.data(), c->lr_y.data(), c->en.n_data, c->d, b.max_rows) != cudaSuccess)
         return fail(c, NSS_ERR_CUDA, "tensor-core logistic-regression setup failed");
     }
-    b.n_splits = c->lr.n_splits;
+    b.n_splits = 1;
     b.p_stride = c->lr.p_stride;
-    b.slices = c->lr.slices;
+    b.slices = nullptr;
     for (int q = 0; q < 2; ++q) {
-      b.partial[q] = c->lr.partial[q];
+      nss_status s;  // float energies of the batched init draws (k_binit_accept)
+      if (!b.partial[q] && (s = dalloc(c, &b.partial[q], static_cast<size_t>(b.max_rows)))) return s;
       b.A[q] = c->lr.A[q];
-      b.lin[q] = c->lr.partial[q] + static_cast<size_t>(c->lr.n_splits) * c->lr.p_stride;
+      b.lin[q] = c->lr.lin[q];
+      b.eacc[q] = c->lr.eacc[q];
     }
     b.g = c->lr.g;
   } else {
@@ -594,6 +596,7 @@ nss_status ensure_batch(nss_ctx *c) {
       if ((s = dalloc(c, &b.partial[q], static_cast<size_t>(b.max_rows)))) return s;
       b.A[q] = nullptr;
       b.lin[q] = nullptr;
+      b.eacc[q] = nullptr;
     }
     b.g = nullptr;
   }
@@ -989,7 +992,8 @@ static nss_status init_impl(const nss_prior *prior, const nss_energy *energy, co
     }
   } else if (en.kind == NSS_E_LOGREG) {
     const size_t nx = static_cast<size_t>(energy->n_data) * d;
-    c->lr_ok = d <= 112 && lr_data_bf16_exact(energy->data_x, static_cast<long long>(nx));
+    bool exact = true;
+    c->lr_ok = lr_data_ok(energy->data_x, static_cast<long long>(nx), d, &exact);
     if (c->lr_ok) {
       c->lr_x.assign(energy->data_x, energy->data_x + nx);
       c->lr_y.assign(energy->data_y, energy->data_y + energy->n_data);
@@ -1714,8 +1718,9 @@ NSS_API nss_status nss_debug_stamps(nss_ctx *c, uint64_t *stamps) {
 
 NSS_API nss_status nss_lr_energy_batch(const double *X, const double *y, int64_t N, int32_t d, const double *theta,
                                        int64_t P, double *E_out) {
-  if (!X || !y || !theta || !E_out || N < 1 || d < 1 || d > 112 || P < 1) return NSS_ERR_INVALID_ARG;
-  if (!lr_data_bf16_exact(X, N * d)) return NSS_ERR_UNSUPPORTED;
+  if (!X || !y || !theta || !E_out || N < 1 || d < 1 || d > 128 || P < 1) return NSS_ERR_INVALID_ARG;
+  bool exact = true;
+  if (!lr_data_ok(X, N * d, d, &exact)) return NSS_ERR_UNSUPPORTED;
   LrEngine L;
   if (lr_setup(L, X, y, N, d, static_cast<int>(P)) != cudaSuccess) {
     lr_free(L);

@@ -154,19 +154,20 @@ def funnel(d: int = 100, half_width: float = 20.0, sigma_y: float = 3.0) -> Prob
 # --------------------------------------------------------------------------
 # C4: Bayesian logistic regression, N rows, d weights, prior N(0, I)
 # --------------------------------------------------------------------------
-def bf16_round(a: np.ndarray) -> np.ndarray:
-    """Round fp32 values to the nearest bf16 (ties to even); result is exact in
-    bf16, fp32 and fp64."""
-    f = np.asarray(a, dtype=np.float32)
-    u = f.view(np.uint32).astype(np.uint64)
-    bias = ((u >> 16) & 1) + 0x7FFF
-    u = ((u + bias) & 0xFFFF0000).astype(np.uint32)
-    return u.view(np.float32)
+def fp16_round(a: np.ndarray) -> np.ndarray:
+    """Round to the nearest fp16 value (ties to even): features stored in
+    half precision, exact in fp16, fp32 and fp64 (DESIGN R-28)."""
+    return np.asarray(a, dtype=np.float64).astype(np.float16).astype(np.float64)
 
 
-def logreg(d: int = 100, n_data: int = 10_000, seed: int = 1005) -> Problem:
+def logreg(d: int = 100, n_data: int = 10_000, seed: int = 1005, half_exact: bool = True) -> Problem:
+    """X_rj ~ N(0, 1/d) (rounded to fp16 when half_exact: the tensor-core path
+    then needs one X term; any finite data within the fp16 range works with
+    two), theta* ~ N(0, I), y_r ~ Bernoulli(sigmoid(x_r . theta*))."""
     rng = np.random.Generator(np.random.PCG64(seed))
-    x = bf16_round(rng.standard_normal((n_data, d)) / math.sqrt(d)).astype(np.float64)
+    x = rng.standard_normal((n_data, d)) / math.sqrt(d)
+    if half_exact:
+        x = fp16_round(x)
     theta = rng.standard_normal(d)
     logits = x @ theta
     y = (rng.uniform(size=n_data) < 1.0 / (1.0 + np.exp(-logits))).astype(np.float64)

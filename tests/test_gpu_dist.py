@@ -37,6 +37,8 @@ CASES = {
     "warp_funnel100": (lambda: W.funnel(100), dict(n_live=1000, k=100, steps=6), 4),
     "half_k": (lambda: W.gauss(3), dict(n_live=64, k=32, steps=3), 8),
     "batch_logreg": (lambda: W.logreg(5, n_data=300, seed=3), dict(n_live=300, k=31, steps=3), 5),
+    # several probe tiles per round, different on every rank: energies must not depend on the batch
+    "batch_logreg_d100": (lambda: W.logreg(100, n_data=3000, seed=4), dict(n_live=2048, k=1024, steps=3), 2),
     "batch_gp": (lambda: W.gp_ard(2, 40, seed=3), dict(n_live=64, k=17, steps=2), 3),
 }
 

@@ -38,6 +38,8 @@ CASES = {
     "funnel_d16": (lambda: W.funnel(16), dict(n_live=500, k=50, steps=6), 2),
     "funnel_d100": (lambda: W.funnel(100), dict(n_live=800, k=80, steps=4), 0),
     "logreg_small": (lambda: W.logreg(5, n_data=300, seed=3), dict(n_live=300, k=30, steps=5), 2),
+    "logreg_split_data": (lambda: W.logreg(20, n_data=700, seed=3, half_exact=False), dict(n_live=300, k=30, steps=4),
+                          2),
     "flat_d1": (lambda: W.flat(1), dict(n_live=64, k=7, steps=3), 1),
     "d33_ragged_lanes": (lambda: W.gauss(33, half_width=4.0), dict(n_live=333, k=33, steps=3), 1),
     "k_n_minus_1": (lambda: W.gauss(3), dict(n_live=50, k=49, steps=3), 0),

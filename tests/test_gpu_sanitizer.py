@@ -6,7 +6,10 @@ unusable), so the test runs only when NSS_SANITIZER names the tool:
     NSS_SANITIZER=memcheck  python -m pytest tests/test_gpu_sanitizer.py
     NSS_SANITIZER=racecheck python -m pytest tests/test_gpu_sanitizer.py
 
-Logs: profiles/r02_sanitizer_<tool>.txt."""
+On this build's GPU pool compute-sanitizer is closed (it answers "closed on
+this pool", profiles/r02_sanitizer_closed.txt): the test then skips, and the
+memory-safety evidence is the parity suite's bounds/edge cases (empty,
+ragged, maximum sizes) against the oracle."""
 import os
 import shutil
 import subprocess
@@ -27,6 +30,8 @@ def test_sanitizer_clean():
            os.path.join(ROOT, "scripts", "sanitize_case.py")]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=3000)
     out = p.stdout + p.stderr
+    if "closed on this pool" in out:
+        pytest.skip("compute-sanitizer is closed on this GPU pool")
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", f"sanitizer_{tool}.txt"), "w") as f:
         f.write(" ".join(cmd) + "\n" + out)
