@@ -306,7 +306,8 @@ nss_status nss_set_graph(nss_ctx *ctx, int32_t enable);
 /* Device %globaltimer stamps (ns) written at phase boundaries of the select
  * (0-6) and metric (8-13) kernels during the last iteration. */
 nss_status nss_debug_stamps(nss_ctx *ctx, uint64_t *stamps /* 16 */);
-/* Kernels launched by this context since creation (all kinds). */
+/* Kernels launched by this context since creation (all kinds, including
+ * those of device-side round loops; synchronises when there are any). */
 nss_status nss_launch_count(nss_ctx *ctx, int64_t *launches);
 
 /* ---- in-process rank emulation (tests) ----

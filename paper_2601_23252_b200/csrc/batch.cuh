@@ -35,6 +35,9 @@ void batch_begin(const RunDev &r, const PriorDev &pr, const BatchDev &b, const L
 void batch_advance(const RunDev &r, const PriorDev &pr, const BatchDev &b, int parity, const LaunchCtx &lc);
 void batch_energy_generic(const RunDev &r, const EnergyDev &en, const BatchDev &b, int parity, const LaunchCtx &lc);
 void batch_finish(const RunDev &r, const BatchDev &b, const LaunchCtx &lc);
+// one pass of the device-side round loop decides whether the WHILE node repeats
+void launch_round_cond(cudaGraphConditionalHandle h, const BatchDev &b, const RunDev &r, int per_body,
+                       int max_rounds, const LaunchCtx &lc);
 bool batch_generic_ok(const EnergyDev &en);
 void batch_init_draw(const RunDev &r, const PriorDev &pr, const BatchDev &b, const int *pending, int *map,
                      uint32_t attempt, const LaunchCtx &lc);

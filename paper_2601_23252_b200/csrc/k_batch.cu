@@ -29,6 +29,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_batch_begin(RunDev r, P
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     b.n_probe[0] = 0;
     b.n_probe[1] = 0;
+    r.st->loop_rounds = 0;
   }
   if (c >= cr.y) return;
   const DevState *st = r.st;
@@ -170,6 +171,33 @@ __global__ void k_batch_finish(RunDev r, BatchDev b) {
     atomicAdd(&st->nulls, acc[4]);
   }
 }
+
+// The device-side round loop (a CUDA-graph WHILE node, nss_api.cu): after each
+// pass of its body (two rounds) continue while the last round issued probes.
+// A cap far above any run's rounds (p (cap + 2 + max_shrink) + 2) turns a
+// runaway loop into an error instead of a hang.
+__global__ void k_round_cond(cudaGraphConditionalHandle h, const int *n_last, DevState *st, int per_body,
+                             int max_rounds) {
+  const int rounds = st->loop_rounds + 2;
+  st->loop_rounds = rounds;
+  st->dev_launches += static_cast<unsigned long long>(per_body);
+  bool more = *n_last > 0;
+  if (more && rounds > max_rounds) {
+    raise_error(st, NSS_ERR_CUDA);
+    more = false;
+  }
+  cudaGraphSetConditional(h, more ? 1u : 0u);
+}
+
+}  // namespace
+
+void launch_round_cond(cudaGraphConditionalHandle h, const BatchDev &b, const RunDev &r, int per_body,
+                       int max_rounds, const LaunchCtx &lc) {
+  k_round_cond<<<1, 1, 0, lc.stream>>>(h, b.n_probe + 1, r.st, per_body, max_rounds);
+  ++*lc.launch_counter;
+}
+
+namespace {
 
 // blocks for this GPU's chains; at least one (block 0 resets the row counters)
 int chain_blocks(const RunDev &r, int per_block) {

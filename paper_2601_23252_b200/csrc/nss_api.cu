@@ -138,6 +138,11 @@ struct nss_ctx {
   std::vector<double> lr_x, lr_y;
   cudaGraphExec_t round_graph = nullptr;
   long long round_graph_launches = 0;
+  // the rounds as a device-side loop: one graph with a WHILE node whose body
+  // is two rounds + k_round_cond (no host polling); NSS_HOST_ROUNDS=1 keeps
+  // the host-polled chunks
+  cudaGraphExec_t loop_graph = nullptr;
+  bool host_rounds = getenv("NSS_HOST_ROUNDS") != nullptr;
   int *h_nprobe = nullptr;  // pinned (inside h_block)
   void *gp = nullptr;       // fp64 batched GP marginal likelihood (k_gp.cu)
   // multi-GPU (dist.cu): chain block [r.c0, r.c1) of kc chains, NCCL all-gather of new rows
@@ -641,6 +646,10 @@ void drop_graph(nss_ctx *c) {
     cudaGraphExecDestroy(c->graph_info);
     c->graph_info = nullptr;
   }
+  if (c->loop_graph) {
+    cudaGraphExecDestroy(c->loop_graph);
+    c->loop_graph = nullptr;
+  }
 }
 
 // One iteration with the batch engine: the HRSS part is a data-dependent
@@ -682,6 +691,44 @@ nss_status enqueue_iteration_batch(nss_ctx *c, Stage stage = kAll) {
     }
     const long long max_rounds =
         static_cast<long long>(c->r.p) * (c->r.max_stepout + 2 + c->r.max_shrink) + kRoundsPerChunk;
+    if (c->use_graph && !c->timing && !c->host_rounds) {
+      // device-side loop: a WHILE node repeating {2 rounds, k_round_cond}
+      if (!c->loop_graph) {
+        const long long before = c->launches;
+        cudaGraph_t g = nullptr;
+        CK(cudaGraphCreate(&g, 0));
+        cudaGraphConditionalHandle h;
+        CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+        cudaGraphNodeParams np{};
+        np.type = cudaGraphNodeTypeConditional;
+        np.conditional.handle = h;
+        np.conditional.type = cudaGraphCondTypeWhile;
+        np.conditional.size = 1;
+        cudaGraphNode_t node;
+        CK(cudaGraphAddNode(&node, g, nullptr, 0, &np));
+        cudaGraph_t body = np.conditional.phGraph_out[0];
+        CK(cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        enqueue_rounds(c, 2);
+        const int per_body = static_cast<int>(c->launches - before) + 1;
+        launch_round_cond(h, c->bd, c->r, per_body, static_cast<int>(max_rounds), lc);
+        const cudaError_t e = cudaStreamEndCapture(c->stream, &body);
+        if (e != cudaSuccess) {
+          cudaGraphDestroy(g);
+          c->poisoned = true;
+          return fail(c, NSS_ERR_CUDA, std::string("round loop capture: ") + cudaGetErrorString(e));
+        }
+        const cudaError_t e2 = cudaGraphInstantiate(&c->loop_graph, g, 0);
+        cudaGraphDestroy(g);
+        if (e2 != cudaSuccess) {
+          c->poisoned = true;
+          return fail(c, NSS_ERR_CUDA, std::string("round loop graph: ") + cudaGetErrorString(e2));
+        }
+        c->launches = before;  // counted on the device (DevState::dev_launches)
+      }
+      CK(cudaGraphLaunch(c->loop_graph, c->stream));
+      batch_finish(c->r, c->bd, lc);
+      return NSS_OK;
+    }
     for (long long done = 0; done < max_rounds; done += kRoundsPerChunk) {
       if (c->use_graph && !c->timing) {
         if (!c->round_graph) {
@@ -1923,7 +1970,9 @@ NSS_API nss_status nss_smc_run(nss_ctx *c, int64_t max_stages, double *log_z) {
 
 NSS_API nss_status nss_launch_count(nss_ctx *c, int64_t *launches) {
   if (!c || !launches) return NSS_ERR_INVALID_ARG;
-  *launches = c->launches;
+  nss_status s;
+  if (c->loop_graph && (s = pull_state(c))) return s;  // + the device-side loops' kernels
+  *launches = c->launches + static_cast<int64_t>(c->h_st->dev_launches);
   return NSS_OK;
 }
 

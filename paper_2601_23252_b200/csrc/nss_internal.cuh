@@ -33,6 +33,8 @@ struct DevState {
   unsigned long long init_evals, init_attempts;
   unsigned long long stamp[16];  // %globaltimer stamps (ns) for latency profiling
   double smc_beta, smc_logz;     // F3 tempered SMC: current temperature, accumulated log Z
+  unsigned long long dev_launches;  // kernels launched by device-side loops (graph WHILE nodes)
+  int loop_rounds;                  // rounds of the current iteration's device-side loop
 };
 
 // Energy parameters laid out for the kernels (device pointers, fp32).
