@@ -60,6 +60,8 @@ template <int NPL>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3) k_batch_advance(RunDev r, PriorDev pr, BatchDev b,
                                                                        int parity) {
   extern __shared__ float sm[];
+  pdl_trigger();  // every block has started: the energy pass may launch (it waits for us)
+  pdl_wait();     // the previous energy pass is complete
   const int wib = threadIdx.x >> 5;
   const int2 cr = chain_range(r);
   const int c = cr.x + blockIdx.x * kWarpsPerBlock + wib;
@@ -178,7 +180,7 @@ __global__ void k_batch_finish(RunDev r, BatchDev b) {
 // runaway loop into an error instead of a hang.
 __global__ void k_round_cond(cudaGraphConditionalHandle h, const int *n_last, DevState *st, int per_body,
                              int max_rounds) {
-  const int rounds = st->loop_rounds + 2;
+  const int rounds = st->loop_rounds + per_body / 2;
   st->loop_rounds = rounds;
   st->dev_launches += static_cast<unsigned long long>(per_body);
   bool more = *n_last > 0;
@@ -217,8 +219,8 @@ void advance_t(const RunDev &r, const PriorDev &pr, const BatchDev &b, int parit
   const size_t smem = static_cast<size_t>(kWarpsPerBlock) * NPL * 32 * sizeof(float);
   NSS_MAX_SMEM(k_batch_advance<NPL>, 160 * 1024);
   NSS_PIN_CARVEOUT(k_batch_advance<NPL>);
-  k_batch_advance<NPL><<<chain_blocks(r, kWarpsPerBlock), kWarpsPerBlock * 32, smem, lc.stream>>>(
-      r, pr, b, parity);
+  launch_maybe_pdl(k_batch_advance<NPL>, dim3(chain_blocks(r, kWarpsPerBlock)), dim3(kWarpsPerBlock * 32), smem,
+                   lc.stream, r, pr, b, parity);
   ++*lc.launch_counter;
 }
 

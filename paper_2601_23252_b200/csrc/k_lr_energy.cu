@@ -45,8 +45,29 @@ constexpr int kSmemA = kSplits * 2 * kAtom;      // splits x 2 k-blocks
 constexpr int kEpiWarps = 16;                    // four per TMEM lane quarter (column quarters)
 constexpr int kColParts = kEpiWarps / 4;         // column parts of a tile (one per epilogue warp of a quarter)
 constexpr int kThreads = 64 + 32 * kEpiWarps;    // warp 0 TMA, warp 1 MMA, warps 2.. epilogue
-constexpr int kUnitsPerSM = 8;
 constexpr int kMaxRing = 4;
+// Every NSS_LR_POLY-th column's exponential on the FMA pipe instead of the
+// MUFU (0: none); measurement builds (NSS_NVCC_EXTRA=-DNSS_LR_POLY=4).
+#ifndef NSS_LR_POLY
+#define NSS_LR_POLY 0
+#endif
+
+// 2^x for x <= 0 on the FMA / ALU pipes only (no MUFU, no conversion): x =
+// j + f with j = rint(x) by the 1.5 2^23 trick, 2^f (|f| <= 1/2) by a degree-5
+// polynomial (relative error 3e-7), 2^j added to the exponent field.  x is
+// clamped at -126 (2^-126 is below every term it meets).
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = x + 12582912.f;
+  const float j = t - 12582912.f;
+  const float f = x - j;
+  float p = fmaf(1.32609e-3f, f, 9.67018e-3f);
+  p = fmaf(p, f, 5.550712e-2f);
+  p = fmaf(p, f, 0.24022224f);
+  p = fmaf(p, f, 0.693147f);
+  p = fmaf(p, f, 1.00000005f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) - 0x4B400000) * 8388608);
+}
 
 // Data-tile width BN (UMMA N): 128 (4 TMEM accumulators of 128 columns) or
 // 256 (half the operand bytes per flop; 2 accumulators of 256 columns, two
@@ -96,14 +117,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   Bars *bars = reinterpret_cast<Bars *>(smem + kSmemA + C::kSmemB);
 
   const int G = gridDim.x;
-  const int n_probe = *n_probe_ptr;
-  const Sched sch(n_probe, n_tiles);
-  if (blockIdx.x == 0 && threadIdx.x == 0 && reset_counter) *reset_counter = 0;  // the next round's row counter
-  int u0, u1;
-  sch.range(blockIdx.x, G, u0, u1);
-  if (n_probe <= 0 || u0 >= u1) return;  // uniform per CTA, before any barrier or TMEM use
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
+  // prologue: nothing the preceding advance kernel writes (programmatic
+  // dependent launch: it overlaps that kernel's tail)
   if (threadIdx.x == 0) {
     tc::mbar_init(&bars->a_full, 1);
     tc::mbar_init(&bars->a_empty, 1);
@@ -117,17 +133,30 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     tc::fence_barrier_init();
   }
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch(&tmA);
+    tc::tma_prefetch(&tmB);
+    if (XS_ == 2) tc::tma_prefetch(&tmB2);
+  }
   if (warp == 1) tc::tmem_alloc<kAcc * BN>(&bars->tmem_base);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
+  pdl_wait();  // the probe rows and their count are complete from here
+  pdl_trigger();
+  const int n_probe = *n_probe_ptr;
+  const Sched sch(n_probe, n_tiles);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && reset_counter) *reset_counter = 0;  // the next round's row counter
+  int u0, u1;
+  sch.range(blockIdx.x, G, u0, u1);
+  if (n_probe <= 0 || u0 >= u1) {  // uniform per CTA
+    if (warp == 1) tc::tmem_dealloc<kAcc * BN>(tmem);
+    return;
+  }
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer ----------------
-    tc::tma_prefetch(&tmA);
-    tc::tma_prefetch(&tmB);
-    if (XS_ == 2) tc::tma_prefetch(&tmB2);
     int it = 0, a_loads = 0, prev_m = -1;
     for (int u = u0; u < u1; ++u, ++it) {
       const int m = u / n_tiles, t = u - m * n_tiles;
@@ -217,7 +246,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int cc = 0; cc < kPartCols; ++cc) {
             const float a = v[cc >> 5][cc & 31];
-            const float e = tc::ex2_approx(-fabsf(a) * 1.4426950408889634f);
+            const float e = (NSS_LR_POLY > 0 && cc % (NSS_LR_POLY > 0 ? NSS_LR_POLY : 1) == NSS_LR_POLY - 1)
+                                ? ex2_poly(-fabsf(a) * 1.4426950408889634f)
+                                : tc::ex2_approx(-fabsf(a) * 1.4426950408889634f);
             if (cc & 1) {
               p1 = fmaf(p1, e, p1);
               s1 += fabsf(a);
@@ -275,8 +306,8 @@ void launch_bn(const CUtensorMap &tmA, const CUtensorMap &tmB, const CUtensorMap
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int n_tiles = (n_data + BN_ - 1) / BN_;
-  k_lr_energy<BN_, XS_><<<sms, kThreads, smem_of<BN_, XS_>(), lc.stream>>>(
-      tmA, tmB, tmB2, eacc, n_probe, reset_counter, p_stride, n_data, n_tiles, (d + 15) / 16);
+  launch_maybe_pdl(k_lr_energy<BN_, XS_>, dim3(sms), dim3(kThreads), smem_of<BN_, XS_>(), lc.stream, tmA, tmB, tmB2,
+                   eacc, n_probe, reset_counter, p_stride, n_data, n_tiles, (d + 15) / 16);
   ++*lc.launch_counter;
 }
 

@@ -143,6 +143,7 @@ struct nss_ctx {
   // the host-polled chunks
   cudaGraphExec_t loop_graph = nullptr;
   bool host_rounds = getenv("NSS_HOST_ROUNDS") != nullptr;
+  int loop_body = getenv("NSS_LOOP_ROUNDS") ? std::max(2, atoi(getenv("NSS_LOOP_ROUNDS")) & ~1) : 16;
   int *h_nprobe = nullptr;  // pinned (inside h_block)
   void *gp = nullptr;       // fp64 batched GP marginal likelihood (k_gp.cu)
   // multi-GPU (dist.cu): chain block [r.c0, r.c1) of kc chains, NCCL all-gather of new rows
@@ -708,7 +709,7 @@ nss_status enqueue_iteration_batch(nss_ctx *c, Stage stage = kAll) {
         CK(cudaGraphAddNode(&node, g, nullptr, 0, &np));
         cudaGraph_t body = np.conditional.phGraph_out[0];
         CK(cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-        enqueue_rounds(c, 2);
+        enqueue_rounds(c, c->loop_body);  // rounds past the last probe are no-ops
         const int per_body = static_cast<int>(c->launches - before) + 1;
         launch_round_cond(h, c->bd, c->r, per_body, static_cast<int>(max_rounds), lc);
         const cudaError_t e = cudaStreamEndCapture(c->stream, &body);

@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "nss.h"
 
@@ -271,6 +272,32 @@ struct LaunchCtx {
   cudaStream_t stream;
   long long *launch_counter;
 };
+
+// Programmatic dependent launch (the batch engine's round kernels): the
+// kernel may start while its predecessor drains (setup overlaps the tail and
+// the launch latency) and waits in pdl_wait() for the predecessor's results;
+// pdl_trigger() lets the successor start.  NSS_NO_PDL=1 launches normally.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+inline bool pdl_enabled() {
+  static const bool on = getenv("NSS_NO_PDL") == nullptr;
+  return on;
+}
+template <typename... KArgs, typename... Args>
+inline void launch_maybe_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                             Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 
 // k_select.cu: A2 delete + A3 dead records + A4 resample (one iteration)
 void launch_select(const RunDev &r, const LaunchCtx &lc);
