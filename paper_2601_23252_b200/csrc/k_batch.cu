@@ -56,9 +56,15 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_batch_begin(RunDev r, P
   }
 }
 
+// resident blocks per SM the advance is compiled for (register budget);
+// measurement builds may change it (NSS_NVCC_EXTRA=-DNSS_ADV_MINB=4)
+#ifndef NSS_ADV_MINB
+#define NSS_ADV_MINB 3
+#endif
+
 template <int NPL>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, 3) k_batch_advance(RunDev r, PriorDev pr, BatchDev b,
-                                                                       int parity) {
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, NSS_ADV_MINB) k_batch_advance(RunDev r, PriorDev pr, BatchDev b,
+                                                                                   int parity) {
   extern __shared__ float sm[];
   pdl_trigger();  // every block has started: the energy pass may launch (it waits for us)
   pdl_wait();     // the previous energy pass is complete
