@@ -377,6 +377,7 @@ def main():
 
     def new_run(seed):
         c = dict(cfg)
+        c["max_dead"] = cfg["n_live"] + cfg["k"] * int(1.6 * T + 50)  # a whole run and its finalisation
         c["seed"] = seed if shard else seed + 1000 * rank
         if shard and world == 1:  # the world-1 NCCL sharded path
             return nss.Sampler(prob, c, stream=stream.cuda_stream, dist=(0, 1, D.nccl_unique_id()))

@@ -35,23 +35,50 @@ __device__ __forceinline__ double *raw_groups(double *sm, int nent, int d, int n
   return yd + static_cast<long long>(rows) * dp;
 }
 
-// Entry e summed over the blocks of segment s in block order.
+// Entry e summed over the blocks of segment s in block order; loads are
+// issued 8 at a time (independent), the additions stay in block order.
 __device__ __forceinline__ double fold_segment(const double *partials, int s, int bps, int e, int nent1,
                                                bool is_min) {
   double acc = is_min ? INFINITY : 0.0;
   const double *p = partials + static_cast<long long>(s) * bps * nent1 + e;
-  int b = 0;
-  for (; b + 7 < bps; b += 8) {  // 8 independent loads in flight (same summation order)
+  for (int b = 0; b < bps; b += 8) {
     double v[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = p[static_cast<long long>(b + q) * nent1];
+    for (int q = 0; q < 8; ++q) v[q] = b + q < bps ? p[static_cast<long long>(b + q) * nent1] : 0.0;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) acc = is_min ? fmin(acc, v[q]) : acc + v[q];
+    for (int q = 0; q < 8; ++q)
+      if (b + q < bps) acc = is_min ? fmin(acc, v[q]) : acc + v[q];
   }
-  for (; b < bps; ++b) {
-    const double v = p[static_cast<long long>(b) * nent1];
-    acc = is_min ? fmin(acc, v) : acc + v;
+  return acc;
+}
+
+// The whole live set's entry e: every segment folded, then the segments in
+// order.  Small blocks-per-segment (the small-d case) load all kSegs x bps
+// partials first, so the fold waits for one round trip instead of kSegs.
+__device__ __forceinline__ double fold_all(const double *partials, int bps, int e, int nent1, bool is_min) {
+  double segs[kSegs];
+  if (bps <= 4) {
+    double v[kSegs * 4];
+#pragma unroll
+    for (int q = 0; q < kSegs * 4; ++q) {
+      const int s = q >> 2, b = q & 3;
+      v[q] = b < bps ? partials[(static_cast<long long>(s) * bps + b) * nent1 + e] : 0.0;
+    }
+#pragma unroll
+    for (int s = 0; s < kSegs; ++s) {
+      double acc = is_min ? INFINITY : 0.0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        if (b < bps) acc = is_min ? fmin(acc, v[s * 4 + b]) : acc + v[s * 4 + b];
+      segs[s] = acc;
+    }
+  } else {
+#pragma unroll
+    for (int s = 0; s < kSegs; ++s) segs[s] = fold_segment(partials, s, bps, e, nent1, is_min);
   }
+  double acc = is_min ? INFINITY : 0.0;
+#pragma unroll
+  for (int s = 0; s < kSegs; ++s) acc = is_min ? fmin(acc, segs[s]) : acc + segs[s];
   return acc;
 }
 
@@ -105,15 +132,20 @@ __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials,
   const int g0 = min(s1, s0 + q_in * chunk), g1 = min(s1, g0 + chunk);
   const int rows = g1 - g0;
   const int dp = r.dp;
+  // one batch of loads (the chunk is contiguous in X) while the shift loads;
+  // the shift is subtracted after the barrier
   for (int i = tid; i < d; i += blockDim.x) shift[i] = r.mshift[i];
-  __syncthreads();
-  // one batch of loads: the chunk is contiguous in X
   {
     const float *src = r.X + static_cast<long long>(g0) * dp;
     for (int q = tid; q < rows * dp; q += blockDim.x) {
       const int c = q % dp;
-      yd[q] = c < d ? static_cast<double>(src[q]) - shift[c] : 0.0;
+      yd[q] = c < d ? static_cast<double>(src[q]) : 0.0;
     }
+  }
+  __syncthreads();
+  for (int q = tid; q < rows * dp; q += blockDim.x) {
+    const int c = q % dp;
+    if (c < d) yd[q] -= shift[c];
   }
   float emin = INFINITY;
   for (int g = g0 + tid; g < g1; g += blockDim.x) emin = fminf(emin, r.E[g]);
@@ -225,10 +257,7 @@ __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials,
     if (mode == 2) {
       acc = partials[e];
     } else {
-      double segs[kSegs];
-#pragma unroll
-      for (int s = 0; s < kSegs; ++s) segs[s] = fold_segment(partials, s, bps, e, nent + 1, is_min);
-      acc = fold_segments(segs, 1, 0, is_min);
+      acc = fold_all(partials, bps, e, nent + 1, is_min);
     }
     if (is_min) {
       sh_emin = static_cast<float>(acc);
@@ -459,10 +488,7 @@ __global__ void __launch_bounds__(128) k_metric_reduce(RunDev r, const double *p
       seg_out[static_cast<long long>(s) * nent1 + e] = fold_segment(partials, seg0 + s, bps, e, nent1, is_min);
     return;
   }
-  double segs[kSegs];
-#pragma unroll
-  for (int s = 0; s < kSegs; ++s) segs[s] = fold_segment(partials, s, bps, e, nent1, is_min);
-  sums[e] = fold_segments(segs, 1, 0, is_min);
+  sums[e] = fold_all(partials, bps, e, nent1, is_min);
 }
 
 // Sharded live set: the kSegs segment rows gathered from every rank (rank q's

@@ -263,6 +263,23 @@ def test_full_run_gpu_vs_oracle_c3_reduced(name):
     _vs_oracle(prob, kw, sorted(runs), oracle_runs=runs)
 
 
+@pytest.mark.parametrize("name", ["logreg", "logreg_split", "gp"])
+def test_full_run_gpu_vs_oracle_batch_engines(name):
+    """Full runs through the batch engine's tensor-core logistic regression
+    (fp16-exact and split data, R-28) and the fused fp64 GP chains, against
+    the oracle's full runs with the same seeds (no analytic log Z exists)."""
+    probs = {"logreg": (lambda: W.logreg(5, n_data=300, seed=3), dict(n_live=300, k=30, steps=5)),
+             "logreg_split": (lambda: W.logreg(8, n_data=200, seed=6, half_exact=False), dict(n_live=300, k=30, steps=8)),
+             "gp": (lambda: W.gp_ard(2, 40, seed=3), dict(n_live=200, k=20, steps=4))}
+    make, kw = probs[name]
+    prob = make()
+    from paper_2601_23252_b200 import nss
+    g = nss.Sampler(prob, W.config(seed=1, **kw))
+    assert g.engine() == "batch"
+    g.close()
+    _vs_oracle(prob, kw, range(1, 4))
+
+
 def _funnel_log_z(d, a, sigma_y):
     """P17 (SURVEY C-8): Z = (2a)^-d int_{-a}^{a} N(y; 0, sigma_y^2)
     erf(a / (sqrt 2 e^{y/2}))^(d-1) dy for the funnel under U[-a, a]^d
