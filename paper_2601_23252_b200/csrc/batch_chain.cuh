@@ -43,51 +43,53 @@ __device__ __forceinline__ void store_chain(const BatchDev &b, int c, const Chai
 }
 
 // energy of probe row `row` of the given parity: the slices are loaded by the
-// lanes in parallel and summed by a fixed shuffle tree (deterministic); every
-// lane returns the total
+// lanes of the chain's group in parallel and summed by a fixed shuffle tree
+// (deterministic); every lane returns the total
+template <int W = 32>
 __device__ __forceinline__ float probe_energy(const BatchDev &b, int parity, int row, int lane) {
   if (b.eacc[parity])  // logistic regression: exact softplus sum + theta~ . g, one rounding
     return static_cast<float>(b.eacc[parity][row] + static_cast<double>(b.lin[parity][row]));
   const int ns = b.slices[parity];
   double acc = 0.0;
-  for (int q = lane; q < ns; q += 32) acc += b.partial[parity][static_cast<long long>(q) * b.p_stride + row];
+  for (int q = lane; q < ns; q += W) acc += b.partial[parity][static_cast<long long>(q) * b.p_stride + row];
   if (b.lin[parity] && lane == 0) acc += static_cast<double>(b.lin[parity][row]);  // logistic regression: theta . g
-  return static_cast<float>(warp_sum_d(acc));
+  return static_cast<float>(group_sum<W>(acc));
 }
 
 // What a probe row holds besides its index: for the tensor-core logistic
 // regression the fp16 hi / lo terms of its coordinates (K padded to 128) and
 // the linear term theta~ . g (theta~ = hi + lo, the terms the tensor cores
 // contract, R-28) -- formed while the row ticket is in flight.
+template <int W>
 struct ProbeTerms {
-  __half hi[4], lo[4];
+  __half hi[128 / W], lo[128 / W];
   float lin;
 };
 
-template <int NPL>
+template <int NPL, int W>
 __device__ __forceinline__ void form_terms(const BatchDev &b, int parity, const float (&xp)[NPL], int d, int lane,
-                                           ProbeTerms &pt) {
+                                           ProbeTerms<W> &pt) {
   if (!b.A[parity]) return;
   float lin = 0.f;
 #pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    const int kk = lane + 32 * t;
+  for (int t = 0; t < 128 / W; ++t) {
+    const int kk = lane + W * t;
     const float v = (t < NPL && kk < d) ? xp[t < NPL ? t : 0] : 0.f;
     pt.hi[t] = __float2half_rn(v);
     pt.lo[t] = __float2half_rn(v - __half2float(pt.hi[t]));
     lin = fmaf(__half2float(pt.hi[t]) + __half2float(pt.lo[t]), __ldg(b.g + kk), lin);
   }
-  pt.lin = warp_sum(lin);
+  pt.lin = group_sum<W>(lin);
 }
 
-template <int NPL>
+template <int NPL, int W>
 __device__ __forceinline__ void emit_probe(const BatchDev &b, int parity, int row, const float (&xp)[NPL], int d,
-                                           int lane, const ProbeTerms &pt) {
+                                           int lane, const ProbeTerms<W> &pt) {
   if (b.A[parity]) {  // logistic regression: only the fp16 terms, no fp32 row
     __half *A = b.A[parity];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int kk = lane + 32 * t;
+    for (int t = 0; t < 128 / W; ++t) {
+      const int kk = lane + W * t;
       A[static_cast<long long>(row) * 128 + kk] = pt.hi[t];
       A[(static_cast<long long>(b.p_stride) + row) * 128 + kk] = pt.lo[t];
     }
@@ -100,20 +102,22 @@ __device__ __forceinline__ void emit_probe(const BatchDev &b, int parity, int ro
   float *dst = b.P[parity] + static_cast<long long>(row) * b.dp;
 #pragma unroll
   for (int t = 0; t < NPL; ++t) {
-    const int i = lane + 32 * t;
+    const int i = lane + W * t;
     if (i < d) dst[i] = xp[t];
   }
 }
 
-// One warp advances chain c: fold in the energies of the probes it issued in
-// the previous round (parity ^ 1), run the sequential HRSS state machine until
-// it needs new energies (probes appended to the rows of `parity`) or finishes
-// its p steps; the state lives in the BatchDev arrays between calls.  sZ:
-// NPL * 32 floats of shared memory owned by the warp.
-template <int NPL>
+// A group of W lanes (a warp, or half a warp: two chains per warp when the
+// directions are precomputed) advances chain c: fold in the energies of the
+// probes it issued in the previous round (parity ^ 1), run the sequential HRSS
+// state machine until it needs new energies (probes appended to the rows of
+// `parity`) or finishes its p steps; the state lives in the BatchDev arrays
+// between calls.  sZ: NPL * 32 floats of shared memory owned by the warp
+// (in-chain directions, W = 32 only).
+template <int NPL, int W = 32>
 __device__ __forceinline__ void advance_chain(const RunDev &r, const PriorDev &pr, const BatchDev &b, int parity,
                                               int c, float *sZ) {
-  const int d = r.d, lane = threadIdx.x & 31;
+  const int d = r.d, lane = threadIdx.x & (W - 1);
   const DevState *st = r.st;
   if (st->terminated || st->error || st->finalised) return;  // uniform (written by other kernels)
   ChainRegs s;
@@ -129,8 +133,11 @@ __device__ __forceinline__ void advance_chain(const RunDev &r, const PriorDev &p
   const int nblk_norm = h >> 2, nblk_all = (h + 3) >> 2;
   const int prev = parity ^ 1;
 
-  float pa[NPL], pb[NPL], x[NPL], v[NPL], xp[NPL];
-  load_prior_lane<NPL>(pr, lane, d, pa, pb);
+  // W = 32: the prior's parameters in registers; half-warp groups read them
+  // per test (register budget)
+  constexpr int NPR = W == 32 ? NPL : 1;
+  float pa[NPR], pb[NPR], x[NPL], v[NPL], xp[NPL];
+  if constexpr (W == 32) load_prior_lane<NPL, W>(pr, lane, d, pa, pb);
   // the direction of the current step: from the precomputed directions when
   // there are any (then never stored back), else the chain's saved copy
   const float *vsrc = (r.Vpre && s.phase != kPhDir)
@@ -138,7 +145,7 @@ __device__ __forceinline__ void advance_chain(const RunDev &r, const PriorDev &p
                           : b.v + static_cast<long long>(c) * b.dp;
 #pragma unroll
   for (int t = 0; t < NPL; ++t) {
-    const int i = lane + 32 * t;
+    const int i = lane + W * t;
     x[t] = i < d ? b.x[static_cast<long long>(c) * b.dp + i] : 0.f;
     v[t] = i < d ? vsrc[i] : 0.f;
   }
@@ -151,8 +158,8 @@ __device__ __forceinline__ void advance_chain(const RunDev &r, const PriorDev &p
   }
   // results of the probes this chain issued last round
   float E0 = 0.f, E1 = 0.f;
-  if (s.row0 >= 0) E0 = probe_energy(b, prev, s.row0, lane);
-  if (s.row1 >= 0) E1 = probe_energy(b, prev, s.row1, lane);
+  if (s.row0 >= 0) E0 = probe_energy<W>(b, prev, s.row0, lane);
+  if (s.row1 >= 0) E1 = probe_energy<W>(b, prev, s.row1, lane);
   bool nan_seen = false;
 
   // in-slice test of x + t v against the prior part (support and height);
@@ -161,7 +168,10 @@ __device__ __forceinline__ void advance_chain(const RunDev &r, const PriorDev &p
 #pragma unroll
     for (int q = 0; q < NPL; ++q) xp[q] = fmaf(tt, v[q], x[q]);
     bool inside;
-    lpp = prior_logp<NPL>(xp, pr, pa, pb, lane, d, inside);
+    if constexpr (W == 32)
+      lpp = prior_logp<NPL, W>(xp, pr, pa, pb, lane, d, inside);
+    else
+      lpp = prior_logp_mem<NPL, W>(xp, pr, lane, d, inside);
     return inside && (lpp >= s.log_y);
   };
   auto issue = [&](float tt) -> int {
@@ -169,10 +179,10 @@ __device__ __forceinline__ void advance_chain(const RunDev &r, const PriorDev &p
     if (lane == 0) row = atomicAdd(&b.n_probe[parity], 1);  // in flight while the terms are formed
 #pragma unroll
     for (int q = 0; q < NPL; ++q) xp[q] = fmaf(tt, v[q], x[q]);
-    ProbeTerms pt;
-    form_terms<NPL>(b, parity, xp, d, lane, pt);
-    row = __shfl_sync(kFull, row, 0);
-    emit_probe<NPL>(b, parity, row, xp, d, lane, pt);
+    ProbeTerms<W> pt;
+    form_terms<NPL, W>(b, parity, xp, d, lane, pt);
+    row = __shfl_sync(group_mask<W>(), row, 0, W);
+    emit_probe<NPL, W>(b, parity, row, xp, d, lane, pt);
     return row;
   };
   auto end_step = [&](int accepted) {
@@ -199,10 +209,10 @@ __device__ __forceinline__ void advance_chain(const RunDev &r, const PriorDev &p
         const float *vr = r.Vpre + (static_cast<long long>(c - chain_range(r).x) * p + j) * r.dp;
 #pragma unroll
         for (int t = 0; t < NPL; ++t) {
-          const int i = lane + 32 * t;
+          const int i = lane + W * t;
           v[t] = i < d ? __ldg(vr + i) : 0.f;
         }
-      } else {
+      } else if constexpr (W == 32) {
       // direction v = L z / |z| (R-6), stream (it, dest, HRSS, j)
       for (int bk = lane; bk < nblk_all; bk += 32) {
         const uint4 u4 = philox_block(r, it, dest, kPhaseHrss, j, bk);
@@ -247,6 +257,8 @@ __device__ __forceinline__ void advance_chain(const RunDev &r, const PriorDev &p
 #pragma unroll
       for (int t = 0; t < NPL; ++t) v[t] *= inv;
       __syncwarp();
+      } else {
+        __trap();  // half-warp groups run only with precomputed directions
       }
       const uint4 hb = philox_block(r, it, dest, kPhaseHrss, j, h >> 2);
       s.log_y = s.lp + logf(u01(word(hb, h & 3)));
@@ -350,7 +362,7 @@ __device__ __forceinline__ void advance_chain(const RunDev &r, const PriorDev &p
   // re-read from the precomputed directions
 #pragma unroll
   for (int t = 0; t < NPL; ++t) {
-    const int i = lane + 32 * t;
+    const int i = lane + W * t;
     if (i < d) {
       if (x_dirty) b.x[static_cast<long long>(c) * b.dp + i] = x[t];
       if (!r.Vpre) b.v[static_cast<long long>(c) * b.dp + i] = v[t];

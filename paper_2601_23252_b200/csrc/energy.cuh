@@ -59,13 +59,28 @@ __device__ __forceinline__ float softplusf(float a) {
   return a > 0.f ? a + log1pf(expf(-a)) : log1pf(expf(a));
 }
 
-// Per-lane prior parameters for the coordinates a lane owns.
-template <int NPL>
+// Lane groups of W lanes (W = 32: a warp; 16: half a warp, two groups per
+// warp): the member mask and sums over the group (fixed xor tree).
+template <int W>
+__device__ __forceinline__ unsigned group_mask() {
+  if constexpr (W == 32) return 0xffffffffu;
+  return ((1u << W) - 1u) << (threadIdx.x & 31 & ~(W - 1));
+}
+template <int W, class T>
+__device__ __forceinline__ T group_sum(T v) {
+  const unsigned m = group_mask<W>();
+#pragma unroll
+  for (int o = W / 2; o > 0; o >>= 1) v += __shfl_xor_sync(m, v, o, W);
+  return v;
+}
+
+// Per-lane prior parameters for the coordinates a lane owns (lane of a group of W).
+template <int NPL, int W = 32>
 __device__ __forceinline__ void load_prior_lane(const PriorDev &pr, int lane, int d, float (&pa)[NPL],
                                                 float (&pb)[NPL]) {
 #pragma unroll
   for (int t = 0; t < NPL; ++t) {
-    const int i = lane + 32 * t;
+    const int i = lane + W * t;
     if (pr.kind == NSS_PRIOR_BOX) {
       pa[t] = i < d ? pr.lo[i] : 0.f;
       pb[t] = i < d ? pr.hi[i] : 0.f;
@@ -286,31 +301,62 @@ __device__ __forceinline__ float corr_energy_split(const float (&x)[NPL], const 
   return 0.5f * tot + en.c;
 }
 
-// log Pi(x) and support test (box: all lanes inside; Gaussian: always inside).
-template <int NPL>
+// log Pi(x) and support test (box: all lanes inside; Gaussian: always inside),
+// over the W lanes of the caller's group.
+template <int NPL, int W = 32>
 __device__ __forceinline__ float prior_logp(const float (&x)[NPL], const PriorDev &pr, const float (&pa)[NPL],
                                             const float (&pb)[NPL], int lane, int d, bool &inside) {
   if (pr.kind == NSS_PRIOR_BOX) {
     bool ok = true;
 #pragma unroll
     for (int t = 0; t < NPL; ++t) {
-      const int i = lane + 32 * t;
+      const int i = lane + W * t;
       if (i < d) ok = ok && (x[t] >= pa[t]) && (x[t] <= pb[t]);
     }
-    inside = __all_sync(kFull, ok);
+    const unsigned m = group_mask<W>();
+    inside = (__ballot_sync(m, ok) & m) == m;
     return pr.log_norm;
   }
   float s = 0.f;
 #pragma unroll
   for (int t = 0; t < NPL; ++t) {
-    const int i = lane + 32 * t;
+    const int i = lane + W * t;
     if (i < d) {
       float u = (x[t] - pa[t]) * pb[t];
       s = fmaf(u, u, s);
     }
   }
   inside = true;
-  return -0.5f * warp_sum(s) + pr.log_norm;
+  return -0.5f * group_sum<W>(s) + pr.log_norm;
+}
+
+// prior_logp with the prior's parameters read from memory per call instead
+// of held in registers (the register-tight half-warp advance).
+template <int NPL, int W>
+__device__ __forceinline__ float prior_logp_mem(const float (&x)[NPL], const PriorDev &pr, int lane, int d,
+                                                bool &inside) {
+  if (pr.kind == NSS_PRIOR_BOX) {
+    bool ok = true;
+#pragma unroll
+    for (int t = 0; t < NPL; ++t) {
+      const int i = lane + W * t;
+      if (i < d) ok = ok && (x[t] >= __ldg(pr.lo + i)) && (x[t] <= __ldg(pr.hi + i));
+    }
+    const unsigned m = group_mask<W>();
+    inside = (__ballot_sync(m, ok) & m) == m;
+    return pr.log_norm;
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int t = 0; t < NPL; ++t) {
+    const int i = lane + W * t;
+    if (i < d) {
+      float u = (x[t] - __ldg(pr.mean + i)) * __ldg(pr.isd + i);
+      s = fmaf(u, u, s);
+    }
+  }
+  inside = true;
+  return -0.5f * group_sum<W>(s) + pr.log_norm;
 }
 
 }  // namespace nss

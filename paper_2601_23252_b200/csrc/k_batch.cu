@@ -62,7 +62,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_batch_begin(RunDev r, P
 #define NSS_ADV_MINB 3
 #endif
 
-template <int NPL>
+// W lanes per chain: 32, or 16 (two chains per warp; large d, where the
+// directions are precomputed): twice the chains in flight per SM for this
+// latency-bound state machine.
+template <int NPL, int W>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, NSS_ADV_MINB) k_batch_advance(RunDev r, PriorDev pr, BatchDev b,
                                                                                    int parity) {
   extern __shared__ float sm[];
@@ -70,9 +73,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, NSS_ADV_MINB) k_batch_adv
   pdl_wait();     // the previous energy pass is complete
   const int wib = threadIdx.x >> 5;
   const int2 cr = chain_range(r);
-  const int c = cr.x + blockIdx.x * kWarpsPerBlock + wib;
-  if (c >= cr.y) return;
-  advance_chain<NPL>(r, pr, b, parity, c, sm + wib * (NPL * 32));
+  const int c = cr.x + (blockIdx.x * kWarpsPerBlock * 32 + static_cast<int>(threadIdx.x)) / W;
+  if (c >= cr.y) return;  // uniform per group
+  advance_chain<NPL, W>(r, pr, b, parity, c, sm + wib * (NPL * 32));
 }
 
 // Generic batched energy (warp per probe row) for kinds with a warp energy.
@@ -220,13 +223,13 @@ void begin_t(const RunDev &r, const PriorDev &pr, const BatchDev &b, const Launc
   ++*lc.launch_counter;
 }
 
-template <int NPL>
+template <int NPL, int W>
 void advance_t(const RunDev &r, const PriorDev &pr, const BatchDev &b, int parity, const LaunchCtx &lc) {
-  const size_t smem = static_cast<size_t>(kWarpsPerBlock) * NPL * 32 * sizeof(float);
-  NSS_MAX_SMEM(k_batch_advance<NPL>, 160 * 1024);
-  NSS_PIN_CARVEOUT(k_batch_advance<NPL>);
-  launch_maybe_pdl(k_batch_advance<NPL>, dim3(chain_blocks(r, kWarpsPerBlock)), dim3(kWarpsPerBlock * 32), smem,
-                   lc.stream, r, pr, b, parity);
+  const size_t smem = W == 32 ? static_cast<size_t>(kWarpsPerBlock) * NPL * 32 * sizeof(float) : 0;
+  NSS_MAX_SMEM((k_batch_advance<NPL, W>), 160 * 1024);
+  NSS_PIN_CARVEOUT((k_batch_advance<NPL, W>));
+  launch_maybe_pdl(k_batch_advance<NPL, W>, dim3(chain_blocks(r, kWarpsPerBlock * 32 / W)),
+                   dim3(kWarpsPerBlock * 32), smem, lc.stream, r, pr, b, parity);
   ++*lc.launch_counter;
 }
 
@@ -279,11 +282,23 @@ void batch_begin(const RunDev &r, const PriorDev &pr, const BatchDev &b, const L
 }
 
 void batch_advance(const RunDev &r, const PriorDev &pr, const BatchDev &b, int parity, const LaunchCtx &lc) {
+  static const bool wide = getenv("NSS_ADV_WARP") != nullptr;  // A/B: one chain per warp
+  if (r.Vpre && !wide) {  // two chains per warp
+    switch ((r.d + 15) / 16) {
+      case 3: advance_t<3, 16>(r, pr, b, parity, lc); return;
+      case 4: advance_t<4, 16>(r, pr, b, parity, lc); return;
+      case 5: advance_t<5, 16>(r, pr, b, parity, lc); return;
+      case 6: advance_t<6, 16>(r, pr, b, parity, lc); return;
+      case 7: advance_t<7, 16>(r, pr, b, parity, lc); return;
+      case 8: advance_t<8, 16>(r, pr, b, parity, lc); return;
+      default: break;
+    }
+  }
   switch ((r.d + 31) / 32) {
-    case 1: advance_t<1>(r, pr, b, parity, lc); break;
-    case 2: advance_t<2>(r, pr, b, parity, lc); break;
-    case 3: advance_t<3>(r, pr, b, parity, lc); break;
-    default: advance_t<4>(r, pr, b, parity, lc); break;
+    case 1: advance_t<1, 32>(r, pr, b, parity, lc); break;
+    case 2: advance_t<2, 32>(r, pr, b, parity, lc); break;
+    case 3: advance_t<3, 32>(r, pr, b, parity, lc); break;
+    default: advance_t<4, 32>(r, pr, b, parity, lc); break;
   }
 }
 
