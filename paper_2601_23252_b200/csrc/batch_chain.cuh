@@ -56,45 +56,29 @@ __device__ __forceinline__ float probe_energy(const BatchDev &b, int parity, int
   return static_cast<float>(group_sum<W>(acc));
 }
 
-// What a probe row holds besides its index: for the tensor-core logistic
-// regression the fp16 hi / lo terms of its coordinates (K padded to 128) and
-// the linear term theta~ . g (theta~ = hi + lo, the terms the tensor cores
-// contract, R-28) -- formed while the row ticket is in flight.
-template <int W>
-struct ProbeTerms {
-  __half hi[128 / W], lo[128 / W];
-  float lin;
-};
-
-template <int NPL, int W>
-__device__ __forceinline__ void form_terms(const BatchDev &b, int parity, const float (&xp)[NPL], int d, int lane,
-                                           ProbeTerms<W> &pt) {
-  if (!b.A[parity]) return;
-  float lin = 0.f;
-#pragma unroll
-  for (int t = 0; t < 128 / W; ++t) {
-    const int kk = lane + W * t;
-    const float v = (t < NPL && kk < d) ? xp[t < NPL ? t : 0] : 0.f;
-    pt.hi[t] = __float2half_rn(v);
-    pt.lo[t] = __float2half_rn(v - __half2float(pt.hi[t]));
-    lin = fmaf(__half2float(pt.hi[t]) + __half2float(pt.lo[t]), __ldg(b.g + kk), lin);
-  }
-  pt.lin = group_sum<W>(lin);
-}
-
+// Probe row `row`: for the tensor-core logistic regression only the fp16 hi /
+// lo terms of its coordinates (K padded to 128) and the linear term
+// theta~ . g (theta~ = hi + lo, the terms the tensor cores contract, R-28),
+// no fp32 row; otherwise the fp32 coordinates.
 template <int NPL, int W>
 __device__ __forceinline__ void emit_probe(const BatchDev &b, int parity, int row, const float (&xp)[NPL], int d,
-                                           int lane, const ProbeTerms<W> &pt) {
-  if (b.A[parity]) {  // logistic regression: only the fp16 terms, no fp32 row
+                                           int lane) {
+  if (b.A[parity]) {
     __half *A = b.A[parity];
+    float lin = 0.f;
 #pragma unroll
     for (int t = 0; t < 128 / W; ++t) {
       const int kk = lane + W * t;
-      A[static_cast<long long>(row) * 128 + kk] = pt.hi[t];
-      A[(static_cast<long long>(b.p_stride) + row) * 128 + kk] = pt.lo[t];
+      const float v = (t < NPL && kk < d) ? xp[t < NPL ? t : 0] : 0.f;
+      const __half hi = __float2half_rn(v);
+      const __half lo = __float2half_rn(v - __half2float(hi));
+      A[static_cast<long long>(row) * 128 + kk] = hi;
+      A[(static_cast<long long>(b.p_stride) + row) * 128 + kk] = lo;
+      lin = fmaf(__half2float(hi) + __half2float(lo), __ldg(b.g + kk), lin);
     }
+    lin = group_sum<W>(lin);
     if (lane == 0) {
-      b.lin[parity][row] = pt.lin;
+      b.lin[parity][row] = lin;
       b.eacc[parity][row] = 0.0;  // the energy pass adds the softplus sums
     }
     return;
@@ -150,12 +134,6 @@ __device__ __forceinline__ void advance_chain(const RunDev &r, const PriorDev &p
     v[t] = i < d ? vsrc[i] : 0.f;
   }
   bool x_dirty = false;
-  // the next step's direction towards L2 (it is read when this step ends,
-  // possibly several rounds later)
-  if (r.Vpre && s.step + 1 < p && lane < ((r.dp * 4 + 127) >> 7)) {
-    const float *nv = r.Vpre + (static_cast<long long>(c - chain_range(r).x) * p + s.step + 1) * r.dp + 32 * lane;
-    asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(nv));
-  }
   // results of the probes this chain issued last round
   float E0 = 0.f, E1 = 0.f;
   if (s.row0 >= 0) E0 = probe_energy<W>(b, prev, s.row0, lane);
@@ -176,13 +154,11 @@ __device__ __forceinline__ void advance_chain(const RunDev &r, const PriorDev &p
   };
   auto issue = [&](float tt) -> int {
     int row = 0;
-    if (lane == 0) row = atomicAdd(&b.n_probe[parity], 1);  // in flight while the terms are formed
+    if (lane == 0) row = atomicAdd(&b.n_probe[parity], 1);
+    row = __shfl_sync(group_mask<W>(), row, 0, W);
 #pragma unroll
     for (int q = 0; q < NPL; ++q) xp[q] = fmaf(tt, v[q], x[q]);
-    ProbeTerms<W> pt;
-    form_terms<NPL, W>(b, parity, xp, d, lane, pt);
-    row = __shfl_sync(group_mask<W>(), row, 0, W);
-    emit_probe<NPL, W>(b, parity, row, xp, d, lane, pt);
+    emit_probe<NPL, W>(b, parity, row, xp, d, lane);
     return row;
   };
   auto end_step = [&](int accepted) {

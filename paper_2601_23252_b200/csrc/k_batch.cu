@@ -282,8 +282,11 @@ void batch_begin(const RunDev &r, const PriorDev &pr, const BatchDev &b, const L
 }
 
 void batch_advance(const RunDev &r, const PriorDev &pr, const BatchDev &b, int parity, const LaunchCtx &lc) {
-  static const bool wide = getenv("NSS_ADV_WARP") != nullptr;  // A/B: one chain per warp
-  if (r.Vpre && !wide) {  // two chains per warp
+  // two chains per warp (NSS_ADV_HALF=1): measured slower at C4 (31.1 vs
+  // 26.4 ms per iteration: 480 B of spills at NPL = 7 and the two halves'
+  // divergent state machines serialise), so one chain per warp by default
+  static const bool half = getenv("NSS_ADV_HALF") != nullptr;
+  if (r.Vpre && half) {
     switch ((r.d + 15) / 16) {
       case 3: advance_t<3, 16>(r, pr, b, parity, lc); return;
       case 4: advance_t<4, 16>(r, pr, b, parity, lc); return;
