@@ -226,9 +226,17 @@ __global__ void __launch_bounds__(256) k_hrss(RunDev r, PriorDev pr, EnergyDev e
 }
 
 // Directions of every (chain, step) of the iteration at once (large d): the
-// same draws and arithmetic as the in-chain direction of k_hrss, one warp per
-// (chain, step) over the whole GPU instead of serially inside each chain:
-// V[(c - c0) p + j] = L z / |z| (Mahalanobis) or L z / |L z|.
+// same draws and arithmetic as the in-chain direction of k_hrss (identical
+// bits: L is lower triangular with exact zeros above the diagonal, so the
+// extra terms of the full-row loop add +-0), over the whole GPU instead of
+// serially inside each chain: V[(c - c0) p + j] = L z / |z| (Mahalanobis) or
+// L z / |L z|.  Persistent grid: every CTA stages L in shared memory once and
+// its warps loop over groups of NB directions; per column m one L element per
+// row and one NB-wide vector of normals feed NB FMAs, so a warp reads L once
+// per NB directions (the shared-memory pipe, not the FMA pipe, bound the
+// one-direction-per-warp version).
+constexpr int kDirNB = 4;
+
 template <int NPL>
 __global__ void __launch_bounds__(256) k_dirs(RunDev r, float *V) {
   extern __shared__ float sm[];
@@ -236,7 +244,7 @@ __global__ void __launch_bounds__(256) k_dirs(RunDev r, float *V) {
   const int d = r.d, lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
   const int ldl = odd_stride(d);
   float *sL = sm;
-  float *sZ = sL + d * ldl + wib * (NPL * 32);
+  float *sZ = sm + ((d * ldl + 3) & ~3) + wib * (d * kDirNB);  // [m][k], 16-byte aligned
   if (threadIdx.x == 0) sh_flag = (r.st->terminated || r.st->error || r.st->finalised) ? 1 : 0;
   for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
     int i = e / d, j = e - i * d;
@@ -244,52 +252,99 @@ __global__ void __launch_bounds__(256) k_dirs(RunDev r, float *V) {
   }
   __syncthreads();
   if (sh_flag) return;
-  const long long q = static_cast<long long>(blockIdx.x) * wpb + wib;  // (c - c0) * p + j
   const int p = r.p;
   const int2 cr = chain_range(r);
-  if (q >= static_cast<long long>(cr.y - cr.x) * p) return;
-  const int c = cr.x + static_cast<int>(q / p), j = static_cast<int>(q % p);
+  const long long work = static_cast<long long>(cr.y - cr.x) * p;
   const uint32_t it = static_cast<uint32_t>(r.st->iter);
-  const int s = r.cdest[c];
   const bool euclid = r.dir_norm == NSS_DIR_EUCLIDEAN;
   const int h = 2 * ((d + 1) / 2);
   const int nblk_norm = h >> 2, nblk_all = (h + 3) >> 2;
-  for (int b = lane; b < nblk_all; b += 32) {
-    uint4 u4 = philox_block(r, it, s, kPhaseHrss, j, b);
-    float u0 = u01(u4.x), u1 = u01(u4.y), u2 = u01(u4.z), u3 = u01(u4.w);
-    float r0 = sqrtf(-2.f * logf(u0)), r1 = sqrtf(-2.f * logf(u2));
-    float s0, c0, s1, c1;
-    sincospif(2.f * u1, &s0, &c0);
-    sincospif(2.f * u3, &s1, &c1);
-    const int i0 = 4 * b;
-    if (i0 < d) sZ[i0] = r0 * c0;
-    if (i0 + 1 < d) sZ[i0 + 1] = r0 * s0;
-    if (b < nblk_norm) {
-      if (i0 + 2 < d) sZ[i0 + 2] = r1 * c1;
-      if (i0 + 3 < d) sZ[i0 + 3] = r1 * s1;
-    }
-  }
-  __syncwarp();
-  float v[NPL], zz = 0.f, vv = 0.f;
+  const long long groups = (work + kDirNB - 1) / kDirNB;
+  for (long long g = static_cast<long long>(blockIdx.x) * wpb + wib; g < groups;
+       g += static_cast<long long>(gridDim.x) * wpb) {
+    // the normals of the group's directions: stream (it, dest, HRSS, j)
 #pragma unroll
-  for (int t = 0; t < NPL; ++t) {
-    const int i = lane + 32 * t;
-    float acc = 0.f;
-    if (i < d) {
-      const float zi = sZ[i];
-      zz = fmaf(zi, zi, zz);
-      const float *row = sL + i * ldl;
-      for (int m = 0; m <= i; ++m) acc = fmaf(row[m], sZ[m], acc);
+    for (int k = 0; k < kDirNB; ++k) {
+      const long long q = g * kDirNB + k;  // (c - c0) p + j
+      const bool real = q < work;
+      const int c = cr.x + static_cast<int>(real ? q / p : 0), j = static_cast<int>(real ? q % p : 0);
+      const int s = r.cdest[c];
+      for (int b = lane; b < nblk_all; b += 32) {
+        float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
+        if (real) {
+          uint4 u4 = philox_block(r, it, s, kPhaseHrss, j, b);
+          float u0 = u01(u4.x), u1 = u01(u4.y), u2 = u01(u4.z), u3 = u01(u4.w);
+          float r0 = sqrtf(-2.f * logf(u0)), r1 = sqrtf(-2.f * logf(u2));
+          float s0, c0, s1, c1;
+          sincospif(2.f * u1, &s0, &c0);
+          sincospif(2.f * u3, &s1, &c1);
+          z0 = r0 * c0;
+          z1 = r0 * s0;
+          z2 = r1 * c1;
+          z3 = r1 * s1;
+        }
+        const int i0 = 4 * b;
+        if (i0 < d) sZ[i0 * kDirNB + k] = z0;
+        if (i0 + 1 < d) sZ[(i0 + 1) * kDirNB + k] = z1;
+        if (b < nblk_norm) {
+          if (i0 + 2 < d) sZ[(i0 + 2) * kDirNB + k] = z2;
+          if (i0 + 3 < d) sZ[(i0 + 3) * kDirNB + k] = z3;
+        }
+      }
     }
-    v[t] = acc;
-    vv = fmaf(acc, acc, vv);
-  }
-  const float inv = 1.f / sqrtf(warp_sum(euclid ? vv : zz));
-  float *out = V + q * r.dp;
+    __syncwarp();
+    // v_k = L z_k: rows lane + 32 t; row block t reaches column 32 t + 31 at most
+    float acc[NPL][kDirNB];
 #pragma unroll
-  for (int t = 0; t < NPL; ++t) {
-    const int i = lane + 32 * t;
-    if (i < d) out[i] = v[t] * inv;
+    for (int t = 0; t < NPL; ++t)
+#pragma unroll
+      for (int k = 0; k < kDirNB; ++k) acc[t][k] = 0.f;
+#pragma unroll
+    for (int t = 0; t < NPL; ++t) {
+      const int i = lane + 32 * t;
+      const float *row = sL + (i < d ? i : 0) * ldl;
+      const int mend = min(d, 32 * t + 32);
+      for (int m = 0; m < mend; ++m) {
+        const float4 z4 = *reinterpret_cast<const float4 *>(sZ + m * kDirNB);
+        const float lm = row[m];
+        acc[t][0] = fmaf(lm, z4.x, acc[t][0]);
+        acc[t][1] = fmaf(lm, z4.y, acc[t][1]);
+        acc[t][2] = fmaf(lm, z4.z, acc[t][2]);
+        acc[t][3] = fmaf(lm, z4.w, acc[t][3]);
+      }
+    }
+    float zz[kDirNB], vv[kDirNB];
+#pragma unroll
+    for (int k = 0; k < kDirNB; ++k) {
+      zz[k] = 0.f;
+      vv[k] = 0.f;
+    }
+#pragma unroll
+    for (int t = 0; t < NPL; ++t) {
+      const int i = lane + 32 * t;
+      if (i < d) {
+#pragma unroll
+        for (int k = 0; k < kDirNB; ++k) {
+          const float zi = sZ[i * kDirNB + k];
+          zz[k] = fmaf(zi, zi, zz[k]);
+          vv[k] = fmaf(acc[t][k], acc[t][k], vv[k]);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kDirNB; ++k) {
+      const long long q = g * kDirNB + k;
+      const float inv = 1.f / sqrtf(warp_sum(euclid ? vv[k] : zz[k]));
+      if (q < work) {
+        float *out = V + q * r.dp;
+#pragma unroll
+        for (int t = 0; t < NPL; ++t) {
+          const int i = lane + 32 * t;
+          if (i < d) out[i] = acc[t][k] * inv;
+        }
+      }
+    }
+    __syncwarp();  // sZ is rewritten by the next group
   }
 }
 
@@ -298,10 +353,15 @@ void launch_dirs_t(const RunDev &r, float *V, const LaunchCtx &lc) {
   const long long work = static_cast<long long>(r.c1 - r.c0) * r.p;
   if (work <= 0) return;
   const int wpb = 8;
-  const size_t smem = (static_cast<size_t>(r.d) * odd_stride(r.d) + static_cast<size_t>(wpb) * NPL * 32) * sizeof(float);
+  const size_t smem = (static_cast<size_t>((r.d * odd_stride(r.d) + 3) & ~3) +
+                       static_cast<size_t>(wpb) * r.d * kDirNB) * sizeof(float);
   if (smem > 48 * 1024) NSS_MAX_SMEM(k_dirs<NPL>, smem);
   NSS_PIN_CARVEOUT(k_dirs<NPL>);
-  k_dirs<NPL><<<static_cast<int>((work + wpb - 1) / wpb), wpb * 32, smem, lc.stream>>>(r, V);
+  // persistent: a few CTAs per SM (L staged once per CTA), no more than the work
+  const long long groups = (work + kDirNB - 1) / kDirNB;
+  const long long want = (groups + wpb - 1) / wpb;
+  const int grid = static_cast<int>(want < 148 * 4 ? want : 148 * 4);
+  k_dirs<NPL><<<grid, wpb * 32, smem, lc.stream>>>(r, V);
   ++*lc.launch_counter;
 }
 
@@ -599,6 +659,10 @@ void launch_hrss(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const
     return;
   }
   launch_dirs(r, lc);  // large d: all directions of the iteration first (k_dirs)
+  if (multi_engine_ok(r, en)) {
+    launch_hrss_multi(r, pr, en, lc);
+    return;
+  }
   NSS_DISPATCH(launch_hrss_t, r, pr, en, lc);
 }
 

@@ -311,6 +311,9 @@ void launch_init(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const
 size_t energy_smem_bytes(const EnergyDev &en);
 bool energy_supported(const EnergyDev &en);
 int hrss_engine(const RunDev &r, const EnergyDev &en);  // 0 warp-cooperative, 1 one probe per lane
+// k_hrss_multi.cu: several chains per warp sharing the factor's loads (correlated Gaussian, large d)
+bool multi_engine_ok(const RunDev &r, const EnergyDev &en);
+void launch_hrss_multi(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc);
 // k_hrss_lane.cu
 bool lane_engine_ok(const RunDev &r, const EnergyDev &en);
 void launch_hrss_lane(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc);
