@@ -663,6 +663,10 @@ void launch_hrss(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const
     launch_hrss_multi(r, pr, en, lc);
     return;
   }
+  if (group_engine_ok(r, en)) {
+    launch_hrss_group(r, pr, en, lc);
+    return;
+  }
   NSS_DISPATCH(launch_hrss_t, r, pr, en, lc);
 }
 

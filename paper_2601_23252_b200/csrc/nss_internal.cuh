@@ -314,6 +314,9 @@ int hrss_engine(const RunDev &r, const EnergyDev &en);  // 0 warp-cooperative, 1
 // k_hrss_multi.cu: several chains per warp sharing the factor's loads (correlated Gaussian, large d)
 bool multi_engine_ok(const RunDev &r, const EnergyDev &en);
 void launch_hrss_multi(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc);
+// k_hrss_group.cu: four speculative probes per warp in groups of 8 lanes (cheap energies, large d)
+bool group_engine_ok(const RunDev &r, const EnergyDev &en);
+void launch_hrss_group(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc);
 // k_hrss_lane.cu
 bool lane_engine_ok(const RunDev &r, const EnergyDev &en);
 void launch_hrss_lane(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc);
