@@ -307,11 +307,14 @@ void launch_group_kind(const RunDev &r, const PriorDev &pr, const EnergyDev &en,
 
 }  // namespace
 
-// Cheap energies at large d with precomputed directions, standard NS
-// (NSS_NO_GROUP=1 keeps the warp engine).
+// Cheap energies at large d with precomputed directions, standard NS.
+// Opt-in (NSS_GROUP=1): at C3b it is parity-green but slower than the warp
+// engine (1.93 vs 1.40 ms per iteration): fewer dependent rounds per step,
+// but each costs more (13 coordinates per lane, 125 registers, the shrink
+// round's four Philox blocks).
 bool group_engine_ok(const RunDev &r, const EnergyDev &en) {
-  static const bool off = getenv("NSS_NO_GROUP") != nullptr;
-  return !off && (en.kind == NSS_E_FUNNEL || en.kind == NSS_E_GAUSS) && r.d > 32 && r.Vpre && !r.tempered &&
+  static const bool on = getenv("NSS_GROUP") != nullptr;
+  return on && (en.kind == NSS_E_FUNNEL || en.kind == NSS_E_GAUSS) && r.d > 32 && r.Vpre && !r.tempered &&
          r.mutation == NSS_MUT_HRSS;
 }
 
