@@ -12,6 +12,8 @@
 // the same round (two probes) without evaluating anything the sequential
 // algorithm would not.
 #pragma once
+#include <type_traits>
+
 #include "batch.cuh"
 #include "energy.cuh"
 
@@ -98,15 +100,30 @@ __device__ __forceinline__ void emit_probe(const BatchDev &b, int parity, int ro
 // `parity`) or finishes its p steps; the state lives in the BatchDev arrays
 // between calls.  sZ: NPL * 32 floats of shared memory owned by the warp
 // (in-chain directions, W = 32 only).
-template <int NPL, int W = 32>
+//
+// Row tickets: with a `ticket` functor (the round-synchronous advance kernel)
+// the chain first runs its state machine recording the probe parameters, then
+// calls ticket(n) exactly once -- every warp of the block does, even with
+// n = 0 -- which hands out n consecutive rows with ONE atomic per block (the
+// round's 10^4 same-address atomics serialised at the L2); without one (the
+// fused GP kernel) every probe takes its row with its own atomic.
+struct NoTicket {
+  __device__ int operator()(int) const { return 0; }
+};
+
+template <int NPL, int W = 32, class Ticket = NoTicket>
 __device__ __forceinline__ void advance_chain(const RunDev &r, const PriorDev &pr, const BatchDev &b, int parity,
-                                              int c, float *sZ) {
+                                              int c, float *sZ, Ticket ticket = Ticket{}) {
+  constexpr bool kDefer = !std::is_same<Ticket, NoTicket>::value;
   const int d = r.d, lane = threadIdx.x & (W - 1);
   const DevState *st = r.st;
   if (st->terminated || st->error || st->finalised) return;  // uniform (written by other kernels)
   ChainRegs s;
   load_chain(b, c, s);
-  if (s.phase == kPhDone) return;
+  if (s.phase == kPhDone) {
+    if constexpr (kDefer) (void)ticket(0);
+    return;
+  }
 
   const uint32_t it = static_cast<uint32_t>(st->iter)  /* set by the select kernel */;
   const int dest = r.cdest[c];
@@ -152,7 +169,13 @@ __device__ __forceinline__ void advance_chain(const RunDev &r, const PriorDev &p
       lpp = prior_logp_mem<NPL, W>(xp, pr, lane, d, inside);
     return inside && (lpp >= s.log_y);
   };
+  float pend_t[2];
+  int npend = 0;
   auto issue = [&](float tt) -> int {
+    if constexpr (kDefer) {  // row after the block's ticket; placeholder -2 - k
+      pend_t[npend] = tt;
+      return -2 - npend++;
+    }
     int row = 0;
     if (lane == 0) row = atomicAdd(&b.n_probe[parity], 1);
     row = __shfl_sync(group_mask<W>(), row, 0, W);
@@ -283,7 +306,7 @@ __device__ __forceinline__ void advance_chain(const RunDev &r, const PriorDev &p
         s.lp1 = lpp;
         break;
       }
-      if (s.row0 >= 0 || s.row1 >= 0) {
+      if (s.row0 != -1 || s.row1 != -1) {
         wait = true;
         break;
       }
@@ -334,6 +357,18 @@ __device__ __forceinline__ void advance_chain(const RunDev &r, const PriorDev &p
     end_step(0);  // shrink cap reached: null move
   }
 
+  if constexpr (kDefer) {
+    // the block's rows, then the recorded probes (the same fp32 points)
+    const int base = ticket(npend);
+    for (int k = 0; k < npend; ++k) {
+      const float tt = pend_t[k == 0 ? 0 : 1];
+#pragma unroll
+      for (int q = 0; q < NPL; ++q) xp[q] = fmaf(tt, v[q], x[q]);
+      emit_probe<NPL, W>(b, parity, base + k, xp, d, lane);
+    }
+    if (s.row0 <= -2) s.row0 = base + (-2 - s.row0);
+    if (s.row1 <= -2) s.row1 = base + (-2 - s.row1);
+  }
   // write back only what changed: x after an accepted step, v when it is not
   // re-read from the precomputed directions
 #pragma unroll

@@ -74,8 +74,32 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, NSS_ADV_MINB) k_batch_adv
   const int wib = threadIdx.x >> 5;
   const int2 cr = chain_range(r);
   const int c = cr.x + (blockIdx.x * kWarpsPerBlock * 32 + static_cast<int>(threadIdx.x)) / W;
-  if (c >= cr.y) return;  // uniform per group
-  advance_chain<NPL, W>(r, pr, b, parity, c, sm + wib * (NPL * 32));
+  if constexpr (W == 32) {
+    // one row ticket per block: every warp reports its probe count once
+    __shared__ int sh_cnt[kWarpsPerBlock], sh_base;
+    auto ticket = [&](int np) -> int {
+      if ((threadIdx.x & 31) == 0) sh_cnt[wib] = np;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int tot = 0;
+        for (int q = 0; q < kWarpsPerBlock; ++q) tot += sh_cnt[q];
+        sh_base = tot ? atomicAdd(&b.n_probe[parity], tot) : 0;
+      }
+      __syncthreads();
+      int off = sh_base;
+      for (int q = 0; q < wib; ++q) off += sh_cnt[q];
+      return off;
+    };
+    if (r.st->terminated || r.st->error || r.st->finalised) return;  // uniform: no ticket at all
+    if (c >= cr.y) {
+      (void)ticket(0);
+      return;
+    }
+    advance_chain<NPL, W>(r, pr, b, parity, c, sm + wib * (NPL * 32), ticket);
+  } else {
+    if (c >= cr.y) return;  // uniform per group
+    advance_chain<NPL, W>(r, pr, b, parity, c, sm + wib * (NPL * 32));
+  }
 }
 
 // Generic batched energy (warp per probe row) for kinds with a warp energy.
