@@ -235,7 +235,10 @@ __global__ void __launch_bounds__(256) k_hrss(RunDev r, PriorDev pr, EnergyDev e
 // row and one NB-wide vector of normals feed NB FMAs, so a warp reads L once
 // per NB directions (the shared-memory pipe, not the FMA pipe, bound the
 // one-direction-per-warp version).
-constexpr int kDirNB = 4;
+#ifndef NSS_DIR_NB
+#define NSS_DIR_NB 8
+#endif
+constexpr int kDirNB = NSS_DIR_NB;  // directions per warp pass (4 or 8)
 
 template <int NPL>
 __global__ void __launch_bounds__(256) k_dirs(RunDev r, float *V) {
@@ -305,12 +308,15 @@ __global__ void __launch_bounds__(256) k_dirs(RunDev r, float *V) {
       const float *row = sL + (i < d ? i : 0) * ldl;
       const int mend = min(d, 32 * t + 32);
       for (int m = 0; m < mend; ++m) {
-        const float4 z4 = *reinterpret_cast<const float4 *>(sZ + m * kDirNB);
         const float lm = row[m];
-        acc[t][0] = fmaf(lm, z4.x, acc[t][0]);
-        acc[t][1] = fmaf(lm, z4.y, acc[t][1]);
-        acc[t][2] = fmaf(lm, z4.z, acc[t][2]);
-        acc[t][3] = fmaf(lm, z4.w, acc[t][3]);
+#pragma unroll
+        for (int k4 = 0; k4 < kDirNB; k4 += 4) {
+          const float4 z4 = *reinterpret_cast<const float4 *>(sZ + m * kDirNB + k4);
+          acc[t][k4 + 0] = fmaf(lm, z4.x, acc[t][k4 + 0]);
+          acc[t][k4 + 1] = fmaf(lm, z4.y, acc[t][k4 + 1]);
+          acc[t][k4 + 2] = fmaf(lm, z4.z, acc[t][k4 + 2]);
+          acc[t][k4 + 3] = fmaf(lm, z4.w, acc[t][k4 + 3]);
+        }
       }
     }
     float zz[kDirNB], vv[kDirNB];
@@ -357,10 +363,18 @@ void launch_dirs_t(const RunDev &r, float *V, const LaunchCtx &lc) {
                        static_cast<size_t>(wpb) * r.d * kDirNB) * sizeof(float);
   if (smem > 48 * 1024) NSS_MAX_SMEM(k_dirs<NPL>, smem);
   NSS_PIN_CARVEOUT(k_dirs<NPL>);
-  // persistent: a few CTAs per SM (L staged once per CTA), no more than the work
+  // persistent: the CTAs that fit at once (L staged once per CTA), no more than the work
+  static int per_sm[64] = {};
+  const int dv = current_device();
+  if (!per_sm[dv]) {
+    int nb = 0, sms = 148;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_dirs<NPL>, wpb * 32, smem);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dv);
+    per_sm[dv] = (nb > 0 ? nb : 1) * sms;
+  }
   const long long groups = (work + kDirNB - 1) / kDirNB;
   const long long want = (groups + wpb - 1) / wpb;
-  const int grid = static_cast<int>(want < 148 * 4 ? want : 148 * 4);
+  const int grid = static_cast<int>(want < per_sm[dv] ? want : per_sm[dv]);
   k_dirs<NPL><<<grid, wpb * 32, smem, lc.stream>>>(r, V);
   ++*lc.launch_counter;
 }
