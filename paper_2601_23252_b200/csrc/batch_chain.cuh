@@ -144,11 +144,18 @@ __device__ __forceinline__ void advance_chain(const RunDev &r, const PriorDev &p
   const float *vsrc = (r.Vpre && s.phase != kPhDir)
                           ? r.Vpre + (static_cast<long long>(c - chain_range(r).x) * p + s.step) * r.dp
                           : b.v + static_cast<long long>(c) * b.dp;
+  // ... and the direction of the next step, loaded with the rest so a step
+  // ending in this call does not wait for it
+  const int jn = s.phase == kPhDir ? s.step : s.step + 1;
+  const bool have_next = r.Vpre && jn < p;
+  const float *vnsrc = r.Vpre + (static_cast<long long>(c - chain_range(r).x) * p + (have_next ? jn : 0)) * r.dp;
+  float vn[NPL];
 #pragma unroll
   for (int t = 0; t < NPL; ++t) {
     const int i = lane + W * t;
     x[t] = i < d ? b.x[static_cast<long long>(c) * b.dp + i] : 0.f;
     v[t] = i < d ? vsrc[i] : 0.f;
+    vn[t] = (have_next && i < d) ? __ldg(vnsrc + i) : 0.f;
   }
   bool x_dirty = false;
   // results of the probes this chain issued last round
@@ -204,7 +211,10 @@ __device__ __forceinline__ void advance_chain(const RunDev &r, const PriorDev &p
         break;
       }
       const int j = s.step;
-      if (r.Vpre) {  // precomputed for this (chain, step) by k_dirs (bit-identical)
+      if (r.Vpre && have_next && j == jn) {  // prefetched with the state
+#pragma unroll
+        for (int t = 0; t < NPL; ++t) v[t] = vn[t];
+      } else if (r.Vpre) {  // precomputed for this (chain, step) by k_dirs (bit-identical)
         const float *vr = r.Vpre + (static_cast<long long>(c - chain_range(r).x) * p + j) * r.dp;
 #pragma unroll
         for (int t = 0; t < NPL; ++t) {
