@@ -145,6 +145,53 @@ __device__ __forceinline__ void mma_rows(const double *Ta, const double *Tb, int
   }
 }
 
+// [K; y^T](i', j) for every row block i' below the diagonal block of column
+// block j, by warps 1-7 while warp 0 factorises that block: the entries are
+// written to the chunk slots L(i', j) will take (row-major, stride LDC), whence
+// the combine step reads them.  Same arithmetic, in the same order, as the
+// on-the-fly generation of the diagonal tile.  The column inputs (scaled by
+// 1/l) are staged in `stage` (free while the diagonal block is factorised)
+// when they fit.
+__device__ __forceinline__ void gen_k_below(const GpDev &g, int j, int kb, const double *par, double *Ls,
+                                            double *stage) {
+  const int N = g.N, D = g.D, j0 = j * PB, lane = threadIdx.x & 31, w = (threadIdx.x >> 5) - 1;
+  constexpr int kGen = kThreads - 32, kGenWarps = kGen / 32;
+  const bool staged = PB * D <= 2 * CT;
+  if (staged) {
+    for (int e = threadIdx.x - 32; e < PB * D; e += kGen) {
+      const int dd = e / PB, c = e - dd * PB;
+      stage[e] = c < kb ? __ldg(g.X + (j0 + c) * D + dd) * par[dd] : 0.0;
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(kGen) : "memory");
+  }
+  const double sf2 = par[D];
+  const int c0 = lane, c1 = lane + 32;
+  for (int row = j0 + PB + w; row <= N; row += kGenWarps) {
+    const int ib = row / PB, r = row - ib * PB;
+    double *o = Ls + (static_cast<long long>(ib) * g.nkc + 2 * j) * CT + r * LDC + lane;
+    double v0, v1;
+    if (row == N) {
+      v0 = c0 < kb ? __ldg(g.y + j0 + c0) : 0.0;
+      v1 = c1 < kb ? __ldg(g.y + j0 + c1) : 0.0;
+    } else {
+      double s0 = 0.0, s1 = 0.0;
+      for (int dd = 0; dd < D; ++dd) {
+        const double il = par[dd];
+        const double xr = __ldg(g.X + row * D + dd) * il;
+        const double xc0 = staged ? stage[dd * PB + c0] : (c0 < kb ? __ldg(g.X + (j0 + c0) * D + dd) * il : 0.0);
+        const double xc1 = staged ? stage[dd * PB + c1] : (c1 < kb ? __ldg(g.X + (j0 + c1) * D + dd) * il : 0.0);
+        const double t0 = xr - xc0, t1 = xr - xc1;
+        s0 = fma(t0, t0, s0);
+        s1 = fma(t1, t1, s1);
+      }
+      v0 = sf2 * exp(-0.5 * s0);
+      v1 = sf2 * exp(-0.5 * s1);
+    }
+    if (c0 < kb) o[0] = v0;
+    if (c1 < kb) o[CT] = v1;
+  }
+}
+
 // Left-looking blocked Cholesky of the (N+1) x N lower trapezoid [K; y^T]
 // (its last row becomes alpha^T = (L^-1 y)^T).  For each 64-wide column
 // block j and each row block i >= j, the 64 x 64 tile
@@ -231,38 +278,56 @@ __device__ __forceinline__ double gp_matrix(const GpDev &g, const float *phi, do
         for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
           for (int q = 0; q < 4; ++q) s[mi][q] = 0.0;
-        for (int dd = 0; dd < D; ++dd) {
-          const double il = sh_par[dd];
-          double xr[4], xc[4];
+        if (!dt) {
+          // generated during the diagonal factorisation (gen_k_below)
+          const double *Ko = Ls + (static_cast<long long>(i) * nkc + 2 * j) * CT;
 #pragma unroll
-          for (int mi = 0; mi < 4; ++mi) xr[mi] = gr[mi] < N ? __ldg(g.X + gr[mi] * D + dd) * il : 0.0;
+          for (int ni = 0; ni < 2; ++ni) {
+            const int cc = n_base + 8 * ni + 2 * tq;
+            const double *o = Ko + (cc >> 5) * CT + (cc & 31);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) xc[q] = gc[q] < N ? __ldg(g.X + gc[q] * D + dd) * il : 0.0;
+            for (int mi = 0; mi < 4; ++mi) {
+              const int r = m_base + 8 * mi + gq;
+              const bool in = i0 + r <= N;
+              const double2 kv = in ? *reinterpret_cast<const double2 *>(o + r * LDC) : make_double2(0.0, 0.0);
+              T[r * LDR + cc] = in && cc < kb ? kv.x - acc[mi][ni][0] : 0.0;
+              T[r * LDR + cc + 1] = in && cc + 1 < kb ? kv.y - acc[mi][ni][1] : 0.0;
+            }
+          }
+        } else {  // the diagonal tile: generated here
+          for (int dd = 0; dd < D; ++dd) {
+            const double il = sh_par[dd];
+            double xr[4], xc[4];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) xr[mi] = gr[mi] < N ? __ldg(g.X + gr[mi] * D + dd) * il : 0.0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) xc[q] = gc[q] < N ? __ldg(g.X + gc[q] * D + dd) * il : 0.0;
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const double t = xr[mi] - xc[q];
+                s[mi][q] = fma(t, t, s[mi][q]);
+              }
+          }
 #pragma unroll
           for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              const double t = xr[mi] - xc[q];
-              s[mi][q] = fma(t, t, s[mi][q]);
+              const int r = gr[mi] - i0, c = gc[q] - j0;
+              const bool ok = gr[mi] <= N && c < kb && (c <= r || gr[mi] >= j0 + kb);
+              double v = 0.0;
+              if (ok) {
+                const double kv = gr[mi] == N ? __ldg(g.y + gc[q])
+                                              : sf2 * exp(-0.5 * s[mi][q]) + (gr[mi] == gc[q] ? diag_add : 0.0);
+                v = kv - acc[mi][q >> 1][q & 1];
+              }
+              if (r < kb)
+                F[r * LDF + c] = v;  // the block to factorise
+              else
+                T[r * LDR + c] = v;
             }
         }
-#pragma unroll
-        for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int r = gr[mi] - i0, c = gc[q] - j0;
-            const bool ok = gr[mi] <= N && c < kb && (!dt || c <= r || gr[mi] >= j0 + kb);
-            double v = 0.0;
-            if (ok) {
-              const double kv = gr[mi] == N ? __ldg(g.y + gc[q])
-                                            : sf2 * exp(-0.5 * s[mi][q]) + (gr[mi] == gc[q] ? diag_add : 0.0);
-              v = kv - acc[mi][q >> 1][q & 1];
-            }
-            if (dt && r < kb)
-              F[r * LDF + c] = v;  // the block to factorise
-            else
-              T[r * LDR + c] = v;
-          }
       }
       __syncthreads();
       GP_PHASE(1);
@@ -279,7 +344,11 @@ __device__ __forceinline__ double gp_matrix(const GpDev &g, const float *phi, do
         //      busy meanwhile ----
         for (int e = tid; e < PB * PB; e += kThreads) W[(e / PB) * LDR + (e % PB)] = 0.0;
         __syncthreads();
-        if (wid == 0) {
+        if (wid != 0) {
+          // warps 1-7 meanwhile: [K; y^T](i', j) of every tile below, into
+          // the slots L(i', j) will take (read back by the combine step)
+          gen_k_below(g, j, kb, sh_par, Ls, Ci);
+        } else {
           bool bad = false;
           double *w0p = W + lane, *w1p = W + lane + 32;
           for (int jj = 0; jj < kb; ++jj) {
