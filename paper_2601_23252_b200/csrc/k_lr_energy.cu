@@ -29,7 +29,9 @@
 // totals stay below 2^28, so each fp64 addition is exact: the energies do not
 // depend on the order of the additions, on the ranges, or on P -- a probe's
 // energy is the same bits in any batch (the sharded runs rely on this).
+#include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "nss_internal.cuh"
 #include "tc_ptx.cuh"
@@ -83,6 +85,15 @@ struct LrCfg {
   static constexpr int kPartCols = BN_ / kColParts;           // columns per epilogue part
   static constexpr int kChunks = kPartCols / 32;              // tcgen05.ld.32x32b.x32 per part
 };
+
+#ifdef NSS_LR_PROF
+// measurement builds (NSS_NVCC_EXTRA=-DNSS_LR_PROF): SM clocks summed over
+// CTAs {MMA waits on X tiles, MMA waits on a free accumulator, MMA waits on
+// the probe tile, epilogue waits on a full accumulator (sum over warps),
+// epilogue busy (sum over warps), CTA span after the dependency wait,
+// prologue up to it, tile pairs}
+__device__ unsigned long long *g_lr_prof;
+#endif
 
 struct __align__(8) Bars {
   uint64_t a_full, a_empty;
@@ -143,7 +154,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
+#ifdef NSS_LR_PROF
+  const long long t_pro = clock64();
+#endif
   pdl_wait();  // the probe rows and their count are complete from here
+#ifdef NSS_LR_PROF
+  const long long t_start = clock64();
+  unsigned long long pw[3] = {0, 0, 0};
+#endif
   pdl_trigger();
   const int n_probe = *n_probe_ptr;
   const Sched sch(n_probe, n_tiles);
@@ -188,15 +206,31 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int m = u / n_tiles;
       if (m != prev_m) {
         if (a_loads > 0) tc::umma_commit(&bars->a_empty);  // every MMA on the old probe tile issued
+#ifdef NSS_LR_PROF
+        const long long ta = clock64();
+#endif
         tc::mbar_wait(&bars->a_full, a_loads & 1);
+#ifdef NSS_LR_PROF
+        pw[2] += clock64() - ta;
+#endif
         tc::tc_fence_after();
         ++a_loads;
         prev_m = m;
       }
       {
         const int st = it % kStages, acc = it % kAcc;
+#ifdef NSS_LR_PROF
+        const long long t0 = clock64();
+#endif
         if (it >= kAcc) tc::mbar_wait(&bars->tempty[acc], ((it / kAcc) - 1) & 1);
+#ifdef NSS_LR_PROF
+        const long long t1 = clock64();
+        pw[1] += t1 - t0;
+#endif
         tc::mbar_wait(&bars->full[st], (it / kStages) & 1);
+#ifdef NSS_LR_PROF
+        pw[0] += clock64() - t1;
+#endif
         tc::tc_fence_after();
         const uint32_t d_tmem = tmem + acc * BN;
         // (A term, X term) products: hi.Xhi, lo.Xhi (+ hi.Xlo when X is split)
@@ -225,7 +259,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int m = u / n_tiles, t = u - m * n_tiles;
       {
         const int acc = it % kAcc;
+#ifdef NSS_LR_PROF
+        const long long te = clock64();
+#endif
         tc::mbar_wait(&bars->tfull[acc], (it / kAcc) & 1);
+#ifdef NSS_LR_PROF
+        const long long tb = clock64();
+        pw[0] += tb - te;
+#endif
         tc::tc_fence_after();
         const int cbase = chalf * kPartCols;
         const int col0 = t * BN + cbase;
@@ -276,6 +317,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         // each product has <= kPartCols / 2 <= 32 factors in (1, 2]: no
         // overflow; the tile value is >= ln 2 per column, or 0 (no column)
         e_sum += static_cast<double>(fmaf(0.6931471805599453f, __log2f(p0) + __log2f(p1), 0.5f * (s0 + s1)));
+#ifdef NSS_LR_PROF
+        pw[1] += clock64() - tb;
+#endif
       }
       // end of this probe tile's part of the range: one exact fp64 atomic per row
       if (u + 1 == u1 || (u + 1) / n_tiles != m) {
@@ -285,8 +329,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
+#ifdef NSS_LR_PROF
+  if (g_lr_prof) {
+    if (warp == 1 && lane == 0)
+      for (int q = 0; q < 3; ++q) atomicAdd(g_lr_prof + q, pw[q]);
+    if (warp >= 2 && lane == 0) {
+      atomicAdd(g_lr_prof + 3, pw[0]);
+      atomicAdd(g_lr_prof + 4, pw[1]);
+    }
+  }
+#endif
   tc::tc_fence_before();
   __syncthreads();
+#ifdef NSS_LR_PROF
+  if (g_lr_prof && threadIdx.x == 0) {
+    atomicAdd(g_lr_prof + 5, static_cast<unsigned long long>(clock64() - t_start));
+    atomicAdd(g_lr_prof + 6, static_cast<unsigned long long>(t_start - t_pro));
+    atomicAdd(g_lr_prof + 7, static_cast<unsigned long long>(u1 - u0));
+  }
+#endif
   if (warp == 1) tc::tmem_dealloc<kAcc * BN>(tmem);
 }
 
@@ -314,6 +375,26 @@ void launch_bn(const CUtensorMap &tmA, const CUtensorMap &tmB, const CUtensorMap
 }  // namespace
 
 size_t lr_energy_smem() { return smem_of<128, 2>(); }
+
+#ifdef NSS_LR_PROF
+static unsigned long long *h_lr_prof = nullptr;
+void lr_prof_init() {
+  if (h_lr_prof) return;
+  cudaMallocManaged(&h_lr_prof, 8 * sizeof(unsigned long long));
+  memset(h_lr_prof, 0, 8 * sizeof(unsigned long long));
+  cudaMemcpyToSymbol(g_lr_prof, &h_lr_prof, sizeof(h_lr_prof));
+}
+void lr_prof_dump() {
+  if (!h_lr_prof) return;
+  cudaDeviceSynchronize();
+  const unsigned long long *p = h_lr_prof;
+  const double span = static_cast<double>(p[5]), epi = 16.0;
+  fprintf(stderr, "lr_prof: %llu tile pairs; per CTA-span: MMA waits X %.3f, accumulator %.3f, probe tile %.3f; "
+          "epilogue waits %.3f busy %.3f (per warp); prologue/span %.3f; span per tile pair %.0f clk\n",
+          p[7], p[0] / span, p[1] / span, p[2] / span, p[3] / epi / span, p[4] / epi / span, p[6] / span,
+          span / static_cast<double>(p[7] ? p[7] : 1));
+}
+#endif
 int lr_energy_splits() { return kSplits; }
 
 

@@ -15,6 +15,10 @@
 namespace nss {
 
 size_t lr_energy_smem();
+#ifdef NSS_LR_PROF
+void lr_prof_init();
+void lr_prof_dump();
+#endif
 void launch_lr_energy(const CUtensorMap &tmA, const CUtensorMap &tmB, const CUtensorMap &tmB2, double *eacc,
                       const int *n_probe, int *reset_counter, int p_stride, int n_data, int d, int bn, int xs,
                       const LaunchCtx &lc);
@@ -100,6 +104,9 @@ bool lr_data_ok(const double *X, long long count, int d, bool *exact) {
 cudaError_t lr_setup(LrEngine &L, const double *X, const double *y, long long N, int d, int max_probe) {
   L.N = N;
   L.d = d;
+#ifdef NSS_LR_PROF
+  lr_prof_init();
+#endif
   bool exact = true;
   if (!lr_data_ok(X, N * d, d, &exact)) return cudaErrorInvalidValue;
   L.xs = exact ? 1 : 2;
@@ -152,6 +159,9 @@ cudaError_t lr_setup(LrEngine &L, const double *X, const double *y, long long N,
 }
 
 void lr_free(LrEngine &L) {
+#ifdef NSS_LR_PROF
+  lr_prof_dump();
+#endif
   cudaFree(L.Xb);
   cudaFree(L.Xl);
   cudaFree(L.g);
