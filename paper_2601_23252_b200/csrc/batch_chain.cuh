@@ -214,7 +214,7 @@ __device__ __forceinline__ void advance_chain(const RunDev &r, const PriorDev &p
       if (r.Vpre && have_next && j == jn) {  // prefetched with the state
 #pragma unroll
         for (int t = 0; t < NPL; ++t) v[t] = vn[t];
-      } else if (r.Vpre) {  // precomputed for this (chain, step) by k_dirs (bit-identical)
+      } else if (r.Vpre) {  // precomputed for this (chain, step) by k_dirs (fp64 tensor-core products)
         const float *vr = r.Vpre + (static_cast<long long>(c - chain_range(r).x) * p + j) * r.dp;
 #pragma unroll
         for (int t = 0; t < NPL; ++t) {

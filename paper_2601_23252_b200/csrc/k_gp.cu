@@ -11,8 +11,9 @@
 // every 64 x 64 tile T = [K; y^T](i, j) - L(i, :j) L(j, :j)^T is accumulated in
 // registers on the fp64 tensor cores (mma.sync m8n8k4 = DMMA, 8 per warp per
 // k-step) from the already stored L panels (streamed through a double-buffered
-// cp.async pipeline), with K(i, j) generated on the fly from X and phi; the
-// diagonal tile is factorised and inverted by one warp, and every tile below
+// cp.async pipeline), with K(i, j) generated on the fly from X and phi (the
+// tiles below the diagonal by warps 1-7 while warp 0 factorises and inverts
+// the diagonal tile, gen_k_below), and every tile below
 // becomes L(i, j) = T L_jj^-T (DMMA).  The y^T row turns into alpha^T =
 // (L^-1 y)^T on the way, so E needs only
 // the pivots (log det) and |alpha|^2.  A non-positive pivot gives E = +inf (K
@@ -98,13 +99,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// D(8x8) += A(8x4) B(4x8) on the fp64 tensor cores: a = A[lane/4][lane%4],
-// b = B[lane%4][lane/4], d = D[lane/4][2 (lane%4) + {0, 1}]
-__device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
-}
+__device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) { dmma_f64(d0, d1, a, b); }
 
 // acc(32 x 16 per warp) += Ta(rows) . Tb(rows)^T over k < KB (KB = 0: kb at
 // run time): 4 x 2 DMMA 8x8 tiles, operand rows at m_base / n_base of

@@ -225,34 +225,37 @@ __global__ void __launch_bounds__(256) k_hrss(RunDev r, PriorDev pr, EnergyDev e
   }
 }
 
-// Directions of every (chain, step) of the iteration at once (large d): the
-// same draws and arithmetic as the in-chain direction of k_hrss (identical
-// bits: L is lower triangular with exact zeros above the diagonal, so the
-// extra terms of the full-row loop add +-0), over the whole GPU instead of
-// serially inside each chain: V[(c - c0) p + j] = L z / |z| (Mahalanobis) or
-// L z / |L z|.  Persistent grid: every CTA stages L in shared memory once and
-// its warps loop over groups of NB directions; per column m one L element per
-// row and one NB-wide vector of normals feed NB FMAs, so a warp reads L once
-// per NB directions (the shared-memory pipe, not the FMA pipe, bound the
-// one-direction-per-warp version).
-#ifndef NSS_DIR_NB
-#define NSS_DIR_NB 8
-#endif
-constexpr int kDirNB = NSS_DIR_NB;  // directions per warp pass (4 or 8)
+// Directions of every (chain, step) of the iteration at once (large d), over
+// the whole GPU instead of serially inside each chain:
+//   V[(c - c0) p + j] = L z / |z| (Mahalanobis, R-6) or L z / |L z|,
+// z the same fp32 normals of stream (iter, dest, HRSS, j) the in-chain
+// direction draws.  The products L z run on the fp64 tensor cores
+// (mma.sync m8n8k4 = DMMA; fp32 inputs are exact in fp64, products exact,
+// sums in fp64) and each component is rounded to fp32 once, after the
+// normalisation: closer to the oracle's fp64 than the fp32 FMA chain of the
+// in-chain path (d <= 32).  One warp takes 8 directions at a time (the DMMA M
+// rows); n-tiles of 8 rows of L (N), k-steps of 4 columns (K), only the
+// k-steps at or left of the diagonal (L lower triangular).  L is staged once
+// per CTA in fp64 (stride = 4 mod 16 doubles: conflict-free fragments),
+// the warp's normals in an 8-row fp64 panel; persistent grid, one CTA per SM.
+constexpr int kDirRows = 8;  // directions per warp pass (DMMA M)
 
-template <int NPL>
-__global__ void __launch_bounds__(256) k_dirs(RunDev r, float *V) {
-  extern __shared__ float sm[];
+__host__ __device__ constexpr int dir_ld(int K) { return ((K + 11) / 16) * 16 + 4; }  // >= K, = 4 mod 16
+
+template <int NT>  // n-tiles of 8 rows held in registers: d <= 8 NT
+__global__ void __launch_bounds__(512, 1) k_dirs(RunDev r, float *V) {
+  extern __shared__ double smd[];
   __shared__ int sh_flag;
   const int d = r.d, lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
-  const int ldl = odd_stride(d);
-  float *sL = sm;
-  float *sZ = sm + ((d * ldl + 3) & ~3) + wib * (d * kDirNB);  // [m][k], 16-byte aligned
+  const int nt = (d + 7) >> 3, K = 8 * nt, ld = dir_ld(K);
+  double *sL = smd;                                 // K x ld: L[i][m], zero outside the d x d lower triangle
+  double *sZ = smd + K * ld + wib * kDirRows * ld;  // this warp's 8 x ld panel of normals
   if (threadIdx.x == 0) sh_flag = (r.st->terminated || r.st->error || r.st->finalised) ? 1 : 0;
-  for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
-    int i = e / d, j = e - i * d;
-    sL[i * ldl + j] = r.L[i * r.dp + j];
+  for (int e = threadIdx.x; e < K * ld; e += blockDim.x) {
+    const int i = e / ld, m = e - i * ld;
+    sL[e] = (i < d && m <= i) ? static_cast<double>(r.L[i * r.dp + m]) : 0.0;
   }
+  for (int e = lane; e < kDirRows * ld; e += 32) sZ[e] = 0.0;  // columns >= d stay zero
   __syncthreads();
   if (sh_flag) return;
   const int p = r.p;
@@ -262,120 +265,98 @@ __global__ void __launch_bounds__(256) k_dirs(RunDev r, float *V) {
   const bool euclid = r.dir_norm == NSS_DIR_EUCLIDEAN;
   const int h = 2 * ((d + 1) / 2);
   const int nblk_norm = h >> 2, nblk_all = (h + 3) >> 2;
-  const long long groups = (work + kDirNB - 1) / kDirNB;
+  const int gq = lane >> 2, tq = lane & 3;
+  const long long groups = (work + kDirRows - 1) / kDirRows;
   for (long long g = static_cast<long long>(blockIdx.x) * wpb + wib; g < groups;
        g += static_cast<long long>(gridDim.x) * wpb) {
-    // the normals of the group's directions: stream (it, dest, HRSS, j)
-#pragma unroll
-    for (int k = 0; k < kDirNB; ++k) {
-      const long long q = g * kDirNB + k;  // (c - c0) p + j
-      const bool real = q < work;
-      const int c = cr.x + static_cast<int>(real ? q / p : 0), j = static_cast<int>(real ? q % p : 0);
-      const int s = r.cdest[c];
-      for (int b = lane; b < nblk_all; b += 32) {
-        float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
-        if (real) {
-          uint4 u4 = philox_block(r, it, s, kPhaseHrss, j, b);
-          float u0 = u01(u4.x), u1 = u01(u4.y), u2 = u01(u4.z), u3 = u01(u4.w);
-          float r0 = sqrtf(-2.f * logf(u0)), r1 = sqrtf(-2.f * logf(u2));
-          float s0, c0, s1, c1;
-          sincospif(2.f * u1, &s0, &c0);
-          sincospif(2.f * u3, &s1, &c1);
-          z0 = r0 * c0;
-          z1 = r0 * s0;
-          z2 = r1 * c1;
-          z3 = r1 * s1;
-        }
-        const int i0 = 4 * b;
-        if (i0 < d) sZ[i0 * kDirNB + k] = z0;
-        if (i0 + 1 < d) sZ[(i0 + 1) * kDirNB + k] = z1;
-        if (b < nblk_norm) {
-          if (i0 + 2 < d) sZ[(i0 + 2) * kDirNB + k] = z2;
-          if (i0 + 3 < d) sZ[(i0 + 3) * kDirNB + k] = z3;
-        }
+    // the normals of the group's directions (row k of the panel)
+    for (int e = lane; e < kDirRows * nblk_all; e += 32) {
+      const int k = e / nblk_all, b = e - k * nblk_all;
+      const long long q = g * kDirRows + k;  // (c - c0) p + j
+      float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
+      if (q < work) {
+        const int c = cr.x + static_cast<int>(q / p), j = static_cast<int>(q % p);
+        const uint4 u4 = philox_block(r, it, r.cdest[c], kPhaseHrss, j, b);
+        const float u0 = u01(u4.x), u1 = u01(u4.y), u2 = u01(u4.z), u3 = u01(u4.w);
+        const float r0 = sqrtf(-2.f * logf(u0)), r1 = sqrtf(-2.f * logf(u2));
+        float s0, c0, s1, c1;
+        sincospif(2.f * u1, &s0, &c0);
+        sincospif(2.f * u3, &s1, &c1);
+        z0 = r0 * c0;
+        z1 = r0 * s0;
+        z2 = r1 * c1;
+        z3 = r1 * s1;
+      }
+      const int i0 = 4 * b;
+      double *zr = sZ + k * ld + i0;
+      if (i0 < d) zr[0] = z0;
+      if (i0 + 1 < d) zr[1] = z1;
+      if (b < nblk_norm) {  // the partial last block carries u_h, u_b in words 2, 3
+        if (i0 + 2 < d) zr[2] = z2;
+        if (i0 + 3 < d) zr[3] = z3;
       }
     }
     __syncwarp();
-    // v_k = L z_k: rows lane + 32 t; row block t reaches column 32 t + 31 at most
-    float acc[NPL][kDirNB];
+    // D(8 directions x 8 rows of n-tile jn) += Z(8 x 4) L(rows, 4 columns)^T
+    double acc[NT][2];
 #pragma unroll
-    for (int t = 0; t < NPL; ++t)
+    for (int jn = 0; jn < NT; ++jn) acc[jn][0] = acc[jn][1] = 0.0;
+    for (int ks = 0; ks < 2 * nt; ++ks) {
+      const double a = sZ[gq * ld + 4 * ks + tq];
+      const double *lb = sL + gq * ld + 4 * ks + tq;
 #pragma unroll
-      for (int k = 0; k < kDirNB; ++k) acc[t][k] = 0.f;
+      for (int jn = 0; jn < NT; ++jn)
+        if (jn < nt && 2 * jn + 1 >= ks) dmma_f64(acc[jn][0], acc[jn][1], a, lb[8 * jn * ld]);
+    }
+    // norms of direction gq: the four lanes of the quad hold its columns / rows
+    double zz = 0.0, vv = 0.0;
+    for (int m = tq; m < K; m += 4) {
+      const double z = sZ[gq * ld + m];
+      zz = fma(z, z, zz);
+    }
 #pragma unroll
-    for (int t = 0; t < NPL; ++t) {
-      const int i = lane + 32 * t;
-      const float *row = sL + (i < d ? i : 0) * ldl;
-      const int mend = min(d, 32 * t + 32);
-      for (int m = 0; m < mend; ++m) {
-        const float lm = row[m];
+    for (int jn = 0; jn < NT; ++jn) vv = fma(acc[jn][0], acc[jn][0], fma(acc[jn][1], acc[jn][1], vv));
+    zz += __shfl_xor_sync(0xffffffffu, zz, 1);
+    zz += __shfl_xor_sync(0xffffffffu, zz, 2);
+    vv += __shfl_xor_sync(0xffffffffu, vv, 1);
+    vv += __shfl_xor_sync(0xffffffffu, vv, 2);
+    const double inv = 1.0 / sqrt(euclid ? vv : zz);
+    const long long q = g * kDirRows + gq;
+    if (q < work) {
+      float *out = V + q * r.dp;
 #pragma unroll
-        for (int k4 = 0; k4 < kDirNB; k4 += 4) {
-          const float4 z4 = *reinterpret_cast<const float4 *>(sZ + m * kDirNB + k4);
-          acc[t][k4 + 0] = fmaf(lm, z4.x, acc[t][k4 + 0]);
-          acc[t][k4 + 1] = fmaf(lm, z4.y, acc[t][k4 + 1]);
-          acc[t][k4 + 2] = fmaf(lm, z4.z, acc[t][k4 + 2]);
-          acc[t][k4 + 3] = fmaf(lm, z4.w, acc[t][k4 + 3]);
-        }
+      for (int jn = 0; jn < NT; ++jn) {
+        const int i = 8 * jn + 2 * tq;
+        if (jn < nt && i + 1 < d)
+          *reinterpret_cast<float2 *>(out + i) =
+              make_float2(static_cast<float>(acc[jn][0] * inv), static_cast<float>(acc[jn][1] * inv));
+        else if (jn < nt && i < d)
+          out[i] = static_cast<float>(acc[jn][0] * inv);
       }
     }
-    float zz[kDirNB], vv[kDirNB];
-#pragma unroll
-    for (int k = 0; k < kDirNB; ++k) {
-      zz[k] = 0.f;
-      vv[k] = 0.f;
-    }
-#pragma unroll
-    for (int t = 0; t < NPL; ++t) {
-      const int i = lane + 32 * t;
-      if (i < d) {
-#pragma unroll
-        for (int k = 0; k < kDirNB; ++k) {
-          const float zi = sZ[i * kDirNB + k];
-          zz[k] = fmaf(zi, zi, zz[k]);
-          vv[k] = fmaf(acc[t][k], acc[t][k], vv[k]);
-        }
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < kDirNB; ++k) {
-      const long long q = g * kDirNB + k;
-      const float inv = 1.f / sqrtf(warp_sum(euclid ? vv[k] : zz[k]));
-      if (q < work) {
-        float *out = V + q * r.dp;
-#pragma unroll
-        for (int t = 0; t < NPL; ++t) {
-          const int i = lane + 32 * t;
-          if (i < d) out[i] = acc[t][k] * inv;
-        }
-      }
-    }
-    __syncwarp();  // sZ is rewritten by the next group
+    __syncwarp();  // the panel is rewritten by the next group
   }
 }
 
-template <int NPL>
+template <int NT>
 void launch_dirs_t(const RunDev &r, float *V, const LaunchCtx &lc) {
   const long long work = static_cast<long long>(r.c1 - r.c0) * r.p;
   if (work <= 0) return;
-  const int wpb = 8;
-  const size_t smem = (static_cast<size_t>((r.d * odd_stride(r.d) + 3) & ~3) +
-                       static_cast<size_t>(wpb) * r.d * kDirNB) * sizeof(float);
-  if (smem > 48 * 1024) NSS_MAX_SMEM(k_dirs<NPL>, smem);
-  NSS_PIN_CARVEOUT(k_dirs<NPL>);
-  // persistent: the CTAs that fit at once (L staged once per CTA), no more than the work
-  static int per_sm[64] = {};
+  const int K = 8 * ((r.d + 7) / 8), ld = dir_ld(K);
+  const size_t l_bytes = static_cast<size_t>(K) * ld * sizeof(double);
+  const size_t z_bytes = static_cast<size_t>(kDirRows) * ld * sizeof(double);
+  int wpb = static_cast<int>((227 * 1024 - 1024 - l_bytes) / z_bytes);
+  wpb = wpb > 16 ? 16 : wpb;
+  const size_t smem = l_bytes + wpb * z_bytes;
+  NSS_MAX_SMEM(k_dirs<NT>, smem);
+  NSS_PIN_CARVEOUT(k_dirs<NT>);
+  static int sms_[64] = {};
   const int dv = current_device();
-  if (!per_sm[dv]) {
-    int nb = 0, sms = 148;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_dirs<NPL>, wpb * 32, smem);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dv);
-    per_sm[dv] = (nb > 0 ? nb : 1) * sms;
-  }
-  const long long groups = (work + kDirNB - 1) / kDirNB;
+  if (!sms_[dv]) cudaDeviceGetAttribute(&sms_[dv], cudaDevAttrMultiProcessorCount, dv);
+  const long long groups = (work + kDirRows - 1) / kDirRows;
   const long long want = (groups + wpb - 1) / wpb;
-  const int grid = static_cast<int>(want < per_sm[dv] ? want : per_sm[dv]);
-  k_dirs<NPL><<<grid, wpb * 32, smem, lc.stream>>>(r, V);
+  const int grid = static_cast<int>(want < sms_[dv] ? want : sms_[dv]);  // persistent: one CTA per SM
+  k_dirs<NT><<<grid, wpb * 32, smem, lc.stream>>>(r, V);
   ++*lc.launch_counter;
 }
 
@@ -632,12 +613,12 @@ void launch_init_t(const RunDev &r, const PriorDev &pr, const EnergyDev &en, con
 
 void launch_dirs(const RunDev &r, const LaunchCtx &lc) {
   if (!r.Vpre) return;
-  switch ((r.d + 31) / 32) {
-    case 1: launch_dirs_t<1>(r, r.Vpre, lc); break;
-    case 2: launch_dirs_t<2>(r, r.Vpre, lc); break;
-    case 3: launch_dirs_t<3>(r, r.Vpre, lc); break;
-    default: launch_dirs_t<4>(r, r.Vpre, lc); break;
-  }
+  if (r.d <= 64)
+    launch_dirs_t<8>(r, r.Vpre, lc);
+  else if (r.d <= 96)
+    launch_dirs_t<12>(r, r.Vpre, lc);
+  else
+    launch_dirs_t<16>(r, r.Vpre, lc);
 }
 
 bool energy_supported(const EnergyDev &en) {

@@ -181,6 +181,14 @@ __device__ __forceinline__ float u01(uint32_t r) {
   return (static_cast<float>(r >> 9) + 0.5f) * 1.1920928955078125e-07f;
 }
 
+// D(8x8) += A(8x4) B(4x8) on the fp64 tensor cores (DMMA): a = A[lane/4][lane%4],
+// b = B[lane%4][lane/4], d = D[lane/4][2 (lane%4) + {0, 1}]
+__device__ __forceinline__ void dmma_f64(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
