@@ -269,44 +269,64 @@ __global__ void __launch_bounds__(512, 1) k_dirs(RunDev r, float *V) {
   const long long groups = (work + kDirRows - 1) / kDirRows;
   for (long long g = static_cast<long long>(blockIdx.x) * wpb + wib; g < groups;
        g += static_cast<long long>(gridDim.x) * wpb) {
-    // the normals of the group's directions (row k of the panel)
-    for (int e = lane; e < kDirRows * nblk_all; e += 32) {
-      const int k = e / nblk_all, b = e - k * nblk_all;
-      const long long q = g * kDirRows + k;  // (c - c0) p + j
-      float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
+    // the group's directions: lanes 0..7 resolve (chain, step, dest) once
+    int my_s = 0, my_j = 0, my_real = 0;
+    if (lane < kDirRows) {
+      const long long q = g * kDirRows + lane;  // (c - c0) p + j
       if (q < work) {
-        const int c = cr.x + static_cast<int>(q / p), j = static_cast<int>(q % p);
-        const uint4 u4 = philox_block(r, it, r.cdest[c], kPhaseHrss, j, b);
-        const float u0 = u01(u4.x), u1 = u01(u4.y), u2 = u01(u4.z), u3 = u01(u4.w);
-        const float r0 = sqrtf(-2.f * logf(u0)), r1 = sqrtf(-2.f * logf(u2));
-        float s0, c0, s1, c1;
-        sincospif(2.f * u1, &s0, &c0);
-        sincospif(2.f * u3, &s1, &c1);
-        z0 = r0 * c0;
-        z1 = r0 * s0;
-        z2 = r1 * c1;
-        z3 = r1 * s1;
+        const long long cq = q / p;
+        my_s = r.cdest[cr.x + static_cast<int>(cq)];
+        my_j = static_cast<int>(q - cq * p);
+        my_real = 1;
       }
-      const int i0 = 4 * b;
-      double *zr = sZ + k * ld + i0;
-      if (i0 < d) zr[0] = z0;
-      if (i0 + 1 < d) zr[1] = z1;
-      if (b < nblk_norm) {  // the partial last block carries u_h, u_b in words 2, 3
-        if (i0 + 2 < d) zr[2] = z2;
-        if (i0 + 3 < d) zr[3] = z3;
+    }
+    // the normals (row k of the panel): lane -> direction k = lane & 7, blocks (lane >> 3) + 4 t
+    {
+      const int k = lane & 7;
+      const int sk = __shfl_sync(0xffffffffu, my_s, k), jk = __shfl_sync(0xffffffffu, my_j, k);
+      const bool realk = __shfl_sync(0xffffffffu, my_real, k) != 0;
+      for (int b = lane >> 3; b < nblk_all; b += 4) {
+        float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
+        if (realk) {
+          const uint4 u4 = philox_block(r, it, sk, kPhaseHrss, jk, b);
+          const float u0 = u01(u4.x), u1 = u01(u4.y), u2 = u01(u4.z), u3 = u01(u4.w);
+          const float r0 = sqrtf(-2.f * logf(u0)), r1 = sqrtf(-2.f * logf(u2));
+          float s0, c0, s1, c1;
+          sincospif(2.f * u1, &s0, &c0);
+          sincospif(2.f * u3, &s1, &c1);
+          z0 = r0 * c0;
+          z1 = r0 * s0;
+          z2 = r1 * c1;
+          z3 = r1 * s1;
+        }
+        const int i0 = 4 * b;
+        double *zr = sZ + k * ld + i0;
+        if (i0 < d) zr[0] = z0;
+        if (i0 + 1 < d) zr[1] = z1;
+        if (b < nblk_norm) {  // the partial last block carries u_h, u_b in words 2, 3
+          if (i0 + 2 < d) zr[2] = z2;
+          if (i0 + 3 < d) zr[3] = z3;
+        }
       }
     }
     __syncwarp();
-    // D(8 directions x 8 rows of n-tile jn) += Z(8 x 4) L(rows, 4 columns)^T
+    // D(8 directions x 8 rows of n-tile jn) = Z(8 x K) L(rows, K)^T over the
+    // k-steps at or left of the diagonal (exact trip counts, two chains)
     double acc[NT][2];
+    const double *pa = sZ + gq * ld + tq;
 #pragma unroll
-    for (int jn = 0; jn < NT; ++jn) acc[jn][0] = acc[jn][1] = 0.0;
-    for (int ks = 0; ks < 2 * nt; ++ks) {
-      const double a = sZ[gq * ld + 4 * ks + tq];
-      const double *lb = sL + gq * ld + 4 * ks + tq;
-#pragma unroll
-      for (int jn = 0; jn < NT; ++jn)
-        if (jn < nt && 2 * jn + 1 >= ks) dmma_f64(acc[jn][0], acc[jn][1], a, lb[8 * jn * ld]);
+    for (int jn = 0; jn < NT; ++jn) {
+      acc[jn][0] = acc[jn][1] = 0.0;
+      if (jn < nt) {
+        const double *pb = sL + (8 * jn + gq) * ld + tq;
+        double e0 = 0.0, e1 = 0.0;
+        for (int k4 = 0; k4 < 8 * jn + 8; k4 += 8) {
+          dmma_f64(acc[jn][0], acc[jn][1], pa[k4], pb[k4]);
+          dmma_f64(e0, e1, pa[k4 + 4], pb[k4 + 4]);
+        }
+        acc[jn][0] += e0;
+        acc[jn][1] += e1;
+      }
     }
     // norms of direction gq: the four lanes of the quad hold its columns / rows
     double zz = 0.0, vv = 0.0;
