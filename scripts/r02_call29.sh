@@ -1,0 +1,7 @@
+cd $GRAFT_REPO_ROOT
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/c29_build.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_dist.py -q -x > gpurun_out/c29_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/c29_pytest.log
+for C in C3b C4; do
+  timeout 900 python bench.py --config $C --steps 20 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/c29_bench_$C.json 2> gpurun_out/c29_bench_$C.err
+done
+NSS_HOST_ROUNDS=1 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_dirs -s 2 -c 1 -o gpurun_out/c29_dirs python bench.py --config C4 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/c29_ncu.log 2>&1
