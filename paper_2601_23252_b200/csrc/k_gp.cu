@@ -542,9 +542,7 @@ bool gp_setup(void **handle, const double *X, const double *y, int N, int D, dou
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // two CTAs (two probe matrices) per SM; NSS_GP_CTAS=1 (measurement A/B): one
-  const char *cps = getenv("NSS_GP_CTAS");
-  sms *= (cps && atoi(cps) == 1) ? 1 : 2;
+  sms *= 2;  // two CTAs (two probe matrices) per SM
   E->grid = sms;
   E->g.N = N;
   E->g.D = D;
