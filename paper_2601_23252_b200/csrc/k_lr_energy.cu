@@ -44,9 +44,6 @@ constexpr int BM = 128;          // probes per tile (UMMA M)
 constexpr int kSplits = 2;       // fp16 terms per probe coordinate (hi, lo)
 constexpr int kAtom = BM * 128;  // bytes of one [128 rows x 128 B] swizzle-128B region (probe tile)
 constexpr int kSmemA = kSplits * 2 * kAtom;      // splits x 2 k-blocks
-constexpr int kEpiWarps = 16;                    // four per TMEM lane quarter (column quarters)
-constexpr int kColParts = kEpiWarps / 4;         // column parts of a tile (one per epilogue warp of a quarter)
-constexpr int kThreads = 64 + 32 * kEpiWarps;    // warp 0 TMA, warp 1 MMA, warps 2.. epilogue
 constexpr int kMaxRing = 4;
 // Every NSS_LR_POLY-th column's exponential on the FMA pipe instead of the
 // MUFU (0: none); measurement builds (NSS_NVCC_EXTRA=-DNSS_LR_POLY=4).
@@ -71,17 +68,22 @@ __device__ __forceinline__ float ex2_poly(float x) {
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) - 0x4B400000) * 8388608);
 }
 
-// Data-tile width BN (UMMA N): 128 (4 TMEM accumulators of 128 columns) or
-// 256 (half the operand bytes per flop; 2 accumulators of 256 columns, two
-// tcgen05.ld per epilogue warp and tile).  XS X terms per stage.
+// Data-tile width BN (UMMA N): 128 (4 TMEM accumulators of 128 columns),
+// 160 (3 accumulators: the MMA may run two tiles ahead of the epilogue; five
+// 32-column parts) or 256 (half the operand bytes per flop of 128; 2
+// accumulators of 256 columns, two tcgen05.ld per epilogue warp and tile).
+// XS X terms per stage.
 template <int BN_, int XS_>
 struct LrCfg {
   static constexpr int BN = BN_;
   static constexpr int XS = XS_;
-  static constexpr int kStages = (BN_ == 128 && XS_ == 1) ? 4 : 2;  // TMA ring depth for X tiles
-  static constexpr int kAcc = BN_ == 128 ? 4 : 2;             // TMEM accumulators (kAcc x BN = 512 columns)
+  static constexpr int kStages = (BN_ <= 160 && XS_ == 1) ? 4 : 2;  // TMA ring depth for X tiles
+  static constexpr int kAcc = 512 / BN_;                      // TMEM accumulators (of the 512 columns)
   static constexpr int kAtomB = BN_ * 128;                    // one [BN rows x 128 B] swizzle-128B region
   static constexpr int kSmemB = kStages * XS_ * 2 * kAtomB;   // stages x X terms x 2 k-blocks
+  static constexpr int kColParts = BN_ == 160 ? 5 : 4;        // column parts of a tile
+  static constexpr int kEpi = 4 * kColParts;                  // epilogue warps: one per (TMEM lane quarter, part)
+  static constexpr int kThreads = 64 + 32 * kEpi;             // warp 0 TMA, warp 1 MMA, warps 2.. epilogue
   static constexpr int kPartCols = BN_ / kColParts;           // columns per epilogue part
   static constexpr int kChunks = kPartCols / 32;              // tcgen05.ld.32x32b.x32 per part
 };
@@ -115,7 +117,7 @@ struct Sched {
 };
 
 template <int BN_, int XS_>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(LrCfg<BN_, XS_>::kThreads, 1)
     k_lr_energy(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmB2, double *eacc, const int *n_probe_ptr, int *reset_counter,
                 int p_stride, int n_data, int n_tiles, int ksteps) {
@@ -140,7 +142,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < kAcc; ++a) {
       tc::mbar_init(&bars->tfull[a], 1);
-      tc::mbar_init(&bars->tempty[a], kEpiWarps);
+      tc::mbar_init(&bars->tempty[a], C::kEpi);
     }
     tc::fence_barrier_init();
   }
@@ -149,7 +151,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::tma_prefetch(&tmB);
     if (XS_ == 2) tc::tma_prefetch(&tmB2);
   }
-  if (warp == 1) tc::tmem_alloc<kAcc * BN>(&bars->tmem_base);
+  if (warp == 1) tc::tmem_alloc<512>(&bars->tmem_base);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
@@ -169,7 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   int u0, u1;
   sch.range(blockIdx.x, G, u0, u1);
   if (n_probe <= 0 || u0 >= u1) {  // uniform per CTA
-    if (warp == 1) tc::tmem_dealloc<kAcc * BN>(tmem);
+    if (warp == 1) tc::tmem_dealloc<512>(tmem);
     return;
   }
 
@@ -333,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (g_lr_prof) {
     if (warp == 1 && lane == 0)
       for (int q = 0; q < 3; ++q) atomicAdd(g_lr_prof + q, pw[q]);
-    if (warp >= 2 && lane == 0) {
+    if (warp == 2 && lane == 0) {  // one epilogue warp
       atomicAdd(g_lr_prof + 3, pw[0]);
       atomicAdd(g_lr_prof + 4, pw[1]);
     }
@@ -348,7 +350,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     atomicAdd(g_lr_prof + 7, static_cast<unsigned long long>(u1 - u0));
   }
 #endif
-  if (warp == 1) tc::tmem_dealloc<kAcc * BN>(tmem);
+  if (warp == 1) tc::tmem_dealloc<512>(tmem);
 }
 
 template <int BN_, int XS_>
@@ -367,7 +369,7 @@ void launch_bn(const CUtensorMap &tmA, const CUtensorMap &tmB, const CUtensorMap
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int n_tiles = (n_data + BN_ - 1) / BN_;
-  launch_maybe_pdl(k_lr_energy<BN_, XS_>, dim3(sms), dim3(kThreads), smem_of<BN_, XS_>(), lc.stream, tmA, tmB, tmB2,
+  launch_maybe_pdl(k_lr_energy<BN_, XS_>, dim3(sms), dim3(LrCfg<BN_, XS_>::kThreads), smem_of<BN_, XS_>(), lc.stream, tmA, tmB, tmB2,
                    eacc, n_probe, reset_counter, p_stride, n_data, n_tiles, (d + 15) / 16);
   ++*lc.launch_counter;
 }
@@ -388,7 +390,7 @@ void lr_prof_dump() {
   if (!h_lr_prof) return;
   cudaDeviceSynchronize();
   const unsigned long long *p = h_lr_prof;
-  const double span = static_cast<double>(p[5]), epi = 16.0;
+  const double span = static_cast<double>(p[5]), epi = 1.0;
   fprintf(stderr, "lr_prof: %llu tile pairs; per CTA-span: MMA waits X %.3f, accumulator %.3f, probe tile %.3f; "
           "epilogue waits %.3f busy %.3f (per warp); prologue/span %.3f; span per tile pair %.0f clk\n",
           p[7], p[0] / span, p[1] / span, p[2] / span, p[3] / epi / span, p[4] / epi / span, p[6] / span,
@@ -406,6 +408,8 @@ void launch_lr_energy(const CUtensorMap &tmA, const CUtensorMap &tmB, const CUte
     launch_bn<128, 2>(tmA, tmB, tmB2, eacc, n_probe, reset_counter, p_stride, n_data, d, lc);
   else if (bn == 256)
     launch_bn<256, 1>(tmA, tmB, tmB2, eacc, n_probe, reset_counter, p_stride, n_data, d, lc);
+  else if (bn == 160)
+    launch_bn<160, 1>(tmA, tmB, tmB2, eacc, n_probe, reset_counter, p_stride, n_data, d, lc);
   else
     launch_bn<128, 1>(tmA, tmB, tmB2, eacc, n_probe, reset_counter, p_stride, n_data, d, lc);
 }

@@ -113,7 +113,10 @@ cudaError_t lr_setup(LrEngine &L, const double *X, const double *y, long long N,
   // data tiles of BN = 256 rows (half the operand bytes per flop of 128; rows
   // past n_pad are zero-filled by TMA); NSS_LR_BN=128 selects 128-row tiles;
   // split data (two X terms per stage) use 128
-  L.bn = (L.xs == 2 || (getenv("NSS_LR_BN") && atoi(getenv("NSS_LR_BN")) == 128)) ? 128 : 256;
+  {
+    const int want = getenv("NSS_LR_BN") ? atoi(getenv("NSS_LR_BN")) : 256;
+    L.bn = L.xs == 2 ? 128 : (want == 128 || want == 160 ? want : 256);
+  }
   L.n_tiles = static_cast<int>((N + L.bn - 1) / L.bn);
   L.n_pad = static_cast<long long>(L.n_tiles) * L.bn;
   L.p_stride = ((max_probe + 127) / 128) * 128;
