@@ -301,6 +301,69 @@ __device__ __forceinline__ float corr_energy_split(const float (&x)[NPL], const 
   return 0.5f * tot + en.c;
 }
 
+// The same energy split over WPC = 4 warps of a chain: the rows' dot products
+// (row block t covers columns [32 t, d)) are laid end to end and cut into four
+// equal runs of columns, so a warp takes at most a few pieces (t, [m0, m1));
+// piece k of row block t leaves its partial dot products in slot (t, k) of
+// `red` (4 x 4 x 32 floats + 4), the chain's 128 threads meet at a named
+// barrier, warp t sums the slots of row block t in slot order and squares,
+// and a second barrier publishes the four row-block sums.  Deterministic
+// (fixed slots and orders); identical result in all four warps.
+template <int NPL>
+__device__ __forceinline__ float corr_energy_split4(const float (&x)[NPL], const EnergyDev &en, const ESm &es,
+                                                    float *wbuf, float *red, int lane, int sub, int bar_id) {
+  const int d = en.d, nb = (d + 31) >> 5;
+#pragma unroll
+  for (int t = 0; t < NPL; ++t) {
+    const int i = lane + 32 * t;
+    if (i < d) wbuf[i] = x[t] - es.mu[i];  // all warps write the same values
+  }
+  __syncwarp();
+  int total = 0;
+  for (int t = 0; t < nb; ++t) total += d - 32 * t;
+  const int lo = sub * total / 4, hi = (sub + 1) * total / 4;
+  int cum = 0;
+  for (int t = 0; t < nb; ++t) {
+    const int len = d - 32 * t;
+    const int a0 = max(lo, cum), a1 = min(hi, cum + len);
+    if (a0 < a1) {
+      const int k = sub - (cum * 4) / total;  // warps before this one in row block t
+      const int i = 32 * t + lane;
+      float s0 = 0.f, s1 = 0.f;
+      if (i < d) {
+        const float *row = es.prec + i * es.ldp;
+        int m = 32 * t + (a0 - cum);
+        const int m1 = 32 * t + (a1 - cum);
+        for (; m + 1 < m1; m += 2) {
+          s0 = fmaf(row[m], wbuf[m], s0);
+          s1 = fmaf(row[m + 1], wbuf[m + 1], s1);
+        }
+        if (m < m1) s0 = fmaf(row[m], wbuf[m], s0);
+      }
+      red[(t * 4 + k) * 32 + lane] = s0 + s1;
+    }
+    cum += len;
+  }
+  asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+  float q = 0.f;
+  if (sub < nb) {  // warp t: row block t
+    const int t = sub;
+    int c0 = 0;
+    for (int u = 0; u < t; ++u) c0 += d - 32 * u;
+    const int first = (c0 * 4) / total, last = ((c0 + d - 32 * t - 1) * 4) / total;
+    float a = 0.f;
+    for (int k = 0; k <= last - first; ++k) a += red[(t * 4 + k) * 32 + lane];
+    if (32 * t + lane < d) q = a * a;
+    q = warp_sum(q);
+    if (lane == 0) red[16 * 32 + t] = q;
+  }
+  asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+  float tot = 0.f;
+  for (int t = 0; t < nb; ++t) tot += red[16 * 32 + t];
+  __syncwarp();
+  return 0.5f * tot + en.c;
+}
+
 // log Pi(x) and support test (box: all lanes inside; Gaussian: always inside),
 // over the W lanes of the caller's group.
 template <int NPL, int W = 32>

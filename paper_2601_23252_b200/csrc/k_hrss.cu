@@ -22,14 +22,16 @@ struct Probe {
   float lp;
 };
 
-// WPC warps per chain: 2 for the correlated Gaussian at large d (the energy
-// rows split over the two warps, corr_energy_split), else 1.  Every warp of a
+// WPC warps per chain: 2 (or 4) for the correlated Gaussian at large d (the
+// energy rows split over the warps, corr_energy_split / corr_energy_split4),
+// else 1.  Every warp of a
 // chain runs the same control flow on the same values; warp 0 writes.
 template <int NPL, int KIND, int WPC>
 __global__ void __launch_bounds__(256) k_hrss(RunDev r, PriorDev pr, EnergyDev en) {
   extern __shared__ float sm[];
   __shared__ int sh_flag;
   __shared__ float sh_red[8 * 4];
+  __shared__ float sh_red4[WPC == 4 ? 2 : 1][WPC == 4 ? 16 * 32 + 4 : 1];  // corr_energy_split4 slots per chain
   const int d = r.d, lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = (blockDim.x >> 5) / WPC;
   const int sub = wib % WPC, cib = wib / WPC;  // warp within the chain, chain within the block
   const int ldl = odd_stride(d);
@@ -152,7 +154,10 @@ __global__ void __launch_bounds__(256) k_hrss(RunDev r, PriorDev pr, EnergyDev e
       float lpp = prior_logp<NPL>(xp, pr, pa, pb, lane, d, inside);
       if (!inside || (!tempered && !(lpp >= log_y))) return false;
       float ep;
-      if constexpr (WPC == 2 && KIND == NSS_E_CORR_GAUSS) {
+      if constexpr (WPC == 4 && KIND == NSS_E_CORR_GAUSS) {
+        ep = es.tri ? corr_energy_split4<NPL>(xp, en, es, sY - sub * (2 * NPL * 32), sh_red4[cib], lane, sub, 1 + cib)
+                    : warp_energy<NPL, KIND>(xp, en, es, sY, lane);
+      } else if constexpr (WPC == 2 && KIND == NSS_E_CORR_GAUSS) {
         ep = es.tri ? corr_energy_split<NPL>(xp, en, es, sY - sub * (2 * NPL * 32), wred, lane, sub, 1 + cib, epar)
                     : warp_energy<NPL, KIND>(xp, en, es, sY, lane);
       } else {
@@ -556,7 +561,7 @@ void launch_hrss_w(const RunDev &r, const PriorDev &pr, const EnergyDev &en, con
   const size_t sl = r.Vpre ? 0 : static_cast<size_t>(r.d) * ldl;
   const size_t smem = (sl + energy_param_floats(KIND, r.d, en.n_comp) +
                        static_cast<size_t>(wpb) * WPC * 2 * NPL * 32) * sizeof(float);
-  if (smem > 48 * 1024) NSS_MAX_SMEM((k_hrss<NPL, KIND, WPC>), smem);
+  NSS_MAX_SMEM((k_hrss<NPL, KIND, WPC>), smem);  // static shared memory counts against the 48 KB default too
   const int blocks = (nc + wpb - 1) / wpb;
   NSS_PIN_CARVEOUT((k_hrss<NPL, KIND, WPC>));
   k_hrss<NPL, KIND, WPC><<<blocks, wpb * WPC * 32, smem, lc.stream>>>(r, pr, en);
@@ -566,8 +571,12 @@ void launch_hrss_w(const RunDev &r, const PriorDev &pr, const EnergyDev &en, con
 template <int NPL, int KIND>
 void launch_hrss_t(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc) {
   if constexpr (KIND == NSS_E_CORR_GAUSS && NPL >= 2) {
-    if (en.ufac) {  // factored energy: rows split over two warps per chain
-      launch_hrss_w<NPL, KIND, 2>(r, pr, en, lc);
+    if (en.ufac) {  // factored energy: rows split over two (NSS_WPC=4: four) warps per chain
+      static const bool four = getenv("NSS_WPC") && atoi(getenv("NSS_WPC")) == 4;
+      if (four)
+        launch_hrss_w<NPL, KIND, 4>(r, pr, en, lc);
+      else
+        launch_hrss_w<NPL, KIND, 2>(r, pr, en, lc);
       return;
     }
   }
@@ -583,11 +592,7 @@ void launch_rw_t(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const
   wpb = wpb < 1 ? 1 : (wpb > 8 ? 8 : wpb);
   const size_t smem = (static_cast<size_t>(r.d) * ldl + energy_param_floats(KIND, r.d, en.n_comp) +
                        static_cast<size_t>(wpb) * 2 * NPL * 32) * sizeof(float);
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && attr < smem) {
-    cudaFuncSetAttribute(k_rw<NPL, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    attr = smem;
-  }
+  NSS_MAX_SMEM((k_rw<NPL, KIND>), smem);  // per device; static shared memory counts against the 48 KB default too
   NSS_PIN_CARVEOUT((k_rw<NPL, KIND>));
   k_rw<NPL, KIND><<<(nc + wpb - 1) / wpb, wpb * 32, smem, lc.stream>>>(r, pr, en);
   ++*lc.launch_counter;
@@ -597,11 +602,7 @@ template <int NPL, int KIND>
 void launch_init_t(const RunDev &r, const PriorDev &pr, const EnergyDev &en, const LaunchCtx &lc) {
   const int wpb = 8;
   const size_t smem = (energy_param_floats(KIND, r.d, en.n_comp) + static_cast<size_t>(wpb) * NPL * 32) * sizeof(float);
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && attr < smem) {
-    cudaFuncSetAttribute(k_init<NPL, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    attr = smem;
-  }
+  NSS_MAX_SMEM((k_init<NPL, KIND>), smem);  // per device; static shared memory counts against the 48 KB default too
   const int blocks = (r.n + wpb - 1) / wpb;
   NSS_PIN_CARVEOUT((k_init<NPL, KIND>));
   k_init<NPL, KIND><<<blocks, wpb * 32, smem, lc.stream>>>(r, pr, en);
