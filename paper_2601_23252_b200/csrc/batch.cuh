@@ -12,12 +12,14 @@ namespace nss {
 
 enum BatchPhase : int { kPhDir = 0, kPhStepOut = 1, kPhShrink = 2, kPhDone = 3 };
 
+constexpr int kChainWords = 8;  // int4 words per chain record (128 bytes)
+
 struct BatchDev {
   int k, dp, max_rows, n_splits, p_stride;
-  // per-chain state (k each)
-  int *phase, *step, *nl, *nr, *ns, *ldone, *rdone, *row0, *row1;
-  float *l0, *r0, *lft, *rgt, *log_y, *e, *lp, *t0, *t1, *lp0, *lp1;
-  unsigned *cnt;              // [5][k]: probes, evals, expansions, shrinks, nulls
+  // per-chain state: one 128-byte record per chain (batch_chain.cuh, ChainRegs
+  // packed: 9 ints, 11 floats, 5 counters {probes, evals, expansions, shrinks,
+  // nulls}), read and written as seven 16-byte words of one cache line
+  int4 *cs;                   // [k][8]
   float *x, *v;               // [k][dp]
   // probe buffers, double-buffered by round parity
   float *P[2];                // [max_rows][dp] probe points (fp32)

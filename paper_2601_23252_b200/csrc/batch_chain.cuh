@@ -26,22 +26,32 @@ struct ChainRegs {
   unsigned c_probe, c_eval, c_exp, c_shr, c_null;
 };
 
+// The chain record (batch.cuh): words 0-8 the ints, 9-19 the floats, 20-24
+// the counters.
+
 __device__ __forceinline__ void load_chain(const BatchDev &b, int c, ChainRegs &s) {
-  s.phase = b.phase[c]; s.step = b.step[c]; s.nl = b.nl[c]; s.nr = b.nr[c]; s.ns = b.ns[c];
-  s.ldone = b.ldone[c]; s.rdone = b.rdone[c]; s.row0 = b.row0[c]; s.row1 = b.row1[c];
-  s.l0 = b.l0[c]; s.r0 = b.r0[c]; s.lft = b.lft[c]; s.rgt = b.rgt[c]; s.log_y = b.log_y[c];
-  s.e = b.e[c]; s.lp = b.lp[c]; s.t0 = b.t0[c]; s.t1 = b.t1[c]; s.lp0 = b.lp0[c]; s.lp1 = b.lp1[c];
-  s.c_probe = b.cnt[c]; s.c_eval = b.cnt[b.k + c]; s.c_exp = b.cnt[2 * b.k + c];
-  s.c_shr = b.cnt[3 * b.k + c]; s.c_null = b.cnt[4 * b.k + c];
+  const int4 *q = b.cs + static_cast<long long>(c) * kChainWords;
+  const int4 w0 = q[0], w1 = q[1], w2 = q[2], w3 = q[3], w4 = q[4], w5 = q[5], w6 = q[6];
+  s.phase = w0.x; s.step = w0.y; s.nl = w0.z; s.nr = w0.w;
+  s.ns = w1.x; s.ldone = w1.y; s.rdone = w1.z; s.row0 = w1.w;
+  s.row1 = w2.x; s.l0 = __int_as_float(w2.y); s.r0 = __int_as_float(w2.z); s.lft = __int_as_float(w2.w);
+  s.rgt = __int_as_float(w3.x); s.log_y = __int_as_float(w3.y); s.e = __int_as_float(w3.z); s.lp = __int_as_float(w3.w);
+  s.t0 = __int_as_float(w4.x); s.t1 = __int_as_float(w4.y); s.lp0 = __int_as_float(w4.z); s.lp1 = __int_as_float(w4.w);
+  s.c_probe = static_cast<unsigned>(w5.x); s.c_eval = static_cast<unsigned>(w5.y);
+  s.c_exp = static_cast<unsigned>(w5.z); s.c_shr = static_cast<unsigned>(w5.w);
+  s.c_null = static_cast<unsigned>(w6.x);
 }
 
 __device__ __forceinline__ void store_chain(const BatchDev &b, int c, const ChainRegs &s) {
-  b.phase[c] = s.phase; b.step[c] = s.step; b.nl[c] = s.nl; b.nr[c] = s.nr; b.ns[c] = s.ns;
-  b.ldone[c] = s.ldone; b.rdone[c] = s.rdone; b.row0[c] = s.row0; b.row1[c] = s.row1;
-  b.l0[c] = s.l0; b.r0[c] = s.r0; b.lft[c] = s.lft; b.rgt[c] = s.rgt; b.log_y[c] = s.log_y;
-  b.e[c] = s.e; b.lp[c] = s.lp; b.t0[c] = s.t0; b.t1[c] = s.t1; b.lp0[c] = s.lp0; b.lp1[c] = s.lp1;
-  b.cnt[c] = s.c_probe; b.cnt[b.k + c] = s.c_eval; b.cnt[2 * b.k + c] = s.c_exp;
-  b.cnt[3 * b.k + c] = s.c_shr; b.cnt[4 * b.k + c] = s.c_null;
+  int4 *q = b.cs + static_cast<long long>(c) * kChainWords;
+  q[0] = make_int4(s.phase, s.step, s.nl, s.nr);
+  q[1] = make_int4(s.ns, s.ldone, s.rdone, s.row0);
+  q[2] = make_int4(s.row1, __float_as_int(s.l0), __float_as_int(s.r0), __float_as_int(s.lft));
+  q[3] = make_int4(__float_as_int(s.rgt), __float_as_int(s.log_y), __float_as_int(s.e), __float_as_int(s.lp));
+  q[4] = make_int4(__float_as_int(s.t0), __float_as_int(s.t1), __float_as_int(s.lp0), __float_as_int(s.lp1));
+  q[5] = make_int4(static_cast<int>(s.c_probe), static_cast<int>(s.c_eval), static_cast<int>(s.c_exp),
+                   static_cast<int>(s.c_shr));
+  q[6] = make_int4(static_cast<int>(s.c_null), 0, 0, 0);
 }
 
 // energy of probe row `row` of the given parity: the slices are loaded by the

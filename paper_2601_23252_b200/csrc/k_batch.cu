@@ -193,9 +193,12 @@ __global__ void k_batch_finish(RunDev r, BatchDev b) {
   if (c < cr.y) {
     const int s = r.cdest[c];
     for (int i = 0; i < r.d; ++i) r.X[static_cast<long long>(s) * r.dp + i] = b.x[static_cast<long long>(c) * b.dp + i];
-    r.E[s] = b.e[c];
+    ChainRegs cs;
+    load_chain(b, c, cs);
+    r.E[s] = cs.e;
     if (r.cpar[c] != s) r.birth[s] = st->e_star;  // a moved survivor (F4) keeps its birth level
-    for (int q = 0; q < 5; ++q) atomicAdd(&acc[q], static_cast<unsigned long long>(b.cnt[q * b.k + c]));
+    const unsigned cn[5] = {cs.c_probe, cs.c_eval, cs.c_exp, cs.c_shr, cs.c_null};
+    for (int q = 0; q < 5; ++q) atomicAdd(&acc[q], static_cast<unsigned long long>(cn[q]));
   }
   __syncthreads();
   if (threadIdx.x == 0) {

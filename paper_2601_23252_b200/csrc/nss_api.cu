@@ -557,13 +557,7 @@ nss_status ensure_batch(nss_ctx *c) {
     b.dp = c->dp;
     b.max_rows = backend >= 2 ? std::max(2 * k, c->r.n) : 2 * k;  // GP / LR also draw the n initial points
     nss_status s;
-    int **ints[] = {&b.phase, &b.step, &b.nl, &b.nr, &b.ns, &b.ldone, &b.rdone, &b.row0, &b.row1};
-    for (int **q : ints)
-      if ((s = dalloc(c, q, k))) return s;
-    float **flts[] = {&b.l0, &b.r0, &b.lft, &b.rgt, &b.log_y, &b.e, &b.lp, &b.t0, &b.t1, &b.lp0, &b.lp1};
-    for (float **q : flts)
-      if ((s = dalloc(c, q, k))) return s;
-    if ((s = dalloc(c, &b.cnt, 5 * static_cast<size_t>(k)))) return s;
+    if ((s = dalloc(c, &b.cs, static_cast<size_t>(k) * kChainWords))) return s;  // one 128-B record per chain
     if ((s = dalloc(c, &b.x, static_cast<size_t>(k) * c->dp))) return s;
     if ((s = dalloc(c, &b.v, static_cast<size_t>(k) * c->dp))) return s;
     for (int q = 0; q < 2; ++q)
