@@ -40,11 +40,11 @@ def test_lr_energy_batch(d, n_data, P, exact):
         assert abs(o.energy(theta[i]) - e_ref[i]) < 1e-9 * max(1, abs(e_ref[i]))
 
 
-@pytest.mark.parametrize("bn", ["128", "256"])
+@pytest.mark.parametrize("bn", ["128", "160", "256"])
 @pytest.mark.parametrize("n_data,P", [(10_000, 300), (1000, 129)])
 def test_lr_energy_batch_tile_widths(bn, n_data, P, monkeypatch):
-    """Both data-tile widths of the tcgen05 pass (N = 256 default, 128 via
-    NSS_LR_BN, read when the engine is set up) against the fp64 reference,
+    """Every data-tile width of the tcgen05 pass (N = 256 default, 128 and 160
+    via NSS_LR_BN, read when the engine is set up) against the fp64 reference,
     including a ragged last data tile (1000 = 3 x 256 + 232)."""
     from paper_2601_23252_b200 import nss
     monkeypatch.setenv("NSS_LR_BN", bn)
