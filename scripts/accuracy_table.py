@@ -65,19 +65,19 @@ def runs(name, prob, cfg, seeds):
 
 
 def main():
+    big = 10_000 + 1000 * 8000  # a full d = 100 run takes several thousand iterations: dead store for 8000
     cases = [
         ("C1 gauss2", W.gauss(2), W.workload("C1")[1], truth_c1(), range(1, 9)),
         ("C2 mog10", W.mog(10), W.workload("C2")[1], None, range(1, 6)),
-        # a full d = 100 run takes several thousand iterations: a dead store for 8000 (3.2 GB of rows)
-        ("C3a corrgauss100", W.workload("C3a")[0], dict(W.workload("C3a")[1], max_dead=10_000 + 1000 * 8000),
-         None, range(1, 4)),
-        ("C3b funnel100", W.workload("C3b")[0], dict(W.workload("C3b")[1], max_dead=10_000 + 1000 * 8000),
-         None, range(1, 4)),
-        ("C3b funnel100 p=3d", W.workload("C3b")[0],
-         dict(W.workload("C3b")[1], max_dead=10_000 + 1000 * 8000, steps=300), None, range(1, 4)),
-        # p = 3d HRSS steps, the paper's setting for high-dimensional problems
-        ("C3a corrgauss100 p=3d", W.workload("C3a")[0],
-         dict(W.workload("C3a")[1], max_dead=10_000 + 1000 * 8000, steps=300), None, range(1, 4)),
+        # the BASELINE C3 settings: p = 3d HRSS steps, the paper's setting for
+        # high-dimensional problems (R-35)
+        ("C3a corrgauss100", W.workload("C3a")[0], dict(W.workload("C3a")[1], max_dead=big), None, range(1, 6)),
+        ("C3b funnel100", W.workload("C3b")[0], dict(W.workload("C3b")[1], max_dead=big), None, range(1, 6)),
+        # p = d, the round-1 setting, for comparison (the known bias at p = d, R-35)
+        ("C3a corrgauss100 p=d", W.workload("C3a")[0], dict(W.workload("C3a")[1], max_dead=big, steps=100), None,
+         range(1, 4)),
+        ("C3b funnel100 p=d", W.workload("C3b")[0], dict(W.workload("C3b")[1], max_dead=big, steps=100), None,
+         range(1, 4)),
     ]
     only = sys.argv[1:]  # optional case-name prefixes
     if only:
