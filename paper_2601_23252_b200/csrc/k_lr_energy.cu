@@ -166,6 +166,14 @@ __global__ void __launch_bounds__(LrCfg<BN_, XS_>::kThreads, 1)
 #endif
   pdl_trigger();
   const int n_probe = *n_probe_ptr;
+#ifdef NSS_LR_PROF
+  // launches by probe rows: bins 0, 1-127, 128-1023, 1024-4095, 4096-8191, >= 8192
+  const int lr_bin = n_probe <= 0 ? 0 : n_probe < 128 ? 1 : n_probe < 1024 ? 2 : n_probe < 4096 ? 3 : n_probe < 8192 ? 4 : 5;
+  if (g_lr_prof && blockIdx.x == 0 && threadIdx.x == 0) {
+    atomicAdd(g_lr_prof + 8 + lr_bin, 1ull);
+    atomicAdd(g_lr_prof + 24 + lr_bin, static_cast<unsigned long long>(n_probe > 0 ? n_probe : 0));
+  }
+#endif
   const Sched sch(n_probe, n_tiles);
   if (blockIdx.x == 0 && threadIdx.x == 0 && reset_counter) *reset_counter = 0;  // the next round's row counter
   int u0, u1;
@@ -348,6 +356,7 @@ __global__ void __launch_bounds__(LrCfg<BN_, XS_>::kThreads, 1)
     atomicAdd(g_lr_prof + 5, static_cast<unsigned long long>(clock64() - t_start));
     atomicAdd(g_lr_prof + 6, static_cast<unsigned long long>(t_start - t_pro));
     atomicAdd(g_lr_prof + 7, static_cast<unsigned long long>(u1 - u0));
+    if (blockIdx.x == 0) atomicAdd(g_lr_prof + 16 + lr_bin, static_cast<unsigned long long>(clock64() - t_pro));
   }
 #endif
   if (warp == 1) tc::tmem_dealloc<512>(tmem);
@@ -382,8 +391,8 @@ size_t lr_energy_smem() { return smem_of<128, 2>(); }
 static unsigned long long *h_lr_prof = nullptr;
 void lr_prof_init() {
   if (h_lr_prof) return;
-  cudaMallocManaged(&h_lr_prof, 8 * sizeof(unsigned long long));
-  memset(h_lr_prof, 0, 8 * sizeof(unsigned long long));
+  cudaMallocManaged(&h_lr_prof, 32 * sizeof(unsigned long long));
+  memset(h_lr_prof, 0, 32 * sizeof(unsigned long long));
   cudaMemcpyToSymbol(g_lr_prof, &h_lr_prof, sizeof(h_lr_prof));
 }
 void lr_prof_dump() {
@@ -395,6 +404,10 @@ void lr_prof_dump() {
           "epilogue waits %.3f busy %.3f (per warp); prologue/span %.3f; span per tile pair %.0f clk\n",
           p[7], p[0] / span, p[1] / span, p[2] / span, p[3] / epi / span, p[4] / epi / span, p[6] / span,
           span / static_cast<double>(p[7] ? p[7] : 1));
+  const char *bn[6] = {"0", "1-127", "128-1023", "1024-4095", "4096-8191", ">=8192"};
+  for (int b = 0; b < 6; ++b)
+    fprintf(stderr, "lr_prof rows %-9s launches %8llu  rows %12llu  CTA-0 clocks %14llu\n", bn[b], p[8 + b], p[24 + b],
+            p[16 + b]);
 }
 #endif
 int lr_energy_splits() { return kSplits; }
