@@ -348,7 +348,7 @@ def main():
         return relaunch_distributed(args)
     if args.impl == "reference":
         return run_reference(args)
-    assert args.warmup >= 3, "timing rules: at least 3 warm-up steps"
+    args.warmup = max(args.warmup, 3)  # timing rules: at least 3 warm-up steps (the line reports the count run)
 
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
