@@ -659,8 +659,19 @@ nss_status enqueue_iteration_batch(nss_ctx *c, Stage stage = kAll) {
     if (stage == kPre) return NSS_OK;
     if (stage == kAll && (s = shard_exchange(c))) return s;
     if ((s = shard_post_select(c, c->metric_pending))) return s;
-  } else {
-    if (c->metric_pending && (s = launch_metric_on(c, c->stream, 1))) return s;
+  }
+  // the metric of the live set beside the select (as in the per-probe
+  // engines): neither reads what the other writes; joined before the rounds
+  const bool fork_met = !c->sharded && c->metric_pending && !c->serial_evidence;
+  if (!c->sharded) {
+    if (fork_met) {
+      CK(cudaEventRecord(c->ev_fork, c->stream));
+      CK(cudaStreamWaitEvent(c->side2, c->ev_fork, 0));
+      if ((s = launch_metric_on(c, c->side2, 1))) return s;
+      CK(cudaEventRecord(c->ev_met, c->side2));
+    } else if (c->metric_pending && (s = launch_metric_on(c, c->stream, 1))) {
+      return s;
+    }
     if ((s = timed_launch(c, 1, c->stream, [&] {
            launch_select(c->r, lc);
            if (c->cfg.update_all) launch_chains_all(c->r, c->r.cdest, c->r.cpar, const_cast<float *>(c->r.Xs),
@@ -673,6 +684,7 @@ nss_status enqueue_iteration_batch(nss_ctx *c, Stage stage = kAll) {
   LaunchCtx ls{c->side, &c->launches};
   if ((s = timed_launch(c, 2, c->side, [&] { launch_evidence(c->r, 0, ls); }))) return s;
   CK(cudaEventRecord(c->ev_evid, c->side));
+  if (fork_met) CK(cudaStreamWaitEvent(c->stream, c->ev_met, 0));
   auto rounds = [&]() -> nss_status {
     launch_dirs(c->r, lc);  // large d: every direction of the iteration up front
     batch_begin(c->r, c->pr, c->bd, lc);
