@@ -159,11 +159,54 @@ __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials,
   }
   __syncthreads();
   if (tid == 0 && blockIdx.x == 0) st->stamp[9] = global_ns();
+  if (d >= kSplitMinD) {
+    // large d: the chunk's Gram matrix sum_r y_r y_r^T on the fp64 tensor
+    // cores -- 8 x 8 tiles of its lower triangle dealt to the warps, each
+    // tile a DMMA chain over the chunk's rows four at a time (A = Y^T,
+    // B = Y; rows past the chunk and columns past d read as zero) -- and the
+    // first moments sum_r y_r by one thread per coordinate
+    const int lane = tid & 31, gq = lane >> 2, tq = lane & 3;
+    const int nt8 = (d + 7) >> 3, ntile = nt8 * (nt8 + 1) / 2;
+    for (int t = tid >> 5; t < ntile; t += static_cast<int>(blockDim.x >> 5)) {
+      int bi = 0;
+      while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
+      const int bl = t - bi * (bi + 1) / 2;
+      const int ia = 8 * bi + gq, la = 8 * bl + gq;
+      double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
+      int r0 = 0;
+      for (; r0 + 8 <= rows; r0 += 8) {
+        const double *y0 = yd + (r0 + tq) * dp, *y1 = y0 + 4 * dp;
+        dmma_f64(c0, c1, ia < d ? y0[ia] : 0.0, la < d ? y0[la] : 0.0);
+        dmma_f64(e0, e1, ia < d ? y1[ia] : 0.0, la < d ? y1[la] : 0.0);
+      }
+      for (; r0 < rows; r0 += 4) {
+        const bool rv = r0 + tq < rows;
+        const double *y0 = yd + (r0 + tq) * dp;
+        dmma_f64(c0, c1, (rv && ia < d) ? y0[ia] : 0.0, (rv && la < d) ? y0[la] : 0.0);
+      }
+      c0 += e0;
+      c1 += e1;
+      const int ic = 8 * bi + gq, lc = 8 * bl + 2 * tq;
+      if (ic < d && lc <= ic) S[ic * (ic + 1) / 2 + lc] = c0;
+      if (ic < d && lc + 1 <= ic) S[ic * (ic + 1) / 2 + lc + 1] = c1;
+    }
+    for (int i = tid; i < d; i += blockDim.x) {
+      double a0 = 0.0, a1 = 0.0;
+      int rr = 0;
+      for (; rr + 1 < rows; rr += 2) {
+        a0 += yd[rr * dp + i];
+        a1 += yd[(rr + 1) * dp + i];
+      }
+      if (rr < rows) a0 += yd[rr * dp + i];
+      S[npair + i] = a0 + a1;
+    }
+  }
   // G row groups per entry when the entries leave threads idle (small d):
   // thread t takes entry t % nent over the rows r = grp, grp + G, ... of the
   // chunk; the G group sums are added in group order (deterministic)
   const int G = nent < static_cast<int>(blockDim.x) ? static_cast<int>(blockDim.x) / nent : 1;
   double *Sg = G > 1 ? raw_groups(sm, nent, d, npair, rows, dp) : S;  // one group: sum straight into S
+  if (d < kSplitMinD) {
   for (int t = tid; t < nent * G; t += blockDim.x) {
     const int e = t % nent, grp = t / nent;
     // four independent accumulators (fixed assignment: row mod 4G) break the
@@ -196,8 +239,9 @@ __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials,
     }
     Sg[grp * nent + e] = (a0 + a1) + (a2 + a3);
   }
+  }
   __syncthreads();
-  if (G > 1)
+  if (G > 1 && d < kSplitMinD)
     for (int e = tid; e < nent; e += blockDim.x) {
       double acc = 0.0;
       for (int g = 0; g < G; ++g) acc += Sg[g * nent + e];
