@@ -352,7 +352,13 @@ __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials,
     // lower triangle: two barriers per panel instead of one per column.
     constexpr int NB = 8;
     const int ty = tid >> 4, tx = tid & 15;
+#ifdef NSS_MET_PROF
+    unsigned long long t_panel = 0;  // measurement builds: ns in the one-warp panel factorisations
+#endif
     for (int j0 = 0; j0 < d; j0 += NB) {
+#ifdef NSS_MET_PROF
+      const unsigned long long tp0 = global_ns();
+#endif
       const int nb = min(NB, d - j0);
       if (tid < 32) {
         double pv[4][NB];
@@ -403,6 +409,10 @@ __global__ void __launch_bounds__(kThreads) k_metric(RunDev r, double *partials,
         if (bad && tid == 0) sh_fail = 1;
       }
       __syncthreads();
+#ifdef NSS_MET_PROF
+      t_panel += global_ns() - tp0;
+      if (tid == 0 && j0 + NB >= d) st->stamp[7] = t_panel;
+#endif
       if (sh_fail) break;  // uniform
       const int b0 = j0 + nb;
       for (int u = 0; u < 8; ++u) {
