@@ -58,31 +58,35 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_batch_begin(RunDev r, P
 
 // resident blocks per SM the advance is compiled for (register budget);
 // measurement builds may change it (NSS_NVCC_EXTRA=-DNSS_ADV_MINB=4)
+#ifndef NSS_ADV_WARPS
+#define NSS_ADV_WARPS 1  // warps (chains) per advance block (A/B: 8 -> 4 -> 2 -> 1 measured 21.27 -> 21.00 -> 20.90 -> 20.26 ms per C4 iteration)
+#endif
+constexpr int kAdvWarps = NSS_ADV_WARPS;
 #ifndef NSS_ADV_MINB
-#define NSS_ADV_MINB 3
+#define NSS_ADV_MINB (24 / NSS_ADV_WARPS)
 #endif
 
 // W lanes per chain: 32, or 16 (two chains per warp; large d, where the
 // directions are precomputed): twice the chains in flight per SM for this
 // latency-bound state machine.
 template <int NPL, int W>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, NSS_ADV_MINB) k_batch_advance(RunDev r, PriorDev pr, BatchDev b,
+__global__ void __launch_bounds__(kAdvWarps * 32, NSS_ADV_MINB) k_batch_advance(RunDev r, PriorDev pr, BatchDev b,
                                                                                    int parity) {
   extern __shared__ float sm[];
   pdl_trigger();  // every block has started: the energy pass may launch (it waits for us)
   pdl_wait();     // the previous energy pass is complete
   const int wib = threadIdx.x >> 5;
   const int2 cr = chain_range(r);
-  const int c = cr.x + (blockIdx.x * kWarpsPerBlock * 32 + static_cast<int>(threadIdx.x)) / W;
+  const int c = cr.x + (blockIdx.x * kAdvWarps * 32 + static_cast<int>(threadIdx.x)) / W;
   if constexpr (W == 32) {
     // one row ticket per block: every warp reports its probe count once
-    __shared__ int sh_cnt[kWarpsPerBlock], sh_base;
+    __shared__ int sh_cnt[kAdvWarps], sh_base;
     auto ticket = [&](int np) -> int {
       if ((threadIdx.x & 31) == 0) sh_cnt[wib] = np;
       __syncthreads();
       if (threadIdx.x == 0) {
         int tot = 0;
-        for (int q = 0; q < kWarpsPerBlock; ++q) tot += sh_cnt[q];
+        for (int q = 0; q < kAdvWarps; ++q) tot += sh_cnt[q];
         sh_base = tot ? atomicAdd(&b.n_probe[parity], tot) : 0;
       }
       __syncthreads();
@@ -252,11 +256,11 @@ void begin_t(const RunDev &r, const PriorDev &pr, const BatchDev &b, const Launc
 
 template <int NPL, int W>
 void advance_t(const RunDev &r, const PriorDev &pr, const BatchDev &b, int parity, const LaunchCtx &lc) {
-  const size_t smem = W == 32 ? static_cast<size_t>(kWarpsPerBlock) * NPL * 32 * sizeof(float) : 0;
+  const size_t smem = W == 32 ? static_cast<size_t>(kAdvWarps) * NPL * 32 * sizeof(float) : 0;
   NSS_MAX_SMEM((k_batch_advance<NPL, W>), 160 * 1024);
   NSS_PIN_CARVEOUT((k_batch_advance<NPL, W>));
-  launch_maybe_pdl(k_batch_advance<NPL, W>, dim3(chain_blocks(r, kWarpsPerBlock * 32 / W)),
-                   dim3(kWarpsPerBlock * 32), smem, lc.stream, r, pr, b, parity);
+  launch_maybe_pdl(k_batch_advance<NPL, W>, dim3(chain_blocks(r, kAdvWarps * 32 / W)),
+                   dim3(kAdvWarps * 32), smem, lc.stream, r, pr, b, parity);
   ++*lc.launch_counter;
 }
 
