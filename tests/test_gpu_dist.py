@@ -183,3 +183,28 @@ def test_two_processes_nccl_bit_identical():
     assert np.array_equal(dx0 + dx1, single.dead()["x"])
     assert np.array_equal(reps0, single.evidence_reps()) and np.array_equal(reps1, reps0)
     assert probes == single.info()["probes"]
+
+
+@pytest.mark.parametrize("name,world,iters", [("C4", 2, 3), ("C4", 8, 2), ("C3a", 4, 3)])
+def test_group_full_size_bit_identical(name, world, iters):
+    """BASELINE sizes (C4: n = 2e4, k = 1e4, d = 100 on the tensor-core batch
+    engine; C3a: the warp engine at p = 300): the sharded decomposition at the
+    real candidate / moment block sizes reproduces the one-GPU run bit for bit."""
+    from paper_2601_23252_b200 import nss
+    prob, cfg = W.workload(name)
+    cfg = dict(cfg, seed=21)
+    single = nss.Sampler(prob, cfg)
+    g = nss.Group(prob, cfg, world)
+    single.steps(iters)
+    g.steps(iters)
+    x, e = g.owned_live()
+    xs, es = single.get_live()
+    assert np.array_equal(xs, x) and np.array_equal(es, e), "live set differs"
+    ds, dg = single.dead(), g.dead()
+    for key in ("e", "n_live", "gid", "birth", "x"):
+        assert np.array_equal(ds[key], dg[key]), f"dead store field {key} differs"
+    assert np.array_equal(single.evidence_reps(), g.members[0].evidence_reps())
+    infos = [m.info() for m in g.members]
+    assert sum(i["energy_evals"] for i in infos) == single.info()["energy_evals"]
+    g.close()
+    single.close()
