@@ -162,7 +162,12 @@ __global__ void __launch_bounds__(kThreads) k_select(RunDev r, unsigned long lon
 
   // ---- dead order: the k selected keys sorted descending ----
   unsigned long long *sorted = gsel + k;
-  sort_desc(gsel, k, sorted, gscratch + (cached ? 0 : n), sbuf);
+  // the key cache / ordinals are dead after the compaction: the sort may use
+  // all of the dynamic shared memory (C4: 16 384 keys on chip instead of
+  // chunked passes through global memory)
+  const int cap = cached ? kSmemKeysMax + kSmemSortMax
+                         : ord32 ? kSmemSortMax + (n * 4) / 8 : kSmemSortMax;
+  sort_desc(gsel, k, sorted, gscratch + (cached ? 0 : n), sm, cap);
   for (int j = tid; j < k; j += blockDim.x) r.dead_gid[j] = static_cast<int>(sorted[j] & 0xffffffffu);
   const float e_star = r.E[static_cast<int>(sorted[k - 1] & 0xffffffffu)];
 

@@ -127,8 +127,10 @@ __device__ void bitonic_desc_chunked(unsigned long long *g, int P, unsigned long
 }
 
 // Sort `cnt` distinct keys descending into out[] (shared or global).
+// sbuf holds `cap` keys (at least kSmemSortMax): sorts of up to cap keys
+// stay in shared memory, larger ones go through gscratch in chunks
 __device__ void sort_desc(const unsigned long long *in, int cnt, unsigned long long *out,
-                          unsigned long long *gscratch, unsigned long long *sbuf) {
+                          unsigned long long *gscratch, unsigned long long *sbuf, int cap = kSmemSortMax) {
   if (cnt <= kRankSortMax) {
     // rank sort: position = number of larger keys (keys are unique); the keys
     // are staged in shared memory and read as broadcasts
@@ -145,10 +147,10 @@ __device__ void sort_desc(const unsigned long long *in, int cnt, unsigned long l
   }
   int P = 1;
   while (P < cnt) P <<= 1;
-  unsigned long long *buf = (P <= kSmemSortMax) ? sbuf : gscratch;
+  unsigned long long *buf = (P <= cap) ? sbuf : gscratch;
   for (int i = threadIdx.x; i < P; i += blockDim.x) buf[i] = (i < cnt) ? in[i] : 0ull;
   __syncthreads();
-  if (P <= kSmemSortMax)
+  if (P <= cap)
     bitonic_desc(buf, P);
   else
     bitonic_desc_chunked(buf, P, sbuf, kSmemSortMax);
